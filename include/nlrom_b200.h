@@ -1,0 +1,210 @@
+/*
+ * nlrom_b200 — C ABI of the B200-native DAE-subspace Newton-step hot path
+ * (arXiv 2102.11026; reference package `nlrom`, /root/reference/pkg).
+ *
+ * The reference has no FFI ("in-process, no external
+ * interfaces"); its drop-in surface is the Python API of `nlrom` (SURVEY.md
+ * §8b). Each entry point below is the native body of one reference operation;
+ * the Python package `nlrom` (this repo) binds them with ctypes
+ * (paper_2102_11026_b200/_lib.py, INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - plain pointers and sizes only; all host arrays C-contiguous float64 / int32;
+ *    matrices row-major; multicomplex part stacks are (2^k, dim, batch) with the
+ *    bitmask slot layout of mcx.py:1-8 (MCArray layout, mcx.py:294-300);
+ *  - the caller owns host arrays (copied in / out); handles own device memory,
+ *    streams and CUDA graphs; results never alias inputs;
+ *  - every call returns an NLROM_* status; the text of the last error is
+ *    available from nlrom_*_last_error();
+ *  - a handle must not be used from two threads at once ("one simulation per
+ *    thread"); calls on different handles are independent.
+ */
+#ifndef NLROM_B200_H
+#define NLROM_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define NLROM_API __attribute__((visibility("default")))
+#else
+#define NLROM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (SURVEY.md §8b "errors") */
+#define NLROM_OK 0
+#define NLROM_ERR_ORDER 1        /* -> nlrom.mcx.OrderError (mcx.py:31-32)            */
+#define NLROM_ERR_DIM 2          /* -> ValueError "dimension mismatch"  */
+#define NLROM_ERR_NONFINITE 3    /* -> FloatingPointError "non-finite"  */
+#define NLROM_ERR_NEWTON 4       /* -> NewtonDivergence with last norm  */
+#define NLROM_ERR_CUDA 5         /* -> RuntimeError                                   */
+#define NLROM_ERR_ARG 6          /* -> ValueError                                     */
+#define NLROM_ERR_NOCACHE 7      /* -> backward without forward         */
+
+/* ------------------------------------------------------------------------- */
+/* generic dense network: densenet.forward / densenet.backward                */
+/* (LayerSpec kinds SPEC.md:111-116)                         */
+/* ------------------------------------------------------------------------- */
+#define NLROM_LAYER_FC 0
+#define NLROM_LAYER_FILTER 1
+#define NLROM_LAYER_SIN 2
+#define NLROM_LAYER_SQUARE 3
+
+typedef struct nlrom_net nlrom_net;
+
+typedef struct {
+  int kind;           /* NLROM_LAYER_*                                          */
+  int in_dim, out_dim;
+  const double* W;    /* FC: (out,in) row-major; FILTER: basis U (dim, n_basis) */
+  const double* b;    /* FC: (out,)                                             */
+  int n_basis;        /* FILTER: n_p                                            */
+} nlrom_layer_desc;
+
+/* densenet.DenseNet upload (replaces in-process numpy weights) */
+NLROM_API int nlrom_net_create(nlrom_net** out, int device, int n_layers, const nlrom_layer_desc* layers);
+NLROM_API void nlrom_net_destroy(nlrom_net* net);
+NLROM_API const char* nlrom_net_last_error(const nlrom_net* net);
+
+/* densenet.forward(net, x) over real (order 0) or multicomplex (order 1..3)
+ * inputs: parts_in (2^order, in_dim, batch) -> parts_out (2^order, out_dim, batch).
+ * True multicomplex arithmetic (recursive sin, mcx.py:63-100). */
+NLROM_API int nlrom_net_forward(nlrom_net* net, int order, const double* parts_in, int batch, double* parts_out);
+
+/* densenet.backward(net, x, upstream), order 0 (real) or 1 (complex-step BP,
+ * PAPER.md:353-366). x_parts (2^o, in, B), up_parts (2^o, out, B) ->
+ * in_cot (2^o, in, B); param_cot (nullable): for each FC layer in order,
+ * dW (2^o, out, in) then db (2^o, out), concatenated. */
+NLROM_API int nlrom_net_backward(nlrom_net* net, int order, const double* x_parts, const double* up_parts,
+                       int batch, double* in_cot, double* param_cot);
+
+/* ------------------------------------------------------------------------- */
+/* reduced simulator context: decoder + FE model + cubature                   */
+/* (daereduce.ReducedModel, elastic.ElasticModel, neucubature.CubatureModel)  */
+/* ------------------------------------------------------------------------- */
+typedef struct nlrom_ctx nlrom_ctx;
+
+typedef struct {
+  /* dims: N free DOFs, n_p linear (PCA) and n_q nonlinear (DAE) coordinates   */
+  int N, n_p, n_q;
+  /* decoder D: n_fc FC layers widths[0]=n_q .. widths[n_fc]=N, sin after all
+     but the last, then the filter I - U U^T       */
+  int n_fc;
+  const int* widths;
+  const double* const* W;   /* W[l]: (widths[l+1], widths[l]) row-major       */
+  const double* const* b;   /* b[l]: (widths[l+1],)                            */
+  const double* U;          /* (N, n_p) row-major, orthonormal columns         */
+  const double* mass;       /* (N,) lumped, free DOFs                          */
+  /* tet mesh (elastic.TetMesh / ElasticModel)                */
+  int n_verts, n_tets;
+  const int* tets;          /* (T,4)                                           */
+  const int* vert_dof;      /* (V,) free-vertex index or -1 if fixed           */
+  const double* Dm_inv;     /* (T,3,3) row-major inverse rest edge matrices    */
+  const double* vol;        /* (T,)                                            */
+  double mu, lambda, alpha; /* StVK Lame parameters, Rayleigh mass damping     */
+  /* cubature set C and weight net (neucubature.CubatureModel)
+     wnet: N -> wn -> wn -> wn (sin) -> T (square), only rows of C are used    */
+  int n_cub;
+  const int* cub_elems;     /* (|C|,) element ids, duplicate-free              */
+  int wnet_width;
+  const double* const* wnet_W; /* 4 layers, (out,in) row-major               */
+  const double* const* wnet_b;
+  /* number of independent simulations sharing this model, batched through one
+     set of kernels (configs[4]: 4096 sims); state arrays are (n_sims, n)      */
+  int n_sims;
+} nlrom_model_desc;
+
+NLROM_API int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc* desc);
+NLROM_API void nlrom_destroy(nlrom_ctx* ctx);
+NLROM_API const char* nlrom_last_error(const nlrom_ctx* ctx);
+
+/* diffops queries with the reference pass structure.
+ * op: one of NLROM_OP_*; vec = v (jvp/hvv/hv/svv) or a (vjp/vhp), may be NULL
+ * for value/jacobian. out sizes: VALUE/JVP/HVV N; JACOBIAN/HV/SVV (N,n_q)
+ * row-major; VJP n_q; VHP (n_q,n_q) row-major.
+ * mode 0: multi-dual arithmetic on eps-scaled slots (eps cancels exactly);
+ * mode 1: literal multicomplex CSFD with the given eps (mcx arithmetic). */
+#define NLROM_OP_VALUE 0
+#define NLROM_OP_JVP 1
+#define NLROM_OP_JACOBIAN 2
+#define NLROM_OP_HVV 3
+#define NLROM_OP_HV 4
+#define NLROM_OP_SVV 5
+#define NLROM_OP_VJP 6
+#define NLROM_OP_VHP 7
+NLROM_API int nlrom_diffop(nlrom_ctx* ctx, int op, const double* q, const double* vec, double eps, int mode, double* out);
+
+/* SimConfig */
+typedef struct {
+  double dt;
+  double newton_tol;
+  int max_iters;
+  int drop_fict;      /* LSD simplification toggle                              */
+  int integration;    /* 0 = cubature (C, wnet weights), 1 = exact_sum          */
+  int line_search;    /* backtracking halving <= 10          */
+  int fixed_iters;    /* > 0: exactly that many Newton steps, no line search    */
+} nlrom_simcfg;
+
+typedef struct {
+  int iters;
+  double res_norm;
+  int status;
+} nlrom_step_info;
+
+/* The fused per-iteration pieces, each at candidate r with state (r_bar, rdot_bar):
+ * rdsim.residual, rdsim.system_jacobian,
+ * rdsim.delta_j, rdsim.fictitious_force. */
+NLROM_API int nlrom_residual(nlrom_ctx* ctx, const double* r, const double* r_bar, const double* rdot_bar,
+                   const double* f_ext, const nlrom_simcfg* cfg, double* phi);
+NLROM_API int nlrom_system_jacobian(nlrom_ctx* ctx, const double* r, const double* r_bar, const double* rdot_bar,
+                          const double* f_ext, const nlrom_simcfg* cfg, double* S);
+NLROM_API int nlrom_delta_j(nlrom_ctx* ctx, const double* q, const double* q_bar, const double* qdot_bar,
+                  double dt, int drop_fict, double* dJ);
+NLROM_API int nlrom_fictitious_force(nlrom_ctx* ctx, const double* q, const double* q_bar, double* f_fict);
+
+/* neucubature: wnet_forward restricted to C and
+ * cubature_integrate: f_red (n), K_red (n,n) row-major,
+ * integration 0 = cubature, 1 = exact_sum (C = all elements, w = 1). */
+NLROM_API int nlrom_wnet_forward(nlrom_ctx* ctx, const double* r, double* w_cub);
+NLROM_API int nlrom_cubature_integrate(nlrom_ctx* ctx, const double* r, int integration, double* f_red, double* K_red);
+
+/* elastic: per-element StVK forces of a full-space displacement u (N,):
+ * f_int (N,) assembled (elastic.internal_force) and, if
+ * want_K, per-element stiffness K_e (T,12,12) (elastic.stiffness, SPEC.md:336-343;
+ * rows/cols vertex-major over the element's 4 vertices, fixed DOFs included). */
+NLROM_API int nlrom_element_forces(nlrom_ctx* ctx, const double* u, int want_K, double* f_int, double* K_elems);
+
+/* elastic.element_reduced_force: J~(r)_e^T f_e(u(r)) for a list
+ * of elements; out (n_elems, n) row-major. */
+NLROM_API int nlrom_element_reduced_forces(nlrom_ctx* ctx, const double* r, const int* elems, int n_elems, double* out);
+
+/* daereduce: u = U p + D(q) (Eq. 9) and J~ = [U, J] (N, n) row-major */
+NLROM_API int nlrom_full_displacement(nlrom_ctx* ctx, const double* r, double* u);
+NLROM_API int nlrom_jtilde(nlrom_ctx* ctx, const double* q, double* Jt);
+
+/* rdsim.step: host state in / out */
+NLROM_API int nlrom_step(nlrom_ctx* ctx, const double* r_bar, const double* rdot_bar, const double* f_ext,
+               const nlrom_simcfg* cfg, double* r_out, double* rdot_out, nlrom_step_info* info);
+
+/* Device-resident variant for torch tensors: all pointers are device pointers
+ * on `stream` (cudaStream_t passed as void*). Fixed-iteration mode only
+ * (cfg->fixed_iters > 0), no host synchronisation inside. */
+NLROM_API int nlrom_step_device(nlrom_ctx* ctx, const double* r_bar, const double* rdot_bar, const double* f_ext,
+                      const nlrom_simcfg* cfg, double* r_out, double* rdot_out, void* stream);
+
+/* Timing hook for bench.py: replays `n_iters` fixed Newton iterations of the
+ * captured CUDA graph at the state last set by nlrom_step*, and returns the
+ * device time (CUDA events on the graph's stream) of the whole replay, plus the
+ * device time of the dominant kernel (last decoder layer), averaged per
+ * iteration. */
+NLROM_API int nlrom_bench_iterations(nlrom_ctx* ctx, int n_iters, int flush_l2, float* ms_total, float* ms_dominant);
+
+/* Number of kernel launches of one Newton iteration (for bench "gpu_launches"). */
+NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NLROM_B200_H */

@@ -1,0 +1,925 @@
+// Reduced simulator context: the per-Newton-iteration hot path of arXiv 2102.11026
+// (rdsim.step) as a CUDA-graph of sm_100a kernels.
+//
+// One Newton iteration = E (evaluate at r) + J (Jacobian + solve):
+//   E: seed jet -> decoder bundle forward (L fp64-DMMA GEMMs with fused jet-sin
+//      epilogues; last layer fused with the filter) -> weight net -> StVK cubature
+//      (+ J~ projection) -> assembly of a and [J~^T M R | J~^T a] partials -> phi, ||phi||
+//   J: vhp = H~^T a by complex-step backprop (dual arithmetic) -> S = reduce + vhp
+//      -> in-CTA LU with partial pivoting -> dr (r += dr in fixed-iteration mode)
+#include <vector>
+#include <string>
+#include <map>
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include "common.cuh"
+#include "epilogues.cuh"
+#include "sim_kernels.cuh"
+
+namespace nlrom {
+void fc_forward(int order, int act, const GemmArgs& g, double* Y, int ldy, const double* bias, double* cache,
+                cudaStream_t st);
+}
+
+using namespace nlrom;
+
+namespace {
+
+using CfgBwd = GemmCfg<16, 16, 1, 1, 4>;
+
+template <int G> using CfgHid = GemmCfg<16, G, 1, 1, 4>;
+template <int G> using CfgOut = GemmCfg<64, G, 4, 1, 1>;
+
+struct CubSet {
+  IBuf elems;
+  int n = 0;
+  IBuf row_ids, row_ptr, entries;
+  int n_rows = 0;
+  int epc = 1, nchunk = 0;
+  DBuf fe_w, part_f, part_K, f;
+};
+
+int gemm_launch_count = 0;
+
+}  // namespace
+
+struct nlrom_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  double last_norm = 0.0;
+  int N = 0, n_p = 0, n_q = 0, n = 0, L = 0, n_sims = 1, T = 0, V = 0;
+  std::vector<int> widths;
+  // decoder
+  std::vector<DBuf> W, WT, b;
+  std::vector<int> ldW, ldWT;
+  DBuf Alast, AlastT, AT, Pb, U, mass;
+  int ldlast = 0, ldAlastT = 0, wL1 = 0;
+  // mesh
+  IBuf elem_rows;
+  DBuf Dm_inv, vol;
+  double mu = 0, lam = 0, alpha = 0;
+  CubSet setC, setAll;
+  // wnet
+  int wn = 0, n_cub = 0;
+  DBuf W1, b1, W2, b2, W3, b3, W4C, b4C;
+  int wsplit = 0, wchunk = 0;
+  DBuf wpart, wC;
+  // bundle
+  int G = 0, gps = 0, Cb = 0, ldq = 0, ldjt = 0, lddj = 0;
+  DBuf X0;
+  std::vector<DBuf> H, cache;
+  std::vector<int> ldH, ldc;
+  DBuf u, value, hvv, Jt, dJ;
+  // assembly / solve
+  int rpc = 64, nchA = 0;
+  DBuf a, partA, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
+  IBuf status;
+  // backward
+  int bsplit = 0, bchunk = 0;
+  DBuf bpart, Delta0, Delta1, Gt;
+  int ldGt = 0;
+  // graphs
+  cudaGraphExec_t gE = nullptr, gJ = nullptr, gIter = nullptr;
+  std::string graph_key;
+  int launches_E = 0, launches_J = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DBuf flush;
+};
+
+namespace {
+
+int fail(nlrom_ctx* c, const Error& e) {
+  if (c) c->err = e.what();
+  return e.code;
+}
+
+template <class K, class... Args>
+void launch(nlrom_ctx* c, K kernel, dim3 grid, dim3 block, size_t smem, Args... args) {
+  kernel<<<grid, block, smem, c->st>>>(args...);
+  NL_CHECK_LAUNCH();
+  ++gemm_launch_count;
+}
+
+int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL, (n + bs - 1) / bs)); }
+
+// ---------------------------------------------------------------- GEMM dispatch
+template <class Epi>
+void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st) {
+  switch (G) {
+    case 8: launch_gemm<CfgHid<8>>(g, e, st); break;
+    case 16: launch_gemm<CfgHid<16>>(g, e, st); break;
+    case 24: launch_gemm<CfgHid<24>>(g, e, st); break;
+    case 32: launch_gemm<CfgHid<32>>(g, e, st); break;
+    case 64: launch_gemm<CfgHid<64>>(g, e, st); break;
+    default: throw Error(NLROM_ERR_ARG, "unsupported jet group size");
+  }
+  ++gemm_launch_count;
+}
+template <class Epi>
+void out_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st) {
+  switch (G) {
+    case 8: launch_gemm<CfgOut<8>>(g, e, st); break;
+    case 16: launch_gemm<CfgOut<16>>(g, e, st); break;
+    case 24: launch_gemm<CfgOut<24>>(g, e, st); break;
+    case 32: launch_gemm<CfgOut<32>>(g, e, st); break;
+    case 64: launch_gemm<CfgOut<64>>(g, e, st); break;
+    default: throw Error(NLROM_ERR_ARG, "unsupported jet group size");
+  }
+  ++gemm_launch_count;
+}
+
+void choose_groups(int n_q, int width, int& G, int& gps) {
+  const int cand[5] = {1, 3, 5, 7, 15};
+  int g = 3;
+  if (const char* env = getenv("NLROM_JET_TANGENTS")) g = atoi(env);
+  else if (n_q <= 15) {
+    for (int c : cand)
+      if (c >= n_q) { g = c; break; }
+  } else {
+    g = 3;
+  }
+  bool ok = false;
+  for (int c : cand) ok |= (c == g);
+  if (!ok) throw Error(NLROM_ERR_ARG, "NLROM_JET_TANGENTS must be one of 1,3,5,7,15");
+  G = 4 + 4 * g;
+  gps = (n_q + g - 1) / g;
+  (void)width;
+}
+
+void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std::vector<int>& rows_host) {
+  s.n = (int)elems.size();
+  s.elems.upload(elems.data(), elems.size());
+  // CSR: unique rows -> (element slot * 12 + l)
+  std::map<int, std::vector<int>> m;
+  for (int i = 0; i < s.n; ++i)
+    for (int l = 0; l < 12; ++l) {
+      int row = rows_host[(size_t)elems[i] * 12 + l];
+      if (row >= 0) m[row].push_back(i * 12 + l);
+    }
+  std::vector<int> ids, ptr{0}, ent;
+  for (auto& kv : m) {
+    ids.push_back(kv.first);
+    for (int e : kv.second) ent.push_back(e);
+    ptr.push_back((int)ent.size());
+  }
+  s.n_rows = (int)ids.size();
+  s.row_ids.upload(ids.data(), ids.size());
+  s.row_ptr.upload(ptr.data(), ptr.size());
+  s.entries.upload(ent.data(), ent.size());
+  const int n = c->n;
+  s.epc = 8;
+  while (s.epc > 1 && (size_t)(2 * s.epc * 12 * n + s.epc * 156) * 8 > 200 * 1024) s.epc /= 2;
+  s.nchunk = std::max(1, ceil_div(std::max(s.n, 1), s.epc));
+  s.fe_w.alloc((size_t)c->n_sims * std::max(s.n, 1) * 12);
+  s.part_f.alloc((size_t)c->n_sims * s.nchunk * n);
+  s.part_K.alloc((size_t)c->n_sims * s.nchunk * n * n);
+  s.f.alloc((size_t)c->n_sims * c->N);
+}
+
+// ----------------------------------------------------------------- E and J phases
+void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
+  const int ncols = c->n_sims * c->Cb;
+  const int nq = c->n_q;
+  launch(c, k_seed_jet, grid1((long long)ncols * nq), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p,
+         (const double*)c->rdbar.p, c->X0.p, c->ldq, c->n_p, nq, c->n, c->G, c->gps, c->n_sims, dt, c->alpha,
+         drop_fict);
+  const double* in = c->X0.p;
+  int ldin = c->ldq;
+  for (int l = 0; l + 1 < c->L; ++l) {
+    GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
+    EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq};
+    hid_gemm(c->G, g, e, c->st);
+    in = c->H[l].p;
+    ldin = c->ldH[l];
+  }
+  // T = (U^T W_L) h  -> columns wL1.. of the last hidden buffer (filter fused as K-extension)
+  {
+    GemmArgs g{c->AT.p, in, round_up(c->wL1, 2), ldin, c->n_p, ncols, c->wL1, 0, 0};
+    EpiStore e{c->H[c->L - 2].p + c->wL1, c->ldlast, 0, nullptr, 1, nullptr};
+    hid_gemm(c->G, g, e, c->st);
+  }
+  {
+    GemmArgs g{c->Alast.p, in, c->ldlast, ldin, c->N, ncols, c->wL1 + c->n_p, 0, 0};
+    EpiJetOut e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
+                c->n_p, nq, c->G, c->gps};
+    out_gemm(c->G, g, e, c->st);
+  }
+}
+
+void wnet_phase(nlrom_ctx* c) {
+  launch(c, k_gemv_splitk, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
+         (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
+  launch(c, k_wnet_tail, c->n_sims, 256, (size_t)2 * c->wn * 8, (const double*)c->wpart.p, c->wsplit, c->wn,
+         (const double*)c->b1.p, (const double*)c->W2.p, (const double*)c->b2.p, (const double*)c->W3.p,
+         (const double*)c->b3.p, (const double*)c->W4C.p, (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
+}
+
+void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted) {
+  CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, weighted ? c->wC.p : nullptr, c->u.p, c->Jt.p,
+            c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk, nullptr, nullptr};
+  size_t smem = (size_t)(2 * s.epc * 12 * c->n + s.epc * 156) * 8;
+  launch(c, k_cubature, dim3(s.nchunk, c->n_sims), 256, smem, a);
+  launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
+         (const int*)s.row_ptr.p, (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N,
+         c->n_sims);
+}
+
+void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
+  AsmArgs A{c->Jt.p, c->ldjt, c->dJ.p, c->lddj, c->mass.p, c->hvv.p, s.f.p, c->fext.p, c->r.p, c->rbar.p,
+            c->rdbar.p, c->a.p, c->partA.p, c->N, c->n, c->n_p, c->n_q, c->rpc, c->nchA, dt, c->alpha, drop_fict};
+  size_t smem = (size_t)(c->rpc * c->n + c->rpc * (c->n + 1) + c->n) * 8;
+  launch(c, k_assemble, dim3(c->nchA, c->n_sims), 256, smem, A);
+  launch(c, k_reduce_phi, c->n_sims, 128, 0, (const double*)c->partA.p, c->nchA, c->n, c->phi.p, c->norm.p);
+}
+
+void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg) {
+  bundle_forward(c, cfg.dt, cfg.drop_fict);
+  CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
+  if (cfg.integration == 0) wnet_phase(c);
+  cubature_phase(c, s, cfg.integration == 0);
+  assemble_phase(c, s, cfg.dt, cfg.drop_fict);
+}
+
+// vhp backward: dual (NS = 2) passes, cache written by the bundle forward.
+void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int npass_per_sim, std::vector<DBuf>& caches,
+                      std::vector<int>& ldcs, DBuf& D0, DBuf& D1, DBuf& Gout, int ldG) {
+  const int ncols = c->n_sims * npass_per_sim * NS;
+  const int M = c->wL1 + c->n_p;
+  launch(c, k_gemv_splitk, dim3(c->bsplit, c->n_sims), 256, 0, (const double*)c->AlastT.p, c->ldAlastT, a_vec,
+         (long long)c->N, M, c->N, c->bchunk, c->bpart.p, c->n_sims);
+  const int l_top = c->L - 2;
+  size_t smem = (size_t)(2 * c->wL1 + c->n_p) * 8;
+  if (NS == 2) {
+    if (mc)
+      launch(c, k_bwd_top<2, 1>, c->n_sims, 256, smem, (const double*)c->bpart.p, c->bsplit, c->wL1, c->n_p,
+             (const double*)c->AT.p, (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p, c->n_sims);
+    else
+      launch(c, k_bwd_top<2, 0>, c->n_sims, 256, smem, (const double*)c->bpart.p, c->bsplit, c->wL1, c->n_p,
+             (const double*)c->AT.p, (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p, c->n_sims);
+  } else {
+    launch(c, k_bwd_top<1, 1>, c->n_sims, 256, smem, (const double*)c->bpart.p, c->bsplit, c->wL1, c->n_p,
+           (const double*)c->AT.p, (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p, c->n_sims);
+  }
+  DBuf* cur = &D0;
+  DBuf* nxt = &D1;
+  for (int l = c->L - 2; l >= 1; --l) {
+    // delta_{l-1} = (W_l^T Delta_l) * act'(z_{l-1})
+    GemmArgs g{c->WT[l].p, cur->p, c->ldWT[l], ldcs[l], c->widths[l], ncols, c->widths[l + 1], 0, 0};
+    if (NS == 2) {
+      if (mc) launch_gemm<CfgBwd>(g, EpiBwdAct<2, ACT_SIN_MC>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
+      else launch_gemm<CfgBwd>(g, EpiBwdAct<2, ACT_SIN_MD>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
+    } else {
+      launch_gemm<CfgBwd>(g, EpiBwdAct<1, ACT_SIN_MC>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
+    }
+    ++gemm_launch_count;
+    std::swap(cur, nxt);
+  }
+  GemmArgs g{c->WT[0].p, cur->p, c->ldWT[0], ldcs[0], c->widths[0], ncols, c->widths[1], 0, 0};
+  launch_gemm<CfgBwd>(g, EpiStore{Gout.p, ldG, 0, nullptr, 1, nullptr}, c->st);
+  ++gemm_launch_count;
+}
+
+void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply) {
+  decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
+  CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
+  const int n = c->n;
+  launch(c, k_reduce_S, grid1((long long)n * n * c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
+         (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p,
+         c->n_sims);
+  launch(c, k_lu_solve, c->n_sims, 256, (size_t)n * (n + 2) * 8, (const double*)c->S.p, (const double*)c->phi.p,
+         c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p);
+}
+
+std::string cfg_key(const nlrom_simcfg& cfg) {
+  char buf[128];
+  snprintf(buf, sizeof buf, "%.17g|%d|%d", cfg.dt, cfg.drop_fict, cfg.integration);
+  return buf;
+}
+
+cudaGraphExec_t capture(nlrom_ctx* c, const std::function<void()>& body, int* count) {
+  gemm_launch_count = 0;
+  cudaGraph_t g;
+  NL_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  try {
+    body();
+  } catch (...) {
+    cudaStreamEndCapture(c->st, &g);
+    throw;
+  }
+  NL_CUDA(cudaStreamEndCapture(c->st, &g));
+  cudaGraphExec_t ex;
+  NL_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  cudaGraphDestroy(g);
+  if (count) *count = gemm_launch_count;
+  return ex;
+}
+
+void ensure_graphs(nlrom_ctx* c, const nlrom_simcfg& cfg) {
+  std::string key = cfg_key(cfg);
+  if (key == c->graph_key && c->gE) return;
+  if (c->gE) cudaGraphExecDestroy(c->gE);
+  if (c->gJ) cudaGraphExecDestroy(c->gJ);
+  if (c->gIter) cudaGraphExecDestroy(c->gIter);
+  c->gE = c->gJ = c->gIter = nullptr;
+  // eager warm-up (sets kernel attributes outside of capture)
+  phase_E(c, cfg);
+  phase_J(c, cfg, false);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  c->gE = capture(c, [&] { phase_E(c, cfg); }, &c->launches_E);
+  c->gJ = capture(c, [&] { phase_J(c, cfg, false); }, &c->launches_J);
+  c->gIter = capture(c, [&] { phase_E(c, cfg); phase_J(c, cfg, true); }, nullptr);
+  c->graph_key = key;
+}
+
+void upload(DBuf& d, const double* h, size_t n) {
+  d.alloc(n);
+  if (n) NL_CUDA(cudaMemcpy(d.p, h, n * 8, cudaMemcpyHostToDevice));
+}
+
+void h2d(nlrom_ctx* c, DBuf& d, const double* h, size_t n) {
+  NL_CUDA(cudaMemcpyAsync(d.p, h, n * 8, cudaMemcpyHostToDevice, c->st));
+}
+void d2h(nlrom_ctx* c, double* h, const DBuf& d, size_t n) {
+  NL_CUDA(cudaMemcpyAsync(h, d.p, n * 8, cudaMemcpyDeviceToHost, c->st));
+}
+
+void set_state(nlrom_ctx* c, const double* r, const double* rbar, const double* rdbar, const double* fext) {
+  const size_t nn = (size_t)c->n_sims * c->n;
+  if (r) h2d(c, c->r, r, nn);
+  if (rbar) h2d(c, c->rbar, rbar, nn);
+  if (rdbar) h2d(c, c->rdbar, rdbar, nn);
+  if (fext) h2d(c, c->fext, fext, (size_t)c->n_sims * c->N);
+}
+
+void check_status(nlrom_ctx* c) {
+  std::vector<int> st(c->n_sims);
+  NL_CUDA(cudaMemcpyAsync(st.data(), c->status.p, c->n_sims * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  for (int s : st)
+    if (s) throw Error(NLROM_ERR_NONFINITE, "singular system Jacobian (zero pivot in LU)");
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+
+extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc* d) {
+  nlrom_ctx* c = nullptr;
+  try {
+    if (!out || !d) throw Error(NLROM_ERR_ARG, "null argument");
+    if (d->n_fc < 2) throw Error(NLROM_ERR_ARG, "decoder needs >= 2 FC layers");
+    if (d->widths[0] != d->n_q || d->widths[d->n_fc] != d->N) throw Error(NLROM_ERR_DIM, "decoder widths do not match (n_q, N)");
+    NL_CUDA(cudaSetDevice(device));
+    c = new nlrom_ctx();
+    c->device = device;
+    NL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    NL_CUDA(cudaEventCreate(&c->ev0));
+    NL_CUDA(cudaEventCreate(&c->ev1));
+    c->n_sims = d->n_sims > 0 ? d->n_sims : 1;
+    c->N = d->N; c->n_p = d->n_p; c->n_q = d->n_q; c->n = d->n_p + d->n_q; c->L = d->n_fc;
+    c->T = d->n_tets; c->V = d->n_verts;
+    c->mu = d->mu; c->lam = d->lambda; c->alpha = d->alpha;
+    c->widths.assign(d->widths, d->widths + d->n_fc + 1);
+    const int N = c->N, n_p = c->n_p, n_q = c->n_q, L = c->L;
+    c->wL1 = c->widths[L - 1];
+    // hidden FC layers 0..L-2 and their transposes
+    c->W.resize(L); c->WT.resize(L); c->b.resize(L); c->ldW.resize(L); c->ldWT.resize(L);
+    for (int l = 0; l < L - 1; ++l) {
+      int in = c->widths[l], o = c->widths[l + 1];
+      c->ldW[l] = round_up(in, 2);
+      c->ldWT[l] = round_up(o, 2);
+      upload_matrix(c->W[l], d->W[l], o, in, c->ldW[l]);
+      std::vector<double> wt((size_t)in * o);
+      for (int r = 0; r < o; ++r)
+        for (int k = 0; k < in; ++k) wt[(size_t)k * o + r] = d->W[l][(size_t)r * in + k];
+      upload_matrix(c->WT[l], wt.data(), in, o, c->ldWT[l]);
+      upload(c->b[l], d->b[l], o);
+    }
+    // last layer fused with the filter: D = [W_L | -U] [h ; U^T W_L h] + P b_L
+    const double* WL = d->W[L - 1];
+    const double* bL = d->b[L - 1];
+    const int w = c->wL1;
+    c->ldlast = round_up(w + n_p, 2);
+    {
+      std::vector<double> A((size_t)N * (w + n_p));
+      for (int r = 0; r < N; ++r) {
+        for (int k = 0; k < w; ++k) A[(size_t)r * (w + n_p) + k] = WL[(size_t)r * w + k];
+        for (int j = 0; j < n_p; ++j) A[(size_t)r * (w + n_p) + w + j] = -d->U[(size_t)r * n_p + j];
+      }
+      upload_matrix(c->Alast, A.data(), N, w + n_p, c->ldlast);
+      c->ldAlastT = round_up(N, 2);
+      std::vector<double> At((size_t)(w + n_p) * N);
+      for (int r = 0; r < N; ++r)
+        for (int k = 0; k < w + n_p; ++k) At[(size_t)k * N + r] = A[(size_t)r * (w + n_p) + k];
+      upload_matrix(c->AlastT, At.data(), w + n_p, N, c->ldAlastT);
+      std::vector<double> ATh((size_t)n_p * w, 0.0), Utb(n_p, 0.0), Pbh(N);
+      for (int r = 0; r < N; ++r)
+        for (int j = 0; j < n_p; ++j) {
+          const double ur = d->U[(size_t)r * n_p + j];
+          Utb[j] += ur * bL[r];
+          for (int k = 0; k < w; ++k) ATh[(size_t)j * w + k] += ur * WL[(size_t)r * w + k];
+        }
+      for (int r = 0; r < N; ++r) {
+        double s = bL[r];
+        for (int j = 0; j < n_p; ++j) s -= d->U[(size_t)r * n_p + j] * Utb[j];
+        Pbh[r] = s;
+      }
+      upload_matrix(c->AT, ATh.data(), n_p, w, round_up(w, 2));
+      upload(c->Pb, Pbh.data(), N);
+      upload(c->U, d->U, (size_t)N * n_p);
+      upload(c->mass, d->mass, N);
+    }
+    // mesh
+    {
+      std::vector<int> rows((size_t)c->T * 12);
+      for (int e = 0; e < c->T; ++e)
+        for (int v = 0; v < 4; ++v) {
+          int dv = d->vert_dof[d->tets[(size_t)e * 4 + v]];
+          for (int a = 0; a < 3; ++a) rows[(size_t)e * 12 + v * 3 + a] = dv >= 0 ? 3 * dv + a : -1;
+        }
+      c->elem_rows.upload(rows.data(), rows.size());
+      upload(c->Dm_inv, d->Dm_inv, (size_t)c->T * 9);
+      upload(c->vol, d->vol, c->T);
+      std::vector<int> cub(d->cub_elems, d->cub_elems + d->n_cub), all(c->T);
+      for (int e = 0; e < c->T; ++e) all[e] = e;
+      build_set(c, c->setC, cub, rows);
+      build_set(c, c->setAll, all, rows);
+    }
+    // weight net (rows of the last layer restricted to C)
+    {
+      c->wn = d->wnet_width;
+      c->n_cub = d->n_cub;
+      const int wn = c->wn;
+      upload_matrix(c->W1, d->wnet_W[0], wn, N, round_up(N, 2));
+      upload(c->b1, d->wnet_b[0], wn);
+      upload(c->W2, d->wnet_W[1], (size_t)wn * wn);
+      upload(c->b2, d->wnet_b[1], wn);
+      upload(c->W3, d->wnet_W[2], (size_t)wn * wn);
+      upload(c->b3, d->wnet_b[2], wn);
+      std::vector<double> w4((size_t)std::max(1, c->n_cub) * wn), b4(std::max(1, c->n_cub));
+      for (int j = 0; j < c->n_cub; ++j) {
+        int e = d->cub_elems[j];
+        if (e < 0 || e >= c->T) throw Error(NLROM_ERR_ARG, "cubature element id out of range");
+        for (int k = 0; k < wn; ++k) w4[(size_t)j * wn + k] = d->wnet_W[3][(size_t)e * wn + k];
+        b4[j] = d->wnet_b[3][e];
+      }
+      upload(c->W4C, w4.data(), w4.size());
+      upload(c->b4C, b4.data(), b4.size());
+      c->wchunk = round_up(std::max(32, ceil_div(N, 148)), 32);
+      c->wsplit = ceil_div(N, c->wchunk);
+      c->wpart.alloc((size_t)c->wsplit * c->n_sims * wn);
+      c->wC.alloc((size_t)c->n_sims * std::max(1, c->n_cub));
+    }
+    // bundle buffers
+    choose_groups(n_q, w, c->G, c->gps);
+    c->Cb = c->G * c->gps;
+    c->ldq = round_up(n_q, 2);
+    const int ncols = c->n_sims * c->Cb;
+    c->X0.alloc((size_t)ncols * c->ldq);
+    c->H.resize(L - 1); c->cache.resize(L - 1); c->ldH.resize(L - 1); c->ldc.resize(L - 1);
+    for (int l = 0; l < L - 1; ++l) {
+      c->ldH[l] = (l == L - 2) ? c->ldlast : round_up(c->widths[l + 1], 2);
+      c->ldc[l] = round_up(c->widths[l + 1], 2);
+      c->H[l].alloc((size_t)ncols * c->ldH[l]);
+      c->cache[l].alloc((size_t)c->n_sims * 2 * n_q * c->ldc[l]);
+    }
+    c->ldjt = c->n;
+    c->lddj = n_q;
+    c->u.alloc((size_t)c->n_sims * N);
+    c->value.alloc((size_t)c->n_sims * N);
+    c->hvv.alloc((size_t)c->n_sims * N);
+    c->Jt.alloc((size_t)c->n_sims * N * c->ldjt);
+    c->dJ.alloc((size_t)c->n_sims * N * c->lddj);
+    {  // constant U block of J~
+      std::vector<double> jt((size_t)N * c->ldjt, 0.0);
+      for (int r = 0; r < N; ++r)
+        for (int j = 0; j < n_p; ++j) jt[(size_t)r * c->ldjt + j] = d->U[(size_t)r * n_p + j];
+      for (int s = 0; s < c->n_sims; ++s)
+        NL_CUDA(cudaMemcpy(c->Jt.p + (size_t)s * N * c->ldjt, jt.data(), jt.size() * 8, cudaMemcpyHostToDevice));
+    }
+    // assembly / solve
+    c->nchA = ceil_div(N, c->rpc);
+    const int n = c->n, S = c->n_sims;
+    c->a.alloc((size_t)S * N);
+    c->partA.alloc((size_t)S * c->nchA * n * (n + 1));
+    c->phi.alloc((size_t)S * n);
+    c->norm.alloc(S);
+    c->S.alloc((size_t)S * n * n);
+    c->dr.alloc((size_t)S * n);
+    c->r.alloc((size_t)S * n);
+    c->rbar.alloc((size_t)S * n);
+    c->rdbar.alloc((size_t)S * n);
+    c->rsave.alloc((size_t)S * n);
+    c->rdot.alloc((size_t)S * n);
+    c->fext.alloc((size_t)S * N);
+    c->tmpN.alloc((size_t)S * N);
+    c->status.alloc(S);
+    // backward
+    c->bchunk = round_up(std::max(32, ceil_div(N, 148)), 32);
+    c->bsplit = ceil_div(N, c->bchunk);
+    c->bpart.alloc((size_t)c->bsplit * S * (w + n_p));
+    int maxw = 0;
+    for (int l = 1; l < L; ++l) maxw = std::max(maxw, round_up(c->widths[l], 2));
+    c->Delta0.alloc((size_t)S * 2 * n_q * maxw);
+    c->Delta1.alloc((size_t)S * 2 * n_q * maxw);
+    c->ldGt = round_up(n_q, 2);
+    c->Gt.alloc((size_t)S * 2 * n_q * c->ldGt);
+    // kernel attributes for large dynamic shared memory
+    NL_CUDA(cudaFuncSetAttribute(k_cubature, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaDeviceSynchronize());
+    *out = c;
+    return NLROM_OK;
+  } catch (const Error& e) {
+    int code = e.code;
+    if (c) nlrom_destroy(c);
+    return code;
+  }
+}
+
+extern "C" void nlrom_destroy(nlrom_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  if (c->gE) cudaGraphExecDestroy(c->gE);
+  if (c->gJ) cudaGraphExecDestroy(c->gJ);
+  if (c->gIter) cudaGraphExecDestroy(c->gIter);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+extern "C" const char* nlrom_last_error(const nlrom_ctx* c) { return c ? c->err.c_str() : "null handle"; }
+
+#define CTX_TRY(c)          \
+  if (!(c)) return NLROM_ERR_ARG; \
+  try {                     \
+    NL_CUDA(cudaSetDevice((c)->device));
+#define CTX_END(c)              \
+  return NLROM_OK;              \
+  }                             \
+  catch (const Error& e) {      \
+    return fail((c), e);        \
+  }
+
+// ---------------------------------------------------------------- diffops (reference passes)
+extern "C" int nlrom_diffop(nlrom_ctx* c, int op, const double* q, const double* vec, double eps, int mode, double* out) {
+  CTX_TRY(c)
+  if (c->n_sims != 1) throw Error(NLROM_ERR_ARG, "diffop requires a single-sim context");
+  if (op < 0 || op > NLROM_OP_VHP) throw Error(NLROM_ERR_ARG, "unknown op");
+  if (mode == 1 && !(eps > 0)) throw Error(NLROM_ERR_ARG, "eps must be > 0 (SPEC.md:206)");
+  const int nq = c->n_q, N = c->N, L = c->L;
+  int order = 0, npass = 1;
+  switch (op) {
+    case NLROM_OP_VALUE: case NLROM_OP_VJP: order = 0; npass = 1; break;
+    case NLROM_OP_JVP: order = 1; npass = 1; break;
+    case NLROM_OP_JACOBIAN: case NLROM_OP_VHP: order = 1; npass = nq; break;
+    case NLROM_OP_HVV: order = 2; npass = 1; break;
+    case NLROM_OP_HV: order = 2; npass = nq; break;
+    case NLROM_OP_SVV: order = 3; npass = nq; break;
+  }
+  const int S = 1 << order, ncols = npass * S;
+  const double scale = mode == 1 ? eps : 1.0;
+  const int act = mode == 1 ? ACT_SIN_MC : ACT_SIN_MD;
+  const bool bwd = (op == NLROM_OP_VJP || op == NLROM_OP_VHP);
+  DBuf dq(nq), dv(std::max(nq, N));
+  h2d(c, dq, q, nq);
+  if (vec) h2d(c, dv, vec, (op == NLROM_OP_VJP || op == NLROM_OP_VHP) ? N : nq);
+  DBuf X0((size_t)ncols * c->ldq);
+  launch(c, k_seed_ref, grid1((long long)ncols * nq), 256, 0, (const double*)dq.p,
+         (const double*)(vec && !bwd ? dv.p : nullptr), X0.p, c->ldq, nq, op, S, npass, scale);
+  std::vector<DBuf> Hs(L - 1), caches(L - 1);
+  std::vector<int> ldcs(L - 1);
+  const double* in = X0.p;
+  int ldin = c->ldq;
+  for (int l = 0; l < L - 1; ++l) {
+    int ldo = (l == L - 2) ? c->ldlast : round_up(c->widths[l + 1], 2);
+    ldcs[l] = ldo;
+    Hs[l].alloc((size_t)ncols * ldo);
+    if (bwd) caches[l].alloc((size_t)ncols * ldo);
+    GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
+    fc_forward(order, act, g, Hs[l].p, ldo, c->b[l].p, bwd ? caches[l].p : nullptr, c->st);
+    in = Hs[l].p;
+    ldin = ldo;
+  }
+  if (!bwd) {
+    GemmArgs gT{c->AT.p, in, round_up(c->wL1, 2), ldin, c->n_p, ncols, c->wL1, 0, 0};
+    fc_forward(0, ACT_NONE, gT, Hs[L - 2].p + c->wL1, c->ldlast, nullptr, nullptr, c->st);
+    const int ldy = round_up(N, 2);
+    DBuf Y((size_t)ncols * ldy);
+    GemmArgs g{c->Alast.p, in, c->ldlast, ldin, N, ncols, c->wL1 + c->n_p, 0, 0};
+    // linear output layer: bias P b on the real slot of every pass (period S)
+    launch_gemm<GemmCfg<64, 64, 2, 2, 1>>(g, EpiStore{Y.p, ldy, 0, c->Pb.p, S, nullptr}, c->st);
+    int slot = (op == NLROM_OP_VALUE) ? 0 : (op == NLROM_OP_JVP || op == NLROM_OP_JACOBIAN) ? 1
+             : (op == NLROM_OP_SVV) ? 7 : 3;
+    double div = std::pow(scale, __builtin_popcount(slot));
+    DBuf o((size_t)N * npass);
+    launch(c, k_extract_slot, grid1((long long)N * npass), 256, 0, (const double*)Y.p, ldy, N, S, npass, slot, div, o.p);
+    d2h(c, out, o, (size_t)N * npass);
+  } else {
+    // caches hold layer pre-activations with ld of their output buffers; the backward
+    // writes Delta with the same ld per layer.
+    int maxld = 0;
+    for (int l = 0; l < L - 1; ++l) maxld = std::max(maxld, ldcs[l]);
+    DBuf D0((size_t)ncols * maxld), D1((size_t)ncols * maxld), Gout((size_t)ncols * c->ldq);
+    DBuf da(N);
+    h2d(c, da, vec, N);
+    decoder_backward(c, da.p, S, mode == 1, npass, caches, ldcs, D0, D1, Gout, c->ldq);
+    if (op == NLROM_OP_VJP) {
+      NL_CUDA(cudaMemcpyAsync(out, Gout.p, nq * 8, cudaMemcpyDeviceToHost, c->st));
+    } else {
+      // vhp[i][k] = Im(G_t[pass k])[i] / eps
+      DBuf o((size_t)nq * nq);
+      launch(c, k_extract_slot, grid1((long long)nq * nq), 256, 0, (const double*)Gout.p, c->ldq, nq, 2, nq, 1, scale,
+             o.p);
+      d2h(c, out, o, (size_t)nq * nq);
+    }
+  }
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+// ---------------------------------------------------------------- fused-path queries
+static void eval_point(nlrom_ctx* c, const nlrom_simcfg& cfg) {
+  ensure_graphs(c, cfg);
+  NL_CUDA(cudaGraphLaunch(c->gE, c->st));
+}
+
+static nlrom_simcfg default_cfg(double dt, int drop_fict, int integration) {
+  nlrom_simcfg s{};
+  s.dt = dt; s.newton_tol = 1e-8; s.max_iters = 20; s.drop_fict = drop_fict; s.integration = integration;
+  s.line_search = 1; s.fixed_iters = 0;
+  return s;
+}
+
+extern "C" int nlrom_residual(nlrom_ctx* c, const double* r, const double* rbar, const double* rdbar,
+                              const double* fext, const nlrom_simcfg* cfg, double* phi) {
+  CTX_TRY(c)
+  set_state(c, r, rbar, rdbar, fext);
+  eval_point(c, *cfg);
+  d2h(c, phi, c->phi, (size_t)c->n_sims * c->n);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_system_jacobian(nlrom_ctx* c, const double* r, const double* rbar, const double* rdbar,
+                                     const double* fext, const nlrom_simcfg* cfg, double* S) {
+  CTX_TRY(c)
+  set_state(c, r, rbar, rdbar, fext);
+  eval_point(c, *cfg);
+  NL_CUDA(cudaGraphLaunch(c->gJ, c->st));
+  d2h(c, S, c->S, (size_t)c->n_sims * c->n * c->n);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+static void bundle_only(nlrom_ctx* c, const double* q, const double* qbar, const double* qdbar, double dt, int drop_fict,
+                        const double* p) {
+  std::vector<double> r(c->n, 0.0), rb(c->n, 0.0), rd(c->n, 0.0);
+  for (int i = 0; i < c->n_q; ++i) {
+    r[c->n_p + i] = q[i];
+    rb[c->n_p + i] = qbar ? qbar[i] : q[i];
+    rd[c->n_p + i] = qdbar ? qdbar[i] : 0.0;
+  }
+  if (p)
+    for (int i = 0; i < c->n_p; ++i) r[i] = p[i];
+  h2d(c, c->r, r.data(), c->n);
+  h2d(c, c->rbar, rb.data(), c->n);
+  h2d(c, c->rdbar, rd.data(), c->n);
+  bundle_forward(c, dt, drop_fict);
+}
+
+extern "C" int nlrom_delta_j(nlrom_ctx* c, const double* q, const double* qbar, const double* qdbar, double dt,
+                             int drop_fict, double* dJ) {
+  CTX_TRY(c)
+  bundle_only(c, q, qbar, qdbar, dt, drop_fict, nullptr);
+  d2h(c, dJ, c->dJ, (size_t)c->N * c->n_q);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_fictitious_force(nlrom_ctx* c, const double* q, const double* qbar, double* f) {
+  CTX_TRY(c)
+  bundle_only(c, q, qbar, nullptr, 1.0, 0, nullptr);
+  launch(c, k_mul, grid1(c->N), 256, 0, (const double*)c->mass.p, (const double*)c->hvv.p, c->tmpN.p, c->N);
+  d2h(c, f, c->tmpN, c->N);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_full_displacement(nlrom_ctx* c, const double* r, double* u) {
+  CTX_TRY(c)
+  bundle_only(c, r + c->n_p, nullptr, nullptr, 1.0, 0, r);
+  d2h(c, u, c->u, c->N);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_jtilde(nlrom_ctx* c, const double* q, double* Jt) {
+  CTX_TRY(c)
+  bundle_only(c, q, nullptr, nullptr, 1.0, 0, nullptr);
+  d2h(c, Jt, c->Jt, (size_t)c->N * c->n);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_wnet_forward(nlrom_ctx* c, const double* r, double* w) {
+  CTX_TRY(c)
+  bundle_only(c, r + c->n_p, nullptr, nullptr, 1.0, 0, r);
+  wnet_phase(c);
+  d2h(c, w, c->wC, c->n_cub);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_cubature_integrate(nlrom_ctx* c, const double* r, int integration, double* f_red, double* K_red) {
+  CTX_TRY(c)
+  bundle_only(c, r + c->n_p, nullptr, nullptr, 1.0, 0, r);
+  CubSet& s = integration == 1 ? c->setAll : c->setC;
+  if (integration == 0) wnet_phase(c);
+  cubature_phase(c, s, integration == 0);
+  DBuf fr(c->n), Kr((size_t)c->n * c->n);
+  launch(c, k_reduce_cub, grid1((long long)c->n * c->n + c->n), 256, 0, (const double*)s.part_f.p,
+         (const double*)s.part_K.p, s.nchunk, c->n, fr.p, Kr.p);
+  d2h(c, f_red, fr, c->n);
+  d2h(c, K_red, Kr, (size_t)c->n * c->n);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+// ---------------------------------------------------------------- step
+static void run_step(nlrom_ctx* c, const nlrom_simcfg& cfg, nlrom_step_info* info) {
+  const int nn = c->n_sims * c->n;
+  ensure_graphs(c, cfg);
+  launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg.dt, nn);
+  if (cfg.fixed_iters > 0) {
+    for (int it = 0; it < cfg.fixed_iters; ++it) NL_CUDA(cudaGraphLaunch(c->gIter, c->st));
+    NL_CUDA(cudaGraphLaunch(c->gE, c->st));
+    check_status(c);
+    double nrm = 0;
+    NL_CUDA(cudaMemcpyAsync(&nrm, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
+    NL_CUDA(cudaStreamSynchronize(c->st));
+    if (info) { info->iters = cfg.fixed_iters; info->res_norm = nrm; info->status = 0; }
+    return;
+  }
+  if (c->n_sims != 1) throw Error(NLROM_ERR_ARG, "adaptive Newton requires a single-sim context");
+  NL_CUDA(cudaGraphLaunch(c->gE, c->st));
+  double nrm = 0;
+  NL_CUDA(cudaMemcpyAsync(&nrm, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  int it = 0;
+  while (nrm > cfg.newton_tol) {
+    if (it >= cfg.max_iters) {
+      c->last_norm = nrm;
+      char buf[160];
+      snprintf(buf, sizeof buf, "Newton did not converge in %d iterations; last residual norm %.3e", cfg.max_iters, nrm);
+      throw Error(NLROM_ERR_NEWTON, buf);
+    }
+    NL_CUDA(cudaGraphLaunch(c->gJ, c->st));
+    check_status(c);
+    NL_CUDA(cudaMemcpyAsync(c->rsave.p, c->r.p, nn * 8, cudaMemcpyDeviceToDevice, c->st));
+    double t = 1.0, ntry = 0;
+    for (int k = 0; k < 11; ++k) {
+      launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rsave.p, (const double*)c->dr.p, t, nn);
+      NL_CUDA(cudaGraphLaunch(c->gE, c->st));
+      NL_CUDA(cudaMemcpyAsync(&ntry, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
+      NL_CUDA(cudaStreamSynchronize(c->st));
+      if (!std::isfinite(ntry)) throw Error(NLROM_ERR_NONFINITE, "non-finite residual");
+      if (!cfg.line_search || ntry < nrm) break;
+      t *= 0.5;
+    }
+    nrm = ntry;
+    ++it;
+  }
+  c->last_norm = nrm;
+  if (info) { info->iters = it; info->res_norm = nrm; info->status = 0; }
+}
+
+extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar, const double* fext,
+                          const nlrom_simcfg* cfg, double* r_out, double* rdot_out, nlrom_step_info* info) {
+  CTX_TRY(c)
+  set_state(c, nullptr, rbar, rdbar, fext);
+  run_step(c, *cfg, info);
+  const int nn = c->n_sims * c->n;
+  launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg->dt, nn);
+  d2h(c, r_out, c->r, nn);
+  d2h(c, rdot_out, c->rdot, nn);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_step_device(nlrom_ctx* c, const double* rbar, const double* rdbar, const double* fext,
+                                 const nlrom_simcfg* cfg, double* r_out, double* rdot_out, void* stream) {
+  CTX_TRY(c)
+  if (cfg->fixed_iters <= 0) throw Error(NLROM_ERR_ARG, "nlrom_step_device needs fixed_iters > 0");
+  cudaStream_t us = (cudaStream_t)stream;
+  const int nn = c->n_sims * c->n;
+  // order the context stream after the caller's stream, copy inputs in
+  NL_CUDA(cudaEventRecord(c->ev0, us));
+  NL_CUDA(cudaStreamWaitEvent(c->st, c->ev0, 0));
+  NL_CUDA(cudaMemcpyAsync(c->rbar.p, rbar, nn * 8, cudaMemcpyDeviceToDevice, c->st));
+  NL_CUDA(cudaMemcpyAsync(c->rdbar.p, rdbar, nn * 8, cudaMemcpyDeviceToDevice, c->st));
+  NL_CUDA(cudaMemcpyAsync(c->fext.p, fext, (size_t)c->n_sims * c->N * 8, cudaMemcpyDeviceToDevice, c->st));
+  ensure_graphs(c, *cfg);
+  launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg->dt, nn);
+  for (int it = 0; it < cfg->fixed_iters; ++it) NL_CUDA(cudaGraphLaunch(c->gIter, c->st));
+  launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg->dt, nn);
+  NL_CUDA(cudaMemcpyAsync(r_out, c->r.p, nn * 8, cudaMemcpyDeviceToDevice, c->st));
+  NL_CUDA(cudaMemcpyAsync(rdot_out, c->rdot.p, nn * 8, cudaMemcpyDeviceToDevice, c->st));
+  NL_CUDA(cudaEventRecord(c->ev1, c->st));
+  NL_CUDA(cudaStreamWaitEvent(us, c->ev1, 0));
+  CTX_END(c)
+}
+
+__global__ void k_flush(double* p, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+extern "C" int nlrom_bench_iterations(nlrom_ctx* c, int n_iters, int flush_l2, float* ms_total, float* ms_dom) {
+  CTX_TRY(c)
+  if (c->graph_key.empty()) throw Error(NLROM_ERR_ARG, "run nlrom_step first (captures the graphs)");
+  if (flush_l2 && !c->flush.p) c->flush.alloc((size_t)32 << 20);  // 256 MB > 126 MB L2
+  float tot = 0.f;
+  for (int i = 0; i < n_iters; ++i) {
+    if (flush_l2) {
+      k_flush<<<1184, 256, 0, c->st>>>(c->flush.p, c->flush.n, (double)i);
+      NL_CHECK_LAUNCH();
+    }
+    NL_CUDA(cudaEventRecord(c->ev0, c->st));
+    NL_CUDA(cudaGraphLaunch(c->gIter, c->st));
+    NL_CUDA(cudaEventRecord(c->ev1, c->st));
+    NL_CUDA(cudaEventSynchronize(c->ev1));
+    float ms = 0.f;
+    NL_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    tot += ms;
+  }
+  *ms_total = tot;
+  // dominant kernel (output decoder layer + fused filter) timed alone on the same stream
+  if (ms_dom) {
+    const int ncols = c->n_sims * c->Cb;
+    const double* in = c->H[c->L - 2].p;
+    GemmArgs g{c->Alast.p, in, c->ldlast, c->ldH[c->L - 2], c->N, ncols, c->wL1 + c->n_p, 0, 0};
+    EpiJetOut e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
+                c->n_p, c->n_q, c->G, c->gps};
+    float dom = 0.f;
+    for (int i = 0; i < n_iters; ++i) {
+      if (flush_l2) {
+        k_flush<<<1184, 256, 0, c->st>>>(c->flush.p, c->flush.n, (double)i);
+        NL_CHECK_LAUNCH();
+      }
+      NL_CUDA(cudaEventRecord(c->ev0, c->st));
+      out_gemm(c->G, g, e, c->st);
+      NL_CUDA(cudaEventRecord(c->ev1, c->st));
+      NL_CUDA(cudaEventSynchronize(c->ev1));
+      float ms = 0.f;
+      NL_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+      dom += ms;
+    }
+    *ms_dom = dom / std::max(1, n_iters);
+  }
+  CTX_END(c)
+}
+
+extern "C" int nlrom_launches_per_iteration(nlrom_ctx* c) { return c ? c->launches_E + c->launches_J : 0; }
+
+extern "C" int nlrom_element_forces(nlrom_ctx* c, const double* u, int want_K, double* f_int, double* K_elems) {
+  CTX_TRY(c)
+  CubSet& s = c->setAll;
+  h2d(c, c->u, u, c->N);
+  DBuf Ke(want_K ? (size_t)c->T * 144 : 0);
+  CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, nullptr, c->u.p, nullptr,
+            c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk,
+            want_K ? Ke.p : nullptr, nullptr};
+  size_t smem = (size_t)(2 * s.epc * 12 * c->n + s.epc * 156) * 8;
+  launch(c, k_cubature, dim3(s.nchunk, 1), 256, smem, a);
+  launch(c, k_scatter_rows, grid1((long long)s.n_rows), 256, 0, (const int*)s.row_ids.p, (const int*)s.row_ptr.p,
+         (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N, 1);
+  d2h(c, f_int, s.f, c->N);
+  if (want_K) d2h(c, K_elems, Ke, (size_t)c->T * 144);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_element_reduced_forces(nlrom_ctx* c, const double* r, const int* elems, int n_elems, double* out) {
+  CTX_TRY(c)
+  if (n_elems <= 0) return NLROM_OK;
+  for (int i = 0; i < n_elems; ++i)
+    if (elems[i] < 0 || elems[i] >= c->T) throw Error(NLROM_ERR_ARG, "element id out of range");
+  bundle_only(c, r + c->n_p, nullptr, nullptr, 1.0, 0, r);
+  IBuf de;
+  de.upload(elems, n_elems);
+  const int epc = c->setAll.epc;
+  const int nch = ceil_div(n_elems, epc);
+  DBuf few((size_t)n_elems * 12), pf((size_t)nch * c->n), pK((size_t)nch * c->n * c->n), fo((size_t)n_elems * c->n);
+  CubArgs a{de.p, n_elems, c->elem_rows.p, c->Dm_inv.p, c->vol.p, nullptr, c->u.p, c->Jt.p,
+            c->N, c->n, c->ldjt, c->mu, c->lam, epc, few.p, pf.p, pK.p, nch, nullptr, fo.p};
+  size_t smem = (size_t)(2 * epc * 12 * c->n + epc * 156) * 8;
+  launch(c, k_cubature, dim3(nch, 1), 256, smem, a);
+  d2h(c, out, fo, (size_t)n_elems * c->n);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}

@@ -1,0 +1,196 @@
+// GEMM epilogues of the CSFD decoder passes (activation fused into the producing GEMM).
+#pragma once
+#include "gemm_f64.cuh"
+#include "mc_device.cuh"
+
+namespace nlrom {
+
+enum ActKind { ACT_NONE = 0, ACT_SIN_MC = 1, ACT_SIN_MD = 2, ACT_SQUARE_MC = 3 };
+
+// Activation over passes of N = 2^order adjacent slot columns.
+//  ACT_SIN_MC    : true multicomplex sin (mcx.py:63-100)
+//  ACT_SIN_MD    : multi-dual sin on eps-scaled slots (SPEC.md:186 truncation)
+//  ACT_SQUARE_MC : multicomplex z*z (square activation)
+// Bias (FC layer) is added to the real slot only (mcx.py:333-338).
+// cache (optional): pre-activation z (same layout as Y) for the backward pass.
+template <int N, int ACT>
+struct EpiAct {
+  double* Y;
+  int ldy;
+  long long strideY;
+  const double* bias;
+  double* cache;
+  __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
+    double* Yz = Y + (size_t)t.z * strideY;
+    double* Cz = cache ? cache + (size_t)t.z * strideY : nullptr;
+    const int npass = t.bn / N;
+    for (int i = tid; i < t.bm * npass; i += nt) {
+      const int p = i / t.bm, ml = i % t.bm;
+      const int m = t.m0 + ml;
+      const int cbase = t.c0 + p * N;
+      if (m >= g.M || cbase >= g.C) continue;
+      double z[N], o[N];
+#pragma unroll
+      for (int s = 0; s < N; ++s) z[s] = t.Cs[(p * N + s) * t.ldc + ml];
+      if (bias) z[0] += bias[m];
+      if (Cz) {
+#pragma unroll
+        for (int s = 0; s < N; ++s) Cz[(size_t)(cbase + s) * ldy + m] = z[s];
+      }
+      if constexpr (ACT == ACT_SIN_MC) {
+        double c[N];
+        mc_sincos<N>(z, o, c);
+      } else if constexpr (ACT == ACT_SIN_MD) {
+        md_sincos<N>(z, o, nullptr);
+      } else if constexpr (ACT == ACT_SQUARE_MC) {
+        mc_mul<N>(z, z, o);
+      } else {
+#pragma unroll
+        for (int s = 0; s < N; ++s) o[s] = z[s];
+      }
+#pragma unroll
+      for (int s = 0; s < N; ++s) Yz[(size_t)(cbase + s) * ldy + m] = o[s];
+    }
+  }
+};
+
+// Backward through an activation of the layer below: d_out = d_in (*) act'(z) in
+// the arithmetic of the pass (N = 1 real, N = 2 complex / dual), z from the cache.
+//   sin    : act'(z) = cos z      (MC: multicomplex cos, MD: multi-dual cos)
+//   square : act'(z) = 2 z
+template <int N, int ACT>
+struct EpiBwdAct {
+  double* Y;
+  int ldy;
+  long long strideY;
+  const double* zcache;  // same layout as Y
+  __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
+    double* Yz = Y + (size_t)t.z * strideY;
+    const double* Zz = zcache + (size_t)t.z * strideY;
+    const int npass = t.bn / N;
+    for (int i = tid; i < t.bm * npass; i += nt) {
+      const int p = i / t.bm, ml = i % t.bm;
+      const int m = t.m0 + ml;
+      const int cbase = t.c0 + p * N;
+      if (m >= g.M || cbase >= g.C) continue;
+      double d[N], z[N], f[N], o[N];
+#pragma unroll
+      for (int s = 0; s < N; ++s) {
+        d[s] = t.Cs[(p * N + s) * t.ldc + ml];
+        z[s] = Zz[(size_t)(cbase + s) * ldy + m];
+      }
+      if constexpr (ACT == ACT_SIN_MC) {
+        double sn[N];
+        mc_sincos<N>(z, sn, f);
+      } else if constexpr (ACT == ACT_SIN_MD) {
+        md_sincos<N>(z, nullptr, f);
+      } else if constexpr (ACT == ACT_SQUARE_MC) {
+#pragma unroll
+        for (int s = 0; s < N; ++s) f[s] = 2.0 * z[s];
+      } else {
+#pragma unroll
+        for (int s = 0; s < N; ++s) f[s] = (s == 0) ? 1.0 : 0.0;
+      }
+      if constexpr (ACT == ACT_SIN_MD) md_mul<N>(d, f, o); else mc_mul<N>(d, f, o);
+#pragma unroll
+      for (int s = 0; s < N; ++s) Yz[(size_t)(cbase + s) * ldy + m] = o[s];
+    }
+  }
+};
+
+// Hidden layer of the fused Newton bundle: tiles of G = BN columns laid out as
+// [base jet (1, s, s^2, r) | nk tangents x (t, ts, ts^2, tr)], see mc_device.cuh.
+// Writes the activated jet, and (optional) the dual cache for the vhp backward in
+// the reference vhp layout (col 2k = real pre-activation z0, col 2k+1 = tangent
+// t-slot pre-activation of direction k, i.e. the order-1 pass q + eps e_k i1).
+struct EpiJet {
+  double* Y;
+  int ldy;
+  long long strideY;
+  const double* bias;
+  double* cache;      // (n_sims * 2 n_q) x ldcache, may be null
+  int ldcache;
+  int group;          // columns per group (== BN)
+  int gps;            // groups per simulation
+  int n_q;            // tangent directions per simulation
+  __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
+    double* Yz = Y + (size_t)t.z * strideY;
+    const int gg = t.c0 / group;              // global group index (tile == group)
+    const int sim = gg / gps, gl = gg % gps;
+    const int nk = (group - 4) / 4;           // tangents per group
+    double* Cz = cache ? cache + (size_t)sim * 2 * n_q * ldcache : nullptr;
+    for (int ml = tid; ml < t.bm; ml += nt) {
+      const int m = t.m0 + ml;
+      if (m >= g.M) continue;
+      double z[4], o[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) z[s] = t.Cs[s * t.ldc + ml];
+      z[0] += bias[m];
+      JetCos jc;
+      jet_sin_base(z, o, jc);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) Yz[(size_t)(t.c0 + s) * ldy + m] = o[s];
+      for (int k = 0; k < nk; ++k) {
+        const int kg = gl * nk + k;           // tangent index within the simulation
+        double y[4], yo[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) y[s] = t.Cs[(4 + 4 * k + s) * t.ldc + ml];
+        jet_tangent(jc, y, yo);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) Yz[(size_t)(t.c0 + 4 + 4 * k + s) * ldy + m] = yo[s];
+        if (Cz && kg < n_q) {
+          Cz[(size_t)(2 * kg) * ldcache + m] = z[0];
+          Cz[(size_t)(2 * kg + 1) * ldcache + m] = y[0];
+        }
+      }
+    }
+  }
+};
+
+// Output layer of the fused bundle (linear + fused filter): from the jet columns
+//   value = D_1, J e_k = D_t, hvv = H(v,v) = 2 D_ss, dJ_k = S(e_k,v,v) + H(e_k,w) = 2 D_tss + D_tr
+// and u = U p + D(q). J is written into J~ = [U, J] (row-major, ldjt), dJ row-major (lddj).
+struct EpiJetOut {
+  const double* bias;    // P b (filtered last bias), real slot only
+  const double* U;       // (N, n_p) row-major
+  const double* r;       // (n_sims, n): p = r[:n_p]
+  double* u;             // (n_sims, N)
+  double* value;         // (n_sims, N) D(q)
+  double* hvv;           // (n_sims, N)
+  double* Jt;            // (n_sims, N, ldjt)
+  double* dJ;            // (n_sims, N, lddj)
+  int ldjt, lddj, n_p, n_q, group, gps;
+  __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
+    const int gg = t.c0 / group;
+    const int sim = gg / gps, gl = gg % gps;
+    const int nk = (group - 4) / 4;
+    const int N = g.M;
+    const size_t sv = (size_t)sim * N;
+    for (int ml = tid; ml < t.bm; ml += nt) {
+      const int m = t.m0 + ml;
+      if (m >= N) continue;
+      if (gl == 0) {
+        const double d1 = t.Cs[0 * t.ldc + ml] + bias[m];
+        const double dss = t.Cs[2 * t.ldc + ml];
+        double up = 0.0;
+        const double* Ur = U + (size_t)m * n_p;
+        const double* pz = r + (size_t)sim * (n_p + n_q);
+        for (int i = 0; i < n_p; ++i) up = fma(Ur[i], pz[i], up);
+        u[sv + m] = up + d1;
+        value[sv + m] = d1;
+        hvv[sv + m] = 2.0 * dss;
+      }
+      double* Jrow = Jt + (sv + m) * ldjt + n_p;
+      double* drow = dJ + (sv + m) * lddj;
+      for (int k = 0; k < nk; ++k) {
+        const int kg = gl * nk + k;
+        if (kg >= n_q) break;
+        const double* col = t.Cs + (4 + 4 * k) * t.ldc + ml;
+        Jrow[kg] = col[0];
+        drow[kg] = 2.0 * col[2 * t.ldc] + col[3 * t.ldc];
+      }
+    }
+  }
+};
+
+}  // namespace nlrom

@@ -1,0 +1,218 @@
+"""GPU parity: every hot-path op through the C ABI against the CPU oracle on the same
+seeded inputs. fp64 path: norm-relative <= 1e-12 unless stated."""
+
+import numpy as np
+import pytest
+
+from conftest import rel
+from helpers import oracle_sim, ocfg
+from oracle import diffops as od, nets as on, reduced as orr, rdsim as ors, elastic as oe
+from oracle import mcx_np as omc
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def cfg1(cuda_ok):
+    from paper_2102_11026_b200.problem import build_problem
+    P = build_problem("cfg1")
+    return P, oracle_sim(P)
+
+
+@pytest.fixture(scope="module")
+def tiny(cuda_ok):
+    from paper_2102_11026_b200.problem import build_problem
+    P = build_problem("tiny")
+    return P, oracle_sim(P)
+
+
+# ------------------------------------------------------------------ generic nets (densenet)
+@pytest.mark.parametrize("order", [0, 1, 2, 3])
+def test_net_forward_multicomplex(cfg1, order):
+    from paper_2102_11026_b200 import densenet
+    from paper_2102_11026_b200.mcx import MCArray
+    P, S = cfg1
+    rng = np.random.default_rng(order)
+    q = rng.uniform(-0.5, 0.5, (1 << order, P.cfg.n_q, 7))
+    q[1:] *= 1e-3
+    got = densenet.forward(P.rm.decoder, MCArray(q)).parts
+    want = on.forward(S.rm.D, q)
+    for s in range(1 << order):
+        assert rel(got[s], want[s]) < 1e-11, s
+
+
+def test_net_square_and_wnet(cfg1):
+    from paper_2102_11026_b200 import densenet
+    P, S = cfg1
+    u = np.random.default_rng(2).standard_normal(P.model.N) * 1e-3
+    got = densenet.forward(P.cm.wnet, u)
+    want = on.forward(S.wnet, u[None, :, None])[0, :, 0]
+    assert rel(got, want) < TOL and np.all(got >= 0)
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_net_backward(cfg1, order):
+    from paper_2102_11026_b200 import densenet
+    from paper_2102_11026_b200.mcx import MCArray
+    P, S = cfg1
+    rng = np.random.default_rng(10 + order)
+    B = 3
+    x = rng.uniform(-0.5, 0.5, (1 << order, P.cfg.n_q, B))
+    if order:
+        x[1] *= 1e-10
+    up = np.zeros((1 << order, P.model.N, B))
+    up[0] = rng.standard_normal((P.model.N, B))
+    got, grads = densenet.backward(P.rm.decoder, MCArray(x), MCArray(up), want_params=True)
+    want, wg = on.backward(S.rm.D, x, up, want_params=True)
+    for s in range(1 << order):
+        assert rel(got.parts[s], want[s]) < 1e-11
+    for (gW, gb), (wW, wb) in zip(grads, wg):
+        gW = gW if order else gW[None]
+        assert rel(gW, wW) < 1e-11
+
+
+# ------------------------------------------------------------------ diffops
+OPS = ["value", "jvp", "jacobian", "hvv", "hv", "svv", "vjp", "vhp"]
+
+
+@pytest.mark.parametrize("mode", ["scaled", "multicomplex"])
+@pytest.mark.parametrize("op", OPS)
+def test_diffops_reduced_ctx(cfg1, op, mode):
+    from paper_2102_11026_b200 import diffops
+    P, S = cfg1
+    q, qb, qdb, *_ = __import__("paper_2102_11026_b200.synth", fromlist=["x"]).random_state(P.cfg.n_p, P.cfg.n_q)
+    v = q - qb
+    a = np.random.default_rng(1).standard_normal(P.model.N)
+    cfg = diffops.DiffConfig(mode=mode)
+    args = {"value": (), "jacobian": (), "jvp": (v,), "hvv": (v,), "hv": (v,), "svv": (v,), "vjp": (a,), "vhp": (a,)}[op]
+    got = getattr(diffops, op)(P.rm, q, *args, cfg=cfg)
+    want = getattr(od, op)(S.rm.D, q, *args)
+    tol = 1e-12 if mode == "scaled" else 1e-9
+    assert rel(got, want) < tol
+
+
+@pytest.mark.parametrize("op", ["jacobian", "hvv", "hv", "svv", "vjp", "vhp"])
+def test_diffops_generic_densenet(cfg1, op):
+    from paper_2102_11026_b200 import diffops
+    P, S = cfg1
+    rng = np.random.default_rng(4)
+    q = rng.uniform(-0.5, 0.5, P.cfg.n_q)
+    v = rng.uniform(-0.05, 0.05, P.cfg.n_q)
+    a = rng.standard_normal(P.model.N)
+    args = {"jacobian": (), "hvv": (v,), "hv": (v,), "svv": (v,), "vjp": (a,), "vhp": (a,)}[op]
+    got = getattr(diffops, op)(P.rm.decoder, q, *args)
+    want = getattr(od, op)(S.rm.D, q, *args)
+    assert rel(got, want) < 1e-9
+
+
+# ------------------------------------------------------------------ fused bundle pieces
+def test_bundle_pieces(cfg1):
+    from paper_2102_11026_b200 import rdsim, daereduce
+    P, S = cfg1
+    r, rb, rdb = P.random_state()
+    q, qb, qdb = r[P.cfg.n_p:], rb[P.cfg.n_p:], rdb[P.cfg.n_p:]
+    assert rel(daereduce.full_displacement(P.rm, r), orr.full_displacement(S.rm, r)) < TOL
+    assert rel(daereduce.jtilde(P.rm, q), orr.jtilde(S.rm, q)) < TOL
+    assert rel(rdsim.fictitious_force(P.rm, q, qb), ors.fictitious_force(S, q, qb)) < 1e-11
+    for drop in (False, True):
+        got = rdsim.delta_j(P.rm, q, qb, qdb, P.cfg.dt, drop_fict=drop)
+        want = ors.delta_j(S, q, qb, qdb, P.cfg.dt, drop)
+        assert rel(got, want) < 1e-11
+
+
+def test_cubature_and_wnet(cfg1):
+    from paper_2102_11026_b200 import neucubature, session
+    P, S = cfg1
+    r, _, _ = P.random_state()
+    w_all = neucubature.wnet_forward(P.cm.wnet, P.rm, r)
+    w_or = orr.wnet_forward(S.wnet, S.rm, r)
+    assert rel(w_all, w_or) < TOL
+    s = session.session_for(P.rm, P.model, P.cm)
+    assert rel(s.wnet_forward_cub(r), w_or[P.cm.C]) < TOL
+    u = orr.full_displacement(S.rm, r)
+    Jt = orr.jtilde(S.rm, r[P.cfg.n_p:])
+    for integ in ("cubature", "exact_sum"):
+        f, K = neucubature.cubature_integrate(P.cm, P.rm, P.model, r, integ)
+        if integ == "cubature":
+            fo, Ko, _ = orr.cubature_integrate(S.model, S.rm, S.cub_elems, w_or[P.cm.C], u, Jt)
+        else:
+            fo, Ko, _ = orr.cubature_integrate(S.model, S.rm, np.arange(S.model.n_tets), np.ones(S.model.n_tets), u, Jt)
+        assert rel(f, fo) < TOL and rel(K, Ko) < TOL
+
+
+def test_elastic_gpu(cfg1):
+    from paper_2102_11026_b200 import elastic
+    P, S = cfg1
+    u = 1e-3 * np.random.default_rng(6).standard_normal(P.model.N)
+    assert rel(elastic.internal_force(P.model, u), oe.internal_force(S.model, u)) < TOL
+    Kg = elastic.stiffness(P.model, u).toarray()
+    assert rel(Kg, oe.stiffness_dense(S.model, u)) < TOL
+    r, _, _ = P.random_state()
+    e = [0, 7, 500]
+    got = elastic.element_reduced_force(P.model, P.rm, r, e)
+    for i, ei in enumerate(e):
+        assert rel(got[i], orr.element_reduced_force(S.model, S.rm, r, ei)) < TOL
+
+
+@pytest.mark.parametrize("integ", ["cubature", "exact_sum"])
+@pytest.mark.parametrize("drop", [False, True])
+def test_residual_and_system_jacobian(cfg1, integ, drop):
+    from paper_2102_11026_b200 import rdsim
+    from paper_2102_11026_b200.daereduce import ReducedState
+    P, S = cfg1
+    r, rb, rdb = P.random_state()
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, integration=integ, drop_fict=drop)
+    st = ReducedState(rb, rdb, cfg.dt)
+    phi = rdsim.residual(P.rm, P.model, st, P.f_ext, cfg, r=r)
+    Sg = rdsim.system_jacobian(P.rm, P.model, st, P.f_ext, cfg, r=r)
+    oc = ocfg(cfg)
+    assert rel(phi, ors.residual(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+    assert rel(Sg, ors.system_jacobian(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+
+
+def test_cfg2_bundle_and_jacobian(cuda_ok):
+    """Metric config (10-layer, width 256, n_q = 30): one Newton iteration's pieces."""
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200 import rdsim
+    from paper_2102_11026_b200.daereduce import ReducedState
+    P = build_problem("cfg2")
+    S = oracle_sim(P)
+    r, rb, rdb = P.random_state()
+    cfg = rdsim.SimConfig(dt=P.cfg.dt)
+    st = ReducedState(rb, rdb, cfg.dt)
+    oc = ocfg(cfg)
+    assert rel(rdsim.residual(P.rm, P.model, st, P.f_ext, cfg, r=r), ors.residual(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+    assert rel(rdsim.system_jacobian(P.rm, P.model, st, P.f_ext, cfg, r=r),
+               ors.system_jacobian(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+
+
+# ------------------------------------------------------------------ step and trajectories
+def test_step_adaptive(cfg1):
+    from paper_2102_11026_b200 import rdsim
+    P, S = cfg1
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, newton_tol=1e-10)
+    st = P.rest_state()
+    ro, rdo = st.r.copy(), st.rdot.copy()
+    for _ in range(5):
+        st, (it, nrm) = rdsim.step(P.rm, P.model, st, P.f_ext, cfg, return_info=True)
+        ro, rdo, ito, nro = ors.step(S, ro, rdo, P.f_ext, ocfg(cfg))
+        assert it == ito and nrm <= cfg.newton_tol
+        assert np.abs(st.r - ro).max() <= 1e-10 * max(np.abs(ro).max(), 1e-12) + 1e-14
+
+
+@pytest.mark.parametrize("integ", ["cubature", "exact_sum"])
+def test_trajectory_100_steps(cfg1, integ):
+    """100-step trajectories, fixed-iteration mode (bitwise-comparable control flow)."""
+    from paper_2102_11026_b200 import rdsim
+    P, S = cfg1
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, integration=integ, fixed_iters=2)
+    st = P.rest_state()
+    ro, rdo = st.r.copy(), st.rdot.copy()
+    worst = 0.0
+    for _ in range(100):
+        st = rdsim.step(P.rm, P.model, st, P.f_ext, cfg)
+        ro, rdo, _, _ = ors.step(S, ro, rdo, P.f_ext, ocfg(cfg))
+        worst = max(worst, np.abs(st.r - ro).max() / max(np.abs(ro).max(), 1e-30))
+    assert worst <= 1e-9, worst

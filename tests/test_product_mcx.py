@@ -1,0 +1,91 @@
+"""nlrom.mcx (product value type) against the reference golden vectors and the reference
+API semantics (pkg/tests/test_mcx.py behaviours, re-derived)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import nlrom
+from nlrom import mcx
+from nlrom.mcx import MultiComplex, MCArray, promote, im_extract, mc_sin, mc_exp, mc_mul, cr_matrix
+
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "mcx_golden.npz"))
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_golden(k):
+    a, b, pos = GOLD[f"a{k}"], GOLD[f"b{k}"], GOLD[f"pos{k}"]
+    got = {"mul": mcx.parts_mul(a, b), "inv": mcx.parts_inv(pos), "sin": mcx.parts_sin(a), "cos": mcx.parts_cos(a),
+           "sinh": mcx.parts_sinh(a), "cosh": mcx.parts_cosh(a), "exp": mcx.parts_exp(a),
+           "epssin": mcx.parts_sin(GOLD[f"epsa{k}"])}
+    for name, g in got.items():
+        want = GOLD[f"{name}{k}"]
+        assert np.abs(g - want).max() <= 5e-16 * max(np.abs(want).max(), 1e-300), name
+    assert np.array_equal(mcx.parts_cr_matrix(a[:, 0, 0]), GOLD[f"cr{k}"])
+
+
+def test_api_semantics():
+    z = promote(2.0, 1)
+    assert z.real == 2.0 and z.im({1}) == 0.0
+    assert promote(0.0, 3).parts.shape == (8,)
+    with pytest.raises(mcx.OrderError):
+        promote(1.0, 4)
+    with pytest.raises(mcx.OrderError):
+        promote(1.0, -1)
+    h = 1e-10
+    w = MultiComplex([2.0, h]) * 3.0
+    assert w.real == 6.0 and w.im({1}) == 3 * h
+    assert np.allclose((MultiComplex([0, 1, 1, 0]) * MultiComplex([0, 1, 1, 0])).parts, [-2, 0, 0, 2])
+    c = MultiComplex([1.0, 2.0]) * promote(3.0, 3)
+    assert c.order == 3 and c.real == 3.0 and c.im({1}) == 6.0
+    with pytest.raises(AttributeError):
+        z.order = 2
+    with pytest.raises(ValueError):
+        z.parts[0] = 5.0
+    with pytest.raises(mcx.OrderError):
+        im_extract(promote(1.0, 1), {2})
+    assert im_extract(MultiComplex([2.0, 1e-5, 1e-5, 0.0]) * MultiComplex([2.0, 1e-5, 1e-5, 0.0]), {1, 2}) == \
+        pytest.approx(2e-10, rel=1e-12)
+    assert mc_sin(MultiComplex([0.0, h])).im({1}) == pytest.approx(np.sinh(h), rel=1e-15)
+    rng = np.random.default_rng(3)
+    for order in range(4):
+        zz = MultiComplex(rng.uniform(0.5, 1.5, 1 << order))
+        assert np.allclose((zz / zz).parts, np.eye(1, 1 << order, 0)[0], atol=1e-13)
+    for fn in (mc_sin, mcx.mc_cos, mcx.mc_sinh, mcx.mc_cosh, mc_exp):
+        for order in range(4):
+            assert np.all(fn(promote(0.3, order)).parts[1:] == 0.0)
+    assert np.array_equal(cr_matrix(MultiComplex([2.0, 5.0])), [[2.0, -5.0], [5.0, 2.0]])
+    with pytest.raises(TypeError):
+        MultiComplex([1.0, 2.0]) * (1 + 2j)
+
+
+def test_ring_and_cr_homomorphism():
+    rng = np.random.default_rng(10)
+    for order in (1, 2, 3):
+        for _ in range(50):
+            a, b = MultiComplex(rng.uniform(-1, 1, 1 << order)), MultiComplex(rng.uniform(-1, 1, 1 << order))
+            rhs = cr_matrix(mc_mul(a, b))
+            assert np.abs(cr_matrix(a) @ cr_matrix(b) - rhs).max() <= 1e-13 * max(np.abs(rhs).max(), 1)
+    rng = np.random.default_rng(9)
+    for _ in range(20):
+        a, b = MultiComplex(rng.uniform(-.5, .5, 8)), MultiComplex(rng.uniform(-.5, .5, 8))
+        assert np.allclose(mc_exp(a + b).parts, (mc_exp(a) * mc_exp(b)).parts, rtol=1e-13, atol=1e-15)
+
+
+def test_mcarray():
+    x = np.array([1.0, -2.0, 3.0])
+    arr = MCArray.promote(x, 2)
+    assert arr.order == 2 and np.array_equal(arr.value, x)
+    assert np.array_equal(arr.scalar(1).parts, promote(-2.0, 2).parts)
+    rng = np.random.default_rng(12)
+    parts = rng.uniform(-1, 1, (8, 5))
+    s = MCArray(parts).sin()
+    for i in range(5):
+        assert np.allclose(s.parts[:, i], mc_sin(MultiComplex(parts[:, i])).parts, rtol=1e-15, atol=0)
+    rng = np.random.default_rng(13)
+    a, b = rng.uniform(-1, 1, (4, 3, 2)), rng.uniform(-1, 1, (4, 3, 2))
+    out = MCArray(a) * MCArray(b)
+    for i in range(3):
+        for j in range(2):
+            assert np.allclose(out.parts[:, i, j], (MultiComplex(a[:, i, j]) * MultiComplex(b[:, i, j])).parts)
