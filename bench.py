@@ -1,0 +1,289 @@
+#!/usr/bin/env python
+"""Benchmark: ms per implicit Newton step (DAE J/H/3rd-order + cubature) at the 10-layer DAE.
+
+Workload (BASELINE.json configs[1]): 35x7x7-cube tet mesh
+(10,290 tets, N = 6,720 free DOFs), 10-layer width-256 sin DAE with n_q = 30 and
+n_p = 30, weight-net cubature with |C| = 500, random-init weights (no checkpoints
+ship with the reference), gravity load, dt = 1/60.
+
+One step = one Newton iteration of rdsim.step in fixed-iteration mode: decoder
+bundle (value, J, hvv, dJ = svv + hv), weight net, StVK cubature + projection,
+assembly of phi and the Eq. 11 system matrix including vhp = H~^T a by complex-step
+backprop, LU with partial pivoting, r += dr -- one CUDA-graph replay.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1: launched by torch.distributed.run; cfg2 is a single mesh that does not shard
+(SURVEY.md §8e "replicas only"), so every rank runs an independent replica.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per implicit Newton step (DAE J/H/3rd-order + cubature) at 10-layer DAE"
+WORKLOAD = "cfg2: 10-layer w256 sin DAE, n_q=30, n_p=30, 10290-tet mesh (N=6720), |C|=500 wnet cubature, fp64"
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    fp64 = None
+    try:
+        fp64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["dmma_tflops"]
+    except Exception:
+        pass
+    return p, fp64
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if n_gpus > 0 else "gloo")
+    return rank, world, local
+
+
+def barrier_max(world, value):
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------- CPU arms
+def oracle_iteration_runner(P):
+    """One Newton iteration of the reference algorithm (numpy fp64 restatement of SPEC
+    rdsim: residual + analytic system Jacobian with the reference pass structure + LU)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import scipy.linalg
+    from helpers import oracle_sim
+    from oracle import rdsim as ors
+    S = oracle_sim(P)
+    r, rb, rdb = P.random_state()
+    oc = ors.OSimConfig(dt=P.cfg.dt)
+    state = (rb, rdb)
+    cur = {"r": r.copy()}
+
+    def one():
+        phi = ors.residual(S, cur["r"], state, P.f_ext, oc)
+        J = ors.system_jacobian(S, cur["r"], state, P.f_ext, oc)
+        cur["r"] = cur["r"] + scipy.linalg.lu_solve(scipy.linalg.lu_factor(J), -phi)
+    return one
+
+
+def cpu_baseline(P, budget_s=12.0, max_iters=30):
+    one = oracle_iteration_runner(P)
+    one()  # warm-up
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while len(times) < max_iters and (len(times) < 3 or time.perf_counter() < t_end):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    return {"value": 1e3 * float(np.median(times)), "unit": "ms", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{len(times)} Newton iterations of the numpy-fp64 oracle (SPEC rdsim residual + "
+                      f"system_jacobian with the 4n_q+2 reference passes + LU) at cfg2, median"}
+
+
+def run_reference(args):
+    rank, world, local = dist_setup(0)
+    if rank != 0:
+        return
+    from paper_2102_11026_b200.problem import build_problem
+    P = build_problem("cfg2")
+    one = oracle_iteration_runner(P)
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    ms = 1e3 * (time.perf_counter() - t0) / args.steps
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8d)",
+        "config": {"workload": WORKLOAD, "parallelism": "host cores (numpy/OpenBLAS threads)"},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{args.steps} Newton iterations of the oracle at cfg2 (mean)"},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    rank, world, local = dist_setup(args.gpus)
+    os.environ["NLROM_DEVICE"] = str(local)
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200 import rdsim
+    from paper_2102_11026_b200.session import session_for
+    P = build_problem("cfg2")
+    s = session_for(P.rm, P.model, P.cm)
+    r, rb, rdb = P.random_state(seed=4 + rank)
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=1)
+    s.step(rb, rdb, P.f_ext, cfg)              # captures the graphs, sets the state
+    s.bench_iterations(max(args.warmup, 3), flush_l2=True)
+
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms_total, ms_dom = s.bench_iterations(args.steps, flush_l2=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms_iter = barrier_max(world, ms_total / args.steps)
+    value = ms_iter / world  # whole-job: world * steps iterations in the max-over-ranks device time
+
+    # e2e through the public API (rdsim.step, host buffers, H2D/D2H inside), 3 fixed iterations/step
+    from paper_2102_11026_b200.daereduce import ReducedState
+    cfg3 = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=3)
+    st = ReducedState(rb, rdb, cfg3.dt)
+    for _ in range(2):
+        rdsim.step(P.rm, P.model, st, P.f_ext, cfg3)
+    n_e2e = max(5, args.steps // 3)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        st = rdsim.step(P.rm, P.model, st, P.f_ext, cfg3)
+    e2e_ms = barrier_max(world, 1e3 * (time.perf_counter() - t0) / (n_e2e * 3)) / world
+    n = P.cfg.n_p + P.cfg.n_q
+    h2d = (2 * n + P.model.N) * 8
+    d2h = 2 * n * 8 + 8
+
+    # roofline of the dominant kernel: output decoder layer + fused filter (fp64 DMMA)
+    pk, fp64 = peaks()
+    G = 4 + 4 * 3 if P.cfg.n_q > 15 else None
+    N, w, n_p, n_q = P.model.N, P.cfg.width, P.cfg.n_p, P.cfg.n_q
+    useful_cols = 4 + 4 * n_q                       # base jet + 4 slots per tangent (no replicas)
+    alg_flops = 2.0 * N * (w + n_p) * useful_cols
+    ref_flops = 2.0 * N * (w + n_p) * (16 * n_q + 5)  # same layer in the reference 4n_q+2 pass structure
+    achieved = alg_flops / (ms_dom * 1e-3) / 1e12
+    peak = fp64 if fp64 else None
+    roof = {"bound": "tensor", "kernel": "gemm_tn_kernel<CfgOut,EpiJetOut> (decoder output layer + filter)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if peak else None, "traffic": None,
+            "peak_source": "profiles/fp64_peak.json: measured DMMA.8x8x4 fp64 (MEASURED_PEAKS.json has no fp64 entry)",
+            "kernel_ms": ms_dom, "algorithmic_flops_per_launch": alg_flops,
+            "reference_pass_structure_flops_per_launch": ref_flops}
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "dominant_traffic.json")))
+        roof["traffic"] = tr.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(P)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random-init weights, SURVEY.md §8d)",
+            "config": {"workload": WORKLOAD, "newton": "fixed-iteration mode, 1 graph replay per step",
+                       "l2": "flushed between timed iterations (256 MB write)", "global_sims": world,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d * 1, "d2h_bytes_per_step": d2h,
+                    "how": "nlrom.rdsim.step (host numpy in/out), fixed_iters=3, wall clock / 3"},
+            "gpu_launches": s.launches_per_iteration() * args.steps,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "hz_at_3_iters": 1000.0 / (3 * value),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

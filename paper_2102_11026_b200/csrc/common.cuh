@@ -79,6 +79,23 @@ struct IBuf {
   IBuf& operator=(const IBuf&) = delete;
 };
 
+// Programmatic dependent launch (kernels are captured with programmatic stream
+// serialisation): wait for the producer grid before touching its outputs; allow the
+// next grid to start its independent prologue (e.g. weight prefetch) early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// 8-byte async global->shared copy: staging loops issue every load before any
+// result is needed (a plain load->st.shared loop serialises on memory latency).
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_all_wait() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 // Upload a (rows, cols) row-major host matrix into a device matrix with leading
 // dimension ld (>= cols); padding is zero.
 void upload_matrix(DBuf& dst, const double* h, int rows, int cols, int ld, int rows_alloc = -1);

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "epilogues.cuh"
 #include "sim_kernels.cuh"
+#include "solve_kernels.cuh"
 
 namespace nlrom {
 void fc_forward(int order, int act, const GemmArgs& g, double* Y, int ldy, const double* bias, double* cache,
@@ -26,10 +27,11 @@ using namespace nlrom;
 
 namespace {
 
-using CfgBwd = GemmCfg<16, 16, 1, 1, 4>;
-
-template <int G> using CfgHid = GemmCfg<16, G, 1, 1, 4>;
-template <int G> using CfgOut = GemmCfg<64, G, 4, 1, 1>;
+// hidden / backward layers (K = 256): 16-row tiles, 4 warps split K, 32-wide K tiles,
+// deep cp.async ring so the whole K extent is in flight (latency-bound regime)
+using CfgBwd = GemmCfg<16, 16, 1, 1, 4, 32, 8>;
+template <int G> using CfgHid = GemmCfg<16, G, 1, 1, 4, 32, (G <= 32 ? 8 : 4)>;
+template <int G> using CfgOut = GemmCfg<64, G, 4, 1, 1, 32, 4>;
 
 struct CubSet {
   IBuf elems;
@@ -54,8 +56,8 @@ struct nlrom_ctx {
   // decoder
   std::vector<DBuf> W, WT, b;
   std::vector<int> ldW, ldWT;
-  DBuf Alast, AlastT, AT, Pb, U, mass;
-  int ldlast = 0, ldAlastT = 0, wL1 = 0;
+  DBuf Alast, AT, Pb, U, mass;
+  int ldlast = 0, wL1 = 0;
   // mesh
   IBuf elem_rows;
   DBuf Dm_inv, vol;
@@ -67,18 +69,18 @@ struct nlrom_ctx {
   int wsplit = 0, wchunk = 0;
   DBuf wpart, wC;
   // bundle
-  int G = 0, gps = 0, Cb = 0, ldq = 0, ldjt = 0, lddj = 0;
+  int G = 0, gps = 0, Cb = 0, Cc = 0, ldq = 0, ldjt = 0, lddj = 0;
   DBuf X0;
   std::vector<DBuf> H, cache;
   std::vector<int> ldH, ldc;
   DBuf u, value, hvv, Jt, dJ;
   // assembly / solve
-  int rpc = 64, nchA = 0;
-  DBuf a, partA, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
+  int rpc = 128, nchA = 0;
+  DBuf a, partA, partPhi, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
   IBuf status;
   // backward
-  int bsplit = 0, bchunk = 0;
-  DBuf bpart, Delta0, Delta1, Gt;
+  int brows = 32, bnch = 0;
+  DBuf bpart, ybuf, Delta0, Delta1, Gt;
   int ldGt = 0;
   // graphs
   cudaGraphExec_t gE = nullptr, gJ = nullptr, gIter = nullptr;
@@ -95,13 +97,23 @@ int fail(nlrom_ctx* c, const Error& e) {
   return e.code;
 }
 
-template <class K, class... Args>
-void launch(nlrom_ctx* c, K kernel, dim3 grid, dim3 block, size_t smem, Args... args) {
-  kernel<<<grid, block, smem, c->st>>>(args...);
-  NL_CHECK_LAUNCH();
+template <class... KArgs, class... Args>
+void launch(nlrom_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL edges in the captured graph
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NL_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
   ++gemm_launch_count;
 }
 
+size_t lu_smem(int n);
 int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL, (n + bs - 1) / bs)); }
 
 // ---------------------------------------------------------------- GEMM dispatch
@@ -170,7 +182,7 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
   s.entries.upload(ent.data(), ent.size());
   const int n = c->n;
   s.epc = 8;
-  while (s.epc > 1 && (size_t)(2 * s.epc * 12 * n + s.epc * 156) * 8 > 200 * 1024) s.epc /= 2;
+  while (s.epc > 1 && (size_t)(2 * s.epc * 12 * gram_ld(n) + s.epc * 162) * 8 > 200 * 1024) s.epc /= 2;
   s.nchunk = std::max(1, ceil_div(std::max(s.n, 1), s.epc));
   s.fe_w.alloc((size_t)c->n_sims * std::max(s.n, 1) * 12);
   s.part_f.alloc((size_t)c->n_sims * s.nchunk * n);
@@ -179,6 +191,18 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
 }
 
 // ----------------------------------------------------------------- E and J phases
+// Decoder output layer + fused filter over the compact columns: D = [W_L | -U][h; U^T W_L h] + P b.
+// The dominant kernel of one Newton iteration (fp64 DMMA, 8 warps, 48 x 128 tiles, one wave).
+using CfgOutC = GemmCfg<48, 128, 2, 4, 1, 32, 3>;
+
+void output_layer(nlrom_ctx* c) {
+  GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->n_p, 0, 0};
+  EpiJetOutC e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
+               c->n_p, c->n_q};
+  launch_gemm<CfgOutC>(g, e, c->st);
+  ++gemm_launch_count;
+}
+
 void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
   const int ncols = c->n_sims * c->Cb;
   const int nq = c->n_q;
@@ -188,30 +212,29 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
   const double* in = c->X0.p;
   int ldin = c->ldq;
   for (int l = 0; l + 1 < c->L; ++l) {
+    // the last hidden layer writes the de-replicated layout (its consumer is linear)
+    const int compact = (l == c->L - 2) ? 1 : 0;
     GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
-    EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq};
+    EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, compact};
     hid_gemm(c->G, g, e, c->st);
     in = c->H[l].p;
     ldin = c->ldH[l];
   }
   // T = (U^T W_L) h  -> columns wL1.. of the last hidden buffer (filter fused as K-extension)
   {
-    GemmArgs g{c->AT.p, in, round_up(c->wL1, 2), ldin, c->n_p, ncols, c->wL1, 0, 0};
+    GemmArgs g{c->AT.p, in, round_up(c->wL1, 2), ldin, c->n_p, c->n_sims * c->Cc, c->wL1, 0, 0};
     EpiStore e{c->H[c->L - 2].p + c->wL1, c->ldlast, 0, nullptr, 1, nullptr};
     hid_gemm(c->G, g, e, c->st);
   }
-  {
-    GemmArgs g{c->Alast.p, in, c->ldlast, ldin, c->N, ncols, c->wL1 + c->n_p, 0, 0};
-    EpiJetOut e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
-                c->n_p, nq, c->G, c->gps};
-    out_gemm(c->G, g, e, c->st);
-  }
+  output_layer(c);
 }
 
 void wnet_phase(nlrom_ctx* c) {
   launch(c, k_gemv_splitk, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
          (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
-  launch(c, k_wnet_tail, c->n_sims, 256, (size_t)2 * c->wn * 8, (const double*)c->wpart.p, c->wsplit, c->wn,
+  const int groups = std::max(1, 256 / c->wn);
+  launch(c, k_wnet_tail, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256,
+         (size_t)((2 + groups) * c->wn + 2 * c->wn * c->wn + 64 * c->wn) * 8, (const double*)c->wpart.p, c->wsplit, c->wn,
          (const double*)c->b1.p, (const double*)c->W2.p, (const double*)c->b2.p, (const double*)c->W3.p,
          (const double*)c->b3.p, (const double*)c->W4C.p, (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
 }
@@ -219,7 +242,7 @@ void wnet_phase(nlrom_ctx* c) {
 void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted) {
   CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, weighted ? c->wC.p : nullptr, c->u.p, c->Jt.p,
             c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk, nullptr, nullptr};
-  size_t smem = (size_t)(2 * s.epc * 12 * c->n + s.epc * 156) * 8;
+  size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162) * 8;
   launch(c, k_cubature, dim3(s.nchunk, c->n_sims), 256, smem, a);
   launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
          (const int*)s.row_ptr.p, (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N,
@@ -228,10 +251,12 @@ void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted) {
 
 void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   AsmArgs A{c->Jt.p, c->ldjt, c->dJ.p, c->lddj, c->mass.p, c->hvv.p, s.f.p, c->fext.p, c->r.p, c->rbar.p,
-            c->rdbar.p, c->a.p, c->partA.p, c->N, c->n, c->n_p, c->n_q, c->rpc, c->nchA, dt, c->alpha, drop_fict};
-  size_t smem = (size_t)(c->rpc * c->n + c->rpc * (c->n + 1) + c->n) * 8;
+            c->rdbar.p, c->a.p, c->partA.p, c->partPhi.p, c->N, c->n, c->n_p, c->n_q, c->rpc, c->nchA, dt,
+            c->alpha, drop_fict};
+  size_t smem = (size_t)(2 * c->rpc * gram_ld(c->n) + 2 * c->rpc + c->n) * 8;
   launch(c, k_assemble, dim3(c->nchA, c->n_sims), 256, smem, A);
-  launch(c, k_reduce_phi, c->n_sims, 128, 0, (const double*)c->partA.p, c->nchA, c->n, c->phi.p, c->norm.p);
+  launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nchA, c->n,
+         c->phi.p, c->norm.p);
 }
 
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg) {
@@ -247,20 +272,22 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
                       std::vector<int>& ldcs, DBuf& D0, DBuf& D1, DBuf& Gout, int ldG) {
   const int ncols = c->n_sims * npass_per_sim * NS;
   const int M = c->wL1 + c->n_p;
-  launch(c, k_gemv_splitk, dim3(c->bsplit, c->n_sims), 256, 0, (const double*)c->AlastT.p, c->ldAlastT, a_vec,
-         (long long)c->N, M, c->N, c->bchunk, c->bpart.p, c->n_sims);
+  launch(c, k_gemv_t, dim3(c->bnch, c->n_sims), 128, 0, (const double*)c->Alast.p, c->ldlast, M, a_vec, c->N,
+         c->brows, c->bpart.p, c->bnch);
+  launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->bpart.p, c->bnch, M,
+         c->ybuf.p);
   const int l_top = c->L - 2;
-  size_t smem = (size_t)(2 * c->wL1 + c->n_p) * 8;
+  dim3 gd(ceil_div(c->wL1, 32), c->n_sims);
   if (NS == 2) {
     if (mc)
-      launch(c, k_bwd_top<2, 1>, c->n_sims, 256, smem, (const double*)c->bpart.p, c->bsplit, c->wL1, c->n_p,
-             (const double*)c->AT.p, (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p, c->n_sims);
+      launch(c, k_bwd_delta<2, 1>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->n_p, (const double*)c->AT.p,
+             (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
     else
-      launch(c, k_bwd_top<2, 0>, c->n_sims, 256, smem, (const double*)c->bpart.p, c->bsplit, c->wL1, c->n_p,
-             (const double*)c->AT.p, (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p, c->n_sims);
+      launch(c, k_bwd_delta<2, 0>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->n_p, (const double*)c->AT.p,
+             (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
   } else {
-    launch(c, k_bwd_top<1, 1>, c->n_sims, 256, smem, (const double*)c->bpart.p, c->bsplit, c->wL1, c->n_p,
-           (const double*)c->AT.p, (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p, c->n_sims);
+    launch(c, k_bwd_delta<1, 1>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->n_p, (const double*)c->AT.p,
+           (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
   }
   DBuf* cur = &D0;
   DBuf* nxt = &D1;
@@ -285,11 +312,19 @@ void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply) {
   decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   const int n = c->n;
-  launch(c, k_reduce_S, grid1((long long)n * n * c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
-         (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p,
-         c->n_sims);
-  launch(c, k_lu_solve, c->n_sims, 256, (size_t)n * (n + 2) * 8, (const double*)c->S.p, (const double*)c->phi.p,
-         c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p);
+  launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
+         (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
+  if (n + 1 <= 64)
+    launch(c, k_lu_solve<4>, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p,
+           c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p);
+  else
+    launch(c, k_lu_solve<8>, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p,
+           c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p);
+}
+
+size_t lu_smem(int n) {
+  const int ld = ((n + 1) & 1) ? (n + 1) : (n + 2);
+  return (size_t)n * ld * 8 + (size_t)n * 4 + 16;
 }
 
 std::string cfg_key(const nlrom_simcfg& cfg) {
@@ -409,11 +444,6 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         for (int j = 0; j < n_p; ++j) A[(size_t)r * (w + n_p) + w + j] = -d->U[(size_t)r * n_p + j];
       }
       upload_matrix(c->Alast, A.data(), N, w + n_p, c->ldlast);
-      c->ldAlastT = round_up(N, 2);
-      std::vector<double> At((size_t)(w + n_p) * N);
-      for (int r = 0; r < N; ++r)
-        for (int k = 0; k < w + n_p; ++k) At[(size_t)k * N + r] = A[(size_t)r * (w + n_p) + k];
-      upload_matrix(c->AlastT, At.data(), w + n_p, N, c->ldAlastT);
       std::vector<double> ATh((size_t)n_p * w, 0.0), Utb(n_p, 0.0), Pbh(N);
       for (int r = 0; r < N; ++r)
         for (int j = 0; j < n_p; ++j) {
@@ -475,6 +505,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     // bundle buffers
     choose_groups(n_q, w, c->G, c->gps);
     c->Cb = c->G * c->gps;
+    c->Cc = 4 + 4 * n_q;  // compact (de-replicated) columns per sim
     c->ldq = round_up(n_q, 2);
     const int ncols = c->n_sims * c->Cb;
     c->X0.alloc((size_t)ncols * c->ldq);
@@ -482,7 +513,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     for (int l = 0; l < L - 1; ++l) {
       c->ldH[l] = (l == L - 2) ? c->ldlast : round_up(c->widths[l + 1], 2);
       c->ldc[l] = round_up(c->widths[l + 1], 2);
-      c->H[l].alloc((size_t)ncols * c->ldH[l]);
+      c->H[l].alloc((size_t)std::max(ncols, c->n_sims * c->Cc) * c->ldH[l]);
       c->cache[l].alloc((size_t)c->n_sims * 2 * n_q * c->ldc[l]);
     }
     c->ldjt = c->n;
@@ -500,10 +531,12 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         NL_CUDA(cudaMemcpy(c->Jt.p + (size_t)s * N * c->ldjt, jt.data(), jt.size() * 8, cudaMemcpyHostToDevice));
     }
     // assembly / solve
+    while (c->rpc > 16 && (size_t)(2 * c->rpc * gram_ld(c->n) + 2 * c->rpc + c->n) * 8 > 200 * 1024) c->rpc /= 2;
     c->nchA = ceil_div(N, c->rpc);
     const int n = c->n, S = c->n_sims;
     c->a.alloc((size_t)S * N);
-    c->partA.alloc((size_t)S * c->nchA * n * (n + 1));
+    c->partA.alloc((size_t)S * c->nchA * n * n);
+    c->partPhi.alloc((size_t)S * c->nchA * n);
     c->phi.alloc((size_t)S * n);
     c->norm.alloc(S);
     c->S.alloc((size_t)S * n * n);
@@ -517,9 +550,10 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->tmpN.alloc((size_t)S * N);
     c->status.alloc(S);
     // backward
-    c->bchunk = round_up(std::max(32, ceil_div(N, 148)), 32);
-    c->bsplit = ceil_div(N, c->bchunk);
-    c->bpart.alloc((size_t)c->bsplit * S * (w + n_p));
+    if (w + n_p > 512) throw Error(NLROM_ERR_ARG, "last hidden width + n_p must be <= 512");
+    c->bnch = ceil_div(N, c->brows);
+    c->bpart.alloc((size_t)c->bnch * S * (w + n_p));
+    c->ybuf.alloc((size_t)S * (w + n_p));
     int maxw = 0;
     for (int l = 1; l < L; ++l) maxw = std::max(maxw, round_up(c->widths[l], 2));
     c->Delta0.alloc((size_t)S * 2 * n_q * maxw);
@@ -528,8 +562,11 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->Gt.alloc((size_t)S * 2 * n_q * c->ldGt);
     // kernel attributes for large dynamic shared memory
     NL_CUDA(cudaFuncSetAttribute(k_cubature, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_wnet_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    if (c->n + 1 > 128) throw Error(NLROM_ERR_ARG, "n_p + n_q must be <= 127");
     NL_CUDA(cudaDeviceSynchronize());
     *out = c;
     return NLROM_OK;
@@ -860,11 +897,6 @@ extern "C" int nlrom_bench_iterations(nlrom_ctx* c, int n_iters, int flush_l2, f
   *ms_total = tot;
   // dominant kernel (output decoder layer + fused filter) timed alone on the same stream
   if (ms_dom) {
-    const int ncols = c->n_sims * c->Cb;
-    const double* in = c->H[c->L - 2].p;
-    GemmArgs g{c->Alast.p, in, c->ldlast, c->ldH[c->L - 2], c->N, ncols, c->wL1 + c->n_p, 0, 0};
-    EpiJetOut e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
-                c->n_p, c->n_q, c->G, c->gps};
     float dom = 0.f;
     for (int i = 0; i < n_iters; ++i) {
       if (flush_l2) {
@@ -872,7 +904,7 @@ extern "C" int nlrom_bench_iterations(nlrom_ctx* c, int n_iters, int flush_l2, f
         NL_CHECK_LAUNCH();
       }
       NL_CUDA(cudaEventRecord(c->ev0, c->st));
-      out_gemm(c->G, g, e, c->st);
+      output_layer(c);
       NL_CUDA(cudaEventRecord(c->ev1, c->st));
       NL_CUDA(cudaEventSynchronize(c->ev1));
       float ms = 0.f;
@@ -894,7 +926,7 @@ extern "C" int nlrom_element_forces(nlrom_ctx* c, const double* u, int want_K, d
   CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, nullptr, c->u.p, nullptr,
             c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk,
             want_K ? Ke.p : nullptr, nullptr};
-  size_t smem = (size_t)(2 * s.epc * 12 * c->n + s.epc * 156) * 8;
+  size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162) * 8;
   launch(c, k_cubature, dim3(s.nchunk, 1), 256, smem, a);
   launch(c, k_scatter_rows, grid1((long long)s.n_rows), 256, 0, (const int*)s.row_ids.p, (const int*)s.row_ptr.p,
          (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N, 1);
@@ -917,7 +949,7 @@ extern "C" int nlrom_element_reduced_forces(nlrom_ctx* c, const double* r, const
   DBuf few((size_t)n_elems * 12), pf((size_t)nch * c->n), pK((size_t)nch * c->n * c->n), fo((size_t)n_elems * c->n);
   CubArgs a{de.p, n_elems, c->elem_rows.p, c->Dm_inv.p, c->vol.p, nullptr, c->u.p, c->Jt.p,
             c->N, c->n, c->ldjt, c->mu, c->lam, epc, few.p, pf.p, pK.p, nch, nullptr, fo.p};
-  size_t smem = (size_t)(2 * epc * 12 * c->n + epc * 156) * 8;
+  size_t smem = (size_t)(2 * epc * 12 * gram_ld(c->n) + epc * 162) * 8;
   launch(c, k_cubature, dim3(nch, 1), 256, smem, a);
   d2h(c, out, fo, (size_t)n_elems * c->n);
   NL_CUDA(cudaStreamSynchronize(c->st));

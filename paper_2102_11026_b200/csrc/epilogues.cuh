@@ -113,12 +113,44 @@ struct EpiJet {
   int group;          // columns per group (== BN)
   int gps;            // groups per simulation
   int n_q;            // tangent directions per simulation
+  int compact;        // 1: write the de-replicated layout [base | n_q tangents] per sim (next layer is linear)
   __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
     double* Yz = Y + (size_t)t.z * strideY;
     const int gg = t.c0 / group;              // global group index (tile == group)
     const int sim = gg / gps, gl = gg % gps;
     const int nk = (group - 4) / 4;           // tangents per group
     double* Cz = cache ? cache + (size_t)sim * 2 * n_q * ldcache : nullptr;
+    const int cs = 4 + 4 * n_q;               // compact columns per sim
+    if (compact) {
+      for (int ml = tid; ml < t.bm; ml += nt) {
+        const int m = t.m0 + ml;
+        if (m >= g.M) continue;
+        double z[4], o[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) z[s] = t.Cs[s * t.ldc + ml];
+        z[0] += bias[m];
+        JetCos jc;
+        jet_sin_base(z, o, jc);
+        if (gl == 0)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) Yz[(size_t)(sim * cs + s) * ldy + m] = o[s];
+        for (int k = 0; k < nk; ++k) {
+          const int kg = gl * nk + k;
+          if (kg >= n_q) break;
+          double y[4], yo[4];
+#pragma unroll
+          for (int s = 0; s < 4; ++s) y[s] = t.Cs[(4 + 4 * k + s) * t.ldc + ml];
+          jet_tangent(jc, y, yo);
+#pragma unroll
+          for (int s = 0; s < 4; ++s) Yz[(size_t)(sim * cs + 4 + 4 * kg + s) * ldy + m] = yo[s];
+          if (Cz) {
+            Cz[(size_t)(2 * kg) * ldcache + m] = z[0];
+            Cz[(size_t)(2 * kg + 1) * ldcache + m] = y[0];
+          }
+        }
+      }
+      return;
+    }
     for (int ml = tid; ml < t.bm; ml += nt) {
       const int m = t.m0 + ml;
       if (m >= g.M) continue;
@@ -142,6 +174,48 @@ struct EpiJet {
           Cz[(size_t)(2 * kg) * ldcache + m] = z[0];
           Cz[(size_t)(2 * kg + 1) * ldcache + m] = y[0];
         }
+      }
+    }
+  }
+};
+
+// Output layer over the de-replicated (compact) column layout: per sim 4 + 4 n_q columns
+// [1, s, s^2, r | (t, ts, ts^2, tr) x n_q]; a tile may hold several sims / tangents.
+struct EpiJetOutC {
+  const double* bias;    // P b (filtered last bias), real slot only
+  const double* U;       // (N, n_p) row-major
+  const double* r;       // (n_sims, n): p = r[:n_p]
+  double* u;             // (n_sims, N)
+  double* value;         // (n_sims, N) D(q)
+  double* hvv;           // (n_sims, N)
+  double* Jt;            // (n_sims, N, ldjt)
+  double* dJ;            // (n_sims, N, lddj)
+  int ldjt, lddj, n_p, n_q;
+  __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
+    const int N = g.M;
+    const int cs = 4 + 4 * n_q;
+    const int ngrp = t.bn / 4;
+    for (int i = tid; i < t.bm * ngrp; i += nt) {
+      const int q = i / t.bm, ml = i % t.bm;
+      const int m = t.m0 + ml;
+      const int c = t.c0 + 4 * q;
+      if (m >= N || c >= g.C) continue;
+      const int sim = c / cs, rem = c % cs;
+      const size_t sv = (size_t)sim * N + m;
+      const double* col = t.Cs + (4 * q) * t.ldc + ml;
+      if (rem == 0) {
+        const double d1 = col[0] + bias[m];
+        double up = 0.0;
+        const double* Ur = U + (size_t)m * n_p;
+        const double* pz = r + (size_t)sim * (n_p + n_q);
+        for (int k = 0; k < n_p; ++k) up = fma(Ur[k], pz[k], up);
+        u[sv] = up + d1;
+        value[sv] = d1;
+        hvv[sv] = 2.0 * col[2 * t.ldc];
+      } else {
+        const int kg = (rem - 4) >> 2;
+        Jt[sv * ldjt + n_p + kg] = col[0];
+        dJ[sv * lddj + kg] = 2.0 * col[2 * t.ldc] + col[3 * t.ldc];
       }
     }
   }

@@ -35,10 +35,11 @@ struct Tile {
   int z;
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int WK_>
+template <int BM_, int BN_, int WM_, int WN_, int WK_, int BK_ = 16, int STAGES_ = 2>
 struct GemmCfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, WK = WK_;
-  static constexpr int BK = 16;
+  static constexpr int BK = BK_;
+  static constexpr int STAGES = STAGES_;
   static constexpr int NT = 32 * WM * WN * WK;
   static constexpr int TM = BM / WM, TN = BN / WN;
   static constexpr int FM = TM / 8, FN = TN / 8;
@@ -46,7 +47,7 @@ struct GemmCfg {
   static constexpr int LDS = BK + 4;        // conflict-free 8-byte fragment loads
   static constexpr int LDC = BM + 2;        // conflict-free accumulator stores
   static constexpr int STAGE = (BM + BN) * LDS;
-  static constexpr int PIPE = 2 * STAGE;
+  static constexpr int PIPE = STAGES * STAGE;
   static constexpr int CT = BN * LDC;
   static constexpr int SMEM_DOUBLES = PIPE > CT ? PIPE : CT;
   static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
@@ -70,8 +71,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 template <class Cfg>
-__device__ __forceinline__ void gemm_load_stage(double* As, double* Bs, const GemmArgs& g, const double* A,
-                                                const double* B, int m0, int c0, int k0, int tid) {
+__device__ __forceinline__ void gemm_load_A(double* As, const GemmArgs& g, const double* A, int m0, int k0, int tid) {
   constexpr int CH = Cfg::BK / 2;  // 16-byte chunks per row
   for (int i = tid; i < Cfg::BM * CH; i += Cfg::NT) {
     int r = i / CH, ck = (i % CH) * 2;
@@ -80,6 +80,25 @@ __device__ __forceinline__ void gemm_load_stage(double* As, double* Bs, const Ge
     const double* src = ok ? (A + (size_t)m * g.lda + k) : A;
     cp_async16(As + r * Cfg::LDS + ck, src, ok);
   }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void gemm_load_B(double* Bs, const GemmArgs& g, const double* B, int c0, int k0, int tid) {
+  constexpr int CH = Cfg::BK / 2;
+  for (int i = tid; i < Cfg::BN * CH; i += Cfg::NT) {
+    int r = i / CH, ck = (i % CH) * 2;
+    int c = c0 + r, k = k0 + ck;
+    bool ok = (c < g.C) && (k < g.K);
+    const double* src = ok ? (B + (size_t)c * g.ldb + k) : B;
+    cp_async16(Bs + r * Cfg::LDS + ck, src, ok);
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void gemm_load_stage(double* As, double* Bs, const GemmArgs& g, const double* A,
+                                                const double* B, int m0, int c0, int k0, int tid) {
+  gemm_load_A<Cfg>(As, g, A, m0, k0, tid);
+  constexpr int CH = Cfg::BK / 2;
   for (int i = tid; i < Cfg::BN * CH; i += Cfg::NT) {
     int r = i / CH, ck = (i % CH) * 2;
     int c = c0 + r, k = k0 + ck;
@@ -108,18 +127,32 @@ __global__ void __launch_bounds__(Cfg::NT) gemm_tn_kernel(GemmArgs g, Epi epi) {
     for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (g.K + Cfg::BK - 1) / Cfg::BK;
-  gemm_load_stage<Cfg>(smem, smem + Cfg::BM * Cfg::LDS, g, A, B, m0, c0, 0, tid);
-  cp_async_commit();
-  for (int kt = 0; kt < nk; ++kt) {
-    double* As = smem + (kt & 1) * Cfg::STAGE;
-    double* Bs = As + Cfg::BM * Cfg::LDS;
-    if (kt + 1 < nk) {
-      double* An = smem + ((kt + 1) & 1) * Cfg::STAGE;
-      gemm_load_stage<Cfg>(An, An + Cfg::BM * Cfg::LDS, g, A, B, m0, c0, (kt + 1) * Cfg::BK, tid);
-    }
+  // STAGES-deep cp.async ring: tiles kt+1 .. kt+STAGES-1 are in flight while tile kt is consumed.
+  // The weight tiles (A) do not depend on the producer kernel: they are requested before the
+  // programmatic-dependency wait, the activation tiles (B) after it.
+#pragma unroll
+  for (int s = 0; s < Cfg::STAGES - 1; ++s)
+    if (s < nk) gemm_load_A<Cfg>(smem + s * Cfg::STAGE, g, A, m0, s * Cfg::BK, tid);
+  pdl_wait();
+  pdl_launch();
+#pragma unroll
+  for (int s = 0; s < Cfg::STAGES - 1; ++s) {
+    if (s < nk) gemm_load_B<Cfg>(smem + s * Cfg::STAGE + Cfg::BM * Cfg::LDS, g, B, c0, s * Cfg::BK, tid);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<Cfg::STAGES - 2>();
     __syncthreads();
+    {
+      const int kn = kt + Cfg::STAGES - 1;  // refill the slot consumed at kt-1 (all warps are past it)
+      if (kn < nk) {
+        double* An = smem + (kn % Cfg::STAGES) * Cfg::STAGE;
+        gemm_load_stage<Cfg>(An, An + Cfg::BM * Cfg::LDS, g, A, B, m0, c0, kn * Cfg::BK, tid);
+      }
+      cp_async_commit();
+    }
+    const double* As = smem + (kt % Cfg::STAGES) * Cfg::STAGE;
+    const double* Bs = As + Cfg::BM * Cfg::LDS;
 #pragma unroll
     for (int kk = 0; kk < Cfg::KS; kk += 4) {
       const int kc = wk * Cfg::KS + kk + (lane & 3);
@@ -133,7 +166,6 @@ __global__ void __launch_bounds__(Cfg::NT) gemm_tn_kernel(GemmArgs g, Epi epi) {
 #pragma unroll
         for (int j = 0; j < Cfg::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    __syncthreads();
   }
   cp_async_wait<0>();
   __syncthreads();
@@ -169,9 +201,17 @@ void launch_gemm(const GemmArgs& g, const Epi& epi, cudaStream_t st, int batch =
                                  Cfg::SMEM_BYTES));
     configured = true;
   }
-  dim3 grid(ceil_div(g.M, Cfg::BM), ceil_div(g.C, Cfg::BN), batch);
-  gemm_tn_kernel<Cfg, Epi><<<grid, Cfg::NT, Cfg::SMEM_BYTES, st>>>(g, epi);
-  NL_CHECK_LAUNCH();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ceil_div(g.M, Cfg::BM), ceil_div(g.C, Cfg::BN), batch);
+  cfg.blockDim = dim3(Cfg::NT);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NL_CUDA(cudaLaunchKernelEx(&cfg, gemm_tn_kernel<Cfg, Epi>, g, epi));
 }
 
 // ------------------------------------------------------------------ epilogues

@@ -3,6 +3,7 @@
 #pragma once
 #include "common.cuh"
 #include "mc_device.cuh"
+#include "gram_dmma.cuh"
 
 namespace nlrom {
 
@@ -15,6 +16,8 @@ namespace nlrom {
 __global__ void k_seed_jet(const double* __restrict__ r, const double* __restrict__ rbar,
                            const double* __restrict__ rdbar, double* __restrict__ X0, int ldx, int n_p, int n_q,
                            int n, int G, int gps, int n_sims, double dt, double alpha, int drop_fict) {
+  pdl_wait();
+  pdl_launch();
   const int cols = gps * G;
   const long long total = (long long)n_sims * cols * n_q;
   const int nk = (G - 4) / 4;
@@ -50,6 +53,8 @@ __global__ void k_seed_jet(const double* __restrict__ r, const double* __restric
 //   scale = eps (literal multicomplex, mode 1) or 1 (scaled multi-dual, mode 0).
 __global__ void k_seed_ref(const double* __restrict__ q, const double* __restrict__ vec, double* __restrict__ X0,
                            int ldx, int n_q, int op, int S, int npass, double scale) {
+  pdl_wait();
+  pdl_launch();
   const long long total = (long long)npass * S * n_q;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     int i = t % n_q;
@@ -71,6 +76,8 @@ __global__ void k_seed_ref(const double* __restrict__ q, const double* __restric
 // Extract slot `slot` of every pass from Y_t (ncols x ldy) into out (N, npass) row-major, / div.
 __global__ void k_extract_slot(const double* __restrict__ Y, int ldy, int N, int S, int npass, int slot, double div,
                                double* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
   const long long total = (long long)N * npass;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     int j = t % npass;
@@ -81,25 +88,55 @@ __global__ void k_extract_slot(const double* __restrict__ Y, int ldy, int N, int
 
 // ------------------------------------------------------------------------ wnet
 // Split-K GEMV: part[s][sim][m] = sum_{k in chunk s} A[m][k] x[sim][k]   (A: M x K row-major, lda)
+// Each warp works on 4 rows at once so 4 independent loads per lane are in flight.
 __global__ void k_gemv_splitk(const double* __restrict__ A, int lda, const double* __restrict__ x, long long strideX,
                               int M, int K, int chunk, double* __restrict__ part, int n_sims) {
+  pdl_wait();
+  pdl_launch();
   const int s = blockIdx.x;
   const int sim = blockIdx.y;
   const int k0 = s * chunk, k1 = min(K, k0 + chunk);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const double* xs = x + (size_t)sim * strideX;
-  for (int m = warp; m < M; m += nw) {
-    const double* Ar = A + (size_t)m * lda;
-    double acc = 0.0;
-    for (int k = k0 + lane; k < k1; k += 32) acc = fma(Ar[k], xs[k], acc);
+  for (int m0 = warp * 4; m0 < M; m0 += nw * 4) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = k0 + lane; k < k1; k += 32) {
+      const double xv = xs[k];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) part[((size_t)s * n_sims + sim) * M + m] = acc;
+      for (int u = 0; u < 4; ++u)
+        if (m0 + u < M) acc[u] = fma(A[(size_t)(m0 + u) * lda + k], xv, acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double v = acc[u];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && m0 + u < M) part[((size_t)s * n_sims + sim) * M + m0 + u] = v;
+    }
   }
 }
 
-// Weight-net tail (1 CTA per sim): h1 = sin(sum parts + b1), h2 = sin(W2 h1 + b2),
-// h3 = sin(W3 h2 + b3), w_C = (W4[C] h3 + b4[C])^2   (PAPER.md:406 square for w >= 0)
+// Weight-net tail, grid (ceil(|C|/64), n_sims): every CTA rebuilds h1..h3 (tiny) and
+// evaluates 64 rows of the C-restricted last layer:
+//   h1 = sin(sum parts + b1), h2 = sin(W2 h1 + b2), h3 = sin(W3 h2 + b3),
+//   w_C = (W4[C] h3 + b4[C])^2   (square keeps w >= 0)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ void wnet_dense_sin(const double* __restrict__ W, const double* __restrict__ b, const double* hin,
+                               double* hout, int wn) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int m = warp; m < wn; m += nw) {
+    double acc = 0.0;
+    for (int k = lane; k < wn; k += 32) acc = fma(W[(size_t)m * wn + k], hin[k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) hout[m] = sin(acc + b[m]);
+  }
+}
+
 __global__ void k_wnet_tail(const double* __restrict__ part, int n_split, int wn, const double* __restrict__ b1,
                             const double* __restrict__ W2, const double* __restrict__ b2, const double* __restrict__ W3,
                             const double* __restrict__ b3, const double* __restrict__ W4C, const double* __restrict__ b4C,
@@ -107,29 +144,48 @@ __global__ void k_wnet_tail(const double* __restrict__ part, int n_split, int wn
   extern __shared__ double sh[];
   double* h1 = sh;
   double* h2 = sh + wn;
-  const int sim = blockIdx.x;
+  double* red = sh + 2 * wn;   // [groups][wn]
+  const int sim = blockIdx.y;
+  const int groups = max(1, (int)blockDim.x / wn);
+  double* W2s = red + groups * wn;   // weights staged in smem up front (one round trip)
+  double* W3s = W2s + wn * wn;
+  double* W4s = W3s + wn * wn;       // this CTA's 64 rows of W4[C]
+  const int j0 = blockIdx.x * 64;
+  const int nrows4 = max(0, min(64, n_cub - j0));
+  for (int t = threadIdx.x; t < wn * wn; t += blockDim.x) {
+    cp_async8(W2s + t, W2 + t);
+    cp_async8(W3s + t, W3 + t);
+  }
+  for (int t = threadIdx.x; t < nrows4 * wn; t += blockDim.x) cp_async8(W4s + t, W4C + (size_t)j0 * wn + t);
+  pdl_wait();
+  pdl_launch();
+  {
+    const int m = threadIdx.x % wn, gidx = threadIdx.x / wn;
+    if (gidx < groups) {
+      double acc = 0.0;
+      for (int s2 = gidx; s2 < n_split; s2 += groups) acc += part[((size_t)s2 * n_sims + sim) * wn + m];
+      red[gidx * wn + m] = acc;
+    }
+  }
+  cp_async_all_wait();
+  __syncthreads();
   for (int m = threadIdx.x; m < wn; m += blockDim.x) {
     double acc = b1[m];
-    for (int s = 0; s < n_split; ++s) acc += part[((size_t)s * n_sims + sim) * wn + m];
+    for (int gidx = 0; gidx < groups; ++gidx) acc += red[gidx * wn + m];
     h1[m] = sin(acc);
   }
   __syncthreads();
-  for (int m = threadIdx.x; m < wn; m += blockDim.x) {
-    double acc = b2[m];
-    for (int k = 0; k < wn; ++k) acc = fma(W2[(size_t)m * wn + k], h1[k], acc);
-    h2[m] = sin(acc);
-  }
+  wnet_dense_sin(W2s, b2, h1, h2, wn);
   __syncthreads();
-  for (int m = threadIdx.x; m < wn; m += blockDim.x) {
-    double acc = b3[m];
-    for (int k = 0; k < wn; ++k) acc = fma(W3[(size_t)m * wn + k], h2[k], acc);
-    h1[m] = sin(acc);
-  }
+  wnet_dense_sin(W3s, b3, h2, h1, wn);
   __syncthreads();
-  for (int j = threadIdx.x; j < n_cub; j += blockDim.x) {
-    double acc = b4C[j];
-    for (int k = 0; k < wn; ++k) acc = fma(W4C[(size_t)j * wn + k], h1[k], acc);
-    wC[(size_t)sim * n_cub + j] = acc * acc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int jj = warp; jj < nrows4; jj += nw) {
+    const int j = j0 + jj;
+    double acc = 0.0;
+    for (int k = lane; k < wn; k += 32) acc = fma(W4s[(size_t)jj * wn + k], h1[k], acc);
+    acc = warp_sum(acc) + b4C[j];
+    if (lane == 0) wC[(size_t)sim * n_cub + j] = acc * acc;
   }
 }
 
@@ -165,32 +221,40 @@ __device__ __forceinline__ void mat3_mul(const double* A, const double* B, doubl
 }
 
 __global__ void k_cubature(CubArgs a) {
+  pdl_wait();
+  pdl_launch();
   extern __shared__ double sh[];
   const int n = a.n;
   const int epc = a.epc;
-  double* Js = sh;                         // [epc][12][n]
-  double* Gs = Js + (size_t)epc * 12 * n;  // [epc][12][n]  (w K J)
-  double* Ks = Gs + (size_t)epc * 12 * n;  // [epc][12][12]
+  const int ldp = gram_ld(n);              // row pitch of the J~ / G panels
+  double* Js = sh;                         // [epc*12][ldp]
+  double* Gs = Js + (size_t)epc * 12 * ldp;  // [epc*12][ldp]  (w K J)
+  double* Ks = Gs + (size_t)epc * 12 * ldp;  // [epc][12][12]
   double* Fs = Ks + (size_t)epc * 144;     // [epc][12]
   const int chunk = blockIdx.x, sim = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const double* u = a.u + (size_t)sim * a.N;
   const double* Jt = a.Jt ? a.Jt + (size_t)sim * a.N * a.ldjt : nullptr;
 
-  // gather the J~ rows of the chunk's elements
-  for (int idx = threadIdx.x; Jt && idx < epc * 12 * n; idx += blockDim.x) {
-    int j = idx % n;
-    int l = (idx / n) % 12;
-    int el = idx / (12 * n);
-    int ei = chunk * epc + el;
-    double val = 0.0;
+  // stage the chunk's 12 DOF rows per element, then gather the J~ rows (independent loads)
+  int* Rw = reinterpret_cast<int*>(Fs + (size_t)epc * 12);  // [epc][12]
+  for (int idx = threadIdx.x; idx < epc * 12; idx += blockDim.x) {
+    const int ei = chunk * epc + idx / 12;
+    int row = -1;
     if (ei < a.n_elems) {
-      int e = a.elems ? a.elems[ei] : ei;
-      int row = a.elem_rows[(size_t)e * 12 + l];
-      if (row >= 0) val = Jt[(size_t)row * a.ldjt + j];
+      const int e = a.elems ? a.elems[ei] : ei;
+      row = a.elem_rows[(size_t)e * 12 + idx % 12];
     }
-    Js[idx] = val;
+    Rw[idx] = row;
   }
+  __syncthreads();
+  for (int idx = threadIdx.x; Jt && idx < epc * 12 * n; idx += blockDim.x) {
+    const int row = Rw[idx / n];
+    double* dst = Js + (idx / n) * ldp + idx % n;
+    if (row >= 0) cp_async8(dst, Jt + (size_t)row * a.ldjt + idx % n);
+    else *dst = 0.0;
+  }
+  cp_async_all_wait();
   // element physics, one warp per element
   for (int el = warp; el < epc; el += nw) {
     int ei = chunk * epc + el;
@@ -204,7 +268,7 @@ __global__ void k_cubature(CubArgs a) {
     int e = a.elems ? a.elems[ei] : ei;
     double ue = 0.0;
     if (lane < 12) {
-      int row = a.elem_rows[(size_t)e * 12 + lane];
+      const int row = Rw[el * 12 + lane];
       ue = row >= 0 ? u[row] : 0.0;
     }
     double uv[12];
@@ -297,7 +361,7 @@ __global__ void k_cubature(CubArgs a) {
       int ei = chunk * epc + el;
       if (ei >= a.n_elems) continue;
       double acc = 0.0;
-      for (int l = 0; l < 12; ++l) acc = fma(Js[(el * 12 + l) * n + i], Fs[el * 12 + l], acc);
+      for (int l = 0; l < 12; ++l) acc = fma(Js[(el * 12 + l) * ldp + i], Fs[el * 12 + l], acc);
       a.fred_out[(size_t)ei * n + i] = acc;
     }
     return;
@@ -308,26 +372,21 @@ __global__ void k_cubature(CubArgs a) {
     int r = (idx / n) % 12;
     int el = idx / (12 * n);
     const double* Kr = Ks + el * 144 + r * 12;
-    const double* Je = Js + (size_t)el * 12 * n;
+    const double* Je = Js + (size_t)el * 12 * ldp;
     double acc = 0.0;
 #pragma unroll
-    for (int c = 0; c < 12; ++c) acc = fma(Kr[c], Je[c * n + j], acc);
-    Gs[idx] = acc;
+    for (int c = 0; c < 12; ++c) acc = fma(Kr[c], Je[c * ldp + j], acc);
+    Gs[(el * 12 + r) * ldp + j] = acc;
   }
   __syncthreads();
-  // partial K~ = sum_rows J~^T G ; partial f~ = sum_rows J~^T (w f)
+  // partial K~ = J~_C^T (w K J~_C) over the chunk's rows on the DMMA pipe; partial f~ = J~_C^T (w f)
   double* pK = a.part_K + ((size_t)sim * a.nchunk + chunk) * n * n;
   const int R = epc * 12;
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-    int i = idx / n, j = idx % n;
-    double acc = 0.0;
-    for (int rr = 0; rr < R; ++rr) acc = fma(Js[rr * n + i], Gs[rr * n + j], acc);
-    pK[idx] = acc;
-  }
+  gram_dmma(Js, ldp, Gs, ldp, R, n, n, pK, n);
   double* pf = a.part_f + ((size_t)sim * a.nchunk + chunk) * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double acc = 0.0;
-    for (int rr = 0; rr < R; ++rr) acc = fma(Js[rr * n + i], Fs[rr], acc);
+    for (int rr = 0; rr < R; ++rr) acc = fma(Js[rr * ldp + i], Fs[rr], acc);
     pf[i] = acc;
   }
 }
@@ -336,6 +395,8 @@ __global__ void k_cubature(CubArgs a) {
 __global__ void k_scatter_rows(const int* __restrict__ row_ids, const int* __restrict__ row_ptr,
                                const int* __restrict__ entries, int n_rows, const double* __restrict__ fe_w,
                                int n_elems, double* __restrict__ f, int N, int n_sims) {
+  pdl_wait();
+  pdl_launch();
   const long long total = (long long)n_rows * n_sims;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     int i = t % n_rows;
@@ -343,268 +404,6 @@ __global__ void k_scatter_rows(const int* __restrict__ row_ids, const int* __res
     double acc = 0.0;
     for (int j = row_ptr[i]; j < row_ptr[i + 1]; ++j) acc += fe_w[(size_t)sim * n_elems * 12 + entries[j]];
     f[(size_t)sim * N + row_ids[i]] = acc;
-  }
-}
-
-// -------------------------------------------------------------------- assembly
-// Per chunk of rows n:  a_n = M_n (J~_n . c) + [M_n hvv_n] + dt^2 (f_n - fext_n),
-//   c = (1 + alpha dt)(r - r_bar) - dt rdot_bar,
-// partial P = sum_n J~_n^T [ M_n R_n | a_n ],  R_n = (1+alpha dt) J~_n + [0, dJ_n].
-struct AsmArgs {
-  const double* Jt; int ldjt;
-  const double* dJ; int lddj;
-  const double* mass;
-  const double* hvv;
-  const double* f;       // cubature / exact scattered force (n_sims, N)
-  const double* fext;    // (n_sims, N)
-  const double* r; const double* rbar; const double* rdbar;
-  double* a;             // (n_sims, N)
-  double* part;          // (n_sims, nchunk, n*(n+1))
-  int N, n, n_p, n_q, rows_per_cta, nchunk;
-  double dt, alpha;
-  int drop_fict;
-};
-
-__global__ void k_assemble(AsmArgs A) {
-  extern __shared__ double sh[];
-  const int n = A.n, n1 = n + 1;
-  const int RC = A.rows_per_cta;
-  double* Js = sh;                    // [RC][n]
-  double* Rs = Js + (size_t)RC * n;   // [RC][n+1]  (M R | a)
-  double* cs = Rs + (size_t)RC * n1;  // [n]
-  const int chunk = blockIdx.x, sim = blockIdx.y;
-  const double ah = A.alpha * A.dt;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    size_t o = (size_t)sim * n + i;
-    cs[i] = (1.0 + ah) * (A.r[o] - A.rbar[o]) - A.dt * A.rdbar[o];
-  }
-  const int row0 = chunk * RC;
-  const double* Jt = A.Jt + (size_t)sim * A.N * A.ldjt;
-  const double* dJ = A.dJ + (size_t)sim * A.N * A.lddj;
-  for (int idx = threadIdx.x; idx < RC * n; idx += blockDim.x) {
-    int rl = idx / n, j = idx % n;
-    int row = row0 + rl;
-    Js[idx] = row < A.N ? Jt[(size_t)row * A.ldjt + j] : 0.0;
-  }
-  __syncthreads();
-  // a_n (one warp per row)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int rl = warp; rl < RC; rl += nw) {
-    int row = row0 + rl;
-    double acc = 0.0;
-    for (int j = lane; j < n; j += 32) acc = fma(Js[rl * n + j], cs[j], acc);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      double av = 0.0;
-      if (row < A.N) {
-        size_t o = (size_t)sim * A.N + row;
-        double m = A.mass[row];
-        av = m * acc + A.dt * A.dt * (A.f[o] - A.fext[o]);
-        if (!A.drop_fict) av += m * A.hvv[o];
-        A.a[o] = av;
-      }
-      Rs[rl * n1 + n] = av;
-    }
-  }
-  for (int idx = threadIdx.x; idx < RC * n; idx += blockDim.x) {
-    int rl = idx / n, j = idx % n;
-    int row = row0 + rl;
-    double v = 0.0;
-    if (row < A.N) {
-      v = (1.0 + ah) * Js[idx];
-      if (j >= A.n_p) v += dJ[(size_t)row * A.lddj + (j - A.n_p)];
-      v *= A.mass[row];
-    }
-    Rs[rl * n1 + j] = v;
-  }
-  __syncthreads();
-  double* P = A.part + ((size_t)sim * A.nchunk + chunk) * n * n1;
-  for (int idx = threadIdx.x; idx < n * n1; idx += blockDim.x) {
-    int i = idx / n1, j = idx % n1;
-    double acc = 0.0;
-    for (int rl = 0; rl < RC; ++rl) acc = fma(Js[rl * n + i], Rs[rl * n1 + j], acc);
-    P[idx] = acc;
-  }
-}
-
-// phi = sum_chunks part[:, n] (one CTA per sim), ||phi||_2
-__global__ void k_reduce_phi(const double* __restrict__ part, int nchunk, int n, double* __restrict__ phi,
-                             double* __restrict__ norm) {
-  const int sim = blockIdx.x;
-  const int n1 = n + 1;
-  __shared__ double red[32];
-  double sq = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < nchunk; ++c) acc += part[(((size_t)sim * nchunk + c) * n + i) * n1 + n];
-    phi[(size_t)sim * n + i] = acc;
-    sq += acc * acc;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    norm[sim] = sqrt(s);
-  }
-}
-
-// S = sum part_A[:, :n] + dt^2 sum part_K + diag(0, vhp);  vhp[i][k] = G_t[2k+1][i]
-__global__ void k_reduce_S(const double* __restrict__ partA, int nchA, const double* __restrict__ partK, int nchK,
-                           const double* __restrict__ Gt, int ldg, int n, int n_p, int n_q, double dt,
-                           double* __restrict__ S, int n_sims) {
-  const long long total = (long long)n * n * n_sims;
-  const int n1 = n + 1;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    int idx = t % (n * n);
-    int sim = t / (n * n);
-    int i = idx / n, j = idx % n;
-    double acc = 0.0;
-    for (int c = 0; c < nchA; ++c) acc += partA[(((size_t)sim * nchA + c) * n + i) * n1 + j];
-    double k = 0.0;
-    for (int c = 0; c < nchK; ++c) k += partK[((size_t)sim * nchK + c) * n * n + idx];
-    acc += dt * dt * k;
-    if (Gt && i >= n_p && j >= n_p) acc += Gt[((size_t)sim * 2 * n_q + 2 * (j - n_p) + 1) * ldg + (i - n_p)];
-    S[(size_t)sim * n * n + idx] = acc;
-  }
-}
-
-// sum of cubature partials (for cubature_integrate): f~ (n), K~ (n,n)
-__global__ void k_reduce_cub(const double* __restrict__ part_f, const double* __restrict__ part_K, int nch, int n,
-                             double* __restrict__ f_red, double* __restrict__ K_red) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * n + n; t += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    if (t < n * n) {
-      for (int c = 0; c < nch; ++c) acc += part_K[(size_t)c * n * n + t];
-      K_red[t] = acc;
-    } else {
-      int i = t - n * n;
-      for (int c = 0; c < nch; ++c) acc += part_f[(size_t)c * n + i];
-      f_red[i] = acc;
-    }
-  }
-}
-
-// --------------------------------------------------------------------------- LU
-// One CTA per sim: LU with partial pivoting of S (n x n) and solve S dr = -phi
-// (SPEC.md:555, 566). If `apply`, r += dr. status[sim] = 1 on a zero pivot.
-__global__ void k_lu_solve(const double* __restrict__ S, const double* __restrict__ phi, double* __restrict__ dr,
-                           double* __restrict__ r, int n, int apply, int* __restrict__ status) {
-  extern __shared__ double sh[];
-  const int sim = blockIdx.x;
-  const int ld = n + 2;
-  double* A = sh;  // [n][n+2], column n = rhs
-  __shared__ int piv;
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) A[(idx / n) * ld + idx % n] = S[(size_t)sim * n * n + idx];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) A[i * ld + n] = -phi[(size_t)sim * n + i];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = 0; k < n; ++k) {
-    if (warp == 0) {
-      double best = -1.0;
-      int bi = k;
-      for (int i = k + lane; i < n; i += 32) {
-        double v = fabs(A[i * ld + k]);
-        if (v > best) { best = v; bi = i; }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-      }
-      if (lane == 0) piv = bi;
-    }
-    __syncthreads();
-    const int p = piv;
-    if (p != k)
-      for (int j = threadIdx.x; j <= n; j += blockDim.x) {
-        double t = A[k * ld + j];
-        A[k * ld + j] = A[p * ld + j];
-        A[p * ld + j] = t;
-      }
-    __syncthreads();
-    const double akk = A[k * ld + k];
-    if (akk == 0.0) {
-      if (threadIdx.x == 0) status[sim] = 1;
-      return;
-    }
-    const int rows = n - k - 1, cols = n - k;  // update rows k+1.., cols k+1..n (incl. rhs)
-    for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
-      int i = k + 1 + idx / cols, j = k + 1 + idx % cols;
-      double l = A[i * ld + k] / akk;
-      A[i * ld + j] -= l * A[k * ld + j];
-    }
-    __syncthreads();
-  }
-  // back substitution (column-oriented)
-  for (int i = n - 1; i >= 0; --i) {
-    double xi = A[i * ld + n] / A[i * ld + i];
-    __syncthreads();
-    for (int j = threadIdx.x; j < i; j += blockDim.x) A[j * ld + n] -= A[j * ld + i] * xi;
-    if (threadIdx.x == 0) A[i * ld + n] = xi;
-    __syncthreads();
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double x = A[i * ld + n];
-    dr[(size_t)sim * n + i] = x;
-    if (apply) r[(size_t)sim * n + i] += x;
-  }
-  if (threadIdx.x == 0) status[sim] = 0;
-  (void)red_v; (void)red_i;
-}
-
-// r = base + t * dr ; predictor r = r_bar + dt rdot_bar ; rdot = (r - r_bar)/dt
-__global__ void k_axpy(double* __restrict__ out, const double* __restrict__ base, const double* __restrict__ d,
-                       double t, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = base[i] + t * d[i];
-}
-__global__ void k_rdot(const double* __restrict__ r, const double* __restrict__ rbar, double* __restrict__ rdot,
-                       double inv_dt, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) rdot[i] = (r[i] - rbar[i]) * inv_dt;
-}
-__global__ void k_mul(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] * b[i];
-}
-
-// Backward top of the decoder (vhp / vjp): y = [W_L | -U]^T a (split-K partials),
-// g = y[:w] + A_T^T y[w:]  (A_T = U^T W_L), then Delta = g * act'(z_{L-1}) in the
-// arithmetic of the passes (NS = 1 real, 2 dual/complex), cache layout (pass*NS + slot).
-template <int NS, int MC>
-__global__ void k_bwd_top(const double* __restrict__ part, int n_split, int w, int n_p, const double* __restrict__ AT,
-                          const double* __restrict__ zc, int ldz, int npass, double* __restrict__ Delta, int n_sims) {
-  extern __shared__ double g[];
-  const int sim = blockIdx.x;
-  const int M = w + n_p;
-  double* y = g + w;
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
-    double acc = 0.0;
-    for (int s = 0; s < n_split; ++s) acc += part[((size_t)s * n_sims + sim) * M + m];
-    y[m] = acc;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < w; i += blockDim.x) {
-    double acc = y[i];
-    for (int j = 0; j < n_p; ++j) acc = fma(AT[(size_t)j * w + i], y[w + j], acc);
-    g[i] = acc;
-  }
-  __syncthreads();
-  const double* Z = zc + (size_t)sim * npass * NS * ldz;
-  double* D = Delta + (size_t)sim * npass * NS * ldz;
-  for (int t = threadIdx.x; t < npass * w; t += blockDim.x) {
-    int i = t % w, p = t / w;
-    double z[NS], f[NS], s[NS];
-#pragma unroll
-    for (int q = 0; q < NS; ++q) z[q] = Z[(size_t)(p * NS + q) * ldz + i];
-    if (MC) mc_sincos<NS>(z, s, f);
-    else md_sincos<NS>(z, s, f);
-#pragma unroll
-    for (int q = 0; q < NS; ++q) D[(size_t)(p * NS + q) * ldz + i] = g[i] * f[q];
   }
 }
 

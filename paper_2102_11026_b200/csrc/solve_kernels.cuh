@@ -1,0 +1,475 @@
+// Assembly of the reduced Newton system, its reductions, the in-CTA LU solve and the
+// top of the vhp backward (rdsim.residual / system_jacobian / step).
+#pragma once
+#include "common.cuh"
+#include "mc_device.cuh"
+#include "gram_dmma.cuh"
+
+namespace nlrom {
+
+// -------------------------------------------------------------------- assembly
+// Per chunk of rows n (one CTA):
+//   a_n = M_n (J~_n . c) + [M_n hvv_n] + dt^2 (f_n - fext_n),  c = (1+alpha dt)(r - r_bar) - dt rdot_bar
+//   part[i][j] = sum_n J~_n[i] M_n R_n[j],  R_n = (1+alpha dt) J~_n + [0, dJ_n]      (n x n)
+//   partphi[i] = sum_n J~_n[i] a_n                                                   (n)
+// The n x n accumulation is register-blocked 4 x 4 per thread.
+struct AsmArgs {
+  const double* Jt; int ldjt;
+  const double* dJ; int lddj;
+  const double* mass;
+  const double* hvv;
+  const double* f;       // scattered cubature / exact force (n_sims, N)
+  const double* fext;    // (n_sims, N)
+  const double* r; const double* rbar; const double* rdbar;
+  double* a;             // (n_sims, N)
+  double* part;          // (n_sims, nchunk, n*n)
+  double* partphi;       // (n_sims, nchunk, n)
+  int N, n, n_p, n_q, rows_per_cta, nchunk;
+  double dt, alpha;
+  int drop_fict;
+};
+
+__global__ void k_assemble(AsmArgs A) {
+  pdl_wait();
+  pdl_launch();
+  extern __shared__ double sh[];
+  const int n = A.n;
+  const int RC = A.rows_per_cta;            // multiple of 4
+  const int ldp = gram_ld(n);
+  double* Js = sh;                          // [RC][ldp]  J~ rows
+  double* Rs = Js + (size_t)RC * ldp;       // [RC][ldp]  M R rows, column n = a
+  double* cs = Rs + (size_t)RC * ldp;       // [n]
+  double* ms = cs + n;                      // [RC] mass
+  double* fs = ms + RC;                     // [RC] row constant of a: dt^2 (f - fext) + M hvv
+  const int chunk = blockIdx.x, sim = blockIdx.y;
+  const double ah = A.alpha * A.dt;
+  const int row0 = chunk * RC;
+  const double* Jt = A.Jt + (size_t)sim * A.N * A.ldjt;
+  const double* dJ = A.dJ + (size_t)sim * A.N * A.lddj;
+  // stage J~ rows into Js and dJ rows into Rs[:, n_p:] (async copies: all loads in flight)
+  for (int idx = threadIdx.x; idx < RC * n; idx += blockDim.x) {
+    const int rl = idx / n, j = idx % n;
+    const int row = row0 + rl;
+    double* js = Js + rl * ldp + j;
+    double* rs = Rs + rl * ldp + j;
+    if (row < A.N) {
+      cp_async8(js, Jt + (size_t)row * A.ldjt + j);
+      if (j >= A.n_p) cp_async8(rs, dJ + (size_t)row * A.lddj + (j - A.n_p));
+    } else {
+      *js = 0.0;
+      *rs = 0.0;
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const size_t o = (size_t)sim * n + i;
+    cs[i] = (1.0 + ah) * (A.r[o] - A.rbar[o]) - A.dt * A.rdbar[o];
+  }
+  for (int rl = threadIdx.x; rl < RC; rl += blockDim.x) {
+    const int row = row0 + rl;
+    double m = 0.0, fc = 0.0;
+    if (row < A.N) {
+      const size_t o = (size_t)sim * A.N + row;
+      m = A.mass[row];
+      fc = A.dt * A.dt * (A.f[o] - A.fext[o]);
+      if (!A.drop_fict) fc += m * A.hvv[o];
+    }
+    ms[rl] = m;
+    fs[rl] = fc;
+  }
+  cp_async_all_wait();
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < RC * n; idx += blockDim.x) {
+    const int rl = idx / n, j = idx % n;
+    const double dj = (j >= A.n_p) ? Rs[rl * ldp + j] : 0.0;
+    Rs[rl * ldp + j] = ((1.0 + ah) * Js[rl * ldp + j] + dj) * ms[rl];
+  }
+  // a_n (one warp per row) into column n of Rs
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int rl = warp; rl < RC; rl += nw) {
+    const int row = row0 + rl;
+    double acc = 0.0;
+    for (int j = lane; j < n; j += 32) acc = fma(Js[rl * ldp + j], cs[j], acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      double av = 0.0;
+      if (row < A.N) {
+        av = ms[rl] * acc + fs[rl];
+        A.a[(size_t)sim * A.N + row] = av;
+      }
+      Rs[rl * ldp + n] = av;
+    }
+  }
+  __syncthreads();
+  // [J~^T M R | J~^T a] for the chunk on the DMMA pipe: n x (n + 1), split into part / partphi
+  double* P = A.part + ((size_t)sim * A.nchunk + chunk) * n * n;
+  double* Pp = A.partphi + ((size_t)sim * A.nchunk + chunk) * n;
+  gram_dmma(Js, ldp, Rs, ldp, RC, n, n, P, n);
+  gram_dmma(Js, ldp, Rs + n, ldp, RC, n, 1, Pp, 1);
+}
+
+// phi = sum_chunks partphi (one CTA per sim; 8 chunk groups per output, smem combine), ||phi||_2
+__global__ void k_reduce_phi(const double* __restrict__ partphi, int nchunk, int n, double* __restrict__ phi,
+                             double* __restrict__ norm) {
+  pdl_wait();
+  pdl_launch();
+  extern __shared__ double sh[];  // [8][n]
+  const int sim = blockIdx.x;
+  const int groups = blockDim.x / 32 > 0 ? 8 : 1;
+  for (int t = threadIdx.x; t < 8 * n; t += blockDim.x) {
+    int i = t % n, gidx = t / n;
+    double acc = 0.0;
+    for (int c = gidx; c < nchunk; c += 8) acc += partphi[((size_t)sim * nchunk + c) * n + i];
+    sh[gidx * n + i] = acc;
+  }
+  __syncthreads();
+  __shared__ double red[32];
+  double sq = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double acc = 0.0;
+#pragma unroll
+    for (int gidx = 0; gidx < 8; ++gidx) acc += sh[gidx * n + i];
+    phi[(size_t)sim * n + i] = acc;
+    sq += acc * acc;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    norm[sim] = sqrt(s);
+  }
+  (void)groups;
+}
+
+// S = sum part_A + dt^2 sum part_K + diag(0, vhp);  vhp[i][k] = G_t[2k+1][i].
+// grid (ceil(n*n/32), n_sims), block 256: 32 outputs x 8 partial groups.
+__global__ void k_reduce_S(const double* __restrict__ partA, int nchA, const double* __restrict__ partK, int nchK,
+                           const double* __restrict__ Gt, int ldg, int n, int n_p, int n_q, double dt,
+                           double* __restrict__ S) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double red[8][32];
+  const int sim = blockIdx.y;
+  const int lane = threadIdx.x & 31, gidx = threadIdx.x >> 5;
+  const int idx = blockIdx.x * 32 + lane;
+  const int nn = n * n;
+  double a = 0.0, k = 0.0;
+  if (idx < nn) {
+    for (int c = gidx; c < nchA; c += 8) a += partA[((size_t)sim * nchA + c) * nn + idx];
+    for (int c = gidx; c < nchK; c += 8) k += partK[((size_t)sim * nchK + c) * nn + idx];
+  }
+  red[gidx][lane] = a + dt * dt * k;
+  __syncthreads();
+  if (gidx == 0 && idx < nn) {
+    double acc = 0.0;
+#pragma unroll
+    for (int g2 = 0; g2 < 8; ++g2) acc += red[g2][lane];
+    const int i = idx / n, j = idx % n;
+    if (Gt && i >= n_p && j >= n_p) acc += Gt[((size_t)sim * 2 * n_q + 2 * (j - n_p) + 1) * ldg + (i - n_p)];
+    S[(size_t)sim * nn + idx] = acc;
+  }
+}
+
+// sum of cubature partials (cubature_integrate): f~ (n), K~ (n,n)
+__global__ void k_reduce_cub(const double* __restrict__ part_f, const double* __restrict__ part_K, int nch, int n,
+                             double* __restrict__ f_red, double* __restrict__ K_red) {
+  pdl_wait();
+  pdl_launch();
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * n + n; t += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (t < n * n) {
+      for (int c = 0; c < nch; ++c) acc += part_K[(size_t)c * n * n + t];
+      K_red[t] = acc;
+    } else {
+      int i = t - n * n;
+      for (int c = 0; c < nch; ++c) acc += part_f[(size_t)c * n + i];
+      f_red[i] = acc;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------- LU
+// One CTA (256 threads = 16 x 16) per sim: Gaussian elimination with partial pivoting
+// on [S | -phi]. The matrix lives in shared memory; thread (ty, tx)
+// owns the NB x NB elements (ty + 16a, tx + 16b), keeps them in registers and writes
+// them back after every update. Every warp finds the pivot itself (exact argmax of
+// |A[i][k]| over unused rows via integer warp reductions on the IEEE bits, lowest row
+// on ties), so a pivot step needs ONE barrier: within a step only unused rows and
+// columns > k are written while the pivot row and column k are read. Pivoting is
+// implicit (rows are marked used instead of swapped: same arithmetic as LU-pp).
+// Back substitution by warp 0 with shuffles. If `apply`, r += dr.
+// status[sim] = 1 on a zero pivot.
+template <int NB>
+__global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, const double* __restrict__ phi,
+                                                   double* __restrict__ dr, double* __restrict__ r, int n, int apply,
+                                                   int* __restrict__ status) {
+  pdl_wait();
+  pdl_launch();
+  constexpr int D = 16 * NB;           // covered rows / columns (n + 1 <= D)
+  constexpr int LDF = D + 1;
+  extern __shared__ double M[];        // [D][LDF]
+  __shared__ int pivrow[D];
+  __shared__ double rdiag[D];
+  const int sim = blockIdx.x;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31;
+  const double* Ss = S + (size_t)sim * n * n;
+  // stage [S | phi] into shared memory with async copies (one round trip for all elements)
+  for (int idx = tid; idx < D * D; idx += 256) {
+    const int i = idx / D, j = idx % D;
+    double* dst = M + i * LDF + j;
+    if (i < n && j < n) cp_async8(dst, Ss + (size_t)i * n + j);
+    else if (i < n && j == n) cp_async8(dst, phi + (size_t)sim * n + i);
+    else *dst = 0.0;
+  }
+  cp_async_all_wait();
+  __syncthreads();
+  double A[NB][NB];
+#pragma unroll
+  for (int a = 0; a < NB; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int i = ty + 16 * a, j = tx + 16 * b;
+      double v = M[i * LDF + j];
+      if (j == n) v = -v;  // rhs = -phi
+      A[a][b] = v;
+    }
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < NB; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (tx + 16 * b == n) M[(ty + 16 * a) * LDF + n] = A[a][b];
+  // rows >= n are never pivots
+  unsigned long long used_lo = 0ull, used_hi = 0ull;  // rows 0..63, 64..127
+  for (int i = n; i < D; ++i) {
+    if (i < 64) used_lo |= 1ull << i;
+    else used_hi |= 1ull << (i - 64);
+  }
+  auto is_used = [&](int i) -> bool {
+    return i < 64 ? ((used_lo >> i) & 1ull) : ((used_hi >> (i - 64)) & 1ull);
+  };
+  bool bad = false;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    // every warp: argmax over the column (rows lane + 32u)
+    double best = -1.0;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int u = 0; u < D / 32; ++u) {
+      const int i = lane + 32 * u;
+      if (!is_used(i)) {
+        const double v = fabs(M[i * LDF + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+    }
+    const unsigned long long key = (best >= 0.0) ? (unsigned long long)__double_as_longlong(best) : 0ull;
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    const int piv = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)bi : 0x7fffffffu);
+    if (!(mhi | mlo) || piv >= n) { bad = true; break; }
+    if (piv < 64) used_lo |= 1ull << piv;
+    else used_hi |= 1ull << (piv - 64);
+    const double rp = 1.0 / M[piv * LDF + k];
+    if (tid == 0) {
+      pivrow[k] = piv;
+      rdiag[k] = rp;
+    }
+    // all operands are loaded before any store: the pivot row and column k are never
+    // written in this step, but the compiler cannot prove it (would serialise LDS/STS)
+    const double* prow = M + piv * LDF;
+    double pr[NB], l[NB];
+    bool act[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) pr[b] = prow[tx + 16 * b];
+#pragma unroll
+    for (int a = 0; a < NB; ++a) {
+      const int i = ty + 16 * a;
+      act[a] = !is_used(i);
+      l[a] = M[i * LDF + k];
+    }
+#pragma unroll
+    for (int a = 0; a < NB; ++a) {
+      const int i = ty + 16 * a;
+      const double la = l[a] * rp;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int j = tx + 16 * b;
+        if (act[a] && j > k) {
+          A[a][b] = fma(-la, pr[b], A[a][b]);
+          M[i * LDF + j] = A[a][b];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) status[sim] = 1;
+    return;
+  }
+  if (tid < 32) {
+    constexpr int NU = (D + 31) / 32;
+    double bv[NU];
+    const double* rowp[NU];  // physical U rows of this lane's unknowns, resolved once
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int t = lane + 32 * u;
+      rowp[u] = M + (t < n ? pivrow[t] : 0) * LDF;
+      bv[u] = (t < n) ? rowp[u][n] : 0.0;
+    }
+#pragma unroll 4
+    for (int t = n - 1; t >= 0; --t) {
+      const int owner = t & 31, slot = t >> 5;
+      const double rd = rdiag[t];
+      double uc[NU];
+#pragma unroll
+      for (int u = 0; u < NU; ++u) uc[u] = rowp[u][t];  // independent of the x chain
+      double bt = 0.0;
+#pragma unroll
+      for (int u = 0; u < NU; ++u)
+        if (u == slot) bt = bv[u];
+      bt = __shfl_sync(0xffffffffu, bt, owner);
+      const double xt = bt * rd;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        const int tt = lane + 32 * u;
+        if (tt < t) bv[u] = fma(-uc[u], xt, bv[u]);
+        else if (tt == t) bv[u] = xt;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int t = lane + 32 * u;
+      if (t < n) {
+        dr[(size_t)sim * n + t] = bv[u];
+        if (apply) r[(size_t)sim * n + t] += bv[u];
+      }
+    }
+    if (lane == 0) status[sim] = 0;
+  }
+}
+
+inline size_t lu_smem_bytes(int n) {
+  const int D = (n + 1 <= 64) ? 64 : 128;
+  return (size_t)D * (D + 1) * 8;
+}
+
+// r = base + t * dr ; rdot = (r - r_bar)/dt ; elementwise product
+__global__ void k_axpy(double* __restrict__ out, const double* __restrict__ base, const double* __restrict__ d,
+                       double t, int n) {
+  pdl_wait();
+  pdl_launch();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = base[i] + t * d[i];
+}
+__global__ void k_rdot(const double* __restrict__ r, const double* __restrict__ rbar, double* __restrict__ rdot,
+                       double inv_dt, int n) {
+  pdl_wait();
+  pdl_launch();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) rdot[i] = (r[i] - rbar[i]) * inv_dt;
+}
+__global__ void k_mul(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out, int n) {
+  pdl_wait();
+  pdl_launch();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] * b[i];
+}
+
+// ------------------------------------------------------------------ vhp backward top
+// y = [W_L | -U]^T a read through the row-major [W_L | -U] (N x ldA) that the forward
+// just streamed (L2-hot): partial sums over row chunks, threads over the M = w + n_p columns.
+__global__ void k_gemv_t(const double* __restrict__ A, int ldA, int M, const double* __restrict__ x, int N,
+                         int rows_per_cta, double* __restrict__ part, int nchunk) {
+  pdl_wait();
+  pdl_launch();
+  const int chunk = blockIdx.x, sim = blockIdx.y;
+  const int r0 = chunk * rows_per_cta, r1 = min(N, r0 + rows_per_cta);
+  const double* xs = x + (size_t)sim * N;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+  for (int n = r0; n < r1; ++n) {
+    const double xv = xs[n];
+    const double* Ar = A + (size_t)n * ldA;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int m = threadIdx.x + u * blockDim.x;
+      if (m < M) acc[u] = fma(Ar[m], xv, acc[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    int m = threadIdx.x + u * blockDim.x;
+    if (m < M) part[((size_t)sim * nchunk + chunk) * M + m] = acc[u];
+  }
+}
+
+// y = sum_chunks part  (grid (ceil(M/32), n_sims), block 256 = 32 outputs x 8 chunk groups)
+__global__ void k_reduce_cols(const double* __restrict__ part, int nchunk, int M, double* __restrict__ y) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double red[8][32];
+  const int sim = blockIdx.y;
+  const int lane = threadIdx.x & 31, gidx = threadIdx.x >> 5;
+  const int m = blockIdx.x * 32 + lane;
+  double acc = 0.0;
+  if (m < M)
+    for (int c = gidx; c < nchunk; c += 8) acc += part[((size_t)sim * nchunk + c) * M + m];
+  red[gidx][lane] = acc;
+  __syncthreads();
+  if (gidx == 0 && m < M) {
+    double s = 0.0;
+#pragma unroll
+    for (int g2 = 0; g2 < 8; ++g2) s += red[g2][lane];
+    y[(size_t)sim * M + m] = s;
+  }
+}
+
+// g = y[:w] + A_T^T y[w:]  (A_T = U^T W_L: the filter's adjoint folded into the last layer),
+// Delta[p*NS + s][i] = (g_i * act'(z_{L-1}))[s] in the arithmetic of the passes
+// (NS = 1 real; 2 dual (MC = 0) or complex (MC = 1)). grid (ceil(w/32), n_sims), block 256.
+template <int NS, int MC>
+__global__ void k_bwd_delta(const double* __restrict__ y, int w, int n_p, const double* __restrict__ AT,
+                            const double* __restrict__ zc, int ldz, int npass, double* __restrict__ Delta) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double g[32];
+  const int sim = blockIdx.y;
+  const int i0 = blockIdx.x * 32;
+  const int M = w + n_p;
+  const double* ys = y + (size_t)sim * M;
+  {
+    // 8 warps x 32 columns: warp w8 sums j = w8, w8+8, ... (loads independent, all in flight)
+    __shared__ double gp[8][32];
+    const int il = threadIdx.x & 31, w8 = threadIdx.x >> 5;
+    const int i = i0 + il;
+    double acc = 0.0;
+    if (i < w)
+      for (int j = w8; j < n_p; j += 8) acc = fma(AT[(size_t)j * w + i], ys[w + j], acc);
+    gp[w8][il] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double s = (i < w) ? ys[i] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += gp[q][il];
+      g[il] = s;
+    }
+  }
+  __syncthreads();
+  const double* Z = zc + (size_t)sim * npass * NS * ldz;
+  double* D = Delta + (size_t)sim * npass * NS * ldz;
+  for (int t = threadIdx.x; t < npass * 32; t += blockDim.x) {
+    const int il = t & 31, p = t >> 5;
+    const int i = i0 + il;
+    if (i >= w) continue;
+    double z[NS], f[NS], s[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) z[q] = Z[(size_t)(p * NS + q) * ldz + i];
+    if (MC) mc_sincos<NS>(z, s, f);
+    else md_sincos<NS>(z, s, f);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) D[(size_t)(p * NS + q) * ldz + i] = g[il] * f[q];
+  }
+}
+
+}  // namespace nlrom

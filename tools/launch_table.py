@@ -1,0 +1,35 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum launch list: one Newton iteration
+(from k_seed_jet to k_lu_solve) of the captured graph, per-kernel device time."""
+import csv
+import io
+import sys
+
+
+def load(path):
+    txt = open(path).read()
+    rows = list(csv.DictReader(io.StringIO(txt[txt.index('"ID"'):])))
+    seq = []
+    for r in rows:
+        n = r["Kernel Name"]
+        short = n.split("(")[0].replace("nlrom::", "").replace("void ", "")
+        for tag in ["EpiJetOut", "EpiJet", "EpiBwdAct", "EpiStore", "EpiAct"]:
+            if tag in n:
+                short = "gemm<" + tag + ">"
+                break
+        seq.append((short, float(r["Metric Value"]) / 1000, r["Grid Size"], r["Block Size"]))
+    return seq
+
+
+def iteration(seq, which=-2):
+    idx = [i for i, s in enumerate(seq) if s[0].endswith("k_seed_jet")]
+    i0 = idx[which]
+    i1 = [i for i in range(i0, len(seq)) if "k_lu_solve" in seq[i][0]][0]
+    return seq[i0:i1 + 1]
+
+
+if __name__ == "__main__":
+    it = iteration(load(sys.argv[1]))
+    tot = sum(s[1] for s in it)
+    for s in it:
+        print(f"{s[0]:26s} {s[1]:8.2f} us {100 * s[1] / tot:5.1f}%  grid {s[2]:14s} block {s[3]}")
+    print(f"total {tot:.1f} us over {len(it)} kernels (ncu: serialised, cold caches)")
