@@ -17,6 +17,7 @@
 #include "epilogues.cuh"
 #include "sim_kernels.cuh"
 #include "solve_kernels.cuh"
+#include "mlp_chain.cuh"
 
 namespace nlrom {
 void fc_forward(int order, int act, const GemmArgs& g, double* Y, int ldy, const double* bias, double* cache,
@@ -48,7 +49,8 @@ int gemm_launch_count = 0;
 
 struct nlrom_ctx {
   int device = 0;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr, st2 = nullptr;
+  cudaEvent_t evFork = nullptr, evJoin = nullptr;
   std::string err;
   double last_norm = 0.0;
   int N = 0, n_p = 0, n_q = 0, n = 0, L = 0, n_sims = 1, T = 0, V = 0;
@@ -57,7 +59,7 @@ struct nlrom_ctx {
   std::vector<DBuf> W, WT, b;
   std::vector<int> ldW, ldWT;
   DBuf Alast, AT, Pb, U, mass;
-  int ldlast = 0, wL1 = 0;
+  int ldlast = 0, wL1 = 0, next = 0;  // next: K-extension of the output layer (0: filter folded)
   // mesh
   IBuf elem_rows;
   DBuf Dm_inv, vol;
@@ -196,14 +198,77 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
 using CfgOutC = GemmCfg<48, 128, 2, 4, 1, 32, 3>;
 
 void output_layer(nlrom_ctx* c) {
-  GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->n_p, 0, 0};
+  GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->next, 0, 0};
   EpiJetOutC e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
                c->n_p, c->n_q};
   launch_gemm<CfgOutC>(g, e, c->st);
   ++gemm_launch_count;
 }
 
+// Fused hidden chain (mlp_chain.cuh): one cluster of CS CTAs per column group.
+template <int R, int G, int CS>
+bool launch_mlp_fwd(nlrom_ctx* c, const MlpFwdArgs& a) {
+  using P = MlpPlan<R, G>;
+  const size_t smem = P::bytes(std::max(c->wL1, c->n_q));
+  if (smem > 227 * 1024) return false;
+  static bool configured = false;
+  if (!configured) {
+    NL_CUDA(cudaFuncSetAttribute(k_mlp_jet_fwd<R, G, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (CS > 8) NL_CUDA(cudaFuncSetAttribute(k_mlp_jet_fwd<R, G, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, c->n_sims * c->gps, 1);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  NL_CUDA(cudaLaunchKernelEx(&cfg, k_mlp_jet_fwd<R, G, CS>, a));
+  ++gemm_launch_count;
+  return true;
+}
+
+bool fused_hidden_forward(nlrom_ctx* c, double dt, int drop_fict) {
+  if (getenv("NLROM_NO_FUSED_MLP")) return false;
+  const int L1 = c->L - 1, w = c->wL1;
+  if (L1 < 1 || L1 > MLP_MAXL) return false;
+  for (int l = 1; l <= L1; ++l)
+    if (c->widths[l] != w) return false;
+  MlpFwdArgs a{};
+  a.r = c->r.p; a.rbar = c->rbar.p; a.rdbar = c->rdbar.p;
+  a.n_p = c->n_p; a.n_q = c->n_q; a.n = c->n; a.dt = dt; a.alpha = c->alpha; a.drop_fict = drop_fict;
+  a.L1 = L1; a.w = w;
+  for (int l = 0; l < L1; ++l) {
+    a.W[l] = c->W[l].p; a.b[l] = c->b[l].p; a.ldW[l] = c->ldW[l]; a.in[l] = c->widths[l];
+    a.cache[l] = c->cache[l].p;
+  }
+  a.ldc = c->ldc[0];
+  a.Hout = c->H[L1 - 1].p;
+  a.ldH = c->ldH[L1 - 1];
+  a.G = c->G; a.gps = c->gps;
+  const int G = c->G;
+  if (w == 256 && G == 16) return launch_mlp_fwd<32, 16, 8>(c, a);
+  if (w == 256 && G == 24) return launch_mlp_fwd<32, 24, 8>(c, a);
+  if (w == 64 && G == 24) return launch_mlp_fwd<8, 24, 8>(c, a);
+  if (w == 64 && G == 16) return launch_mlp_fwd<8, 16, 8>(c, a);
+  if (w == 40 && G == 24) return launch_mlp_fwd<8, 24, 5>(c, a);
+  if (w == 8 && G == 16) return launch_mlp_fwd<8, 16, 1>(c, a);
+  return false;
+}
+
 void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
+  if (fused_hidden_forward(c, dt, drop_fict)) {
+    output_layer(c);
+    return;
+  }
   const int ncols = c->n_sims * c->Cb;
   const int nq = c->n_q;
   launch(c, k_seed_jet, grid1((long long)ncols * nq), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p,
@@ -220,8 +285,7 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
     in = c->H[l].p;
     ldin = c->ldH[l];
   }
-  // T = (U^T W_L) h  -> columns wL1.. of the last hidden buffer (filter fused as K-extension)
-  {
+  if (c->next) {  // T = (U^T W_L) h -> columns wL1.. of the last hidden buffer (filter as K-extension)
     GemmArgs g{c->AT.p, in, round_up(c->wL1, 2), ldin, c->n_p, c->n_sims * c->Cc, c->wL1, 0, 0};
     EpiStore e{c->H[c->L - 2].p + c->wL1, c->ldlast, 0, nullptr, 1, nullptr};
     hid_gemm(c->G, g, e, c->st);
@@ -232,9 +296,8 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
 void wnet_phase(nlrom_ctx* c) {
   launch(c, k_gemv_splitk, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
          (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
-  const int groups = std::max(1, 256 / c->wn);
-  launch(c, k_wnet_tail, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256,
-         (size_t)((2 + groups) * c->wn + 2 * c->wn * c->wn + 64 * c->wn) * 8, (const double*)c->wpart.p, c->wsplit, c->wn,
+  const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + c->wsplit * c->wn) * 8;
+  launch(c, k_wnet_tail, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm, (const double*)c->wpart.p, c->wsplit, c->wn,
          (const double*)c->b1.p, (const double*)c->W2.p, (const double*)c->b2.p, (const double*)c->W3.p,
          (const double*)c->b3.p, (const double*)c->W4C.p, (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
 }
@@ -249,12 +312,28 @@ void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted) {
          c->n_sims);
 }
 
-void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
+void assemble_launch(nlrom_ctx* c, CubSet& s, double dt, int drop_fict, int mode) {
   AsmArgs A{c->Jt.p, c->ldjt, c->dJ.p, c->lddj, c->mass.p, c->hvv.p, s.f.p, c->fext.p, c->r.p, c->rbar.p,
             c->rdbar.p, c->a.p, c->partA.p, c->partPhi.p, c->N, c->n, c->n_p, c->n_q, c->rpc, c->nchA, dt,
-            c->alpha, drop_fict};
+            c->alpha, drop_fict, mode};
   size_t smem = (size_t)(2 * c->rpc * gram_ld(c->n) + 2 * c->rpc + c->n) * 8;
   launch(c, k_assemble, dim3(c->nchA, c->n_sims), 256, smem, A);
+}
+
+// The mass block J~^T M [(1+alpha dt)U, (1+alpha dt)J + dJ] depends only on the decoder bundle:
+// it runs on a side stream (a parallel graph branch) while the weight net, the cubature and
+// the a-vector -- the critical path -- run on the main stream.
+void mass_block_fork(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
+  NL_CUDA(cudaEventRecord(c->evFork, c->st));
+  NL_CUDA(cudaStreamWaitEvent(c->st2, c->evFork, 0));
+  std::swap(c->st, c->st2);
+  assemble_launch(c, s, dt, drop_fict, 1);
+  std::swap(c->st, c->st2);
+  NL_CUDA(cudaEventRecord(c->evJoin, c->st2));
+}
+
+void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
+  assemble_launch(c, s, dt, drop_fict, 2);
   launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nchA, c->n,
          c->phi.p, c->norm.p);
 }
@@ -262,16 +341,18 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg) {
   bundle_forward(c, cfg.dt, cfg.drop_fict);
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
+  mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
   if (cfg.integration == 0) wnet_phase(c);
   cubature_phase(c, s, cfg.integration == 0);
   assemble_phase(c, s, cfg.dt, cfg.drop_fict);
+  NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin, 0));  // join the mass-block branch
 }
 
 // vhp backward: dual (NS = 2) passes, cache written by the bundle forward.
 void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int npass_per_sim, std::vector<DBuf>& caches,
                       std::vector<int>& ldcs, DBuf& D0, DBuf& D1, DBuf& Gout, int ldG) {
   const int ncols = c->n_sims * npass_per_sim * NS;
-  const int M = c->wL1 + c->n_p;
+  const int M = c->wL1 + c->next;
   launch(c, k_gemv_t, dim3(c->bnch, c->n_sims), 128, 0, (const double*)c->Alast.p, c->ldlast, M, a_vec, c->N,
          c->brows, c->bpart.p, c->bnch);
   launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->bpart.p, c->bnch, M,
@@ -280,13 +361,13 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
   dim3 gd(ceil_div(c->wL1, 32), c->n_sims);
   if (NS == 2) {
     if (mc)
-      launch(c, k_bwd_delta<2, 1>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->n_p, (const double*)c->AT.p,
+      launch(c, k_bwd_delta<2, 1>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->next, (const double*)c->AT.p,
              (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
     else
-      launch(c, k_bwd_delta<2, 0>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->n_p, (const double*)c->AT.p,
+      launch(c, k_bwd_delta<2, 0>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->next, (const double*)c->AT.p,
              (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
   } else {
-    launch(c, k_bwd_delta<1, 1>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->n_p, (const double*)c->AT.p,
+    launch(c, k_bwd_delta<1, 1>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->next, (const double*)c->AT.p,
            (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
   }
   DBuf* cur = &D0;
@@ -410,6 +491,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c = new nlrom_ctx();
     c->device = device;
     NL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    NL_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreate(&c->ev0));
     NL_CUDA(cudaEventCreate(&c->ev1));
     c->n_sims = d->n_sims > 0 ? d->n_sims : 1;
@@ -432,19 +516,15 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       upload_matrix(c->WT[l], wt.data(), in, o, c->ldWT[l]);
       upload(c->b[l], d->b[l], o);
     }
-    // last layer fused with the filter: D = [W_L | -U] [h ; U^T W_L h] + P b_L
+    // last layer fused with the filter: D = P (W_L h + b_L) = (P W_L) h + P b_L with
+    // P = I - U U^T folded into the weights once at upload (no filter GEMM per iteration).
     const double* WL = d->W[L - 1];
     const double* bL = d->b[L - 1];
     const int w = c->wL1;
-    c->ldlast = round_up(w + n_p, 2);
+    c->next = 0;
+    c->ldlast = round_up(w, 2);
     {
-      std::vector<double> A((size_t)N * (w + n_p));
-      for (int r = 0; r < N; ++r) {
-        for (int k = 0; k < w; ++k) A[(size_t)r * (w + n_p) + k] = WL[(size_t)r * w + k];
-        for (int j = 0; j < n_p; ++j) A[(size_t)r * (w + n_p) + w + j] = -d->U[(size_t)r * n_p + j];
-      }
-      upload_matrix(c->Alast, A.data(), N, w + n_p, c->ldlast);
-      std::vector<double> ATh((size_t)n_p * w, 0.0), Utb(n_p, 0.0), Pbh(N);
+      std::vector<double> ATh((size_t)n_p * w, 0.0), Utb(n_p, 0.0), Pbh(N), A((size_t)N * w);
       for (int r = 0; r < N; ++r)
         for (int j = 0; j < n_p; ++j) {
           const double ur = d->U[(size_t)r * n_p + j];
@@ -455,7 +535,13 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         double s = bL[r];
         for (int j = 0; j < n_p; ++j) s -= d->U[(size_t)r * n_p + j] * Utb[j];
         Pbh[r] = s;
+        for (int k = 0; k < w; ++k) {
+          double a = WL[(size_t)r * w + k];
+          for (int j = 0; j < n_p; ++j) a -= d->U[(size_t)r * n_p + j] * ATh[(size_t)j * w + k];
+          A[(size_t)r * w + k] = a;
+        }
       }
+      upload_matrix(c->Alast, A.data(), N, w, c->ldlast);
       upload_matrix(c->AT, ATh.data(), n_p, w, round_up(w, 2));
       upload(c->Pb, Pbh.data(), N);
       upload(c->U, d->U, (size_t)N * n_p);
@@ -587,6 +673,9 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->st) cudaStreamDestroy(c->st);
+  if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->evFork) cudaEventDestroy(c->evFork);
+  if (c->evJoin) cudaEventDestroy(c->evJoin);
   delete c;
 }
 
@@ -644,11 +733,13 @@ extern "C" int nlrom_diffop(nlrom_ctx* c, int op, const double* q, const double*
     ldin = ldo;
   }
   if (!bwd) {
-    GemmArgs gT{c->AT.p, in, round_up(c->wL1, 2), ldin, c->n_p, ncols, c->wL1, 0, 0};
-    fc_forward(0, ACT_NONE, gT, Hs[L - 2].p + c->wL1, c->ldlast, nullptr, nullptr, c->st);
+    if (c->next) {
+      GemmArgs gT{c->AT.p, in, round_up(c->wL1, 2), ldin, c->n_p, ncols, c->wL1, 0, 0};
+      fc_forward(0, ACT_NONE, gT, Hs[L - 2].p + c->wL1, c->ldlast, nullptr, nullptr, c->st);
+    }
     const int ldy = round_up(N, 2);
     DBuf Y((size_t)ncols * ldy);
-    GemmArgs g{c->Alast.p, in, c->ldlast, ldin, N, ncols, c->wL1 + c->n_p, 0, 0};
+    GemmArgs g{c->Alast.p, in, c->ldlast, ldin, N, ncols, c->wL1 + c->next, 0, 0};
     // linear output layer: bias P b on the real slot of every pass (period S)
     launch_gemm<GemmCfg<64, 64, 2, 2, 1>>(g, EpiStore{Y.p, ldy, 0, c->Pb.p, S, nullptr}, c->st);
     int slot = (op == NLROM_OP_VALUE) ? 0 : (op == NLROM_OP_JVP || op == NLROM_OP_JACOBIAN) ? 1

@@ -1,0 +1,211 @@
+// Fused hidden-layer chain of the decoder bundle on thread-block clusters.
+//
+// The per-layer GEMMs of the hidden chain are tiny (w x w x 16 columns per group,
+// ~21 MFLOP per layer at cfg2) and latency-bound as separate kernels. Here one
+// cluster of CS CTAs carries one column group [base jet | nk tangents] through ALL
+// hidden layers: CTA `rank` owns output rows [rank*R, rank*R + R) of every layer
+// (R = w / CS), computes them on the fp64 tensor pipe (DMMA) from the full
+// activation of the previous layer held in its shared memory, applies the jet-sin
+// epilogue, and broadcasts its slice into every CTA of the cluster through
+// distributed shared memory; one cluster barrier per layer. The next layer's weight
+// slice is prefetched with cp.async while the current layer computes.
+// Columns of different groups are independent across layers (every group carries
+// its own copy of the base jet), so clusters never talk to each other.
+#pragma once
+#include <cooperative_groups.h>
+#include "common.cuh"
+#include "gemm_f64.cuh"
+#include "mc_device.cuh"
+
+namespace nlrom {
+
+constexpr int MLP_MAXL = 16;
+
+struct MlpFwdArgs {
+  // seed of the jet (same as k_seed_jet)
+  const double* r;
+  const double* rbar;
+  const double* rdbar;
+  int n_p, n_q, n;
+  double dt, alpha;
+  int drop_fict;
+  // hidden layers l = 0 .. L1-1: W[l] (w x in[l]) row-major with ld ldW[l]; out dim w
+  int L1, w;
+  const double* W[MLP_MAXL];
+  const double* b[MLP_MAXL];
+  int ldW[MLP_MAXL];
+  int in[MLP_MAXL];
+  // outputs
+  double* cache[MLP_MAXL];  // vhp caches: (n_sims * 2 n_q) x ldc per layer
+  int ldc;
+  double* Hout;  // compact activation of the last hidden layer: (n_sims * (4 + 4 n_q)) x ldH
+  int ldH;
+  int G, gps;
+};
+
+// shared-memory plan (doubles): X[2][KP][LDX] | Wb[2][R][LDWS] | Bb[2][R] | Ys[G][R+1] | Os[R][LDX]
+// (KP = KMAX rounded up to 16; padding rows / columns are zero)
+template <int R, int G>
+struct MlpPlan {
+  static constexpr int LDX = ((G + 7) / 8) * 8 + 4;  // == 4 or 12 (mod 16): conflict-free fragments
+  static __host__ __device__ int kp(int kmax) { return (kmax + 15) & ~15; }
+  static __host__ __device__ int ldws(int kmax) { return kp(kmax) + 4; }
+  static __host__ __device__ size_t bytes(int kmax) {
+    return (size_t)(2 * kp(kmax) * LDX + 2 * R * ldws(kmax) + 2 * R + G * (R + 1) + R * LDX) * 8;
+  }
+};
+
+// weight slice (R rows, K columns; the device weights are zero-padded to an even ld) + bias slice
+template <int R>
+__device__ __forceinline__ void mlp_load_w(double* Wb, double* Bb, int ldws, const double* W, int ldW,
+                                           const double* b, int r0, int K, int tid, int nt) {
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  const int Kp = (K + 15) & ~15;  // columns [K, Kp) are zero-filled (cp.async src-size 0)
+  for (int rr = warp; rr < R; rr += nw)
+    for (int k = 2 * lane; k < Kp; k += 64) {
+      const bool ok = k < K;  // K even or the device weights are zero-padded to an even ld
+      cp_async16(Wb + rr * ldws + k, ok ? W + (size_t)(r0 + rr) * ldW + k : W, ok);
+    }
+  for (int i = tid; i < R; i += nt) cp_async8(Bb + i, b + r0 + i);
+}
+
+template <int R, int G, int CS>
+__global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  using P = MlpPlan<R, G>;
+  extern __shared__ __align__(16) double sm[];
+  const int kmax = P::kp(max(a.w, a.n_q));
+  const int LDX = P::LDX;
+  const int LDWS = P::ldws(kmax);
+  constexpr int NTH = 256;
+  // buffers addressed arithmetically (a pointer array indexed by l & 1 would live in local memory)
+  auto Xb = [&](int i) { return sm + i * kmax * LDX; };
+  auto Wbuf = [&](int i) { return sm + 2 * kmax * LDX + i * R * LDWS; };
+  auto Bbuf = [&](int i) { return sm + 2 * kmax * LDX + 2 * R * LDWS + i * R; };
+  double* Ys = sm + 2 * kmax * LDX + 2 * R * LDWS + 2 * R;  // [G][R+1]
+  double* Os = Ys + G * (R + 1);                               // [R][LDX] outgoing slice
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)cluster.block_rank();
+  const int r0 = rank * R;
+  const int gg = blockIdx.y;                 // global group = sim * gps + gl
+  const int sim = gg / a.gps, gl = gg % a.gps;
+  const int nk = (G - 4) / 4;
+  const int cs = 4 + 4 * a.n_q;
+
+  // layer-0 weights do not depend on the producer: prefetch before the dependency wait
+  mlp_load_w<R>(Wbuf(0), Bbuf(0), LDWS, a.W[0], a.ldW[0], a.b[0], r0, a.in[0], tid, NTH);
+  cp_async_commit();
+  pdl_wait();
+  pdl_launch();
+  // seed of this group: X[0][i][c], i < n_q; rows n_q .. kmax of both X buffers are zero
+  for (int t = tid; t < (kmax - a.n_q) * LDX; t += NTH) {
+    Xb(0)[a.n_q * LDX + t] = 0.0;
+    Xb(1)[a.n_q * LDX + t] = 0.0;
+  }
+  for (int t = tid; t < a.n_q * G; t += NTH) {
+    const int i = t / G, cl = t % G;
+    const double* rs = a.r + (size_t)sim * a.n;
+    const double q = rs[a.n_p + i];
+    const double v = q - a.rbar[(size_t)sim * a.n + a.n_p + i];
+    const double qdb = a.rdbar[(size_t)sim * a.n + a.n_p + i];
+    double val = 0.0;
+    if (cl < 4) {
+      if (cl == 0) val = q;
+      else if (cl == 1) val = a.drop_fict ? 0.0 : v;
+      else if (cl == 3) val = (a.drop_fict ? (1.0 + a.alpha * a.dt) : (3.0 + a.alpha * a.dt)) * v - a.dt * qdb;
+    } else {
+      const int k = (cl - 4) >> 2, s = (cl - 4) & 3;
+      if (s == 0 && gl * nk + k == i) val = 1.0;
+    }
+    Xb(0)[i * LDX + cl] = val;
+  }
+  for (int l = 0; l < a.L1; ++l) {
+    const int K = a.in[l];
+    double* Xc = Xb(l & 1);
+    double* Xn = Xb((l + 1) & 1);
+    if (l + 1 < a.L1)
+      mlp_load_w<R>(Wbuf((l + 1) & 1), Bbuf((l + 1) & 1), LDWS, a.W[l + 1], a.ldW[l + 1], a.b[l + 1], r0, a.in[l + 1],
+                    tid, NTH);
+    cp_async_commit();
+    cp_async_wait<1>();  // this layer's weights have landed
+    __syncthreads();
+    // DMMA: warp -> 8x8 tiles of the R x G slice, 4 interleaved K chains; K padded to 16 with zeros
+    const double* Ws = Wbuf(l & 1);
+    constexpr int TM = R / 8, TN = G / 8, NT = TM * TN;
+    const int Kp = (K + 15) & ~15;
+    for (int tile = warp; tile < NT; tile += NTH / 32) {
+      const int tm = tile % TM, tn = tile / TM;
+      double c[4][2] = {};
+      const double* wrow = Ws + (tm * 8 + (lane >> 2)) * LDWS + (lane & 3);
+      const double* xcol = Xc + (lane & 3) * LDX + tn * 8 + (lane >> 2);
+      for (int k0 = 0; k0 < Kp; k0 += 16) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], wrow[k0 + 4 * u], xcol[(k0 + 4 * u) * LDX]);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = tm * 8 + (lane >> 2), col = tn * 8 + 2 * (lane & 3) + e;
+        Ys[col * (R + 1) + row] = (c[0][e] + c[1][e]) + (c[2][e] + c[3][e]);
+      }
+    }
+    __syncthreads();
+    // jet-sin epilogue on the R rows; broadcast the activated slice to every CTA of the cluster
+    const bool last = (l + 1 == a.L1);
+    for (int t = tid; t < R * (1 + nk); t += NTH) {
+      const int rr = t % R, unit = t / R;  // unit 0: base jet, unit 1 + k: tangent k
+      const int m = r0 + rr;
+      double z[4], o[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) z[s] = Ys[s * (R + 1) + rr];
+      z[0] += Bbuf(l & 1)[rr];
+      JetCos jc;
+      jet_sin_base(z, o, jc);
+      int col = 0;
+      int kg = -1;
+      if (unit > 0) {
+        const int k = unit - 1;
+        kg = gl * nk + k;
+        double y[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) y[s] = Ys[(4 + 4 * k + s) * (R + 1) + rr];
+        if (kg < a.n_q) {
+          double* Cz = a.cache[l] + (size_t)sim * 2 * a.n_q * a.ldc;
+          Cz[(size_t)(2 * kg) * a.ldc + m] = z[0];
+          Cz[(size_t)(2 * kg + 1) * a.ldc + m] = y[0];
+        }
+        jet_tangent(jc, y, o);
+        col = 4 + 4 * k;
+      }
+      if (last) {
+        // compact layout for the linear output layer: base once per sim, tangents by index
+        if (unit == 0 && gl == 0) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s) a.Hout[(size_t)(sim * cs + s) * a.ldH + m] = o[s];
+        } else if (unit > 0 && kg < a.n_q) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s) a.Hout[(size_t)(sim * cs + 4 + 4 * kg + s) * a.ldH + m] = o[s];
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) Os[rr * LDX + col + s] = o[s];
+      }
+    }
+    if (!last) {
+      // broadcast the R x G slice to every CTA of the cluster: warp -> destination CTA,
+      // 16-byte distributed-shared-memory stores of whole rows
+      __syncthreads();
+      constexpr int C2 = G / 2;  // 16-byte chunks per row
+      for (int dst = warp; dst < CS; dst += NTH / 32) {
+        double* Xr = cluster.map_shared_rank(Xn, dst);
+        for (int t = lane; t < R * C2; t += 32) {
+          const int rr = t / C2, c2 = (t % C2) * 2;
+          *reinterpret_cast<double2*>(Xr + (r0 + rr) * LDX + c2) = *reinterpret_cast<const double2*>(Os + rr * LDX + c2);
+        }
+      }
+    }
+    cluster.sync();  // next activation complete in every CTA; Xc, Ys and Os free for reuse
+  }
+}
+
+}  // namespace nlrom

@@ -126,6 +126,8 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// hout = sin(W hin + b): warp-per-row dot products into hout, then one thread per row
+// evaluates the (long, fp64) sin so the sins run in parallel, not one per warp in sequence.
 __device__ void wnet_dense_sin(const double* __restrict__ W, const double* __restrict__ b, const double* hin,
                                double* hout, int wn) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -133,59 +135,67 @@ __device__ void wnet_dense_sin(const double* __restrict__ W, const double* __res
     double acc = 0.0;
     for (int k = lane; k < wn; k += 32) acc = fma(W[(size_t)m * wn + k], hin[k], acc);
     acc = warp_sum(acc);
-    if (lane == 0) hout[m] = sin(acc + b[m]);
+    if (lane == 0) hout[m] = acc + b[m];
   }
+  __syncthreads();
+  for (int m = threadIdx.x; m < wn; m += blockDim.x) hout[m] = sin(hout[m]);
 }
 
 __global__ void k_wnet_tail(const double* __restrict__ part, int n_split, int wn, const double* __restrict__ b1,
                             const double* __restrict__ W2, const double* __restrict__ b2, const double* __restrict__ W3,
                             const double* __restrict__ b3, const double* __restrict__ W4C, const double* __restrict__ b4C,
                             int n_cub, double* __restrict__ wC, int n_sims) {
+  // Every global input is staged with async copies in two batches (constants before the
+  // programmatic-dependency wait, the producer's partial sums after it): each dependent
+  // global round trip costs ~0.5-1 us here, so none may sit inside a loop.
   extern __shared__ double sh[];
-  double* h1 = sh;
-  double* h2 = sh + wn;
-  double* red = sh + 2 * wn;   // [groups][wn]
   const int sim = blockIdx.y;
-  const int groups = max(1, (int)blockDim.x / wn);
-  double* W2s = red + groups * wn;   // weights staged in smem up front (one round trip)
-  double* W3s = W2s + wn * wn;
-  double* W4s = W3s + wn * wn;       // this CTA's 64 rows of W4[C]
   const int j0 = blockIdx.x * 64;
   const int nrows4 = max(0, min(64, n_cub - j0));
+  double* h1 = sh;                    // [wn]
+  double* h2 = h1 + wn;               // [wn]
+  double* bs = h2 + wn;               // b1 | b2 | b3 | b4[rows]   [3 wn + 64]
+  double* W2s = bs + 3 * wn + 64;     // [wn][wn]
+  double* W3s = W2s + wn * wn;        // [wn][wn]
+  double* W4s = W3s + wn * wn;        // [64][wn]
+  double* ps = W4s + 64 * wn;         // [n_split][wn] partial sums of layer 1
   for (int t = threadIdx.x; t < wn * wn; t += blockDim.x) {
     cp_async8(W2s + t, W2 + t);
     cp_async8(W3s + t, W3 + t);
   }
   for (int t = threadIdx.x; t < nrows4 * wn; t += blockDim.x) cp_async8(W4s + t, W4C + (size_t)j0 * wn + t);
+  for (int t = threadIdx.x; t < wn; t += blockDim.x) {
+    cp_async8(bs + t, b1 + t);
+    cp_async8(bs + wn + t, b2 + t);
+    cp_async8(bs + 2 * wn + t, b3 + t);
+  }
+  for (int t = threadIdx.x; t < nrows4; t += blockDim.x) cp_async8(bs + 3 * wn + t, b4C + j0 + t);
   pdl_wait();
   pdl_launch();
-  {
-    const int m = threadIdx.x % wn, gidx = threadIdx.x / wn;
-    if (gidx < groups) {
-      double acc = 0.0;
-      for (int s2 = gidx; s2 < n_split; s2 += groups) acc += part[((size_t)s2 * n_sims + sim) * wn + m];
-      red[gidx * wn + m] = acc;
-    }
-  }
+  for (int t = threadIdx.x; t < n_split * wn; t += blockDim.x)
+    cp_async8(ps + t, part + ((size_t)(t / wn) * n_sims + sim) * wn + t % wn);
   cp_async_all_wait();
   __syncthreads();
   for (int m = threadIdx.x; m < wn; m += blockDim.x) {
-    double acc = b1[m];
-    for (int gidx = 0; gidx < groups; ++gidx) acc += red[gidx * wn + m];
-    h1[m] = sin(acc);
+    double acc[4] = {bs[m], 0.0, 0.0, 0.0};
+    int s2 = 0;
+    for (; s2 + 3 < n_split; s2 += 4)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += ps[(s2 + u) * wn + m];
+    for (; s2 < n_split; ++s2) acc[0] += ps[s2 * wn + m];
+    h1[m] = sin((acc[0] + acc[1]) + (acc[2] + acc[3]));
   }
   __syncthreads();
-  wnet_dense_sin(W2s, b2, h1, h2, wn);
+  wnet_dense_sin(W2s, bs + wn, h1, h2, wn);
   __syncthreads();
-  wnet_dense_sin(W3s, b3, h2, h1, wn);
+  wnet_dense_sin(W3s, bs + 2 * wn, h2, h1, wn);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int jj = warp; jj < nrows4; jj += nw) {
-    const int j = j0 + jj;
     double acc = 0.0;
     for (int k = lane; k < wn; k += 32) acc = fma(W4s[(size_t)jj * wn + k], h1[k], acc);
-    acc = warp_sum(acc) + b4C[j];
-    if (lane == 0) wC[(size_t)sim * n_cub + j] = acc * acc;
+    acc = warp_sum(acc) + bs[3 * wn + jj];
+    if (lane == 0) wC[(size_t)sim * n_cub + j0 + jj] = acc * acc;
   }
 }
 
@@ -248,11 +258,16 @@ __global__ void k_cubature(CubArgs a) {
     Rw[idx] = row;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; Jt && idx < epc * 12 * n; idx += blockDim.x) {
-    const int row = Rw[idx / n];
-    double* dst = Js + (idx / n) * ldp + idx % n;
-    if (row >= 0) cp_async8(dst, Jt + (size_t)row * a.ldjt + idx % n);
-    else *dst = 0.0;
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int rr = warp; Jt && rr < epc * 12; rr += nw) {  // warp per J~ row: no div / mod
+      const int row = Rw[rr];
+      double* dst = Js + rr * ldp;
+      for (int j = lane; j < n; j += 32) {
+        if (row >= 0) cp_async8(dst + j, Jt + (size_t)row * a.ldjt + j);
+        else dst[j] = 0.0;
+      }
+    }
   }
   cp_async_all_wait();
   // element physics, one warp per element
@@ -366,17 +381,23 @@ __global__ void k_cubature(CubArgs a) {
     }
     return;
   }
-  // G_e = (w K_e) J~_e   (12 x n)
-  for (int idx = threadIdx.x; idx < epc * 12 * n; idx += blockDim.x) {
-    int j = idx % n;
-    int r = (idx / n) % 12;
-    int el = idx / (12 * n);
-    const double* Kr = Ks + el * 144 + r * 12;
-    const double* Je = Js + (size_t)el * 12 * ldp;
-    double acc = 0.0;
+  // G_e = (w K_e) J~_e   (12 x n): warp per (element, row), lanes over columns
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int rr = warp; rr < epc * 12; rr += nw) {
+      const int el = rr / 12;
+      const double* Kr = Ks + rr * 12;  // = el * 144 + (rr % 12) * 12
+      const double* Je = Js + (size_t)el * 12 * ldp;
+      double kr[12];
 #pragma unroll
-    for (int c = 0; c < 12; ++c) acc = fma(Kr[c], Je[c * ldp + j], acc);
-    Gs[(el * 12 + r) * ldp + j] = acc;
+      for (int c = 0; c < 12; ++c) kr[c] = Kr[c];
+      for (int j = lane; j < n; j += 32) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) acc = fma(kr[c], Je[c * ldp + j], acc);
+        Gs[rr * ldp + j] = acc;
+      }
+    }
   }
   __syncthreads();
   // partial K~ = J~_C^T (w K J~_C) over the chunk's rows on the DMMA pipe; partial f~ = J~_C^T (w f)

@@ -27,6 +27,7 @@ struct AsmArgs {
   int N, n, n_p, n_q, rows_per_cta, nchunk;
   double dt, alpha;
   int drop_fict;
+  int mode;              // 0: both, 1: mass block only (part), 2: a and J~^T a only (a, partphi)
 };
 
 __global__ void k_assemble(AsmArgs A) {
@@ -54,7 +55,7 @@ __global__ void k_assemble(AsmArgs A) {
     double* rs = Rs + rl * ldp + j;
     if (row < A.N) {
       cp_async8(js, Jt + (size_t)row * A.ldjt + j);
-      if (j >= A.n_p) cp_async8(rs, dJ + (size_t)row * A.lddj + (j - A.n_p));
+      if (A.mode != 2 && j >= A.n_p) cp_async8(rs, dJ + (size_t)row * A.lddj + (j - A.n_p));
     } else {
       *js = 0.0;
       *rs = 0.0;
@@ -70,22 +71,25 @@ __global__ void k_assemble(AsmArgs A) {
     if (row < A.N) {
       const size_t o = (size_t)sim * A.N + row;
       m = A.mass[row];
-      fc = A.dt * A.dt * (A.f[o] - A.fext[o]);
-      if (!A.drop_fict) fc += m * A.hvv[o];
+      if (A.mode != 1) {
+        fc = A.dt * A.dt * (A.f[o] - A.fext[o]);
+        if (!A.drop_fict) fc += m * A.hvv[o];
+      }
     }
     ms[rl] = m;
     fs[rl] = fc;
   }
   cp_async_all_wait();
   __syncthreads();
-  for (int idx = threadIdx.x; idx < RC * n; idx += blockDim.x) {
-    const int rl = idx / n, j = idx % n;
-    const double dj = (j >= A.n_p) ? Rs[rl * ldp + j] : 0.0;
-    Rs[rl * ldp + j] = ((1.0 + ah) * Js[rl * ldp + j] + dj) * ms[rl];
-  }
+  if (A.mode != 2)
+    for (int idx = threadIdx.x; idx < RC * n; idx += blockDim.x) {
+      const int rl = idx / n, j = idx % n;
+      const double dj = (j >= A.n_p) ? Rs[rl * ldp + j] : 0.0;
+      Rs[rl * ldp + j] = ((1.0 + ah) * Js[rl * ldp + j] + dj) * ms[rl];
+    }
   // a_n (one warp per row) into column n of Rs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int rl = warp; rl < RC; rl += nw) {
+  for (int rl = warp; A.mode != 1 && rl < RC; rl += nw) {
     const int row = row0 + rl;
     double acc = 0.0;
     for (int j = lane; j < n; j += 32) acc = fma(Js[rl * ldp + j], cs[j], acc);
@@ -104,8 +108,8 @@ __global__ void k_assemble(AsmArgs A) {
   // [J~^T M R | J~^T a] for the chunk on the DMMA pipe: n x (n + 1), split into part / partphi
   double* P = A.part + ((size_t)sim * A.nchunk + chunk) * n * n;
   double* Pp = A.partphi + ((size_t)sim * A.nchunk + chunk) * n;
-  gram_dmma(Js, ldp, Rs, ldp, RC, n, n, P, n);
-  gram_dmma(Js, ldp, Rs + n, ldp, RC, n, 1, Pp, 1);
+  if (A.mode != 2) gram_dmma(Js, ldp, Rs, ldp, RC, n, n, P, n);
+  if (A.mode != 1) gram_dmma(Js, ldp, Rs + n, ldp, RC, n, 1, Pp, 1);
 }
 
 // phi = sum_chunks partphi (one CTA per sim; 8 chunk groups per output, smem combine), ||phi||_2

@@ -21,7 +21,7 @@ def load(path):
 
 
 def iteration(seq, which=-2):
-    idx = [i for i, s in enumerate(seq) if s[0].endswith("k_seed_jet")]
+    idx = [i for i, s in enumerate(seq) if s[0].endswith("k_seed_jet") or "k_mlp_jet_fwd" in s[0]]
     i0 = idx[which]
     i1 = [i for i in range(i0, len(seq)) if "k_lu_solve" in seq[i][0]][0]
     return seq[i0:i1 + 1]
