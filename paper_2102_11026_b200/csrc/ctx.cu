@@ -389,8 +389,70 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
   ++gemm_launch_count;
 }
 
+// Fused vhp backward chain (mlp_chain.cuh): g = (P W_L)^T a, then one cluster per 8 passes.
+template <int R, int CS>
+bool launch_mlp_bwd(nlrom_ctx* c, const MlpBwdArgs& a, int groups, bool dry) {
+  const size_t smem = mlp_bwd_smem<R>(c->wL1);
+  if (smem > 227 * 1024) return false;
+  if (dry) return true;
+  static bool configured = false;
+  if (!configured) {
+    NL_CUDA(cudaFuncSetAttribute(k_mlp_dual_bwd<R, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (CS > 8) NL_CUDA(cudaFuncSetAttribute(k_mlp_dual_bwd<R, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, groups, 1);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  NL_CUDA(cudaLaunchKernelEx(&cfg, k_mlp_dual_bwd<R, CS>, a));
+  ++gemm_launch_count;
+  return true;
+}
+
+bool fused_vhp_backward(nlrom_ctx* c) {
+  if (getenv("NLROM_NO_FUSED_MLP") || c->next) return false;
+  const int L1 = c->L - 1, w = c->wL1;
+  if (L1 < 1 || L1 > MLP_MAXL) return false;
+  for (int l = 1; l <= L1; ++l)
+    if (c->widths[l] != w) return false;
+  const int M = w;
+  MlpBwdArgs a{};
+  a.g = c->ybuf.p; a.L1 = L1; a.w = w; a.n_q = c->n_q;
+  for (int l = 0; l < L1; ++l) {
+    a.WT[l] = c->WT[l].p; a.ldWT[l] = c->ldWT[l]; a.cache[l] = c->cache[l].p;
+  }
+  a.ldc = c->ldc[0]; a.Gt = c->Gt.p; a.ldG = c->ldGt;
+  a.gpb = ceil_div(c->n_q, 8);
+  const int groups = c->n_sims * a.gpb;
+  auto go = [&](bool dry) -> bool {
+    if (w == 256) return launch_mlp_bwd<16, 16>(c, a, groups, dry);
+    if (w == 64) return launch_mlp_bwd<8, 8>(c, a, groups, dry);
+    if (w == 40) return launch_mlp_bwd<8, 5>(c, a, groups, dry);
+    if (w == 8) return launch_mlp_bwd<8, 1>(c, a, groups, dry);
+    return false;
+  };
+  if (!go(true)) return false;
+  launch(c, k_gemv_t, dim3(c->bnch, c->n_sims), 128, 0, (const double*)c->Alast.p, c->ldlast, M, (const double*)c->a.p,
+         c->N, c->brows, c->bpart.p, c->bnch);
+  launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->bpart.p, c->bnch, M,
+         c->ybuf.p);
+  return go(false);
+}
+
 void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply) {
-  decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
+  if (!fused_vhp_backward(c))
+    decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   const int n = c->n;
   launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,

@@ -209,3 +209,159 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
 }
 
 }  // namespace nlrom
+
+namespace nlrom {
+
+// Fused vhp backward chain (complex-step BP in dual arithmetic):
+//   Delta_{L-2} = g (*) cos(z_{L-2}),  Delta_{l-1} = (W_l^T Delta_l) (*) cos(z_{l-1}),  G = W_0^T Delta_0
+// per column group of 8 passes (16 columns: real / dual slot of each pass), one cluster
+// per group, CTA rank owns rows [rank*R, rank*R + R) of every stage; same DSMEM
+// broadcast scheme as k_mlp_jet_fwd. z are the pre-activation caches of the forward.
+struct MlpBwdArgs {
+  const double* g;          // (n_sims, w): W_L^T P a
+  int L1, w, n_q;
+  const double* WT[MLP_MAXL];  // WT[l]: (in_l x ldWT[l]) = W_l^T, rows in_l (w for l >= 1, n_q for l = 0)
+  int ldWT[MLP_MAXL];
+  const double* cache[MLP_MAXL];  // (n_sims * 2 n_q) x ldc
+  int ldc;
+  double* Gt;               // (n_sims * 2 n_q) x ldG
+  int ldG;
+  int gpb;                  // groups (of 8 passes) per sim
+};
+
+template <int R, int CS>
+__global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int G = 16, NTH = 256;
+  using P = MlpPlan<R, G>;
+  extern __shared__ __align__(16) double sm[];
+  const int kmax = P::kp(a.w);
+  const int LDX = P::LDX;
+  const int LDWS = P::ldws(kmax);
+  auto Xb = [&](int i) { return sm + i * kmax * LDX; };
+  auto Wbuf = [&](int i) { return sm + 2 * kmax * LDX + i * R * LDWS; };
+  auto Zbuf = [&](int i) { return sm + 2 * kmax * LDX + 2 * R * LDWS + i * R * G; };  // [R][G] cache slice
+  double* Ys = sm + 2 * kmax * LDX + 2 * R * LDWS + 2 * R * G;  // [G][R+1]
+  double* Os = Ys + G * (R + 1);                                 // [R][LDX]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)cluster.block_rank();
+  const int r0 = rank * R;
+  const int gg = blockIdx.y, sim = gg / a.gpb, gl = gg % a.gpb;
+  const int L1 = a.L1;
+  // stage s = 0 .. L1: s = 0 builds Delta_{L1-1}; stage s >= 1 multiplies by W_{L1-s}^T;
+  // stages 1 .. L1-1 end with cos(z_{L1-1-s}); stage L1 writes G.
+  auto load_w = [&](int l, int buf) {  // rows r0.. of W_l^T (in_l rows), K = w
+    const int rows = (l == 0) ? a.n_q : a.w;
+    const int Kp = (a.w + 15) & ~15;
+    for (int rr = warp; rr < R; rr += NTH / 32)
+      for (int k = 2 * lane; k < Kp; k += 64) {
+        const bool ok = (r0 + rr < rows) && (k < a.w);
+        cp_async16(Wbuf(buf) + rr * LDWS + k, ok ? a.WT[l] + (size_t)(r0 + rr) * a.ldWT[l] + k : a.WT[l], ok);
+      }
+  };
+  auto load_z = [&](int l, int buf) {  // cache_l rows r0.. for the group's 16 columns
+    const double* C = a.cache[l] + (size_t)sim * 2 * a.n_q * a.ldc;
+    for (int t = tid; t < R * G; t += NTH) {
+      const int rr = t % R, col = t / R;
+      const int p = gl * 8 + col / 2;
+      double* dst = Zbuf(buf) + rr * G + col;
+      if (p < a.n_q && r0 + rr < a.w) cp_async8(dst, C + (size_t)(2 * p + (col & 1)) * a.ldc + r0 + rr);
+      else *dst = 0.0;
+    }
+  };
+  // prologue: constants (weights of the first multiply, stage 1) before the dependency wait
+  load_w(L1 - 1, 1);
+  cp_async_commit();
+  pdl_wait();
+  pdl_launch();
+  load_z(L1 - 1, 0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int s = 0; s <= L1; ++s) {
+    const int l = L1 - s;  // stage s >= 1 multiplies by W_l^T (l = L1 - s)
+    // prefetch the next stage's weights and cache slice
+    if (s + 1 <= L1 && s >= 1) load_w(l - 1, (s + 1) & 1);
+    if (s + 1 <= L1 - 1) load_z(L1 - 1 - (s + 1) + 0, (s + 1) & 1);
+    cp_async_commit();
+    if (s >= 1) {
+      double* Xc = Xb(s & 1);
+      const double* Ws = Wbuf(s & 1);
+      constexpr int TM = R / 8, TN = G / 8, NT = TM * TN;
+      const int Kp = (a.w + 15) & ~15;
+      cp_async_wait<1>();
+      __syncthreads();
+      for (int tile = warp; tile < NT; tile += NTH / 32) {
+        const int tm = tile % TM, tn = tile / TM;
+        double c[4][2] = {};
+        const double* wrow = Ws + (tm * 8 + (lane >> 2)) * LDWS + (lane & 3);
+        const double* xcol = Xc + (lane & 3) * LDX + tn * 8 + (lane >> 2);
+        for (int k0 = 0; k0 < Kp; k0 += 16) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], wrow[k0 + 4 * u], xcol[(k0 + 4 * u) * LDX]);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int row = tm * 8 + (lane >> 2), col = tn * 8 + 2 * (lane & 3) + e;
+          Ys[col * (R + 1) + row] = (c[0][e] + c[1][e]) + (c[2][e] + c[3][e]);
+        }
+      }
+      __syncthreads();
+    }
+    if (s == L1) {
+      // G = W_0^T Delta_0: rows i < n_q
+      for (int t = tid; t < R * G; t += NTH) {
+        const int rr = t % R, col = t / R;
+        const int i = r0 + rr, p = gl * 8 + col / 2;
+        if (i < a.n_q && p < a.n_q)
+          a.Gt[((size_t)sim * 2 * a.n_q + 2 * p + (col & 1)) * a.ldG + i] = Ys[col * (R + 1) + rr];
+      }
+      break;
+    }
+    // Delta rows of this CTA: (input (*) cos(z)) in dual arithmetic, z = cache of layer L1-1-s
+    const double* Z = Zbuf(s & 1);
+    for (int t = tid; t < R * 8; t += NTH) {
+      const int rr = t % R, j = t / R;
+      const int m = r0 + rr;
+      double d0, d1;
+      if (s == 0) {
+        d0 = a.g[(size_t)sim * a.w + m];
+        d1 = 0.0;
+      } else {
+        d0 = Ys[(2 * j) * (R + 1) + rr];
+        d1 = Ys[(2 * j + 1) * (R + 1) + rr];
+      }
+      const double z0 = Z[rr * G + 2 * j], z1 = Z[rr * G + 2 * j + 1];
+      double sn, cs;
+      sincos(z0, &sn, &cs);
+      // dual cos(z0 + z1 e) = cos z0 - sin z0 z1 e ; (d0 + d1 e)(f0 + f1 e) = d0 f0 + (d0 f1 + d1 f0) e
+      Os[rr * LDX + 2 * j] = d0 * cs;
+      Os[rr * LDX + 2 * j + 1] = fma(d0, -sn * z1, d1 * cs);
+    }
+    __syncthreads();
+    {
+      double* Xn = Xb((s + 1) & 1);
+      constexpr int C2 = G / 2;
+      for (int dst = warp; dst < CS; dst += NTH / 32) {
+        double* Xr = cluster.map_shared_rank(Xn, dst);
+        for (int t = lane; t < R * C2; t += 32) {
+          const int rr = t / C2, c2 = (t % C2) * 2;
+          if (r0 + rr < a.w)
+            *reinterpret_cast<double2*>(Xr + (r0 + rr) * LDX + c2) =
+                *reinterpret_cast<const double2*>(Os + rr * LDX + c2);
+        }
+      }
+    }
+    cluster.sync();
+  }
+}
+
+template <int R>
+inline size_t mlp_bwd_smem(int w) {
+  using P = MlpPlan<R, 16>;
+  const int kp = P::kp(w);
+  return (size_t)(2 * kp * P::LDX + 2 * R * P::ldws(kp) + 2 * R * 16 + 16 * (R + 1) + R * P::LDX) * 8;
+}
+
+}  // namespace nlrom
