@@ -222,24 +222,38 @@ def run_ours(args):
     h2d = (2 * n + P.model.N) * 8
     d2h = 2 * n * 8 + 8
 
-    # roofline of the dominant kernel: output decoder layer + fused filter (fp64 DMMA)
+    # roofline of the dominant kernel: every stage timed live with CUDA events on the context
+    # stream (L2 flushed before each launch); the largest device-time share is "dominant".
     pk, fp64 = peaks()
-    G = 4 + 4 * 3 if P.cfg.n_q > 15 else None
-    N, w, n_p, n_q = P.model.N, P.cfg.width, P.cfg.n_p, P.cfg.n_q
-    useful_cols = 4 + 4 * n_q                       # base jet + 4 slots per tangent (no replicas)
-    alg_flops = 2.0 * N * (w + n_p) * useful_cols
-    ref_flops = 2.0 * N * (w + n_p) * (16 * n_q + 5)  # same layer in the reference 4n_q+2 pass structure
-    achieved = alg_flops / (ms_dom * 1e-3) / 1e12
+    stage_ms = s.bench_kernels(max(20, args.steps // 4), flush_l2=True)
+    N, w, n_p, n_q, L = P.model.N, P.cfg.width, P.cfg.n_p, P.cfg.n_q, P.cfg.n_fc
+    n = n_p + n_q
+    cols = 4 + 4 * n_q                      # jet columns without the per-group base replicas
+    hidden_mac = n_q * w + (L - 2) * w * w  # sum_l in_l * out_l over the L-1 sin layers
+    stages = [
+        ("k_mlp_jet_fwd (fused hidden jet chain, fp64 DMMA, cluster/DSMEM)", 2.0 * cols * hidden_mac,
+         (16 * n_q + 5) * 2.0 * hidden_mac),
+        ("gemm_tn_kernel<CfgOutC,EpiJetOutC> (decoder output layer, filter folded)", 2.0 * N * w * cols,
+         (16 * n_q + 5) * (2.0 * N * w + 4.0 * N * n_p)),
+        ("k_gemv_t + k_mlp_dual_bwd (vhp complex-step backprop chain)",
+         2.0 * N * w + 2.0 * (2 * n_q) * (hidden_mac - n_q * w + n_q * w), (2 * n_q + 1) * 2.0 * (hidden_mac + N * w)),
+        ("k_lu_solve (in-CTA LU with partial pivoting)", 2.0 * n ** 3 / 3.0, 2.0 * n ** 3 / 3.0),
+    ]
+    k = int(np.argmax(stage_ms))
+    name, alg_flops, ref_flops = stages[k]
+    achieved = alg_flops / (stage_ms[k] * 1e-3) / 1e12
     peak = fp64 if fp64 else None
-    roof = {"bound": "tensor", "kernel": "gemm_tn_kernel<CfgOut,EpiJetOut> (decoder output layer + filter)",
+    roof = {"bound": "tensor", "kernel": name,
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if peak else None, "traffic": None,
             "peak_source": "profiles/fp64_peak.json: measured DMMA.8x8x4 fp64 (MEASURED_PEAKS.json has no fp64 entry)",
-            "kernel_ms": ms_dom, "algorithmic_flops_per_launch": alg_flops,
-            "reference_pass_structure_flops_per_launch": ref_flops}
+            "kernel_ms": stage_ms[k], "algorithmic_flops_per_launch": alg_flops,
+            "reference_pass_structure_flops_per_launch": ref_flops,
+            "stages_ms": {st[0].split(" ")[0]: ms for st, ms in zip(stages, stage_ms)},
+            "share_of_step": stage_ms[k] / ms_iter}
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "dominant_traffic.json")))
-        roof["traffic"] = tr.get("dram_bytes_per_launch")
+        roof["traffic"] = tr.get(name.split(" ")[0], {}).get("dram_bytes_per_launch")
     except Exception:
         pass
 

@@ -201,6 +201,11 @@ NLROM_API int nlrom_step_device(nlrom_ctx* ctx, const double* r_bar, const doubl
  * iteration. */
 NLROM_API int nlrom_bench_iterations(nlrom_ctx* ctx, int n_iters, int flush_l2, float* ms_total, float* ms_dominant);
 
+/* Device time per stage (CUDA events on the context stream, averaged over n_iters):
+ * ms4[0] hidden jet chain, ms4[1] decoder output layer, ms4[2] vhp backward chain,
+ * ms4[3] LU solve. Used by bench.py to pick and time the dominant kernel. */
+NLROM_API int nlrom_bench_kernels(nlrom_ctx* ctx, int n_iters, int flush_l2, float* ms4);
+
 /* Number of kernel launches of one Newton iteration (for bench "gpu_launches"). */
 NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
 

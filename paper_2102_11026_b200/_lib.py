@@ -25,7 +25,7 @@ EXPORTED = [
     "nlrom_system_jacobian", "nlrom_delta_j", "nlrom_fictitious_force", "nlrom_wnet_forward",
     "nlrom_cubature_integrate", "nlrom_full_displacement", "nlrom_jtilde", "nlrom_step", "nlrom_step_device",
     "nlrom_bench_iterations", "nlrom_launches_per_iteration", "nlrom_element_forces",
-    "nlrom_element_reduced_forces",
+    "nlrom_element_reduced_forces", "nlrom_bench_kernels",
 ]
 
 
@@ -95,6 +95,7 @@ def lib():
             "nlrom_step_device": (C.c_int, [vp, vp, vp, vp, C.POINTER(SimCfg), vp, vp, vp]),
             "nlrom_bench_iterations": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
             "nlrom_launches_per_iteration": (C.c_int, [vp]),
+            "nlrom_bench_kernels": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
             "nlrom_element_forces": (C.c_int, [vp, dp, C.c_int, dp, dp]),
             "nlrom_element_reduced_forces": (C.c_int, [vp, dp, ip, C.c_int, dp]),
         }

@@ -1069,6 +1069,55 @@ extern "C" int nlrom_bench_iterations(nlrom_ctx* c, int n_iters, int flush_l2, f
   CTX_END(c)
 }
 
+// Per-stage device time (CUDA events on the context stream, L2 optionally flushed before
+// each launch), averaged over n_iters: [0] hidden jet chain (fused cluster kernel),
+// [1] decoder output layer, [2] vhp backward chain, [3] LU solve.
+extern "C" int nlrom_bench_kernels(nlrom_ctx* c, int n_iters, int flush_l2, float* ms4) {
+  CTX_TRY(c)
+  if (c->graph_key.empty()) throw Error(NLROM_ERR_ARG, "run nlrom_step first (captures the graphs)");
+  if (flush_l2 && !c->flush.p) c->flush.alloc((size_t)32 << 20);
+  const double dt = 1.0 / 60.0;
+  auto stage = [&](int which) {
+    switch (which) {
+      case 0:
+        if (!fused_hidden_forward(c, dt, 0)) bundle_forward(c, dt, 0);
+        break;
+      case 1: output_layer(c); break;
+      case 2:
+        if (!fused_vhp_backward(c))
+          decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
+        break;
+      default: {
+        const int n = c->n;
+        if (n + 1 <= 64)
+          launch(c, k_lu_solve<4>, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p,
+                 c->dr.p, c->r.p, n, 0, c->status.p);
+        else
+          launch(c, k_lu_solve<8>, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p,
+                 c->dr.p, c->r.p, n, 0, c->status.p);
+      }
+    }
+  };
+  for (int w = 0; w < 4; ++w) {
+    float acc = 0.f;
+    for (int i = 0; i < n_iters; ++i) {
+      if (flush_l2) {
+        k_flush<<<1184, 256, 0, c->st>>>(c->flush.p, c->flush.n, (double)i);
+        NL_CHECK_LAUNCH();
+      }
+      NL_CUDA(cudaEventRecord(c->ev0, c->st));
+      stage(w);
+      NL_CUDA(cudaEventRecord(c->ev1, c->st));
+      NL_CUDA(cudaEventSynchronize(c->ev1));
+      float ms = 0.f;
+      NL_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+      acc += ms;
+    }
+    ms4[w] = acc / std::max(1, n_iters);
+  }
+  CTX_END(c)
+}
+
 extern "C" int nlrom_launches_per_iteration(nlrom_ctx* c) { return c ? c->launches_E + c->launches_J : 0; }
 
 extern "C" int nlrom_element_forces(nlrom_ctx* c, const double* u, int want_K, double* f_int, double* K_elems) {

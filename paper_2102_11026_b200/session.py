@@ -209,6 +209,12 @@ class Session:
         self._chk(self._L.nlrom_bench_iterations(self._h, int(n_iters), int(flush_l2), C.byref(tot), C.byref(dom)))
         return tot.value, dom.value
 
+    def bench_kernels(self, n_iters, flush_l2=True):
+        """Device ms per launch of [hidden jet chain, output layer, vhp backward chain, LU]."""
+        out = (C.c_float * 4)()
+        self._chk(self._L.nlrom_bench_kernels(self._h, int(n_iters), int(flush_l2), out))
+        return list(out)
+
     def launches_per_iteration(self):
         return int(self._L.nlrom_launches_per_iteration(self._h))
 

@@ -20,10 +20,15 @@ def load(path):
     return seq
 
 
-def iteration(seq, which=-2):
-    idx = [i for i, s in enumerate(seq) if s[0].endswith("k_seed_jet") or "k_mlp_jet_fwd" in s[0]]
-    i0 = idx[which]
-    i1 = [i for i in range(i0, len(seq)) if "k_lu_solve" in seq[i][0]][0]
+def iteration(seq):
+    """Last complete Newton iteration: seed/jet-chain ... cubature ... LU."""
+    starts = [i for i, s in enumerate(seq) if s[0].endswith("k_seed_jet") or "k_mlp_jet_fwd" in s[0]]
+    best = None
+    for i0 in starts:
+        ends = [i for i in range(i0, len(seq)) if "k_lu_solve" in seq[i][0]]
+        if ends and any("k_cubature" in s[0] for s in seq[i0:ends[0]]):
+            best = (i0, ends[0])
+    i0, i1 = best
     return seq[i0:i1 + 1]
 
 
