@@ -33,6 +33,8 @@ namespace {
 using CfgBwd = GemmCfg<16, 16, 1, 1, 4, 32, 8>;
 template <int G> using CfgHid = GemmCfg<16, G, 1, 1, 4, 32, (G <= 32 ? 8 : 4)>;
 template <int G> using CfgOut = GemmCfg<64, G, 4, 1, 1, 32, 4>;
+// batched (many sims): 64 x 128 tiles, 8 warps, 32-wide K tiles, 3 stages
+using CfgBig = GemmCfg<64, 128, 2, 4, 1, 32, 3>;
 
 struct CubSet {
   IBuf elems;
@@ -59,7 +61,10 @@ struct nlrom_ctx {
   std::vector<DBuf> W, WT, b;
   std::vector<int> ldW, ldWT;
   DBuf Alast, AT, Pb, U, mass;
-  int ldlast = 0, wL1 = 0, next = 0;  // next: K-extension of the output layer (0: filter folded)
+  int ldlast = 0, wL1 = 0, next = 0;
+  bool batched = false;  // many sims: big-tile per-layer GEMMs instead of the latency kernels
+  DBuf AlastT;           // (P W_L)^T (w x ldAT), batched backward top
+  int ldAT = 0;  // next: K-extension of the output layer (0: filter folded)
   // mesh
   IBuf elem_rows;
   DBuf Dm_inv, vol;
@@ -120,7 +125,12 @@ int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL
 
 // ---------------------------------------------------------------- GEMM dispatch
 template <class Epi>
-void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st) {
+void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st, bool big = false) {
+  if (big && 128 % G == 0) {
+    launch_gemm<CfgBig>(g, e, st);
+    ++gemm_launch_count;
+    return;
+  }
   switch (G) {
     case 8: launch_gemm<CfgHid<8>>(g, e, st); break;
     case 16: launch_gemm<CfgHid<16>>(g, e, st); break;
@@ -237,7 +247,7 @@ bool launch_mlp_fwd(nlrom_ctx* c, const MlpFwdArgs& a) {
 }
 
 bool fused_hidden_forward(nlrom_ctx* c, double dt, int drop_fict) {
-  if (getenv("NLROM_NO_FUSED_MLP")) return false;
+  if (getenv("NLROM_NO_FUSED_MLP") || c->batched) return false;
   const int L1 = c->L - 1, w = c->wL1;
   if (L1 < 1 || L1 > MLP_MAXL) return false;
   for (int l = 1; l <= L1; ++l)
@@ -281,7 +291,7 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
     const int compact = (l == c->L - 2) ? 1 : 0;
     GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
     EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, compact};
-    hid_gemm(c->G, g, e, c->st);
+    hid_gemm(c->G, g, e, c->st, c->batched);
     in = c->H[l].p;
     ldin = c->ldH[l];
   }
@@ -294,10 +304,19 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
 }
 
 void wnet_phase(nlrom_ctx* c) {
-  launch(c, k_gemv_splitk, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
-         (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
-  const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + c->wsplit * c->wn) * 8;
-  launch(c, k_wnet_tail, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm, (const double*)c->wpart.p, c->wsplit, c->wn,
+  int nsplit = c->wsplit;
+  if (c->batched) {
+    // layer 1 for all sims as one GEMM: part (n_sims x wn) = u (n_sims x N) W1^T
+    GemmArgs g{c->W1.p, c->u.p, round_up(c->N, 2), c->N, c->wn, c->n_sims, c->N, 0, 0};
+    launch_gemm<CfgBig>(g, EpiStore{c->wpart.p, c->wn, 0, nullptr, 1, nullptr}, c->st);
+    ++gemm_launch_count;
+    nsplit = 1;
+  } else {
+    launch(c, k_gemv_splitk, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
+           (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
+  }
+  const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + nsplit * c->wn) * 8;
+  launch(c, k_wnet_tail, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm, (const double*)c->wpart.p, nsplit, c->wn,
          (const double*)c->b1.p, (const double*)c->W2.p, (const double*)c->b2.p, (const double*)c->W3.p,
          (const double*)c->b3.p, (const double*)c->W4C.p, (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
 }
@@ -353,10 +372,17 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
                       std::vector<int>& ldcs, DBuf& D0, DBuf& D1, DBuf& Gout, int ldG) {
   const int ncols = c->n_sims * npass_per_sim * NS;
   const int M = c->wL1 + c->next;
-  launch(c, k_gemv_t, dim3(c->bnch, c->n_sims), 128, 0, (const double*)c->Alast.p, c->ldlast, M, a_vec, c->N,
-         c->brows, c->bpart.p, c->bnch);
-  launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->bpart.p, c->bnch, M,
-         c->ybuf.p);
+  if (c->batched && c->AlastT.p && !c->next) {
+    // y (n_sims x w) = a (n_sims x N) (P W_L): one GEMM for all sims
+    GemmArgs g{c->AlastT.p, a_vec, c->ldAT, c->N, M, c->n_sims, c->N, 0, 0};
+    launch_gemm<CfgBig>(g, EpiStore{c->ybuf.p, M, 0, nullptr, 1, nullptr}, c->st);
+    ++gemm_launch_count;
+  } else {
+    launch(c, k_gemv_t, dim3(c->bnch, c->n_sims), 128, 0, (const double*)c->Alast.p, c->ldlast, M, a_vec, c->N,
+           c->brows, c->bpart.p, c->bnch);
+    launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->bpart.p, c->bnch, M,
+           c->ybuf.p);
+  }
   const int l_top = c->L - 2;
   dim3 gd(ceil_div(c->wL1, 32), c->n_sims);
   if (NS == 2) {
@@ -377,6 +403,7 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
     GemmArgs g{c->WT[l].p, cur->p, c->ldWT[l], ldcs[l], c->widths[l], ncols, c->widths[l + 1], 0, 0};
     if (NS == 2) {
       if (mc) launch_gemm<CfgBwd>(g, EpiBwdAct<2, ACT_SIN_MC>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
+      else if (c->batched) launch_gemm<CfgBig>(g, EpiBwdAct<2, ACT_SIN_MD>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
       else launch_gemm<CfgBwd>(g, EpiBwdAct<2, ACT_SIN_MD>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
     } else {
       launch_gemm<CfgBwd>(g, EpiBwdAct<1, ACT_SIN_MC>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
@@ -385,7 +412,8 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
     std::swap(cur, nxt);
   }
   GemmArgs g{c->WT[0].p, cur->p, c->ldWT[0], ldcs[0], c->widths[0], ncols, c->widths[1], 0, 0};
-  launch_gemm<CfgBwd>(g, EpiStore{Gout.p, ldG, 0, nullptr, 1, nullptr}, c->st);
+  if (c->batched) launch_gemm<CfgBig>(g, EpiStore{Gout.p, ldG, 0, nullptr, 1, nullptr}, c->st);
+  else launch_gemm<CfgBwd>(g, EpiStore{Gout.p, ldG, 0, nullptr, 1, nullptr}, c->st);
   ++gemm_launch_count;
 }
 
@@ -421,7 +449,7 @@ bool launch_mlp_bwd(nlrom_ctx* c, const MlpBwdArgs& a, int groups, bool dry) {
 }
 
 bool fused_vhp_backward(nlrom_ctx* c) {
-  if (getenv("NLROM_NO_FUSED_MLP") || c->next) return false;
+  if (getenv("NLROM_NO_FUSED_MLP") || c->next || c->batched) return false;
   const int L1 = c->L - 1, w = c->wL1;
   if (L1 < 1 || L1 > MLP_MAXL) return false;
   for (int l = 1; l <= L1; ++l)
@@ -604,6 +632,13 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         }
       }
       upload_matrix(c->Alast, A.data(), N, w, c->ldlast);
+      if (c->n_sims > 1) {
+        std::vector<double> At((size_t)w * N);
+        for (int r = 0; r < N; ++r)
+          for (int k = 0; k < w; ++k) At[(size_t)k * N + r] = A[(size_t)r * w + k];
+        c->ldAT = round_up(N, 2);
+        upload_matrix(c->AlastT, At.data(), w, N, c->ldAT);
+      }
       upload_matrix(c->AT, ATh.data(), n_p, w, round_up(w, 2));
       upload(c->Pb, Pbh.data(), N);
       upload(c->U, d->U, (size_t)N * n_p);
@@ -654,6 +689,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     choose_groups(n_q, w, c->G, c->gps);
     c->Cb = c->G * c->gps;
     c->Cc = 4 + 4 * n_q;  // compact (de-replicated) columns per sim
+    c->batched = c->n_sims * c->Cb >= 2048 || getenv("NLROM_BATCHED") != nullptr;
     c->ldq = round_up(n_q, 2);
     const int ncols = c->n_sims * c->Cb;
     c->X0.alloc((size_t)ncols * c->ldq);

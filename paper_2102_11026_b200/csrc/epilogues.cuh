@@ -110,66 +110,47 @@ struct EpiJet {
   const double* bias;
   double* cache;      // (n_sims * 2 n_q) x ldcache, may be null
   int ldcache;
-  int group;          // columns per group (== BN)
+  int group;          // columns per group (BN is a multiple of it)
   int gps;            // groups per simulation
   int n_q;            // tangent directions per simulation
   int compact;        // 1: write the de-replicated layout [base | n_q tangents] per sim (next layer is linear)
   __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
     double* Yz = Y + (size_t)t.z * strideY;
-    const int gg = t.c0 / group;              // global group index (tile == group)
-    const int sim = gg / gps, gl = gg % gps;
     const int nk = (group - 4) / 4;           // tangents per group
-    double* Cz = cache ? cache + (size_t)sim * 2 * n_q * ldcache : nullptr;
     const int cs = 4 + 4 * n_q;               // compact columns per sim
-    if (compact) {
-      for (int ml = tid; ml < t.bm; ml += nt) {
-        const int m = t.m0 + ml;
-        if (m >= g.M) continue;
-        double z[4], o[4];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) z[s] = t.Cs[s * t.ldc + ml];
-        z[0] += bias[m];
-        JetCos jc;
-        jet_sin_base(z, o, jc);
-        if (gl == 0)
-#pragma unroll
-          for (int s = 0; s < 4; ++s) Yz[(size_t)(sim * cs + s) * ldy + m] = o[s];
-        for (int k = 0; k < nk; ++k) {
-          const int kg = gl * nk + k;
-          if (kg >= n_q) break;
-          double y[4], yo[4];
-#pragma unroll
-          for (int s = 0; s < 4; ++s) y[s] = t.Cs[(4 + 4 * k + s) * t.ldc + ml];
-          jet_tangent(jc, y, yo);
-#pragma unroll
-          for (int s = 0; s < 4; ++s) Yz[(size_t)(sim * cs + 4 + 4 * kg + s) * ldy + m] = yo[s];
-          if (Cz) {
-            Cz[(size_t)(2 * kg) * ldcache + m] = z[0];
-            Cz[(size_t)(2 * kg + 1) * ldcache + m] = y[0];
-          }
-        }
-      }
-      return;
-    }
-    for (int ml = tid; ml < t.bm; ml += nt) {
+    const int ngt = t.bn / group;             // groups in this tile
+    for (int i = tid; i < t.bm * ngt; i += nt) {
+      const int gt = i / t.bm, ml = i % t.bm;
       const int m = t.m0 + ml;
-      if (m >= g.M) continue;
+      const int cg = t.c0 + gt * group;       // first column of the group
+      if (m >= g.M || cg >= g.C) continue;
+      const int gg = cg / group;
+      const int sim = gg / gps, gl = gg % gps;
+      double* Cz = cache ? cache + (size_t)sim * 2 * n_q * ldcache : nullptr;
+      const double* cs0 = t.Cs + (gt * group) * t.ldc + ml;
       double z[4], o[4];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) z[s] = t.Cs[s * t.ldc + ml];
+      for (int s = 0; s < 4; ++s) z[s] = cs0[s * t.ldc];
       z[0] += bias[m];
       JetCos jc;
       jet_sin_base(z, o, jc);
+      if (!compact) {
 #pragma unroll
-      for (int s = 0; s < 4; ++s) Yz[(size_t)(t.c0 + s) * ldy + m] = o[s];
+        for (int s = 0; s < 4; ++s) Yz[(size_t)(cg + s) * ldy + m] = o[s];
+      } else if (gl == 0) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) Yz[(size_t)(sim * cs + s) * ldy + m] = o[s];
+      }
       for (int k = 0; k < nk; ++k) {
         const int kg = gl * nk + k;           // tangent index within the simulation
+        if (compact && kg >= n_q) break;
         double y[4], yo[4];
 #pragma unroll
-        for (int s = 0; s < 4; ++s) y[s] = t.Cs[(4 + 4 * k + s) * t.ldc + ml];
+        for (int s = 0; s < 4; ++s) y[s] = cs0[(4 + 4 * k + s) * t.ldc];
         jet_tangent(jc, y, yo);
+        const size_t col = compact ? (size_t)(sim * cs + 4 + 4 * kg) : (size_t)(cg + 4 + 4 * k);
 #pragma unroll
-        for (int s = 0; s < 4; ++s) Yz[(size_t)(t.c0 + 4 + 4 * k + s) * ldy + m] = yo[s];
+        for (int s = 0; s < 4; ++s) Yz[(col + s) * ldy + m] = yo[s];
         if (Cz && kg < n_q) {
           Cz[(size_t)(2 * kg) * ldcache + m] = z[0];
           Cz[(size_t)(2 * kg + 1) * ldcache + m] = y[0];

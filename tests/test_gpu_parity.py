@@ -216,3 +216,45 @@ def test_trajectory_100_steps(cfg1, integ):
         ro, rdo, _, _ = ors.step(S, ro, rdo, P.f_ext, ocfg(cfg))
         worst = max(worst, np.abs(st.r - ro).max() / max(np.abs(ro).max(), 1e-30))
     assert worst <= 1e-9, worst
+
+
+# ------------------------------------------------------------------ independent sims in one context
+@pytest.mark.parametrize("batched", [False, True])
+def test_multi_sim(cfg1, batched, monkeypatch):
+    """n_sims independent simulations through one context == the single-sim oracle per sim.
+    batched=True forces the big-tile per-layer GEMM path used for thousands of sims (cfg5)."""
+    from paper_2102_11026_b200 import rdsim
+    from paper_2102_11026_b200.session import Session
+    P, S = cfg1
+    if batched:
+        monkeypatch.setenv("NLROM_BATCHED", "1")
+    ns = 3
+    sess = Session(P.rm, P.model, P.cm, n_sims=ns)
+    sess._ncub_cache = len(P.cm.C)
+    states = [P.random_state(seed=40 + i) for i in range(ns)]
+    r, rb, rdb = (np.concatenate([s[j] for s in states]) for j in range(3))
+    fext = np.tile(P.f_ext, ns)
+    n = P.cfg.n_p + P.cfg.n_q
+    for integ in ("cubature", "exact_sum"):
+        for drop in (False, True):
+            cfg = rdsim.SimConfig(dt=P.cfg.dt, integration=integ, drop_fict=drop)
+            phi = sess.residual(r, rb, rdb, fext, cfg).reshape(ns, n)
+            Sg = sess.system_jacobian(r, rb, rdb, fext, cfg)
+            oc = ocfg(cfg)
+            for i, (ri, rbi, rdbi) in enumerate(states):
+                assert rel(phi[i], ors.residual(S, ri, (rbi, rdbi), P.f_ext, oc)) < 1e-11, (integ, drop, i)
+                assert rel(Sg[i], ors.system_jacobian(S, ri, (rbi, rdbi), P.f_ext, oc)) < 1e-11, (integ, drop, i)
+    # fixed-iteration steps from rest under per-sim load scales
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=2)
+    scales = [1.0, 0.5, 2.0]
+    fs = np.concatenate([s * P.f_ext for s in scales])
+    st = P.rest_state()
+    rb = np.tile(st.r, ns)
+    rdb = np.tile(st.rdot, ns)
+    for _ in range(3):
+        rb, rdb, _, _ = sess.step(rb, rdb, fs, cfg)
+    for i, s in enumerate(scales):
+        ro, rdo = st.r.copy(), st.rdot.copy()
+        for _ in range(3):
+            ro, rdo, _, _ = ors.step(S, ro, rdo, s * P.f_ext, ocfg(cfg))
+        assert np.abs(rb.reshape(ns, n)[i] - ro).max() <= 1e-10 * np.abs(ro).max(), i
