@@ -122,6 +122,88 @@ def barrier(world):
         dist.barrier()
 
 
+# --------------------------------------------------------------------------- roofline helpers
+def jet_groups(n_q, batched):
+    """Mirror of ctx.cu choose_groups: (columns per group G, groups per sim)."""
+    if batched:
+        g = min((1, 3, 7, 15), key=lambda c: ((4 + 4 * c) * (-(-n_q // c)), c))
+    else:
+        g = next((c for c in (1, 3, 5, 7, 15) if c >= n_q), 3) if n_q <= 15 else 3
+    return 4 + 4 * g, -(-n_q // g)
+
+
+def decoder_flops(P, n_sims=1):
+    """(F_dec per sim per §8d, executed flops per sim of our collapsed passes)."""
+    c = P.cfg
+    N, w, n_p, n_q, L = P.model.N, c.width, c.n_p, c.n_q, c.n_fc
+    widths = [n_q] + [w] * (L - 1) + [N]
+    mac = sum(a * b for a, b in zip(widths[:-1], widths[1:]))
+    hidden_mac = mac - w * N
+    F = (18 * n_q + 6) * (2.0 * mac + 4.0 * N * n_p)
+    G, gps = jet_groups(n_q, n_sims * (4 + 4 * n_q) >= 2048)
+    hid_cols = gps * G                               # grouped jet columns through the sin layers
+    out_cols = 4 + 4 * n_q                           # compact columns through the output layer
+    executed = 2.0 * hid_cols * hidden_mac + 2.0 * out_cols * N * w + 2.0 * N * w + 2.0 * (2 * n_q) * hidden_mac
+    return F, executed
+
+
+def decoder_roofline(P, stage_ms, n_sims, fp64):
+    F, ex = decoder_flops(P, n_sims)
+    dec_ms = stage_ms[0] + stage_ms[1] + stage_ms[2]
+    achieved = F * n_sims / (dec_ms * 1e-3) / 1e12
+    executed = ex * n_sims / (dec_ms * 1e-3) / 1e12
+    return {"bound": "tensor",
+            "kernel": "decoder bundle: k_mlp_jet_fwd (hidden jet chain) + output GEMM (EpiJetOutC) + "
+                      "k_gemv_t/k_mlp_dual_bwd (vhp backprop chain), fp64 DMMA",
+            "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+            "frac": (achieved / fp64) if fp64 else None, "traffic": None,
+            "peak_source": "profiles/fp64_peak.json: measured DMMA.8x8x4 fp64 (MEASURED_PEAKS.json has no fp64 entry)",
+            "kernel_ms": dec_ms, "algorithmic_flops_per_launch": F * n_sims,
+            "algorithmic_def": "SURVEY.md §8d F_dec = (18 n_q+6)(2 sum in*out + 4 N n_p) per sim (reference pass structure)",
+            "executed_flops_per_launch": ex * n_sims, "executed_tflops": executed,
+            "executed_frac": (executed / fp64) if fp64 else None,
+            "stages_ms": {"k_mlp_jet_fwd": stage_ms[0], "output_gemm": stage_ms[1], "vhp_bwd": stage_ms[2]}}
+
+
+def batched_leg(args, rank, world):
+    """cfg5: 4096 independent 10-layer DAE sims, sharded over the ranks with
+    no data-path collective; one graph replay = one Newton iteration of every local sim."""
+    import torch
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200 import rdsim
+    from paper_2102_11026_b200.session import Session
+    P = build_problem("cfg5")
+    total = args.batched_sims
+    lo, hi = rank * total // world, (rank + 1) * total // world
+    ns = hi - lo
+    n = P.cfg.n_p + P.cfg.n_q
+    rng = np.random.default_rng(4 + lo)
+    rb = rng.uniform(-0.05, 0.05, ns * n)
+    rdb = rng.uniform(-0.1, 0.1, ns * n)
+    s = Session(P.rm, P.model, P.cm, n_sims=ns)
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=1)
+    s.step(rb, rdb, np.tile(P.f_ext, ns), cfg)
+    iters = 10
+    s.bench_iterations(3, flush_l2=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    tot, _ = s.bench_iterations(iters, flush_l2=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = barrier_max(world, tot / iters)
+    _, fp64 = peaks()
+    stage_ms = s.bench_kernels(3, flush_l2=True)
+    roof = decoder_roofline(P, stage_ms, ns, fp64)
+    launches = s.launches_per_iteration()
+    del s
+    return {"workload": "cfg5: %d independent sims (10-layer w256 DAE, n_q=20, n_p=10, N=960, |C|=100), "
+                        "%d per GPU, no per-iteration collective" % (total, ns),
+            "scaling": "strong (total sims fixed)", "ms_per_iteration": ms,
+            "sim_iterations_per_s": total * 1e3 / ms, "iterations": iters,
+            "l2": "flushed between timed iterations", "decoder_roofline_rank0": roof,
+            "gpu_launches_per_iteration": launches}
+
+
 # --------------------------------------------------------------------------- CPU arms
 def oracle_iteration_runner(P):
     """One Newton iteration of the reference algorithm (numpy fp64 restatement of SPEC
@@ -222,40 +304,26 @@ def run_ours(args):
     h2d = (2 * n + P.model.N) * 8
     d2h = 2 * n * 8 + 8
 
-    # roofline of the dominant kernel: every stage timed live with CUDA events on the context
-    # stream (L2 flushed before each launch); the largest device-time share is "dominant".
+    # roofline: every stage timed live with CUDA events on the context stream (L2 flushed
+    # before each launch). The decoder bundle (hidden jet chain + output layer + vhp
+    # backward chain) is the dominant unit (>= 60% of the step); its algorithmic work is
+    # SURVEY.md §8d F_dec = (18 n_q + 6)(2 sum_l in_l out_l + 4 N n_p) per sim, the
+    # reference's pass structure. Executed flops of the collapsed passes are reported beside it.
     pk, fp64 = peaks()
     stage_ms = s.bench_kernels(max(20, args.steps // 4), flush_l2=True)
-    N, w, n_p, n_q, L = P.model.N, P.cfg.width, P.cfg.n_p, P.cfg.n_q, P.cfg.n_fc
-    n = n_p + n_q
-    cols = 4 + 4 * n_q                      # jet columns without the per-group base replicas
-    hidden_mac = n_q * w + (L - 2) * w * w  # sum_l in_l * out_l over the L-1 sin layers
-    stages = [
-        ("k_mlp_jet_fwd (fused hidden jet chain, fp64 DMMA, cluster/DSMEM)", 2.0 * cols * hidden_mac,
-         (16 * n_q + 5) * 2.0 * hidden_mac),
-        ("gemm_tn_kernel<CfgOutC,EpiJetOutC> (decoder output layer, filter folded)", 2.0 * N * w * cols,
-         (16 * n_q + 5) * (2.0 * N * w + 4.0 * N * n_p)),
-        ("k_gemv_t + k_mlp_dual_bwd (vhp complex-step backprop chain)",
-         2.0 * N * w + 2.0 * (2 * n_q) * (hidden_mac - n_q * w + n_q * w), (2 * n_q + 1) * 2.0 * (hidden_mac + N * w)),
-        ("k_lu_solve (in-CTA LU with partial pivoting)", 2.0 * n ** 3 / 3.0, 2.0 * n ** 3 / 3.0),
-    ]
-    k = int(np.argmax(stage_ms))
-    name, alg_flops, ref_flops = stages[k]
-    achieved = alg_flops / (stage_ms[k] * 1e-3) / 1e12
-    peak = fp64 if fp64 else None
-    roof = {"bound": "tensor", "kernel": name,
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": (achieved / peak) if peak else None, "traffic": None,
-            "peak_source": "profiles/fp64_peak.json: measured DMMA.8x8x4 fp64 (MEASURED_PEAKS.json has no fp64 entry)",
-            "kernel_ms": stage_ms[k], "algorithmic_flops_per_launch": alg_flops,
-            "reference_pass_structure_flops_per_launch": ref_flops,
-            "stages_ms": {st[0].split(" ")[0]: ms for st, ms in zip(stages, stage_ms)},
-            "share_of_step": stage_ms[k] / ms_iter}
+    roof = decoder_roofline(P, stage_ms, 1, fp64)
+    roof["share_of_step"] = roof["kernel_ms"] / ms_iter
+    roof["lu_ms"] = stage_ms[3]
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "dominant_traffic.json")))
-        roof["traffic"] = tr.get(name.split(" ")[0], {}).get("dram_bytes_per_launch")
+        roof["traffic"] = sum(tr.get(k, {}).get("dram_bytes_per_launch", 0) for k in
+                              ("k_mlp_jet_fwd", "gemm_tn_kernel<CfgOutC,EpiJetOutC>", "k_gemv_t", "k_mlp_dual_bwd")) or None
     except Exception:
         pass
+
+    batched = None
+    if not args.no_batched:
+        batched = batched_leg(args, rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -273,6 +341,7 @@ def run_ours(args):
                     "how": "nlrom.rdsim.step (host numpy in/out), fixed_iters=3, wall clock / 3"},
             "gpu_launches": s.launches_per_iteration() * args.steps,
             "roofline": roof,
+            "batched_cfg5": batched,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "hz_at_3_iters": 1000.0 / (3 * value),
@@ -290,6 +359,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batched", action="store_true", help="skip the cfg5 4096-sim throughput leg")
+    ap.add_argument("--batched-sims", type=int, default=4096)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -33,8 +33,10 @@ namespace {
 using CfgBwd = GemmCfg<16, 16, 1, 1, 4, 32, 8>;
 template <int G> using CfgHid = GemmCfg<16, G, 1, 1, 4, 32, (G <= 32 ? 8 : 4)>;
 template <int G> using CfgOut = GemmCfg<64, G, 4, 1, 1, 32, 4>;
-// batched (many sims): 64 x 128 tiles, 8 warps, 32-wide K tiles, 3 stages
-using CfgBig = GemmCfg<64, 128, 2, 4, 1, 32, 3>;
+// batched (many sims): 64 x 128 tiles, 8 warps, 16-wide K tiles, 3 stages: 90 KB smem so two
+// CTAs share an SM and one's epilogue overlaps the other's DMMA loop (tools/probes/gemm_probe.cu:
+// 26.7 TFLOP/s vs 22.1 for 32-wide K tiles at one CTA per SM, M = K = 256, 393k columns)
+using CfgBig = GemmCfg<64, 128, 2, 4, 1, 16, 3>;
 
 struct CubSet {
   IBuf elems;
@@ -154,11 +156,18 @@ void out_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st) {
   ++gemm_launch_count;
 }
 
-void choose_groups(int n_q, int width, int& G, int& gps) {
+void choose_groups(int n_q, int width, bool batched, int& G, int& gps) {
   const int cand[5] = {1, 3, 5, 7, 15};
   int g = 3;
   if (const char* env = getenv("NLROM_JET_TANGENTS")) g = atoi(env);
-  else if (n_q <= 15) {
+  else if (batched) {
+    // big 128-column tiles: G | 128, fewest executed columns G * ceil(n_q / g)
+    int best = 1 << 30;
+    for (int c : {1, 3, 7, 15}) {
+      const int cols = (4 + 4 * c) * ((n_q + c - 1) / c);
+      if (cols < best) { best = cols; g = c; }
+    }
+  } else if (n_q <= 15) {
     for (int c : cand)
       if (c >= n_q) { g = c; break; }
   } else {
@@ -211,7 +220,8 @@ void output_layer(nlrom_ctx* c) {
   GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->next, 0, 0};
   EpiJetOutC e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
                c->n_p, c->n_q};
-  launch_gemm<CfgOutC>(g, e, c->st);
+  if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
+  else launch_gemm<CfgOutC>(g, e, c->st);
   ++gemm_launch_count;
 }
 
@@ -686,10 +696,10 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       c->wC.alloc((size_t)c->n_sims * std::max(1, c->n_cub));
     }
     // bundle buffers
-    choose_groups(n_q, w, c->G, c->gps);
-    c->Cb = c->G * c->gps;
     c->Cc = 4 + 4 * n_q;  // compact (de-replicated) columns per sim
-    c->batched = c->n_sims * c->Cb >= 2048 || getenv("NLROM_BATCHED") != nullptr;
+    c->batched = c->n_sims * c->Cc >= 2048 || getenv("NLROM_BATCHED") != nullptr;
+    choose_groups(n_q, w, c->batched, c->G, c->gps);
+    c->Cb = c->G * c->gps;
     c->ldq = round_up(n_q, 2);
     const int ncols = c->n_sims * c->Cb;
     c->X0.alloc((size_t)ncols * c->ldq);
