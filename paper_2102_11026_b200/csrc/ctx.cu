@@ -167,6 +167,8 @@ void choose_groups(int n_q, int width, bool batched, int& G, int& gps) {
       const int cols = (4 + 4 * c) * ((n_q + c - 1) / c);
       if (cols < best) { best = cols; g = c; }
     }
+  } else if (width > 64) {
+    g = 3;  // wide decoders: G = 16 is the fused hidden chain that fits in shared memory
   } else if (n_q <= 15) {
     for (int c : cand)
       if (c >= n_q) { g = c; break; }
@@ -488,6 +490,20 @@ bool fused_vhp_backward(nlrom_ctx* c) {
   return go(false);
 }
 
+// In-CTA LU-pp solve of every sim's Eq. 11 system; register block sized to n + 1.
+void launch_lu(nlrom_ctx* c, bool apply) {
+  const int n = c->n;
+  auto go = [&](auto kern) {
+    launch(c, kern, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
+           c->r.p, n, apply ? 1 : 0, c->status.p);
+  };
+  switch (lu_nb(n)) {
+    case 4: go(k_lu_solve<4>); break;
+    case 6: go(k_lu_solve<6>); break;
+    default: go(k_lu_solve<8>); break;
+  }
+}
+
 void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply) {
   if (!fused_vhp_backward(c))
     decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
@@ -495,12 +511,7 @@ void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply) {
   const int n = c->n;
   launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
          (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
-  if (n + 1 <= 64)
-    launch(c, k_lu_solve<4>, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p,
-           c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p);
-  else
-    launch(c, k_lu_solve<8>, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p,
-           c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p);
+  launch_lu(c, apply);
 }
 
 size_t lu_smem(int n) {
@@ -759,6 +770,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     if (c->n + 1 > 128) throw Error(NLROM_ERR_ARG, "n_p + n_q must be <= 127");
     NL_CUDA(cudaDeviceSynchronize());
@@ -1135,12 +1147,8 @@ extern "C" int nlrom_bench_kernels(nlrom_ctx* c, int n_iters, int flush_l2, floa
         break;
       default: {
         const int n = c->n;
-        if (n + 1 <= 64)
-          launch(c, k_lu_solve<4>, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p,
-                 c->dr.p, c->r.p, n, 0, c->status.p);
-        else
-          launch(c, k_lu_solve<8>, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p,
-                 c->dr.p, c->r.p, n, 0, c->status.p);
+        (void)n;
+        launch_lu(c, false);
       }
     }
   };

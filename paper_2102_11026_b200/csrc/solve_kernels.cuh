@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
       const double la = l[a] * rp;
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
+        if (NB > 4 && 16 * b + 15 <= k) continue;  // column block already eliminated (uniform)
         const int j = tx + 16 * b;
         if (act[a] && j > k) {
           A[a][b] = fma(-la, pr[b], A[a][b]);
@@ -356,8 +357,9 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
   }
 }
 
+inline int lu_nb(int n) { return (n + 1 <= 64) ? 4 : (n + 1 <= 96) ? 6 : 8; }
 inline size_t lu_smem_bytes(int n) {
-  const int D = (n + 1 <= 64) ? 64 : 128;
+  const int D = 16 * lu_nb(n);
   return (size_t)D * (D + 1) * 8;
 }
 

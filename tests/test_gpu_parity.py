@@ -258,3 +258,26 @@ def test_multi_sim(cfg1, batched, monkeypatch):
         for _ in range(3):
             ro, rdo, _, _ = ors.step(S, ro, rdo, s * P.f_ext, ocfg(cfg))
         assert np.abs(rb.reshape(ns, n)[i] - ro).max() <= 1e-10 * np.abs(ro).max(), i
+
+
+# ------------------------------------------------------------------ cfg3 corners (latent-dim x depth sweep)
+@pytest.mark.parametrize("n_q,L,n_p", [(5, 4, 30), (64, 16, 30), (48, 6, 30), (64, 4, 62), (10, 5, 30)])
+def test_cfg3_corners(cuda_ok, n_q, L, n_p):
+    """cfg2 mesh with n_q in 5..64 and depth 4..16 (fused-chain and LU size limits)."""
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200 import rdsim
+    from paper_2102_11026_b200.daereduce import ReducedState
+    P = build_problem("cfg2", n_q=n_q, n_fc=L, n_p=n_p)   # n = 126 exercises the widest LU block
+    S = oracle_sim(P)
+    r, rb, rdb = P.random_state()
+    cfg = rdsim.SimConfig(dt=P.cfg.dt)
+    st = ReducedState(rb, rdb, cfg.dt)
+    oc = ocfg(cfg)
+    assert rel(rdsim.residual(P.rm, P.model, st, P.f_ext, cfg, r=r), ors.residual(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+    assert rel(rdsim.system_jacobian(P.rm, P.model, st, P.f_ext, cfg, r=r),
+               ors.system_jacobian(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+    cfgf = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=2)
+    st0 = P.rest_state()
+    got = rdsim.step(P.rm, P.model, st0, P.f_ext, cfgf)
+    ro, _, _, _ = ors.step(S, st0.r.copy(), st0.rdot.copy(), P.f_ext, ocfg(cfgf))
+    assert np.abs(got.r - ro).max() <= 1e-10 * np.abs(ro).max()
