@@ -165,6 +165,53 @@ def decoder_roofline(P, stage_ms, n_sims, fp64):
             "stages_ms": {"k_mlp_jet_fwd": stage_ms[0], "output_gemm": stage_ms[1], "vhp_bwd": stage_ms[2]}}
 
 
+def coupled_leg(args, rank, world):
+    """cfg4: the 320-string puffer ball, strings sharded over the ranks, the core
+    replicated; per Newton iteration one graph per rank + ONE allreduce of 16 doubles (NCCL on
+    the context stream) + the core solve / string update. Device time per iteration with CUDA
+    events on the context stream, L2 flushed before every iteration, max over ranks."""
+    import torch
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200 import rdsim, synth
+    from paper_2102_11026_b200.substructure import Core, Scene
+    P = build_problem("cfg4")
+    k = args.strings
+    R = synth.string_frames(k)
+    f_world = np.tile(P.f_ext, (k, 1))
+    m_core = 2.0 * float(P.model.mass[0::3].sum())
+    sc = Scene(P.rm, P.model, P.cm, R, f_world, Core(m_core, 50.0, np.array([0.0, -9.81 * m_core, 0.0])))
+    rb, rdb, cb, cdb = synth.coupled_state(k, P.cfg.n_p, P.cfg.n_q)
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=1)
+    sc.step(rb, rdb, cb, cdb, cfg)          # captures the graphs
+    sc.begin(rb, rdb, cb, cdb, cfg)
+    flush = torch.empty(32 << 20, dtype=torch.float64, device=sc.partial.device)
+    iters = 20
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for _ in range(3):
+        sc.eval(True); sc.reduce(); sc.update(1, 1.0)
+    barrier(world)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(sc.stream):
+        for e0, e1 in evs:
+            flush.fill_(1.0)
+            e0.record(sc.stream)
+            sc.eval(True)
+            sc.reduce()
+            sc.update(1, 1.0)
+            e1.record(sc.stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = barrier_max(world, sum(e0.elapsed_time(e1) for e0, e1 in evs) / iters)
+    _, _, _, _, _, nrm = sc.step(rb, rdb, cb, cdb, rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=3))
+    return {"workload": "cfg4: puffer ball, %d strings x (36x3x3 tets, N=1728, n_p=10, n_q=5, 8-layer w64 DAE, "
+                        "|C|=36) on a translating core, %d strings on rank 0" % (k, sc.hi - sc.lo),
+            "scaling": "strong (total strings fixed)", "ms_per_newton_iteration": ms,
+            "string_iterations_per_s": k * 1e3 / ms, "exchange": "1 allreduce of 16 fp64 per iteration"
+            + (" (NCCL)" if world > 1 else " (single rank: none)"),
+            "residual_after_3_iters": nrm, "l2": "flushed before every iteration",
+            "gpu_launches_per_iteration": sc.launches_per_iteration()}
+
+
 def batched_leg(args, rank, world):
     """cfg5: 4096 independent 10-layer DAE sims, sharded over the ranks with
     no data-path collective; one graph replay = one Newton iteration of every local sim."""
@@ -324,6 +371,9 @@ def run_ours(args):
     batched = None
     if not args.no_batched:
         batched = batched_leg(args, rank, world)
+    coupled = None
+    if not args.no_coupled:
+        coupled = coupled_leg(args, rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -342,6 +392,7 @@ def run_ours(args):
             "gpu_launches": s.launches_per_iteration() * args.steps,
             "roofline": roof,
             "batched_cfg5": batched,
+            "coupled_cfg4": coupled,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "hz_at_3_iters": 1000.0 / (3 * value),
@@ -361,6 +412,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batched", action="store_true", help="skip the cfg5 4096-sim throughput leg")
     ap.add_argument("--batched-sims", type=int, default=4096)
+    ap.add_argument("--no-coupled", action="store_true", help="skip the cfg4 320-string coupled leg")
+    ap.add_argument("--strings", type=int, default=320)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -209,6 +209,36 @@ NLROM_API int nlrom_bench_kernels(nlrom_ctx* ctx, int n_iters, int flush_l2, flo
 /* Number of kernel launches of one Newton iteration (for bench "gpu_launches"). */
 NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
 
+/* The context's CUDA stream (cudaStream_t) -- every call above is ordered on it; a host
+ * that interleaves its own collectives (NCCL) with the coupled phases below uses it. */
+NLROM_API int nlrom_stream(nlrom_ctx* ctx, void** stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Substructured scene (SURVEY.md §8e, cfg4 puffer ball, PAPER.md:84/580/603). No reference
+ * interface exists (the reference has no coupled scenes); the model is
+ * oracle/coupled.py. This context's n_sims sims are strings [lo, hi) of a scene of k_total
+ * strings sharing the networks, attached to a translating core (3 DOFs) replicated on every
+ * rank. One Newton iteration on every rank:
+ *   nlrom_coupled_eval(ctx, cfg, 1, partial)          16 doubles into device buffer `partial`
+ *   allreduce-sum(partial -> total) over the ranks     (host: NCCL on nlrom_stream; skip at 1 rank)
+ *   nlrom_coupled_update(ctx, cfg, total, 1, 1.0, 0)  Schur solve for the core, r_s / c update
+ * mode 0: residual norm only (after eval(jacobian=0)); mode 1: direction + apply(t);
+ * mode 2: re-apply the last direction with step t (line search). norm_host (optional) receives
+ * ||[phi_1 .. phi_k, phi_c]||_2 (synchronises). */
+NLROM_API int nlrom_coupled_setup(nlrom_ctx* ctx, const double* R /* n_sims x 3 x 3, string -> world */,
+                                  const double* f_world /* n_sims x N */, int k_total, double m_core,
+                                  double k_core, const double* f_core /* 3 */);
+NLROM_API int nlrom_coupled_begin(nlrom_ctx* ctx, const double* r_bar, const double* rdot_bar,
+                                  const double* c_bar /* 3 */, const double* cdot_bar /* 3 */,
+                                  const nlrom_simcfg* cfg);
+NLROM_API int nlrom_coupled_eval(nlrom_ctx* ctx, const nlrom_simcfg* cfg, int jacobian, double* partial_dev);
+NLROM_API int nlrom_coupled_update(nlrom_ctx* ctx, const nlrom_simcfg* cfg, const double* total_dev, int mode,
+                                   double t, double* norm_host);
+NLROM_API int nlrom_coupled_read(nlrom_ctx* ctx, double dt, double* r, double* rdot, double* core_c,
+                                 double* core_cdot);
+/* kernel launches of one coupled Newton iteration (eval graph + update) */
+NLROM_API int nlrom_coupled_launches(nlrom_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,9 @@ EXPORTED = [
     "nlrom_system_jacobian", "nlrom_delta_j", "nlrom_fictitious_force", "nlrom_wnet_forward",
     "nlrom_cubature_integrate", "nlrom_full_displacement", "nlrom_jtilde", "nlrom_step", "nlrom_step_device",
     "nlrom_bench_iterations", "nlrom_launches_per_iteration", "nlrom_element_forces",
-    "nlrom_element_reduced_forces", "nlrom_bench_kernels",
+    "nlrom_element_reduced_forces", "nlrom_bench_kernels", "nlrom_stream", "nlrom_coupled_setup",
+    "nlrom_coupled_begin", "nlrom_coupled_eval", "nlrom_coupled_update", "nlrom_coupled_read",
+    "nlrom_coupled_launches",
 ]
 
 
@@ -98,6 +100,13 @@ def lib():
             "nlrom_bench_kernels": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
             "nlrom_element_forces": (C.c_int, [vp, dp, C.c_int, dp, dp]),
             "nlrom_element_reduced_forces": (C.c_int, [vp, dp, ip, C.c_int, dp]),
+            "nlrom_stream": (C.c_int, [vp, C.POINTER(vp)]),
+            "nlrom_coupled_setup": (C.c_int, [vp, dp, dp, C.c_int, C.c_double, C.c_double, dp]),
+            "nlrom_coupled_begin": (C.c_int, [vp, dp, dp, dp, dp, C.POINTER(SimCfg)]),
+            "nlrom_coupled_eval": (C.c_int, [vp, C.POINTER(SimCfg), C.c_int, vp]),
+            "nlrom_coupled_update": (C.c_int, [vp, C.POINTER(SimCfg), vp, C.c_int, C.c_double, dp]),
+            "nlrom_coupled_read": (C.c_int, [vp, C.c_double, dp, dp, dp, dp]),
+            "nlrom_coupled_launches": (C.c_int, [vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -18,6 +18,7 @@
 #include "sim_kernels.cuh"
 #include "solve_kernels.cuh"
 #include "mlp_chain.cuh"
+#include "coupled_kernels.cuh"
 
 namespace nlrom {
 void fc_forward(int order, int act, const GemmArgs& g, double* Y, int ldy, const double* bias, double* cache,
@@ -97,6 +98,13 @@ struct nlrom_ctx {
   int launches_E = 0, launches_J = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DBuf flush;
+  // substructured scene (coupled_kernels.cuh): strings of this rank + replicated core
+  bool coupled = false;
+  DBuf cpR, cpFloc, cpFsum, cpCore, cpBlocks, cpCb, cpX, cpFcore;
+  double cp_m_core = 0, cp_k_core = 0, cp_m_string = 0, cp_m_total = 0;
+  cudaGraphExec_t gC[2] = {nullptr, nullptr};
+  std::string cp_key[2];
+  int launches_C[2] = {0, 0};
 };
 
 namespace {
@@ -491,27 +499,29 @@ bool fused_vhp_backward(nlrom_ctx* c) {
 }
 
 // In-CTA LU-pp solve of every sim's Eq. 11 system; register block sized to n + 1.
-void launch_lu(nlrom_ctx* c, bool apply) {
+// Extra right-hand sides (xrhs, nx columns of n per sim) are solved alongside -phi into xout.
+void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 0, double* xout = nullptr) {
   const int n = c->n;
   auto go = [&](auto kern) {
-    launch(c, kern, c->n_sims, 256, lu_smem_bytes(n), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
-           c->r.p, n, apply ? 1 : 0, c->status.p);
+    launch(c, kern, c->n_sims, 256, lu_smem_bytes(n + nx), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
+           c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout);
   };
-  switch (lu_nb(n)) {
+  switch (lu_nb(n + nx)) {
     case 4: go(k_lu_solve<4>); break;
     case 6: go(k_lu_solve<6>); break;
     default: go(k_lu_solve<8>); break;
   }
 }
 
-void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply) {
+void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply, const double* xrhs = nullptr, int nx = 0,
+             double* xout = nullptr) {
   if (!fused_vhp_backward(c))
     decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   const int n = c->n;
   launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
          (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
-  launch_lu(c, apply);
+  launch_lu(c, apply, xrhs, nx, xout);
 }
 
 size_t lu_smem(int n) {
@@ -772,7 +782,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    if (c->n + 1 > 128) throw Error(NLROM_ERR_ARG, "n_p + n_q must be <= 127");
+    if (c->n + 4 > 128) throw Error(NLROM_ERR_ARG, "n_p + n_q must be <= 124");
     NL_CUDA(cudaDeviceSynchronize());
     *out = c;
     return NLROM_OK;
@@ -790,6 +800,8 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->gE) cudaGraphExecDestroy(c->gE);
   if (c->gJ) cudaGraphExecDestroy(c->gJ);
   if (c->gIter) cudaGraphExecDestroy(c->gIter);
+  for (auto g : c->gC)
+    if (g) cudaGraphExecDestroy(g);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->st) cudaStreamDestroy(c->st);
@@ -1210,4 +1222,160 @@ extern "C" int nlrom_element_reduced_forces(nlrom_ctx* c, const double* r, const
   d2h(c, out, fo, (size_t)n_elems * c->n);
   NL_CUDA(cudaStreamSynchronize(c->st));
   CTX_END(c)
+}
+
+// =========================================================================== substructured scene
+// this context's sims are strings [lo, hi) of a scene of k_total strings
+// on a translating core; the host drives one Newton iteration as
+//   nlrom_coupled_eval(jacobian=1) -> allreduce(partial, 16 doubles) -> nlrom_coupled_update(mode 1)
+// (model: oracle/coupled.py; kernels: coupled_kernels.cuh).
+
+namespace {
+
+void coupled_body(nlrom_ctx* c, const nlrom_simcfg& cfg, int jac, double* partial) {
+  const double h = cfg.dt, ah = c->alpha * cfg.dt;
+  const int S = c->n_sims, n = c->n;
+  launch(c, k_cp_fext, grid1((long long)S * c->N), 256, 0, (const double*)c->cpFloc.p, (const double*)c->cpR.p,
+         (const double*)c->cpCore.p, (const double*)c->mass.p, c->N, S, h, ah, c->fext.p);
+  phase_E(c, cfg);
+  launch(c, k_cp_blocks, S, 256, 0, (const double*)c->Jt.p, c->ldjt, (const double*)c->dJ.p, c->lddj,
+         (const double*)c->hvv.p, (const double*)c->mass.p, (const double*)c->cpR.p, c->N, n, c->n_q, cfg.drop_fict,
+         ah, c->cpBlocks.p, c->cpCb.p);
+  if (jac) phase_J(c, cfg, false, c->cpCb.p, 3, c->cpX.p);
+  CpPartialArgs A{c->cpR.p, c->cpBlocks.p, c->cpFsum.p, c->cpCore.p, c->r.p, c->rbar.p, c->rdbar.p, c->phi.p,
+                  c->cpX.p, c->dr.p, S, n, c->n_p, c->n_q, h, ah, c->cp_m_string, jac, partial};
+  launch(c, k_cp_partial, 1, 256, 0, A);
+}
+
+void coupled_graph(nlrom_ctx* c, const nlrom_simcfg& cfg, int jac, double* partial) {
+  char buf[64];
+  snprintf(buf, sizeof buf, "|%p", (void*)partial);
+  const std::string key = cfg_key(cfg) + buf;
+  if (c->gC[jac] && c->cp_key[jac] == key) return;
+  if (c->gC[jac]) cudaGraphExecDestroy(c->gC[jac]);
+  c->gC[jac] = nullptr;
+  coupled_body(c, cfg, jac, partial);  // eager warm-up (kernel attributes outside capture)
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  c->gC[jac] = capture(c, [&] { coupled_body(c, cfg, jac, partial); }, &c->launches_C[jac]);
+  c->cp_key[jac] = key;
+}
+
+void require_coupled(nlrom_ctx* c) {
+  if (!c->coupled) throw Error(NLROM_ERR_ARG, "call nlrom_coupled_setup first");
+}
+
+}  // namespace
+
+extern "C" int nlrom_stream(nlrom_ctx* c, void** stream) {
+  CTX_TRY(c)
+  if (!stream) throw Error(NLROM_ERR_ARG, "null argument");
+  *stream = (void*)c->st;
+  CTX_END(c)
+}
+
+extern "C" int nlrom_coupled_setup(nlrom_ctx* c, const double* R, const double* f_world, int k_total, double m_core,
+                                   double k_core, const double* f_core) {
+  CTX_TRY(c)
+  if (!R || !f_world || !f_core) throw Error(NLROM_ERR_ARG, "null argument");
+  if (k_total < c->n_sims) throw Error(NLROM_ERR_DIM, "k_total must cover this context's strings");
+  const int S = c->n_sims, N = c->N, n = c->n;
+  std::vector<double> mass(N), floc((size_t)S * N), fsum((size_t)S * 3, 0.0);
+  NL_CUDA(cudaMemcpy(mass.data(), c->mass.p, N * 8, cudaMemcpyDeviceToHost));
+  double ms = 0.0;
+  for (int i = 0; i < N; i += 3) ms += mass[i];
+  for (int s = 0; s < S; ++s) {
+    const double* Rs = R + (size_t)s * 9;
+    for (int v = 0; v < N / 3; ++v) {
+      const double* fw = f_world + (size_t)s * N + 3 * v;
+      for (int d = 0; d < 3; ++d) {
+        floc[(size_t)s * N + 3 * v + d] = Rs[0 * 3 + d] * fw[0] + Rs[1 * 3 + d] * fw[1] + Rs[2 * 3 + d] * fw[2];
+        fsum[(size_t)s * 3 + d] += fw[d];
+      }
+    }
+  }
+  upload(c->cpR, R, (size_t)S * 9);
+  upload(c->cpFloc, floc.data(), floc.size());
+  upload(c->cpFsum, fsum.data(), fsum.size());
+  upload(c->cpFcore, f_core, 3);
+  c->cpCore.alloc(CORE_SIZE);
+  c->cpBlocks.alloc((size_t)S * (3 * (n + c->n_q) + 3));
+  c->cpCb.alloc((size_t)S * 3 * n);
+  c->cpX.alloc((size_t)S * 3 * n);
+  c->cp_m_core = m_core;
+  c->cp_k_core = k_core;
+  c->cp_m_string = ms;
+  c->cp_m_total = m_core + (double)k_total * ms;
+  c->coupled = true;
+  CTX_END(c)
+}
+
+extern "C" int nlrom_coupled_begin(nlrom_ctx* c, const double* r_bar, const double* rdot_bar, const double* c_bar,
+                                   const double* cdot_bar, const nlrom_simcfg* cfg) {
+  CTX_TRY(c)
+  require_coupled(c);
+  const int nn = c->n_sims * c->n;
+  set_state(c, nullptr, r_bar, rdot_bar, nullptr);
+  double core[CORE_SIZE] = {};
+  for (int a = 0; a < 3; ++a) {
+    core[CORE_C + a] = c_bar[a] + cfg->dt * cdot_bar[a];
+    core[CORE_CBAR + a] = c_bar[a];
+    core[CORE_CDBAR + a] = cdot_bar[a];
+  }
+  NL_CUDA(cudaMemcpyAsync(c->cpCore.p, core, sizeof core, cudaMemcpyHostToDevice, c->st));
+  launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg->dt, nn);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_coupled_eval(nlrom_ctx* c, const nlrom_simcfg* cfg, int jacobian, double* partial_dev) {
+  CTX_TRY(c)
+  require_coupled(c);
+  if (!partial_dev) throw Error(NLROM_ERR_ARG, "null partial buffer");
+  const int j = jacobian ? 1 : 0;
+  coupled_graph(c, *cfg, j, partial_dev);
+  NL_CUDA(cudaGraphLaunch(c->gC[j], c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_coupled_update(nlrom_ctx* c, const nlrom_simcfg* cfg, const double* total_dev, int mode, double t,
+                                    double* norm_host) {
+  CTX_TRY(c)
+  require_coupled(c);
+  const double h = cfg->dt, ah = c->alpha * cfg->dt;
+  const int nn = c->n_sims * c->n;
+  if (mode == 0 || mode == 1)
+    launch(c, k_cp_update, 1, 32, 0, total_dev, c->cpCore.p, h, ah, c->cp_m_core, c->cp_m_total, c->cp_k_core,
+           (const double*)c->cpFcore.p, mode);
+  if (mode == 1) NL_CUDA(cudaMemcpyAsync(c->rsave.p, c->r.p, (size_t)nn * 8, cudaMemcpyDeviceToDevice, c->st));
+  if (mode == 1 || mode == 2)
+    launch(c, k_cp_apply, grid1(nn), 256, 0, c->r.p, (const double*)c->rsave.p, (const double*)c->dr.p,
+           (const double*)c->cpX.p, c->cpCore.p, c->n_sims, c->n, t);
+  if (norm_host) {
+    check_status(c);
+    NL_CUDA(cudaMemcpyAsync(norm_host, c->cpCore.p + CORE_NORM, 8, cudaMemcpyDeviceToHost, c->st));
+    NL_CUDA(cudaStreamSynchronize(c->st));
+  }
+  CTX_END(c)
+}
+
+extern "C" int nlrom_coupled_read(nlrom_ctx* c, double dt, double* r, double* rdot, double* core_c, double* core_cdot) {
+  CTX_TRY(c)
+  require_coupled(c);
+  const int nn = c->n_sims * c->n;
+  launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / dt, nn);
+  double core[CORE_SIZE];
+  check_status(c);
+  d2h(c, r, c->r, nn);
+  d2h(c, rdot, c->rdot, nn);
+  NL_CUDA(cudaMemcpyAsync(core, c->cpCore.p, sizeof core, cudaMemcpyDeviceToHost, c->st));
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  for (int a = 0; a < 3; ++a) {
+    core_c[a] = core[CORE_C + a];
+    core_cdot[a] = (core[CORE_C + a] - core[CORE_CBAR + a]) / dt;
+  }
+  CTX_END(c)
+}
+
+extern "C" int nlrom_coupled_launches(nlrom_ctx* c) {
+  return c ? c->launches_C[1] + 2 : 0;
 }

@@ -209,7 +209,8 @@ __global__ void k_reduce_cub(const double* __restrict__ part_f, const double* __
 template <int NB>
 __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, const double* __restrict__ phi,
                                                    double* __restrict__ dr, double* __restrict__ r, int n, int apply,
-                                                   int* __restrict__ status) {
+                                                   int* __restrict__ status, const double* __restrict__ xrhs, int nx,
+                                                   double* __restrict__ xout) {
   pdl_wait();
   pdl_launch();
   constexpr int D = 16 * NB;           // covered rows / columns (n + 1 <= D)
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     double* dst = M + i * LDF + j;
     if (i < n && j < n) cp_async8(dst, Ss + (size_t)i * n + j);
     else if (i < n && j == n) cp_async8(dst, phi + (size_t)sim * n + i);
+    else if (i < n && j > n && j <= n + nx) cp_async8(dst, xrhs + ((size_t)sim * nx + (j - n - 1)) * n + i);
     else *dst = 0.0;
   }
   cp_async_all_wait();
@@ -315,7 +317,10 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     if (tid == 0) status[sim] = 1;
     return;
   }
-  if (tid < 32) {
+  // back substitution: warp 0 for -phi (column n), warp w for extra right-hand side w
+  const int warp = tid >> 5;
+  if (warp <= nx) {
+    const int col = n + warp;
     constexpr int NU = (D + 31) / 32;
     double bv[NU];
     const double* rowp[NU];  // physical U rows of this lane's unknowns, resolved once
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     for (int u = 0; u < NU; ++u) {
       const int t = lane + 32 * u;
       rowp[u] = M + (t < n ? pivrow[t] : 0) * LDF;
-      bv[u] = (t < n) ? rowp[u][n] : 0.0;
+      bv[u] = (t < n) ? rowp[u][col] : 0.0;
     }
 #pragma unroll 4
     for (int t = n - 1; t >= 0; --t) {
@@ -349,14 +354,19 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     for (int u = 0; u < NU; ++u) {
       const int t = lane + 32 * u;
       if (t < n) {
-        dr[(size_t)sim * n + t] = bv[u];
-        if (apply) r[(size_t)sim * n + t] += bv[u];
+        if (warp == 0) {
+          dr[(size_t)sim * n + t] = bv[u];
+          if (apply) r[(size_t)sim * n + t] += bv[u];
+        } else {
+          xout[((size_t)sim * nx + warp - 1) * n + t] = bv[u];
+        }
       }
     }
-    if (lane == 0) status[sim] = 0;
+    if (tid == 0) status[sim] = 0;
   }
 }
 
+// n: unknowns + extra right-hand sides (D >= n + 1 columns incl. -phi)
 inline int lu_nb(int n) { return (n + 1 <= 64) ? 4 : (n + 1 <= 96) ? 6 : 8; }
 inline size_t lu_smem_bytes(int n) {
   const int D = 16 * lu_nb(n);

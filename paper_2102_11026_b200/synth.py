@@ -209,3 +209,34 @@ def gravity(mass: np.ndarray, g: float = -9.81):
     f = np.zeros_like(mass)
     f[1::3] = mass[1::3] * g
     return f
+
+
+def string_frames(k: int) -> np.ndarray:
+    """(k, 3, 3) rotations string frame -> world for k strings on a sphere (puffer ball,
+    PAPER.md:84): local +x (the string axis, fixed face at x = 0) -> the s-th Fibonacci-sphere
+    direction; the other two columns complete a right-handed orthonormal frame."""
+    i = np.arange(k) + 0.5
+    z = 1.0 - 2.0 * i / k
+    rho = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = np.pi * (3.0 - np.sqrt(5.0)) * i
+    d = np.stack([rho * np.cos(phi), rho * np.sin(phi), z], axis=1)
+    R = np.zeros((k, 3, 3))
+    for s in range(k):
+        e1 = d[s]
+        helper = np.array([0.0, 0.0, 1.0]) if abs(e1[2]) < 0.9 else np.array([1.0, 0.0, 0.0])
+        e2 = np.cross(helper, e1)
+        e2 /= np.linalg.norm(e2)
+        e3 = np.cross(e1, e2)
+        R[s] = np.stack([e1, e2, e3], axis=1)
+    return R
+
+
+def coupled_state(k: int, n_p: int, n_q: int, seed: int = 7, scale: float = 0.1):
+    """Small seeded per-string states (r_bar, rdot_bar) (k, n) and core (c_bar, cdot_bar)."""
+    rng = np.random.default_rng(seed)
+    n = n_p + n_q
+    rb = scale * rng.uniform(-0.5, 0.5, (k, n))
+    rb[:, :n_p] *= 1e-2
+    rdb = scale * rng.uniform(-1.0, 1.0, (k, n))
+    rdb[:, :n_p] *= 1e-2
+    return rb, rdb, 1e-3 * rng.uniform(-1, 1, 3), 1e-2 * rng.uniform(-1, 1, 3)

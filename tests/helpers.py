@@ -18,3 +18,14 @@ def oracle_sim(P):
 def ocfg(cfg, **kw):
     return ors.OSimConfig(**{k: getattr(cfg, k) for k in ("dt", "newton_tol", "max_iters", "drop_fict",
                                                           "integration", "line_search", "fixed_iters")}, **kw)
+
+
+def coupled_setup(P, k, k_core=50.0):
+    """Scene arrays shared by the product and the oracle: k strings of problem P on a core."""
+    from oracle import coupled as oc
+    R = synth.string_frames(k)
+    f_world = np.tile(P.f_ext, (k, 1))
+    m_core = 2.0 * float(P.model.mass[0::3].sum())
+    f_core = np.array([0.0, -9.81 * m_core, 0.0])
+    scene = oc.OScene(oracle_sim(P), R, f_world, m_core=m_core, k_core=k_core, f_core=f_core)
+    return R, f_world, m_core, k_core, f_core, scene
