@@ -209,6 +209,13 @@ NLROM_API int nlrom_bench_kernels(nlrom_ctx* ctx, int n_iters, int flush_l2, flo
 /* Number of kernel launches of one Newton iteration (for bench "gpu_launches"). */
 NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
 
+/* Profiling: prefix-graph timing of one Newton iteration. For k = 1..min(cap, launches) the
+ * first k launches are captured as a graph and timed over n_iters replays (L2 flushed before
+ * each): ms[k-1] - ms[k-2] is launch k's marginal in-graph cost. names receives the kernel
+ * names ('\n'-separated); n_launches the number of prefixes timed. */
+NLROM_API int nlrom_bench_prefix(nlrom_ctx* ctx, int n_iters, int flush_l2, int cap, float* ms, char* names,
+                                 int names_len, int* n_launches);
+
 /* The context's CUDA stream (cudaStream_t) -- every call above is ordered on it; a host
  * that interleaves its own collectives (NCCL) with the coupled phases below uses it. */
 NLROM_API int nlrom_stream(nlrom_ctx* ctx, void** stream);

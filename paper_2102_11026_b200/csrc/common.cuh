@@ -1,5 +1,6 @@
 // Shared helpers for the nlrom_b200 sm_100a kernels.
 #pragma once
+#include <vector>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -25,6 +26,20 @@ struct Error : std::runtime_error {
 #define NL_CHECK_LAUNCH() NL_CUDA(cudaGetLastError())
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Launch gate for prefix-graph profiling (nlrom_bench_prefix): while a budget is set, only the
+// first `budget` kernel launches are issued and their entry points are logged.
+constexpr int kNoBudget = 1 << 30;
+inline int& launch_budget() { static int b = kNoBudget; return b; }
+inline std::vector<const void*>& launch_log() { static std::vector<const void*> v; return v; }
+inline bool launch_gate(const void* fn) {
+  int& b = launch_budget();
+  if (b >= kNoBudget) return true;
+  if (b <= 0) return false;
+  --b;
+  launch_log().push_back(fn);
+  return true;
+}
 inline int round_up(int a, int b) { return ceil_div(a, b) * b; }
 
 // Device buffer (owning). Zero-initialised so padded rows / columns read as 0.

@@ -8,6 +8,8 @@
 //   J: vhp = H~^T a by complex-step backprop (dual arithmetic) -> S = reduce + vhp
 //      -> in-CTA LU with partial pivoting -> dr (r += dr in fixed-iteration mode)
 #include <vector>
+#include <cstring>
+#include <cstdio>
 #include <string>
 #include <map>
 #include <algorithm>
@@ -116,6 +118,7 @@ int fail(nlrom_ctx* c, const Error& e) {
 
 template <class... KArgs, class... Args>
 void launch(nlrom_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  if (!launch_gate((const void*)kernel)) return;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -238,13 +241,18 @@ void output_layer(nlrom_ctx* c) {
 // Fused hidden chain (mlp_chain.cuh): one cluster of CS CTAs per column group.
 template <int R, int G, int CS>
 bool launch_mlp_fwd(nlrom_ctx* c, const MlpFwdArgs& a) {
-  using P = MlpPlan<R, G>;
-  const size_t smem = P::bytes(std::max(c->wL1, c->n_q));
+  // DSMEM stores + cluster barrier per layer; NLROM_ASYNC_CHAIN=1 selects the st.async /
+  // per-source mbarrier / TMA-weight variant (correct, but slower at cfg2 so far:
+  // tools/probes/chain_probe.cu)
+  static const bool sync_chain = getenv("NLROM_ASYNC_CHAIN") == nullptr;
+  const int kmax = std::max(c->wL1, c->n_q);
+  const size_t smem = sync_chain ? MlpPlan<R, G>::bytes(kmax) : MlpAsyncPlan<R, G, CS>::bytes(kmax);
   if (smem > 227 * 1024) return false;
+  auto kern = sync_chain ? k_mlp_jet_fwd<R, G, CS> : k_mlp_jet_fwd_async<R, G, CS>;
   static bool configured = false;
   if (!configured) {
-    NL_CUDA(cudaFuncSetAttribute(k_mlp_jet_fwd<R, G, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (CS > 8) NL_CUDA(cudaFuncSetAttribute(k_mlp_jet_fwd<R, G, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    NL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (CS > 8) NL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -261,7 +269,8 @@ bool launch_mlp_fwd(nlrom_ctx* c, const MlpFwdArgs& a) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  NL_CUDA(cudaLaunchKernelEx(&cfg, k_mlp_jet_fwd<R, G, CS>, a));
+  if (!launch_gate((const void*)kern)) return true;
+  NL_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   ++gemm_launch_count;
   return true;
 }
@@ -463,6 +472,7 @@ bool launch_mlp_bwd(nlrom_ctx* c, const MlpBwdArgs& a, int groups, bool dry) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  if (!launch_gate((const void*)k_mlp_dual_bwd<R, CS>)) return true;
   NL_CUDA(cudaLaunchKernelEx(&cfg, k_mlp_dual_bwd<R, CS>, a));
   ++gemm_launch_count;
   return true;
@@ -491,10 +501,19 @@ bool fused_vhp_backward(nlrom_ctx* c) {
     return false;
   };
   if (!go(true)) return false;
-  launch(c, k_gemv_t, dim3(c->bnch, c->n_sims), 128, 0, (const double*)c->Alast.p, c->ldlast, M, (const double*)c->a.p,
-         c->N, c->brows, c->bpart.p, c->bnch);
-  launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->bpart.p, c->bnch, M,
-         c->ybuf.p);
+  if (M % 2 == 0 && c->ldlast % 2 == 0 && M <= 512) {
+    // 24-row chunks over ~280 CTAs; the chain's prologue sums the partials (no reduce launch)
+    const int rows = 24, nch = ceil_div(c->N, rows);
+    launch(c, k_gemv_t2, dim3(nch, c->n_sims), 256, 0, (const double*)c->Alast.p, c->ldlast, M,
+           (const double*)c->a.p, c->N, rows, c->bpart.p, nch);
+    a.gpart = c->bpart.p;
+    a.gnch = nch;
+  } else {
+    launch(c, k_gemv_t, dim3(c->bnch, c->n_sims), 128, 0, (const double*)c->Alast.p, c->ldlast, M,
+           (const double*)c->a.p, c->N, c->brows, c->bpart.p, c->bnch);
+    launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->bpart.p, c->bnch, M,
+           c->ybuf.p);
+  }
   return go(false);
 }
 
@@ -767,7 +786,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     // backward
     if (w + n_p > 512) throw Error(NLROM_ERR_ARG, "last hidden width + n_p must be <= 512");
     c->bnch = ceil_div(N, c->brows);
-    c->bpart.alloc((size_t)c->bnch * S * (w + n_p));
+    c->bpart.alloc((size_t)std::max(c->bnch, ceil_div(N, 24)) * S * (w + n_p));
     c->ybuf.alloc((size_t)S * (w + n_p));
     int maxw = 0;
     for (int l = 1; l < L; ++l) maxw = std::max(maxw, round_up(c->widths[l], 2));
@@ -1185,6 +1204,72 @@ extern "C" int nlrom_bench_kernels(nlrom_ctx* c, int n_iters, int flush_l2, floa
 }
 
 extern "C" int nlrom_launches_per_iteration(nlrom_ctx* c) { return c ? c->launches_E + c->launches_J : 0; }
+
+// Prefix-graph timing: for k = 1 .. n, capture the first k launches of one Newton iteration
+// (E + J + update) as a graph and time n_iters replays (L2 flushed before each); ms[k-1] is the
+// mean device time of prefix k, so ms[k-1] - ms[k-2] is launch k's marginal in-graph cost
+// (PDL overlap included). names: '\n'-separated kernel names of the n launches.
+extern "C" int nlrom_bench_prefix(nlrom_ctx* c, int n_iters, int flush_l2, int cap, float* ms, char* names,
+                                  int names_len, int* n_launches) {
+  CTX_TRY(c)
+  if (c->graph_key.empty()) throw Error(NLROM_ERR_ARG, "run nlrom_step first (captures the graphs)");
+  if (flush_l2 && !c->flush.p) c->flush.alloc((size_t)32 << 20);
+  nlrom_simcfg cfg = default_cfg(1.0 / 60.0, 0, 0);
+  {
+    const std::string& key = c->graph_key;  // dt | drop_fict | integration of the captured graphs
+    double dt;
+    int drop, integ;
+    if (sscanf(key.c_str(), "%lf|%d|%d", &dt, &drop, &integ) == 3) cfg = default_cfg(dt, drop, integ);
+  }
+  const int total = c->launches_E + c->launches_J;
+  const int n = std::min(cap, total);
+  std::string nm;
+  NL_CUDA(cudaMemcpyAsync(c->rsave.p, c->r.p, (size_t)c->n_sims * c->n * 8, cudaMemcpyDeviceToDevice, c->st));
+  for (int k = 1; k <= n; ++k) {
+    launch_budget() = k;
+    launch_log().clear();
+    cudaGraphExec_t g = nullptr;
+    try {
+      g = capture(c, [&] { phase_E(c, cfg); phase_J(c, cfg, true); }, nullptr);
+    } catch (...) {
+      launch_budget() = kNoBudget;
+      throw;
+    }
+    launch_budget() = kNoBudget;
+    if (k == n)
+      for (const void* f : launch_log()) {
+        const char* s = nullptr;
+        if (cudaFuncGetName(&s, f) == cudaSuccess && s) nm += s;
+        nm += "\n";
+      }
+    float acc = 0.f;
+    for (int i = 0; i < n_iters + 1; ++i) {
+      NL_CUDA(cudaMemcpyAsync(c->r.p, c->rsave.p, (size_t)c->n_sims * c->n * 8, cudaMemcpyDeviceToDevice, c->st));
+      if (flush_l2) {
+        k_flush<<<1184, 256, 0, c->st>>>(c->flush.p, c->flush.n, (double)i);
+        NL_CHECK_LAUNCH();
+      }
+      NL_CUDA(cudaEventRecord(c->ev0, c->st));
+      NL_CUDA(cudaGraphLaunch(g, c->st));
+      NL_CUDA(cudaEventRecord(c->ev1, c->st));
+      NL_CUDA(cudaEventSynchronize(c->ev1));
+      float t = 0.f;
+      NL_CUDA(cudaEventElapsedTime(&t, c->ev0, c->ev1));
+      if (i) acc += t;  // first replay warms the instantiated graph
+    }
+    cudaGraphExecDestroy(g);
+    ms[k - 1] = acc / std::max(1, n_iters);
+  }
+  NL_CUDA(cudaMemcpyAsync(c->r.p, c->rsave.p, (size_t)c->n_sims * c->n * 8, cudaMemcpyDeviceToDevice, c->st));
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  if (names && names_len > 0) {
+    const size_t m = std::min(nm.size(), (size_t)names_len - 1);
+    memcpy(names, nm.data(), m);
+    names[m] = 0;
+  }
+  if (n_launches) *n_launches = n;
+  CTX_END(c)
+}
 
 extern "C" int nlrom_element_forces(nlrom_ctx* c, const double* u, int want_K, double* f_int, double* K_elems) {
   CTX_TRY(c)

@@ -201,6 +201,7 @@ void launch_gemm(const GemmArgs& g, const Epi& epi, cudaStream_t st, int batch =
                                  Cfg::SMEM_BYTES));
     configured = true;
   }
+  if (!launch_gate((const void*)gemm_tn_kernel<Cfg, Epi>)) return;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ceil_div(g.M, Cfg::BM), ceil_div(g.C, Cfg::BN), batch);
   cfg.blockDim = dim3(Cfg::NT);

@@ -420,6 +420,55 @@ __global__ void k_gemv_t(const double* __restrict__ A, int ldA, int M, const dou
   }
 }
 
+// Same product for the fused vhp chain: 256 threads = 128 column pairs (16-byte loads) x 2 row
+// phases, every load of a thread issued back to back; the per-chunk partials are summed by
+// the consumer (k_mlp_dual_bwd prologue), so no separate reduction launch. M even, ldA even.
+__global__ void __launch_bounds__(256) k_gemv_t2(const double* __restrict__ A, int ldA, int M,
+                                                 const double* __restrict__ x, int N, int rows_per_cta,
+                                                 double* __restrict__ part, int nchunk) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double red[512];
+  const int chunk = blockIdx.x, sim = blockIdx.y;
+  const int r0 = chunk * rows_per_cta, r1 = min(N, r0 + rows_per_cta);
+  const double* xs = x + (size_t)sim * N;
+  const int cp = threadIdx.x & 127, ph = threadIdx.x >> 7;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const int c0 = 2 * cp + 256 * g;
+    if (c0 < M) {
+#pragma unroll 12
+      for (int n = r0 + ph; n < r1; n += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(A + (size_t)n * ldA + c0);
+        const double xv = xs[n];
+        acc[g][0] = fma(v.x, xv, acc[g][0]);
+        acc[g][1] = fma(v.y, xv, acc[g][1]);
+      }
+    }
+  }
+  if (ph == 1)
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const int c0 = 2 * cp + 256 * g;
+      if (c0 < M) {
+        red[c0] = acc[g][0];
+        red[c0 + 1] = acc[g][1];
+      }
+    }
+  __syncthreads();
+  if (ph == 0)
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      const int c0 = 2 * cp + 256 * g;
+      if (c0 < M) {
+        double* o = part + ((size_t)sim * nchunk + chunk) * M + c0;
+        o[0] = acc[g][0] + red[c0];
+        o[1] = acc[g][1] + red[c0 + 1];
+      }
+    }
+}
+
 // y = sum_chunks part  (grid (ceil(M/32), n_sims), block 256 = 32 outputs x 8 chunk groups)
 __global__ void k_reduce_cols(const double* __restrict__ part, int nchunk, int M, double* __restrict__ y) {
   pdl_wait();

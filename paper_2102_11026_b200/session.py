@@ -215,6 +215,16 @@ class Session:
         self._chk(self._L.nlrom_bench_kernels(self._h, int(n_iters), int(flush_l2), out))
         return list(out)
 
+    def bench_prefix(self, n_iters=50, flush_l2=True, cap=64):
+        """[(kernel name, marginal in-graph ms)] for the launches of one Newton iteration."""
+        ms = (C.c_float * cap)()
+        buf = C.create_string_buffer(8192)
+        cnt = C.c_int()
+        self._chk(self._L.nlrom_bench_prefix(self._h, int(n_iters), int(flush_l2), cap, ms, buf, 8192, C.byref(cnt)))
+        names = buf.value.decode().split("\n")[:cnt.value]
+        vals = list(ms)[:cnt.value]
+        return [(nm, v - (vals[i - 1] if i else 0.0)) for i, (nm, v) in enumerate(zip(names, vals))], vals
+
     def launches_per_iteration(self):
         return int(self._L.nlrom_launches_per_iteration(self._h))
 
