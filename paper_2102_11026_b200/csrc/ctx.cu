@@ -57,7 +57,7 @@ int gemm_launch_count = 0;
 struct nlrom_ctx {
   int device = 0;
   cudaStream_t st = nullptr, st2 = nullptr;
-  cudaEvent_t evFork = nullptr, evJoin = nullptr;
+  cudaEvent_t evFork = nullptr, evJoin = nullptr, evFork2 = nullptr, evJoin2 = nullptr;
   std::string err;
   double last_norm = 0.0;
   int N = 0, n_p = 0, n_q = 0, n = 0, L = 0, n_sims = 1, T = 0, V = 0;
@@ -65,6 +65,8 @@ struct nlrom_ctx {
   // decoder
   std::vector<DBuf> W, WT, b;
   std::vector<int> ldW, ldWT;
+  std::vector<DBuf> Wp, WTp;  // fused chains: padded copies (one TMA bulk copy per CTA slice)
+  int ldpf = 0, ldpb = 0;
   DBuf Alast, AT, Pb, U, mass;
   int ldlast = 0, wL1 = 0, next = 0;
   bool batched = false;  // many sims: big-tile per-layer GEMMs instead of the latency kernels
@@ -287,9 +289,12 @@ bool fused_hidden_forward(nlrom_ctx* c, double dt, int drop_fict) {
   a.L1 = L1; a.w = w;
   for (int l = 0; l < L1; ++l) {
     a.W[l] = c->W[l].p; a.b[l] = c->b[l].p; a.ldW[l] = c->ldW[l]; a.in[l] = c->widths[l];
+    a.Wp[l] = c->Wp[l].p;
     a.cache[l] = c->cache[l].p;
   }
   a.ldc = c->ldc[0];
+  a.ldp = c->ldpf;
+  if (c->ldpf != round_up(std::max(w, c->n_q), 16) + 4) return false;  // padded layout == smem slice layout
   a.Hout = c->H[L1 - 1].p;
   a.ldH = c->ldH[L1 - 1];
   a.G = c->G; a.gps = c->gps;
@@ -380,20 +385,31 @@ void mass_block_fork(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   NL_CUDA(cudaEventRecord(c->evJoin, c->st2));
 }
 
+// a and the J~^T a partials on the critical path; phi = sum of partials and S_base = mass block
+// + dt^2 K~ (no vhp) on the side branch (after the mass block), joined where they are consumed.
 void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   assemble_launch(c, s, dt, drop_fict, 2);
+  NL_CUDA(cudaEventRecord(c->evFork2, c->st));
+  NL_CUDA(cudaStreamWaitEvent(c->st2, c->evFork2, 0));
+  std::swap(c->st, c->st2);
   launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nchA, c->n,
          c->phi.p, c->norm.p);
+  const int n = c->n;
+  launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
+         (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, dt, c->S.p);
+  std::swap(c->st, c->st2);
+  NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));
 }
 
-void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg) {
+// join_side = false leaves the phi / S_base branch open for phase_J (one-graph Newton iteration)
+void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
   bundle_forward(c, cfg.dt, cfg.drop_fict);
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
   if (cfg.integration == 0) wnet_phase(c);
   cubature_phase(c, s, cfg.integration == 0);
   assemble_phase(c, s, cfg.dt, cfg.drop_fict);
-  NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin, 0));  // join the mass-block branch
+  if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));  // phi, S_base (and the mass block)
 }
 
 // vhp backward: dual (NS = 2) passes, cache written by the bundle forward.
@@ -489,8 +505,11 @@ bool fused_vhp_backward(nlrom_ctx* c) {
   a.g = c->ybuf.p; a.L1 = L1; a.w = w; a.n_q = c->n_q;
   for (int l = 0; l < L1; ++l) {
     a.WT[l] = c->WT[l].p; a.ldWT[l] = c->ldWT[l]; a.cache[l] = c->cache[l].p;
+    a.WTp[l] = c->WTp[l].p;
   }
   a.ldc = c->ldc[0]; a.Gt = c->Gt.p; a.ldG = c->ldGt;
+  a.ldpb = c->ldpb;
+  if (c->ldpb != round_up(w, 16) + 4) return false;
   a.gpb = ceil_div(c->n_q, 8);
   const int groups = c->n_sims * a.gpb;
   auto go = [&](bool dry) -> bool {
@@ -519,12 +538,21 @@ bool fused_vhp_backward(nlrom_ctx* c) {
 
 // In-CTA LU-pp solve of every sim's Eq. 11 system; register block sized to n + 1.
 // Extra right-hand sides (xrhs, nx columns of n per sim) are solved alongside -phi into xout.
-void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 0, double* xout = nullptr) {
+void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 0, double* xout = nullptr,
+               bool add_vhp = false) {
   const int n = c->n;
+  const double* Gt = add_vhp ? (const double*)c->Gt.p : nullptr;
   auto go = [&](auto kern) {
     launch(c, kern, c->n_sims, 256, lu_smem_bytes(n + nx), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
-           c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout);
+           c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt, c->n_p);
   };
+  // k_lu_cols (column-cyclic, one producer warp per pivot step) is correct but slower than the
+  // row-block kernel on B200 (tools/probes/lu_probe.cu: 47 vs 33 us at n = 60): opt-in only
+  if (n <= LUC_D && n + 1 + nx <= 8 * LUC_CPW && getenv("NLROM_LU_COLS")) {
+    launch(c, k_lu_cols, c->n_sims, 256, luc_smem_bytes(), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
+           c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt, c->n_p);
+    return;
+  }
   switch (lu_nb(n + nx)) {
     case 4: go(k_lu_solve<4>); break;
     case 6: go(k_lu_solve<6>); break;
@@ -532,15 +560,21 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
   }
 }
 
+// side_open: phase E left its phi / S_base branch unjoined (captured in the same graph)
 void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply, const double* xrhs = nullptr, int nx = 0,
-             double* xout = nullptr) {
+             double* xout = nullptr, bool side_open = false) {
   if (!fused_vhp_backward(c))
     decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
+  if (side_open) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));  // S_base, phi from phase E's branch
+  launch_lu(c, apply, xrhs, nx, xout, true);  // S = S_base + diag(0, vhp) while staging
+}
+
+// S with the vhp block (system_jacobian API; the Newton iteration adds it inside the LU)
+void full_S(nlrom_ctx* c, const nlrom_simcfg& cfg) {
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   const int n = c->n;
   launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
          (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
-  launch_lu(c, apply, xrhs, nx, xout);
 }
 
 size_t lu_smem(int n) {
@@ -585,7 +619,7 @@ void ensure_graphs(nlrom_ctx* c, const nlrom_simcfg& cfg) {
   NL_CUDA(cudaStreamSynchronize(c->st));
   c->gE = capture(c, [&] { phase_E(c, cfg); }, &c->launches_E);
   c->gJ = capture(c, [&] { phase_J(c, cfg, false); }, &c->launches_J);
-  c->gIter = capture(c, [&] { phase_E(c, cfg); phase_J(c, cfg, true); }, nullptr);
+  c->gIter = capture(c, [&] { phase_E(c, cfg, false); phase_J(c, cfg, true, nullptr, 0, nullptr, true); }, nullptr);
   c->graph_key = key;
 }
 
@@ -634,6 +668,8 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     NL_CUDA(cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evFork2, cudaEventDisableTiming));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evJoin2, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreate(&c->ev0));
     NL_CUDA(cudaEventCreate(&c->ev1));
     c->n_sims = d->n_sims > 0 ? d->n_sims : 1;
@@ -655,6 +691,26 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         for (int k = 0; k < in; ++k) wt[(size_t)k * o + r] = d->W[l][(size_t)r * in + k];
       upload_matrix(c->WT[l], wt.data(), in, o, c->ldWT[l]);
       upload(c->b[l], d->b[l], o);
+    }
+    {  // padded copies for the fused chains: W_l as (w x ldpf), W_l^T as (w x ldpb), zero padded
+      int kmax = n_q;
+      for (int l = 1; l < L; ++l) kmax = std::max(kmax, c->widths[l]);
+      c->ldpf = round_up(kmax, 16) + 4;
+      c->ldpb = round_up(c->wL1, 16) + 4;
+      c->Wp.resize(L - 1);
+      c->WTp.resize(L - 1);
+      for (int l = 0; l < L - 1; ++l) {
+        const int in = c->widths[l], o = c->widths[l + 1];
+        const int rows = std::max(o, kmax);
+        std::vector<double> wp((size_t)rows * c->ldpf, 0.0), wtp((size_t)std::max(rows, in) * c->ldpb, 0.0);
+        for (int r = 0; r < o; ++r)
+          for (int k = 0; k < in; ++k) {
+            wp[(size_t)r * c->ldpf + k] = d->W[l][(size_t)r * in + k];
+            if (o <= c->ldpb - 4) wtp[(size_t)k * c->ldpb + r] = d->W[l][(size_t)r * in + k];
+          }
+        upload(c->Wp[l], wp.data(), wp.size());
+        upload(c->WTp[l], wtp.data(), wtp.size());
+      }
     }
     // last layer fused with the filter: D = P (W_L h + b_L) = (P W_L) h + P b_L with
     // P = I - U U^T folded into the weights once at upload (no filter GEMM per iteration).
@@ -827,6 +883,8 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->st2) cudaStreamDestroy(c->st2);
   if (c->evFork) cudaEventDestroy(c->evFork);
   if (c->evJoin) cudaEventDestroy(c->evJoin);
+  if (c->evFork2) cudaEventDestroy(c->evFork2);
+  if (c->evJoin2) cudaEventDestroy(c->evJoin2);
   delete c;
 }
 
@@ -951,6 +1009,7 @@ extern "C" int nlrom_system_jacobian(nlrom_ctx* c, const double* r, const double
   set_state(c, r, rbar, rdbar, fext);
   eval_point(c, *cfg);
   NL_CUDA(cudaGraphLaunch(c->gJ, c->st));
+  full_S(c, *cfg);
   d2h(c, S, c->S, (size_t)c->n_sims * c->n * c->n);
   NL_CUDA(cudaStreamSynchronize(c->st));
   CTX_END(c)
@@ -1230,7 +1289,7 @@ extern "C" int nlrom_bench_prefix(nlrom_ctx* c, int n_iters, int flush_l2, int c
     launch_log().clear();
     cudaGraphExec_t g = nullptr;
     try {
-      g = capture(c, [&] { phase_E(c, cfg); phase_J(c, cfg, true); }, nullptr);
+      g = capture(c, [&] { phase_E(c, cfg, false); phase_J(c, cfg, true, nullptr, 0, nullptr, true); }, nullptr);
     } catch (...) {
       launch_budget() = kNoBudget;
       throw;

@@ -45,6 +45,8 @@ struct MlpFwdArgs {
   const double* b[MLP_MAXL];
   int ldW[MLP_MAXL];
   int in[MLP_MAXL];
+  const double* Wp[MLP_MAXL];  // W[l] re-laid out (w x ldp, zero padded) so one TMA bulk copy lands a slice
+  int ldp;                     // == MlpPlan::ldws(kmax)
   // outputs
   double* cache[MLP_MAXL];  // vhp caches: (n_sims * 2 n_q) x ldc per layer
   int ldc;
@@ -61,7 +63,7 @@ struct MlpPlan {
   static __host__ __device__ int kp(int kmax) { return (kmax + 15) & ~15; }
   static __host__ __device__ int ldws(int kmax) { return kp(kmax) + 4; }
   static __host__ __device__ size_t bytes(int kmax) {
-    return (size_t)(2 * kp(kmax) * LDX + 2 * R * ldws(kmax) + 2 * R + G * (R + 1) + R * LDX) * 8;
+    return (size_t)(2 * kp(kmax) * LDX + 2 * R * ldws(kmax) + 2 * R + G * (R + 1) + R * LDX) * 8 + 16;
   }
 };
 
@@ -103,9 +105,21 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
   const int nk = (G - 4) / 4;
   const int cs = 4 + 4 * a.n_q;
 
-  // layer-0 weights do not depend on the producer: prefetch before the dependency wait
-  mlp_load_w<R>(Wbuf(0), Bbuf(0), LDWS, a.W[0], a.ldW[0], a.b[0], r0, a.in[0], tid, NTH);
-  cp_async_commit();
+  // weight + bias slices land by ONE TMA bulk copy each (padded global layout), on a
+  // per-buffer mbarrier; issued one layer ahead by thread 0
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(Os + R * LDX);
+  auto issue_w = [&](int l) {
+    uint64_t* bar = wbar + (l & 1);
+    mbar_expect_tx(bar, (uint32_t)(R * LDWS * 8 + R * 8));
+    tma_g2s(Wbuf(l & 1), a.Wp[l] + (size_t)r0 * LDWS, (uint32_t)(R * LDWS * 8), bar);
+    tma_g2s(Bbuf(l & 1), a.b[l] + r0, (uint32_t)(R * 8), bar);
+  };
+  if (tid == 0) {
+    mbar_init(wbar, 1);
+    mbar_init(wbar + 1, 1);
+    fence_mbar_init();
+    issue_w(0);  // layer-0 weights do not depend on the producer: before the dependency wait
+  }
   pdl_wait();
   pdl_launch();
   // seed of this group: X[0][i][c], i < n_q; rows n_q .. kmax of both X buffers are zero
@@ -134,13 +148,10 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
     const int K = a.in[l];
     double* Xc = Xb(l & 1);
     double* Xn = Xb((l + 1) & 1);
-    if (l + 1 < a.L1)
-      mlp_load_w<R>(Wbuf((l + 1) & 1), Bbuf((l + 1) & 1), LDWS, a.W[l + 1], a.ldW[l + 1], a.b[l + 1], r0, a.in[l + 1],
-                    tid, NTH);
-    cp_async_commit();
+    if (l + 1 < a.L1 && tid == 0) issue_w(l + 1);  // buffer (l+1)&1 was last read by layer l-1
     CHAIN_MARK(l, 0);
-    cp_async_wait<1>();  // this layer's weights have landed
-    __syncthreads();
+    if (l == 0) __syncthreads();  // seed (barrier init) visible
+    mbar_wait(wbar + (l & 1), (l >> 1) & 1);  // this layer's weights have landed
     CHAIN_MARK(l, 1);
     // DMMA: warp -> 8x8 tiles of the R x G slice, 4 interleaved K chains; K padded to 16 with zeros
     const double* Ws = Wbuf(l & 1);
@@ -267,24 +278,19 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd_async(MlpFwdArgs a) {
   const int cs = 4 + 4 * a.n_q;
   constexpr uint32_t SLICE = R * G * 8;  // bytes one source delivers per layer
 
-  auto issue_weights = [&](int l) {  // one thread: layer l's weight rows + bias slice -> buffer l & 1
-    const int K2 = (a.in[l] + 1) & ~1;  // device weights are zero-padded to an even ld
+  auto issue_weights = [&](int l) {  // one thread: layer l's weight + bias slices -> buffer l & 1
     uint64_t* bar = wbar + (l & 1);
-    mbar_expect_tx(bar, (uint32_t)(R * K2 * 8 + R * 8));
-    double* Wb = Wbuf(l & 1);
-    for (int rr = 0; rr < R; ++rr) tma_g2s(Wb + rr * LDWS, a.W[l] + (size_t)(r0 + rr) * a.ldW[l], K2 * 8, bar);
+    mbar_expect_tx(bar, (uint32_t)(R * LDWS * 8 + R * 8));
+    tma_g2s(Wbuf(l & 1), a.Wp[l] + (size_t)r0 * LDWS, (uint32_t)(R * LDWS * 8), bar);
     tma_g2s(Bbuf(l & 1), a.b[l] + r0, R * 8, bar);
   };
 
-  // zero both weight buffers (K padding columns stay zero), init the barriers
-  for (int t = tid; t < 2 * R * LDWS; t += NTH) Wbuf(0)[t] = 0.0;
   if (tid == 0) {
     mbar_init(wbar + 0, 1);
     mbar_init(wbar + 1, 1);
     for (int i = 0; i < 2 * CS; ++i) mbar_init(xbar + i, 1);
     fence_mbar_init();
   }
-  fence_proxy_async();  // generic zero stores before the async-proxy TMA writes
   __syncthreads();
   if (tid == 0) {
     issue_weights(0);  // producer-independent: before the dependency wait
@@ -431,6 +437,8 @@ struct MlpBwdArgs {
   int L1, w, n_q;
   const double* WT[MLP_MAXL];  // WT[l]: (in_l x ldWT[l]) = W_l^T, rows in_l (w for l >= 1, n_q for l = 0)
   int ldWT[MLP_MAXL];
+  const double* WTp[MLP_MAXL];  // W_l^T re-laid out (w x ldpb, zero padded rows / columns): one TMA per slice
+  int ldpb;
   const double* cache[MLP_MAXL];  // (n_sims * 2 n_q) x ldc
   int ldc;
   double* Gt;               // (n_sims * 2 n_q) x ldG
@@ -460,15 +468,18 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
   const int L1 = a.L1;
   // stage s = 0 .. L1: s = 0 builds Delta_{L1-1}; stage s >= 1 multiplies by W_{L1-s}^T;
   // stages 1 .. L1-1 end with cos(z_{L1-1-s}); stage L1 writes G.
-  auto load_w = [&](int l, int buf) {  // rows r0.. of W_l^T (in_l rows), K = w
-    const int rows = (l == 0) ? a.n_q : a.w;
-    const int Kp = (a.w + 15) & ~15;
-    for (int rr = warp; rr < R; rr += NTH / 32)
-      for (int k = 2 * lane; k < Kp; k += 64) {
-        const bool ok = (r0 + rr < rows) && (k < a.w);
-        cp_async16(Wbuf(buf) + rr * LDWS + k, ok ? a.WT[l] + (size_t)(r0 + rr) * a.ldWT[l] + k : a.WT[l], ok);
-      }
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(Os + R * LDX);
+  auto load_w = [&](int l, int buf) {  // rows r0.. of W_l^T (zero beyond in_l), K = w: one TMA bulk copy
+    if (tid == 0) {
+      mbar_expect_tx(wbar + buf, (uint32_t)(R * LDWS * 8));
+      tma_g2s(Wbuf(buf), a.WTp[l] + (size_t)r0 * LDWS, (uint32_t)(R * LDWS * 8), wbar + buf);
+    }
   };
+  if (tid == 0) {
+    mbar_init(wbar, 1);
+    mbar_init(wbar + 1, 1);
+    fence_mbar_init();
+  }
   auto load_z = [&](int l, int buf) {  // cache_l rows r0.. for the group's 16 columns
     const double* C = a.cache[l] + (size_t)sim * 2 * a.n_q * a.ldc;
     for (int t = tid; t < R * G; t += NTH) {
@@ -515,6 +526,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
       constexpr int TM = R / 8, TN = G / 8, NT = TM * TN;
       const int Kp = (a.w + 15) & ~15;
       cp_async_wait<1>();
+      mbar_wait(wbar + (s & 1), ((s - 1) >> 1) & 1);
       __syncthreads();
       for (int tile = warp; tile < NT; tile += NTH / 32) {
         const int tm = tile % TM, tn = tile / TM;
@@ -585,7 +597,7 @@ template <int R>
 inline size_t mlp_bwd_smem(int w) {
   using P = MlpPlan<R, 16>;
   const int kp = P::kp(w);
-  return (size_t)(2 * kp * P::LDX + 2 * R * P::ldws(kp) + 2 * R * 16 + 16 * (R + 1) + R * P::LDX) * 8;
+  return (size_t)(2 * kp * P::LDX + 2 * R * P::ldws(kp) + 2 * R * 16 + 16 * (R + 1) + R * P::LDX) * 8 + 16;
 }
 
 }  // namespace nlrom

@@ -210,7 +210,8 @@ template <int NB>
 __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, const double* __restrict__ phi,
                                                    double* __restrict__ dr, double* __restrict__ r, int n, int apply,
                                                    int* __restrict__ status, const double* __restrict__ xrhs, int nx,
-                                                   double* __restrict__ xout) {
+                                                   double* __restrict__ xout, const double* __restrict__ Gt, int ldg,
+                                                   int n_p) {
   pdl_wait();
   pdl_launch();
   constexpr int D = 16 * NB;           // covered rows / columns (n + 1 <= D)
@@ -240,6 +241,9 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
       const int i = ty + 16 * a, j = tx + 16 * b;
       double v = M[i * LDF + j];
       if (j == n) v = -v;  // rhs = -phi
+      // S = S_base + diag(0, vhp): vhp[i][k] = G_t[2k+1][i] (k_reduce_S without G_t built S_base)
+      if (Gt && i >= n_p && j >= n_p && i < n && j < n)
+        v += Gt[((size_t)sim * 2 * (n - n_p) + 2 * (j - n_p) + 1) * ldg + (i - n_p)];
       A[a][b] = v;
     }
   __syncthreads();
@@ -364,6 +368,236 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     }
     if (tid == 0) status[sim] = 0;
   }
+}
+
+// Column-cyclic variant for n <= 64 and n + 1 + nx <= 72 columns: warp w owns columns
+// w, w + 8, ...; lane holds rows lane and lane + 32 of them in registers. Pivot step k is
+// produced by ONE warp (the owner of column k: pivot search with REDUX, reciprocal,
+// multipliers into shared memory) and consumed by the other seven through a named barrier
+// (bar.arrive / bar.sync, two alternating ids), so a step costs one producer->consumer
+// hand-off instead of a full CTA barrier plus redundant pivot searches in every warp.
+// Same arithmetic as k_lu_solve (m = a_ik / a_pk, a_ij -= m a_pj on unused rows).
+__device__ __forceinline__ void named_bar_arrive(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int cnt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+
+constexpr int LUC_CPW = 9, LUC_D = 64, LUC_LDF = 8 * LUC_CPW + 1;
+#ifdef LU_TRACE
+__device__ long long g_lu_trace[80];
+__device__ long long g_lu_trace2[16];
+#define LU_MARK(i) \
+  if (threadIdx.x == 0) g_lu_trace[i] = clock64();
+#define LU_MARK2(w, i) \
+  if (threadIdx.x == 32 * (w)) g_lu_trace2[i] = clock64();
+#else
+#define LU_MARK(i)
+#define LU_MARK2(w, i)
+#endif
+inline size_t luc_smem_bytes() { return (size_t)LUC_D * LUC_LDF * 8; }
+
+__global__ void __launch_bounds__(256) k_lu_cols(const double* __restrict__ S, const double* __restrict__ phi,
+                                                 double* __restrict__ dr, double* __restrict__ r, int n, int apply,
+                                                 int* __restrict__ status, const double* __restrict__ xrhs, int nx,
+                                                 double* __restrict__ xout, const double* __restrict__ Gt, int ldg,
+                                                 int n_p) {
+  LU_MARK(0);
+  pdl_wait();
+  pdl_launch();
+  LU_MARK(1);
+  constexpr int CPW = LUC_CPW, D = LUC_D, LDF = LUC_LDF;
+  extern __shared__ double M[];  // [D][LDF]: eliminated matrix for the back substitution
+  __shared__ double mul[2][D];
+  __shared__ int pivrow[D];
+  __shared__ double rdiag[D];
+  const unsigned FULL = 0xffffffffu;
+  const int sim = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(FULL, tid >> 5, 0);  // provably warp-uniform
+  const int ncol = n + 1 + nx;
+  const double* Ss = S + (size_t)sim * n * n;
+  double A[CPW][2];
+#pragma unroll
+  for (int j = 0; j < CPW; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = warp + 8 * j, row = lane + 32 * h;
+      double v = 0.0;
+      if (row < n) {
+        if (c < n) {
+          v = Ss[(size_t)row * n + c];
+          if (Gt && row >= n_p && c >= n_p) v += Gt[((size_t)sim * 2 * (n - n_p) + 2 * (c - n_p) + 1) * ldg + (row - n_p)];
+        }
+        else if (c == n) v = -phi[(size_t)sim * n + row];
+        else if (c < ncol) v = xrhs[((size_t)sim * nx + (c - n - 1)) * n + row];
+      }
+      A[j][h] = v;
+    }
+  bool used0 = lane >= n, used1 = lane + 32 >= n;
+  bool bad = false;
+  LU_MARK(2);
+  // pivot step k by its owner warp: search column k (slot k >> 3), publish multipliers and the
+  // pivot row through shared memory, release the consumers of barrier 1 + (k & 1)
+  auto produce = [&](int k, int& piv, double& m0, double& m1) -> bool {
+    const int jk = k >> 3;
+    if (k == 11) LU_MARK2(3, 3);
+    double ak0 = 0.0, ak1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < CPW; ++j)
+      if (j == jk) { ak0 = A[j][0]; ak1 = A[j][1]; }
+    const double v0 = used0 ? -1.0 : fabs(ak0), v1 = used1 ? -1.0 : fabs(ak1);
+    double best = v0;
+    int bi = lane;
+    if (v1 > best) { best = v1; bi = lane + 32; }
+    const unsigned long long key = (best >= 0.0) ? (unsigned long long)__double_as_longlong(best) : 0ull;
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mhi = __reduce_max_sync(FULL, hi);
+    const unsigned mlo = __reduce_max_sync(FULL, hi == mhi ? lo : 0u);
+    piv = (int)__reduce_min_sync(FULL, (hi == mhi && lo == mlo) ? (unsigned)bi : 0x7fffffffu);
+    if (k == 11) LU_MARK2(3, 4);
+    const bool ok = (mhi | mlo) && piv < n;
+    const double pv = __shfl_sync(FULL, piv < 32 ? ak0 : ak1, piv & 31);  // convergent: every lane
+    if (ok) {
+      const double rp = 1.0 / pv;
+      if (k == 11 && rp != 12345.0) LU_MARK2(3, 5);
+      // the pivot row is marked used by the caller once its step k-1 updates are done
+      m0 = (used0 || piv == lane) ? 0.0 : ak0 * rp;
+      m1 = (used1 || piv == lane + 32) ? 0.0 : ak1 * rp;
+      mul[k & 1][lane] = m0;
+      mul[k & 1][lane + 32] = m1;
+      if (lane == 0) {
+        pivrow[k] = piv;
+        rdiag[k] = rp;
+      }
+    } else if (lane == 0) {
+      pivrow[k] = -1;
+    }
+    if (k == 11) LU_MARK2(3, 6);
+    named_bar_arrive(1 + (k & 1), 256);
+    return ok;
+  };
+  // column update of one owned slot j for pivot step k (shuffle executed by the whole warp)
+  auto update = [&](int j, int piv, double m0, double m1, bool on) {
+    double src = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj)
+      if (jj == j) src = (piv < 32) ? A[jj][0] : A[jj][1];
+    const double pr = __shfl_sync(FULL, src, piv & 31);
+#pragma unroll
+    for (int jj = 0; jj < CPW; ++jj)
+      if (on && jj == j) {
+        if (!used0) A[jj][0] = fma(-m0, pr, A[jj][0]);
+        if (!used1) A[jj][1] = fma(-m1, pr, A[jj][1]);
+      }
+  };
+  int piv = 0;
+  double m0 = 0.0, m1 = 0.0;
+  if (warp == 0 && n > 0) {
+    if (!produce(0, piv, m0, m1)) bad = true;
+    if (piv == lane) used0 = true;
+    if (piv == lane + 32) used1 = true;
+  }
+  for (int k = 0; k < n && !bad; ++k) {
+    LU_MARK(8 + k);
+    if (warp != (k & 7)) {  // consumer of step k (the owner already holds piv, m0, m1)
+      if (k == 10) LU_MARK2(3, 0);
+      named_bar_sync(1 + (k & 1), 256);
+      if (k == 10) LU_MARK2(3, 1);
+      piv = pivrow[k];
+      if (piv < 0) { bad = true; break; }
+      if (piv == lane) used0 = true;
+      if (piv == lane + 32) used1 = true;
+      m0 = mul[k & 1][lane];
+      m1 = mul[k & 1][lane + 32];
+    }
+    const int next = k + 1;
+    // this warp's first owned column after k: for the owner of k + 1 it IS column k + 1
+    const int j1 = (k >= warp) ? ((k - warp) >> 3) + 1 : 0;
+    const int c1 = warp + 8 * j1;
+    update(j1, piv, m0, m1, c1 < ncol);
+    if (k == 10) LU_MARK2(3, 2);
+    int piv_n = 0;
+    double m0_n = 0.0, m1_n = 0.0;
+    const bool owner_next = next < n && warp == (next & 7);
+    if (owner_next && !produce(next, piv_n, m0_n, m1_n)) bad = true;  // look-ahead: publish step k + 1
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) {
+      const int c = warp + 8 * j;
+      const double pr = __shfl_sync(FULL, piv < 32 ? A[j][0] : A[j][1], piv & 31);
+      if (j > j1 && c < ncol) {
+        if (!used0) A[j][0] = fma(-m0, pr, A[j][0]);
+        if (!used1) A[j][1] = fma(-m1, pr, A[j][1]);
+      }
+    }
+    const int jskip = owner_next ? 1 : -1;
+    if (jskip >= 0) {
+      piv = piv_n;
+      m0 = m0_n;
+      m1 = m1_n;
+      if (piv == lane) used0 = true;
+      if (piv == lane + 32) used1 = true;
+    }
+  }
+  LU_MARK(3);
+  __syncthreads();
+  LU_MARK(4);
+  if (bad) {
+    if (tid == 0) status[sim] = 1;
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) {
+    const int c = warp + 8 * j;
+    if (c < ncol) {
+      M[lane * LDF + c] = A[j][0];
+      M[(lane + 32) * LDF + c] = A[j][1];
+    }
+  }
+  __syncthreads();
+  if (warp <= nx) {  // back substitution: warp 0 for -phi, warp w for extra right-hand side w
+    const int col = n + warp;
+    constexpr int NU = 2;
+    double bv[NU];
+    const double* rowp[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int t = lane + 32 * u;
+      rowp[u] = M + (t < n ? pivrow[t] : 0) * LDF;
+      bv[u] = (t < n) ? rowp[u][col] : 0.0;
+    }
+#pragma unroll 4
+    for (int t = n - 1; t >= 0; --t) {
+      const int owner = t & 31, slot = t >> 5;
+      const double rd = rdiag[t];
+      double uc[NU];
+#pragma unroll
+      for (int u = 0; u < NU; ++u) uc[u] = rowp[u][t];
+      double bt = (slot == 0) ? bv[0] : bv[1];
+      bt = __shfl_sync(FULL, bt, owner);
+      const double xt = bt * rd;
+#pragma unroll
+      for (int u = 0; u < NU; ++u) {
+        const int tt = lane + 32 * u;
+        if (tt < t) bv[u] = fma(-uc[u], xt, bv[u]);
+        else if (tt == t) bv[u] = xt;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const int t = lane + 32 * u;
+      if (t < n) {
+        if (warp == 0) {
+          dr[(size_t)sim * n + t] = bv[u];
+          if (apply) r[(size_t)sim * n + t] += bv[u];
+        } else {
+          xout[((size_t)sim * nx + warp - 1) * n + t] = bv[u];
+        }
+      }
+    }
+    if (tid == 0) status[sim] = 0;
+  }
+  LU_MARK(5);
 }
 
 // n: unknowns + extra right-hand sides (D >= n + 1 columns incl. -phi)

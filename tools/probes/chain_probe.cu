@@ -32,9 +32,20 @@ int main() {
   a.rdbar = dev(n, true);
   a.n_p = np; a.n_q = nq; a.n = n; a.dt = 1.0 / 60; a.alpha = 0.1; a.drop_fict = 0;
   a.L1 = L1; a.w = w;
+  const int ldp = 256 + 4;
+  a.ldp = ldp;
   for (int l = 0; l < L1; ++l) {
     const int in = l ? w : nq;
     a.W[l] = dev((size_t)w * in, true);
+    {
+      std::vector<double> wp((size_t)w * ldp, 0.0);
+      for (int r = 0; r < w; ++r)
+        for (int k = 0; k < in; ++k) wp[(size_t)r * ldp + k] = h[(size_t)r * in + k];
+      double* d;
+      cudaMalloc(&d, wp.size() * 8);
+      cudaMemcpy(d, wp.data(), wp.size() * 8, cudaMemcpyHostToDevice);
+      a.Wp[l] = d;
+    }
     a.b[l] = dev(w, true);
     a.ldW[l] = in;
     a.in[l] = in;
