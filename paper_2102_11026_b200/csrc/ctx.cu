@@ -45,6 +45,7 @@ struct CubSet {
   IBuf elems;
   int n = 0;
   IBuf row_ids, row_ptr, entries;
+  IBuf rowptr_full;  // (N + 1) CSR over all free-DOF rows (same entries), gathered by k_assemble_a
   int n_rows = 0;
   int epc = 1, nchunk = 0;
   DBuf fe_w, part_f, part_K, f;
@@ -90,6 +91,7 @@ struct nlrom_ctx {
   DBuf u, value, hvv, Jt, dJ;
   // assembly / solve
   int rpc = 128, nchA = 0;
+  int rpcM = 128, nchM = 0;  // row chunking of the mass block (finer: more CTAs for its Gram)
   DBuf a, partA, partPhi, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
   IBuf status;
   // backward
@@ -104,6 +106,9 @@ struct nlrom_ctx {
   DBuf flush;
   // substructured scene (coupled_kernels.cuh): strings of this rank + replicated core
   bool coupled = false;
+  // mass block on a side branch beside the weight net (default) or, with NLROM_MASS_LATE, beside
+  // the vhp chain (measured slower: the 16-CTA clusters cannot co-schedule with it)
+  bool mass_early = getenv("NLROM_MASS_LATE") == nullptr;
   DBuf cpR, cpFloc, cpFsum, cpCore, cpBlocks, cpCb, cpX, cpFcore;
   double cp_m_core = 0, cp_k_core = 0, cp_m_string = 0, cp_m_total = 0;
   cudaGraphExec_t gC[2] = {nullptr, nullptr};
@@ -213,11 +218,17 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
     ptr.push_back((int)ent.size());
   }
   s.n_rows = (int)ids.size();
+  {
+    std::vector<int> full((size_t)c->N + 1, 0);
+    for (size_t k = 0; k < ids.size(); ++k) full[(size_t)ids[k] + 1] = ptr[k + 1] - ptr[k];
+    for (int r = 0; r < c->N; ++r) full[(size_t)r + 1] += full[r];
+    s.rowptr_full.upload(full.data(), full.size());
+  }
   s.row_ids.upload(ids.data(), ids.size());
   s.row_ptr.upload(ptr.data(), ptr.size());
   s.entries.upload(ent.data(), ent.size());
   const int n = c->n;
-  s.epc = 8;
+  s.epc = 4;  // 4 elements (48 DOF rows) per CTA: ~125 CTAs for |C| = 500, shorter per-CTA chains
   while (s.epc > 1 && (size_t)(2 * s.epc * 12 * gram_ld(n) + s.epc * 162) * 8 > 200 * 1024) s.epc /= 2;
   s.nchunk = std::max(1, ceil_div(std::max(s.n, 1), s.epc));
   s.fe_w.alloc((size_t)c->n_sims * std::max(s.n, 1) * 12);
@@ -350,16 +361,24 @@ void wnet_phase(nlrom_ctx* c) {
            (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
   }
   const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + nsplit * c->wn) * 8;
+  if (c->wn % 2 == 0 && 256 % c->wn == 0 && (c->n_sims == 1 || nsplit == 1)) {
+    launch(c, k_wnet_tail2, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm + 16,
+           (const double*)c->wpart.p, nsplit, c->wn, (const double*)c->b1.p, (const double*)c->W2.p,
+           (const double*)c->b2.p, (const double*)c->W3.p, (const double*)c->b3.p, (const double*)c->W4C.p,
+           (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
+    return;
+  }
   launch(c, k_wnet_tail, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm, (const double*)c->wpart.p, nsplit, c->wn,
          (const double*)c->b1.p, (const double*)c->W2.p, (const double*)c->b2.p, (const double*)c->W3.p,
          (const double*)c->b3.p, (const double*)c->W4C.p, (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
 }
 
-void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted) {
+void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true) {
   CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, weighted ? c->wC.p : nullptr, c->u.p, c->Jt.p,
             c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk, nullptr, nullptr};
   size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162) * 8;
   launch(c, k_cubature, dim3(s.nchunk, c->n_sims), 256, smem, a);
+  if (scatter)
   launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
          (const int*)s.row_ptr.p, (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N,
          c->n_sims);
@@ -376,11 +395,25 @@ void assemble_launch(nlrom_ctx* c, CubSet& s, double dt, int drop_fict, int mode
 // The mass block J~^T M [(1+alpha dt)U, (1+alpha dt)J + dJ] depends only on the decoder bundle:
 // it runs on a side stream (a parallel graph branch) while the weight net, the cubature and
 // the a-vector -- the critical path -- run on the main stream.
+size_t mass_smem(nlrom_ctx* c) {
+  return (size_t)(2 * c->rpcM * c->ldjt + c->rpcM * c->lddj + c->rpcM) * 8 + 16;
+}
+
+void mass_block_launch(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
+  if (c->rpcM != c->rpc || (c->ldjt == gram_ld(c->n) && c->lddj % 2 == 0 && mass_smem(c) <= 220 * 1024)) {
+    launch(c, k_assemble_mass, dim3(c->nchM, c->n_sims), 256, mass_smem(c), (const double*)c->Jt.p, c->ldjt,
+           (const double*)c->dJ.p, c->lddj, (const double*)c->mass.p, c->N, c->n, c->n_p, c->rpcM, c->nchM,
+           c->alpha * dt, c->partA.p);
+  } else {
+    assemble_launch(c, s, dt, drop_fict, 1);
+  }
+}
+
 void mass_block_fork(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   NL_CUDA(cudaEventRecord(c->evFork, c->st));
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evFork, 0));
   std::swap(c->st, c->st2);
-  assemble_launch(c, s, dt, drop_fict, 1);
+  mass_block_launch(c, s, dt, drop_fict);
   std::swap(c->st, c->st2);
   NL_CUDA(cudaEventRecord(c->evJoin, c->st2));
 }
@@ -388,14 +421,25 @@ void mass_block_fork(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 // a and the J~^T a partials on the critical path; phi = sum of partials and S_base = mass block
 // + dt^2 K~ (no vhp) on the side branch (after the mass block), joined where they are consumed.
 void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
-  assemble_launch(c, s, dt, drop_fict, 2);
+  if (c->rpc <= 128 && c->n <= 128) {
+    AsmAArgs A{c->Jt.p, c->ldjt, c->mass.p, c->hvv.p, c->fext.p, c->r.p, c->rbar.p, c->rdbar.p,
+               s.rowptr_full.p, s.entries.p, s.fe_w.p, std::max(s.n, 1), c->a.p, c->partPhi.p,
+               c->N, c->n, c->rpc, c->nchA, dt, c->alpha, drop_fict};
+    launch(c, k_assemble_a, dim3(c->nchA, c->n_sims), 256, 0, A);
+  } else {
+    launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
+           (const int*)s.row_ptr.p, (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N,
+           c->n_sims);
+    assemble_launch(c, s, dt, drop_fict, 2);
+  }
   NL_CUDA(cudaEventRecord(c->evFork2, c->st));
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evFork2, 0));
   std::swap(c->st, c->st2);
   launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nchA, c->n,
          c->phi.p, c->norm.p);
+  if (!c->mass_early) mass_block_launch(c, s, dt, drop_fict);  // mass block, overlapping the vhp chain
   const int n = c->n;
-  launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
+  launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
          (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, dt, c->S.p);
   std::swap(c->st, c->st2);
   NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));
@@ -405,9 +449,9 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
   bundle_forward(c, cfg.dt, cfg.drop_fict);
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
-  mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
+  if (c->mass_early) mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
   if (cfg.integration == 0) wnet_phase(c);
-  cubature_phase(c, s, cfg.integration == 0);
+  cubature_phase(c, s, cfg.integration == 0, false);  // forces gathered per row by the assembly
   assemble_phase(c, s, cfg.dt, cfg.drop_fict);
   if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));  // phi, S_base (and the mass block)
 }
@@ -573,7 +617,7 @@ void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply, const double* xr
 void full_S(nlrom_ctx* c, const nlrom_simcfg& cfg) {
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   const int n = c->n;
-  launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchA,
+  launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
          (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
 }
 
@@ -806,7 +850,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       c->H[l].alloc((size_t)std::max(ncols, c->n_sims * c->Cc) * c->ldH[l]);
       c->cache[l].alloc((size_t)c->n_sims * 2 * n_q * c->ldc[l]);
     }
-    c->ldjt = c->n;
+    c->ldjt = gram_ld(c->n);  // J~ rows pitched like the Gram panels: one TMA copy per row chunk
     c->lddj = n_q;
     c->u.alloc((size_t)c->n_sims * N);
     c->value.alloc((size_t)c->n_sims * N);
@@ -823,9 +867,15 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     // assembly / solve
     while (c->rpc > 16 && (size_t)(2 * c->rpc * gram_ld(c->n) + 2 * c->rpc + c->n) * 8 > 200 * 1024) c->rpc /= 2;
     c->nchA = ceil_div(N, c->rpc);
+    c->rpcM = c->rpc;
+    if (c->ldjt == gram_ld(c->n) && c->lddj % 2 == 0) {
+      c->rpcM = 64;
+      while (c->rpcM > 16 && mass_smem(c) > 200 * 1024) c->rpcM /= 2;
+    }
+    c->nchM = ceil_div(N, c->rpcM);
     const int n = c->n, S = c->n_sims;
     c->a.alloc((size_t)S * N);
-    c->partA.alloc((size_t)S * c->nchA * n * n);
+    c->partA.alloc((size_t)S * std::max(c->nchA, c->nchM) * n * n);
     c->partPhi.alloc((size_t)S * c->nchA * n);
     c->phi.alloc((size_t)S * n);
     c->norm.alloc(S);
@@ -853,7 +903,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     // kernel attributes for large dynamic shared memory
     NL_CUDA(cudaFuncSetAttribute(k_cubature, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_wnet_tail2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_assemble_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1060,7 +1112,8 @@ extern "C" int nlrom_full_displacement(nlrom_ctx* c, const double* r, double* u)
 extern "C" int nlrom_jtilde(nlrom_ctx* c, const double* q, double* Jt) {
   CTX_TRY(c)
   bundle_only(c, q, nullptr, nullptr, 1.0, 0, nullptr);
-  d2h(c, Jt, c->Jt, (size_t)c->N * c->n);
+  NL_CUDA(cudaMemcpy2DAsync(Jt, (size_t)c->n * 8, c->Jt.p, (size_t)c->ldjt * 8, (size_t)c->n * 8, c->N,
+                            cudaMemcpyDeviceToHost, c->st));
   NL_CUDA(cudaStreamSynchronize(c->st));
   CTX_END(c)
 }

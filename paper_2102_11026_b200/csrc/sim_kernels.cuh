@@ -1,6 +1,7 @@
 // Non-GEMM kernels of the reduced Newton step: seeds, wnet, StVK cubature,
 // assembly, reductions, in-CTA LU with partial pivoting.
 #pragma once
+#include "cluster_async.cuh"
 #include "common.cuh"
 #include "mc_device.cuh"
 #include "gram_dmma.cuh"
@@ -199,6 +200,95 @@ __global__ void k_wnet_tail(const double* __restrict__ part, int n_split, int wn
   }
 }
 
+// Same tail with TMA bulk staging (one copy per weight matrix / bias / partial block, on two
+// mbarriers: constants before the dependency wait, the producer's partials after it) and
+// tpr = blockDim / wn threads per output row (short FMA chains + a 2-level shuffle) instead of
+// a warp per row. Needs wn even, blockDim % wn == 0, partials contiguous per sim.
+__device__ __forceinline__ double wnet_row_tpr(const double* __restrict__ W, int wn, const double* hin, int m, int q,
+                                               int tpr) {
+  const int per = wn / tpr;
+  double acc = 0.0;
+  for (int i = 0; i < per; ++i) {
+    const int k = q + tpr * ((i + m) % per);  // rotated walk: rows of a warp hit different banks
+    acc = fma(W[(size_t)m * wn + k], hin[k], acc);
+  }
+  for (int o = tpr >> 1; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_wnet_tail2(const double* __restrict__ part, int n_split, int wn,
+                                                    const double* __restrict__ b1, const double* __restrict__ W2,
+                                                    const double* __restrict__ b2, const double* __restrict__ W3,
+                                                    const double* __restrict__ b3, const double* __restrict__ W4C,
+                                                    const double* __restrict__ b4C, int n_cub, double* __restrict__ wC,
+                                                    int n_sims) {
+  extern __shared__ __align__(16) double sh[];
+  const int sim = blockIdx.y, tid = threadIdx.x;
+  const int j0 = blockIdx.x * 64;
+  const int nrows4 = max(0, min(64, n_cub - j0));
+  double* h1 = sh;
+  double* h2 = h1 + wn;
+  double* bs = h2 + wn;            // b1 | b2 | b3   [3 wn]
+  double* W2s = bs + 3 * wn + 64;
+  double* W3s = W2s + wn * wn;
+  double* W4s = W3s + wn * wn;     // [64][wn]
+  double* ps = W4s + 64 * wn;      // [n_split][wn]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ps + n_split * wn);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+    const uint32_t mat = (uint32_t)(wn * wn * 8), vec = (uint32_t)(wn * 8);
+    mbar_expect_tx(bar, 2 * mat + (uint32_t)(nrows4 * wn * 8) + 3 * vec);
+    tma_g2s(W2s, W2, mat, bar);
+    tma_g2s(W3s, W3, mat, bar);
+    if (nrows4) tma_g2s(W4s, W4C + (size_t)j0 * wn, (uint32_t)(nrows4 * wn * 8), bar);
+    tma_g2s(bs, b1, vec, bar);
+    tma_g2s(bs + wn, b2, vec, bar);
+    tma_g2s(bs + 2 * wn, b3, vec, bar);
+  }
+  pdl_wait();
+  pdl_launch();
+  if (tid == 0) {
+    const uint32_t pb = (uint32_t)(n_split * wn * 8);
+    mbar_expect_tx(bar + 1, pb);
+    tma_g2s(ps, part + (size_t)sim * (n_split == 1 ? wn : 0), pb, bar + 1);
+  }
+  __syncthreads();
+  mbar_wait(bar + 1, 0);
+  mbar_wait(bar, 0);
+  for (int m = tid; m < wn; m += blockDim.x) {
+    double acc[4] = {bs[m], 0.0, 0.0, 0.0};
+    int s2 = 0;
+    for (; s2 + 3 < n_split; s2 += 4)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += ps[(s2 + u) * wn + m];
+    for (; s2 < n_split; ++s2) acc[0] += ps[s2 * wn + m];
+    h1[m] = sin((acc[0] + acc[1]) + (acc[2] + acc[3]));
+  }
+  __syncthreads();
+  const int tpr = blockDim.x / wn, m = tid / tpr, q = tid % tpr;
+  {
+    const double v = wnet_row_tpr(W2s, wn, h1, m, q, tpr);
+    if (q == 0) h2[m] = sin(v + bs[wn + m]);
+  }
+  __syncthreads();
+  {
+    const double v = wnet_row_tpr(W3s, wn, h2, m, q, tpr);
+    if (q == 0) h1[m] = sin(v + bs[2 * wn + m]);
+  }
+  __syncthreads();
+  for (int r0 = 0; r0 < nrows4; r0 += wn) {
+    const int jj = r0 + m;
+    const bool ok = jj < nrows4;
+    const double v = wnet_row_tpr(W4s, wn, h1, ok ? jj : 0, q, tpr);
+    if (q == 0 && ok) {
+      const double z = v + b4C[j0 + jj];
+      wC[(size_t)sim * n_cub + j0 + jj] = z * z;
+    }
+  }
+}
+
 // -------------------------------------------------------------------- cubature
 // One warp per element: StVK (P1 tet, one-point quadrature) force f_e and stiffness
 // K_e, weighted by w_e; then the CTA projects with the element's
@@ -263,9 +353,16 @@ __global__ void k_cubature(CubArgs a) {
     for (int rr = warp; Jt && rr < epc * 12; rr += nw) {  // warp per J~ row: no div / mod
       const int row = Rw[rr];
       double* dst = Js + rr * ldp;
-      for (int j = lane; j < n; j += 32) {
-        if (row >= 0) cp_async8(dst + j, Jt + (size_t)row * a.ldjt + j);
-        else dst[j] = 0.0;
+      if ((a.ldjt & 1) == 0 && (ldp & 1) == 0) {  // 16-byte chunks (both pitches even)
+        for (int j = 2 * lane; j < n; j += 64) {
+          if (row >= 0) cp_async16(dst + j, Jt + (size_t)row * a.ldjt + j, true);
+          else dst[j] = dst[j + 1] = 0.0;
+        }
+      } else {
+        for (int j = lane; j < n; j += 32) {
+          if (row >= 0) cp_async8(dst + j, Jt + (size_t)row * a.ldjt + j);
+          else dst[j] = 0.0;
+        }
       }
     }
   }

@@ -1,6 +1,7 @@
 // Assembly of the reduced Newton system, its reductions, the in-CTA LU solve and the
 // top of the vhp backward (rdsim.residual / system_jacobian / step).
 #pragma once
+#include "cluster_async.cuh"
 #include "common.cuh"
 #include "mc_device.cuh"
 #include "gram_dmma.cuh"
@@ -110,6 +111,128 @@ __global__ void k_assemble(AsmArgs A) {
   double* Pp = A.partphi + ((size_t)sim * A.nchunk + chunk) * n;
   if (A.mode != 2) gram_dmma(Js, ldp, Rs, ldp, RC, n, n, P, n);
   if (A.mode != 1) gram_dmma(Js, ldp, Rs + n, ldp, RC, n, 1, Pp, 1);
+}
+
+// Mass block of the system matrix for one chunk of RC rows (the side-branch half of the
+// assembly, mode 1 of k_assemble): partA[chunk] = J~_rows^T M [(1+ah) U, (1+ah) J + dJ]_rows.
+// J~ rows (global pitch ldjt == the Gram panel pitch), dJ rows and the masses land by three TMA
+// bulk copies; the Gram product runs on the DMMA pipe.
+__global__ void __launch_bounds__(256) k_assemble_mass(const double* __restrict__ Jt, int ldjt,
+                                                       const double* __restrict__ dJ, int lddj,
+                                                       const double* __restrict__ mass, int N, int n, int n_p,
+                                                       int RC, int nchunk, double ah, double* __restrict__ part) {
+  pdl_wait();
+  pdl_launch();
+  extern __shared__ __align__(16) double sh[];
+  const int ldp = ldjt;
+  double* Js = sh;                     // [RC][ldp]
+  double* Rs = Js + (size_t)RC * ldp;  // [RC][ldp]
+  double* Ds = Rs + (size_t)RC * ldp;  // [RC][lddj]
+  double* ms = Ds + (size_t)RC * lddj; // [RC]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ms + RC);
+  const int chunk = blockIdx.x, sim = blockIdx.y, tid = threadIdx.x;
+  const int row0 = chunk * RC, nrow = min(RC, N - row0);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const uint32_t bj = (uint32_t)(nrow * ldjt * 8), bd = (uint32_t)(nrow * lddj * 8), bm = (uint32_t)(nrow * 8);
+    mbar_expect_tx(bar, bj + bd + (nrow % 2 == 0 ? bm : 0));
+    tma_g2s(Js, Jt + ((size_t)sim * N + row0) * ldjt, bj, bar);
+    tma_g2s(Ds, dJ + ((size_t)sim * N + row0) * lddj, bd, bar);
+    if (nrow % 2 == 0) tma_g2s(ms, mass + row0, bm, bar);
+  }
+  if (nrow % 2 != 0)
+    for (int i = tid; i < nrow; i += blockDim.x) ms[i] = mass[row0 + i];
+  for (int t = tid; t < (RC - nrow) * ldp; t += blockDim.x) {  // zero tail rows of the last chunk
+    Js[(size_t)nrow * ldp + t] = 0.0;
+    Rs[(size_t)nrow * ldp + t] = 0.0;
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  for (int t = tid; t < nrow * n; t += blockDim.x) {
+    const int rl = t / n, j = t % n;
+    const double dj = (j >= n_p) ? Ds[rl * lddj + (j - n_p)] : 0.0;
+    Rs[rl * ldp + j] = ((1.0 + ah) * Js[rl * ldp + j] + dj) * ms[rl];
+  }
+  __syncthreads();
+  gram_dmma(Js, ldp, Rs, ldp, RC, n, n, part + ((size_t)sim * nchunk + chunk) * n * n, n);
+}
+
+// The critical-path half of the assembly for one chunk of RC <= 128 rows, with the weighted
+// element forces gathered per row through a full-row CSR (no separate scatter launch):
+//   a_row = m (J~_row . c) + dt^2 (f_row - fext_row) + m hvv_row,   f_row = sum_{(e,l) -> row} w_e f_e[l]
+//   partphi[chunk] = J~_chunk^T a_chunk
+// 256 threads: 2 per row for the dot products and the gather, then 4 row quarters x 64 columns.
+struct AsmAArgs {
+  const double* Jt; int ldjt;
+  const double* mass; const double* hvv; const double* fext;
+  const double* r; const double* rbar; const double* rdbar;
+  const int* rowptr;       // (N + 1): CSR over all free-DOF rows
+  const int* entries;      // element slot * 12 + l
+  const double* fe_w;      // (n_sims, n_elems, 12)
+  int n_elems;
+  double* a; double* partphi;
+  int N, n, RC, nchunk;
+  double dt, alpha;
+  int drop_fict;
+};
+
+__global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double cs[128];
+  __shared__ double as[128];
+  __shared__ double red[4][64];
+  const int chunk = blockIdx.x, sim = blockIdx.y, tid = threadIdx.x;
+  const int n = A.n;
+  const double ah = A.alpha * A.dt;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const size_t o = (size_t)sim * n + i;
+    cs[i] = (1.0 + ah) * (A.r[o] - A.rbar[o]) - A.dt * A.rdbar[o];
+  }
+  __syncthreads();
+  const int row0 = chunk * A.RC;
+  const double* Jsim = A.Jt + (size_t)sim * A.N * A.ldjt;
+  {
+    const int rl = tid >> 1, h = tid & 1;
+    const int row = row0 + rl;
+    double acc = 0.0, fs = 0.0;
+    if (rl < A.RC && row < A.N) {
+      const double* Jr = Jsim + (size_t)row * A.ldjt;
+      for (int j = h; j < n; j += 2) acc = fma(Jr[j], cs[j], acc);
+      const double* fw = A.fe_w + (size_t)sim * A.n_elems * 12;
+      for (int k = A.rowptr[row] + h; k < A.rowptr[row + 1]; k += 2) fs += fw[A.entries[k]];
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    fs += __shfl_xor_sync(0xffffffffu, fs, 1);
+    if (h == 0 && rl < A.RC) {
+      double av = 0.0;
+      if (row < A.N) {
+        const size_t o = (size_t)sim * A.N + row;
+        const double m = A.mass[row];
+        av = m * acc + A.dt * A.dt * (fs - A.fext[o]);
+        if (!A.drop_fict) av += m * A.hvv[o];
+        A.a[o] = av;
+      }
+      as[rl] = av;
+    }
+  }
+  __syncthreads();
+  const int q = tid >> 6, jl = tid & 63;
+  for (int j0 = 0; j0 < n; j0 += 64) {
+    const int j = j0 + jl;
+    double acc = 0.0;
+    if (j < n)
+      for (int rl = q; rl < A.RC; rl += 4) {
+        const int row = row0 + rl;
+        if (row < A.N) acc = fma(Jsim[(size_t)row * A.ldjt + j], as[rl], acc);
+      }
+    red[q][jl] = acc;
+    __syncthreads();
+    if (q == 0 && j < n)
+      A.partphi[((size_t)sim * A.nchunk + chunk) * n + j] = (red[0][jl] + red[1][jl]) + (red[2][jl] + red[3][jl]);
+    __syncthreads();
+  }
 }
 
 // phi = sum_chunks partphi (one CTA per sim; 8 chunk groups per output, smem combine), ||phi||_2
