@@ -364,7 +364,7 @@ def run_ours(args):
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "dominant_traffic.json")))
         roof["traffic"] = sum(tr.get(k, {}).get("dram_bytes_per_launch", 0) for k in
-                              ("k_mlp_jet_fwd", "gemm_tn_kernel<CfgOutC,EpiJetOutC>", "k_gemv_t", "k_mlp_dual_bwd")) or None
+                              ("k_mlp_jet_fwd", "gemm_tn_kernel<CfgOutC,EpiJetOutC>", "k_mlp_dual_bwd")) or None
     except Exception:
         pass
 
