@@ -69,6 +69,14 @@ __device__ __forceinline__ void tma_g2s(void* dst, const void* src, uint32_t byt
                : "memory");
 }
 
+// named CTA barriers (ids 1..15; 0 is __syncthreads): producer arrive / consumer sync
+__device__ __forceinline__ void named_bar_arrive(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int cnt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

@@ -21,6 +21,7 @@
 #include "solve_kernels.cuh"
 #include "mlp_chain.cuh"
 #include "coupled_kernels.cuh"
+#include "gemm_ws.cuh"
 
 namespace nlrom {
 void fc_forward(int order, int act, const GemmArgs& g, double* Y, int ldy, const double* bias, double* cache,
@@ -241,12 +242,16 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
 // Decoder output layer + fused filter over the compact columns: D = [W_L | -U][h; U^T W_L h] + P b.
 // The dominant kernel of one Newton iteration (fp64 DMMA, 8 warps, 48 x 128 tiles, one wave).
 using CfgOutC = GemmCfg<48, 128, 2, 4, 1, 32, 3>;
+// same tiling on the warp-specialised TMA pipeline (gemm_ws.cuh): 6 swizzled stages, one
+// producer warp; 13% faster on this shape (tools/probes/gemm_ws_probe.cu), bitwise identical
+using CfgOutWs = WsCfg<48, 128, 2, 4, 6>;
 
 void output_layer(nlrom_ctx* c) {
   GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->next, 0, 0};
   EpiJetOutC e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
                c->n_p, c->n_q};
   if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
+  else if (c->ldlast % 2 == 0 && !getenv("NLROM_NO_WS_GEMM")) launch_gemm_ws<CfgOutWs>(g, e, c->st);
   else launch_gemm<CfgOutC>(g, e, c->st);
   ++gemm_launch_count;
 }

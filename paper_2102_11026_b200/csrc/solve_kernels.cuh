@@ -329,6 +329,18 @@ __global__ void k_reduce_cub(const double* __restrict__ part_f, const double* __
 // implicit (rows are marked used instead of swapped: same arithmetic as LU-pp).
 // Back substitution by warp 0 with shuffles. If `apply`, r += dr.
 // status[sim] = 1 on a zero pivot.
+// 1/p on the pivot critical path: MUFU reciprocal seed + two Newton steps (error <= 1 ulp;
+// the IEEE-rounded division costs ~3x the latency here). |p| is a partial pivot, never
+// denormal for a non-singular Newton matrix.
+__device__ __forceinline__ double recip_fast(double p) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+  double e = fma(-p, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-p, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <int NB>
 __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, const double* __restrict__ phi,
                                                    double* __restrict__ dr, double* __restrict__ r, int n, int apply,
@@ -406,7 +418,7 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     if (!(mhi | mlo) || piv >= n) { bad = true; break; }
     if (piv < 64) used_lo |= 1ull << piv;
     else used_hi |= 1ull << (piv - 64);
-    const double rp = 1.0 / M[piv * LDF + k];
+    const double rp = recip_fast(M[piv * LDF + k]);
     if (tid == 0) {
       pivrow[k] = piv;
       rdiag[k] = rp;
@@ -500,12 +512,6 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
 // (bar.arrive / bar.sync, two alternating ids), so a step costs one producer->consumer
 // hand-off instead of a full CTA barrier plus redundant pivot searches in every warp.
 // Same arithmetic as k_lu_solve (m = a_ik / a_pk, a_ij -= m a_pj on unused rows).
-__device__ __forceinline__ void named_bar_arrive(int id, int cnt) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void named_bar_sync(int id, int cnt) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
-}
 
 constexpr int LUC_CPW = 9, LUC_D = 64, LUC_LDF = 8 * LUC_CPW + 1;
 #ifdef LU_TRACE

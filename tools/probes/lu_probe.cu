@@ -34,15 +34,15 @@ int main() {
     };
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     float ms;
-    for (int w = 0; w < 3; ++w) k_lu_solve<4><<<1, 256, lu_smem_bytes(n)>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr);
+    for (int w = 0; w < 3; ++w) k_lu_solve<4><<<1, 256, lu_smem_bytes(n)>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr, nullptr, 0, 0);
     cudaEventRecord(a);
-    for (int r = 0; r < 200; ++r) k_lu_solve<4><<<1, 256, lu_smem_bytes(n)>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr);
+    for (int r = 0; r < 200; ++r) k_lu_solve<4><<<1, 256, lu_smem_bytes(n)>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr, nullptr, 0, 0);
     cudaEventRecord(b); cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b);
     check("k_lu_solve", ms);
-    for (int w = 0; w < 3; ++w) k_lu_cols<<<1, 256, luc_smem_bytes()>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr);
+    for (int w = 0; w < 3; ++w) k_lu_cols<<<1, 256, luc_smem_bytes()>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr, nullptr, 0, 0);
     cudaEventRecord(a);
-    for (int r = 0; r < 200; ++r) k_lu_cols<<<1, 256, luc_smem_bytes()>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr);
+    for (int r = 0; r < 200; ++r) k_lu_cols<<<1, 256, luc_smem_bytes()>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr, nullptr, 0, 0);
     cudaEventRecord(b); cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b);
     check("k_lu_cols", ms);
