@@ -93,6 +93,7 @@ struct nlrom_ctx {
   // assembly / solve
   int rpc = 128, nchA = 0;
   int rpcM = 128, nchM = 0;  // row chunking of the mass block (finer: more CTAs for its Gram)
+  int s_ctas = getenv("NLROM_S_CTAS") ? atoi(getenv("NLROM_S_CTAS")) : 1 << 20;  // side-branch S reduction CTAs
   DBuf a, partA, partPhi, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
   IBuf status;
   // backward
@@ -444,7 +445,8 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
          c->phi.p, c->norm.p);
   if (!c->mass_early) mass_block_launch(c, s, dt, drop_fict);  // mass block, overlapping the vhp chain
   const int n = c->n;
-  launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
+  const int sblocks = std::min(ceil_div(n * n, 32), c->s_ctas);
+  launch(c, k_reduce_S, dim3(sblocks, c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
          (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, dt, c->S.p);
   std::swap(c->st, c->st2);
   NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));

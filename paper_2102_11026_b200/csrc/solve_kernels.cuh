@@ -278,25 +278,30 @@ __global__ void k_reduce_S(const double* __restrict__ partA, int nchA, const dou
                            double* __restrict__ S) {
   pdl_wait();
   pdl_launch();
+  // block-stride over 32-output blocks: the side-branch launch uses few CTAs so that it does not
+  // hold SMs the concurrently scheduled 16-CTA clusters of the vhp chain need
   __shared__ double red[8][32];
   const int sim = blockIdx.y;
   const int lane = threadIdx.x & 31, gidx = threadIdx.x >> 5;
-  const int idx = blockIdx.x * 32 + lane;
   const int nn = n * n;
-  double a = 0.0, k = 0.0;
-  if (idx < nn) {
-    for (int c = gidx; c < nchA; c += 8) a += partA[((size_t)sim * nchA + c) * nn + idx];
-    for (int c = gidx; c < nchK; c += 8) k += partK[((size_t)sim * nchK + c) * nn + idx];
-  }
-  red[gidx][lane] = a + dt * dt * k;
-  __syncthreads();
-  if (gidx == 0 && idx < nn) {
-    double acc = 0.0;
+  for (int ob = blockIdx.x; ob * 32 < nn; ob += gridDim.x) {
+    const int idx = ob * 32 + lane;
+    double a = 0.0, k = 0.0;
+    if (idx < nn) {
+      for (int c = gidx; c < nchA; c += 8) a += partA[((size_t)sim * nchA + c) * nn + idx];
+      for (int c = gidx; c < nchK; c += 8) k += partK[((size_t)sim * nchK + c) * nn + idx];
+    }
+    red[gidx][lane] = a + dt * dt * k;
+    __syncthreads();
+    if (gidx == 0 && idx < nn) {
+      double acc = 0.0;
 #pragma unroll
-    for (int g2 = 0; g2 < 8; ++g2) acc += red[g2][lane];
-    const int i = idx / n, j = idx % n;
-    if (Gt && i >= n_p && j >= n_p) acc += Gt[((size_t)sim * 2 * n_q + 2 * (j - n_p) + 1) * ldg + (i - n_p)];
-    S[(size_t)sim * nn + idx] = acc;
+      for (int g2 = 0; g2 < 8; ++g2) acc += red[g2][lane];
+      const int i = idx / n, j = idx % n;
+      if (Gt && i >= n_p && j >= n_p) acc += Gt[((size_t)sim * 2 * n_q + 2 * (j - n_p) + 1) * ldg + (i - n_p)];
+      S[(size_t)sim * nn + idx] = acc;
+    }
+    __syncthreads();
   }
 }
 
