@@ -514,15 +514,18 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
 }
 
 // Fused vhp backward chain (mlp_chain.cuh): g = (P W_L)^T a, then one cluster per 8 passes.
-template <int R, int CS>
-bool launch_mlp_bwd(nlrom_ctx* c, const MlpBwdArgs& a, int groups, bool dry) {
-  const size_t smem = mlp_bwd_smem<R>(c->wL1);
+template <int R, int CS, int G = 16>
+bool launch_mlp_bwd(nlrom_ctx* c, MlpBwdArgs a, int dry) {
+  a.gpb = ceil_div(c->n_q, G / 2);
+  const int groups = c->n_sims * a.gpb;
+  const size_t smem = mlp_bwd_smem<R, G>(c->wL1);
   if (smem > 227 * 1024) return false;
   if (dry) return true;
   static bool configured = false;
   if (!configured) {
-    NL_CUDA(cudaFuncSetAttribute(k_mlp_dual_bwd<R, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (CS > 8) NL_CUDA(cudaFuncSetAttribute(k_mlp_dual_bwd<R, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    NL_CUDA(cudaFuncSetAttribute(k_mlp_dual_bwd<R, CS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (CS > 8)
+      NL_CUDA(cudaFuncSetAttribute(k_mlp_dual_bwd<R, CS, G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -539,8 +542,8 @@ bool launch_mlp_bwd(nlrom_ctx* c, const MlpBwdArgs& a, int groups, bool dry) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  if (!launch_gate((const void*)k_mlp_dual_bwd<R, CS>)) return true;
-  NL_CUDA(cudaLaunchKernelEx(&cfg, k_mlp_dual_bwd<R, CS>, a));
+  if (!launch_gate((const void*)k_mlp_dual_bwd<R, CS, G>)) return true;
+  NL_CUDA(cudaLaunchKernelEx(&cfg, k_mlp_dual_bwd<R, CS, G>, a));
   ++gemm_launch_count;
   return true;
 }
@@ -561,19 +564,25 @@ bool fused_vhp_backward(nlrom_ctx* c) {
   a.ldc = c->ldc[0]; a.Gt = c->Gt.p; a.ldG = c->ldGt;
   a.ldpb = c->ldpb;
   if (c->ldpb != round_up(w, 16) + 4) return false;
-  a.gpb = ceil_div(c->n_q, 8);
-  const int groups = c->n_sims * a.gpb;
+  static const int bwd_cfg = getenv("NLROM_BWD_CFG") ? atoi(getenv("NLROM_BWD_CFG")) : 0;
   auto go = [&](bool dry) -> bool {
-    if (w == 256) return launch_mlp_bwd<16, 16>(c, a, groups, dry);
-    if (w == 64) return launch_mlp_bwd<8, 8>(c, a, groups, dry);
-    if (w == 40) return launch_mlp_bwd<8, 5>(c, a, groups, dry);
-    if (w == 8) return launch_mlp_bwd<8, 1>(c, a, groups, dry);
+    if (w == 256) {
+      // 4 dual passes (8 columns) per 8-CTA cluster halve the DSMEM bytes each CTA broadcasts per
+      // stage relative to 8 passes on 16-CTA clusters (the stage is broadcast-bound)
+      if (bwd_cfg == 1) return launch_mlp_bwd<16, 16, 16>(c, a, dry);
+      if (bwd_cfg == 2) return launch_mlp_bwd<16, 16, 8>(c, a, dry);
+      return launch_mlp_bwd<32, 8, 8>(c, a, dry);
+    }
+    if (w == 64) return launch_mlp_bwd<8, 8>(c, a, dry);
+    if (w == 40) return launch_mlp_bwd<8, 5>(c, a, dry);
+    if (w == 8) return launch_mlp_bwd<8, 1>(c, a, dry);
     return false;
   };
   if (!go(true)) return false;
   if (M % 2 == 0 && c->ldlast % 2 == 0 && M <= 512) {
     // 24-row chunks over ~280 CTAs; the chain's prologue sums the partials (no reduce launch)
-    const int rows = 24, nch = ceil_div(c->N, rows);
+    static const int rows = getenv("NLROM_GEMV_ROWS") ? atoi(getenv("NLROM_GEMV_ROWS")) : 24;
+    const int nch = ceil_div(c->N, rows);
     launch(c, k_gemv_t2, dim3(nch, c->n_sims), 256, 0, (const double*)c->Alast.p, c->ldlast, M,
            (const double*)c->a.p, c->N, rows, c->bpart.p, nch);
     a.gpart = c->bpart.p;
@@ -899,7 +908,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     // backward
     if (w + n_p > 512) throw Error(NLROM_ERR_ARG, "last hidden width + n_p must be <= 512");
     c->bnch = ceil_div(N, c->brows);
-    c->bpart.alloc((size_t)std::max(c->bnch, ceil_div(N, 24)) * S * (w + n_p));
+    c->bpart.alloc((size_t)std::max(c->bnch, ceil_div(N, 8)) * S * (w + n_p));
     c->ybuf.alloc((size_t)S * (w + n_p));
     int maxw = 0;
     for (int l = 1; l < L; ++l) maxw = std::max(maxw, round_up(c->widths[l], 2));

@@ -446,11 +446,12 @@ struct MlpBwdArgs {
   int gpb;                  // groups (of 8 passes) per sim
 };
 
-template <int R, int CS>
+template <int R, int CS, int GB = 16>
 __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  constexpr int G = 16, NTH = 256;
+  constexpr int G = GB, NTH = 256;  // G columns = G / 2 dual passes per group
+  constexpr int PG = G / 2;
   using P = MlpPlan<R, G>;
   extern __shared__ __align__(16) double sm[];
   const int kmax = P::kp(a.w);
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
     const double* C = a.cache[l] + (size_t)sim * 2 * a.n_q * a.ldc;
     for (int t = tid; t < R * G; t += NTH) {
       const int rr = t % R, col = t / R;
-      const int p = gl * 8 + col / 2;
+      const int p = gl * PG + col / 2;
       double* dst = Zbuf(buf) + rr * G + col;
       if (p < a.n_q && r0 + rr < a.w) cp_async8(dst, C + (size_t)(2 * p + (col & 1)) * a.ldc + r0 + rr);
       else *dst = 0.0;
@@ -549,7 +550,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
       // G = W_0^T Delta_0: rows i < n_q
       for (int t = tid; t < R * G; t += NTH) {
         const int rr = t % R, col = t / R;
-        const int i = r0 + rr, p = gl * 8 + col / 2;
+        const int i = r0 + rr, p = gl * PG + col / 2;
         if (i < a.n_q && p < a.n_q)
           a.Gt[((size_t)sim * 2 * a.n_q + 2 * p + (col & 1)) * a.ldG + i] = Ys[col * (R + 1) + rr];
       }
@@ -557,7 +558,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
     }
     // Delta rows of this CTA: (input (*) cos(z)) in dual arithmetic, z = cache of layer L1-1-s
     const double* Z = Zbuf(s & 1);
-    for (int t = tid; t < R * 8; t += NTH) {
+    for (int t = tid; t < R * PG; t += NTH) {
       const int rr = t % R, j = t / R;
       const int m = r0 + rr;
       double d0, d1;
@@ -593,11 +594,11 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
   }
 }
 
-template <int R>
+template <int R, int G = 16>
 inline size_t mlp_bwd_smem(int w) {
-  using P = MlpPlan<R, 16>;
+  using P = MlpPlan<R, G>;
   const int kp = P::kp(w);
-  return (size_t)(2 * kp * P::LDX + 2 * R * P::ldws(kp) + 2 * R * 16 + 16 * (R + 1) + R * P::LDX) * 8 + 16;
+  return (size_t)(2 * kp * P::LDX + 2 * R * P::ldws(kp) + 2 * R * G + G * (R + 1) + R * P::LDX) * 8 + 16;
 }
 
 }  // namespace nlrom
