@@ -5,7 +5,8 @@ import importlib
 import sys
 
 _impl = importlib.import_module("paper_2102_11026_b200")
-_MODULES = ("mcx", "densenet", "diffops", "elastic", "daereduce", "neucubature", "rdsim")
+_MODULES = ("mcx", "densenet", "diffops", "elastic", "daereduce", "neucubature", "rdsim", "artifacts",
+            "substructure")
 
 
 def __getattr__(name):
