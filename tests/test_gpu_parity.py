@@ -305,3 +305,53 @@ def test_loaded_artifacts_same_device_results(cfg1, tmp_path):
     assert np.array_equal(a, b)
     assert np.array_equal(rdsim.system_jacobian(P.rm, P.model, st, P.f_ext, cfg, r=r),
                           rdsim.system_jacobian(rm2, model2, st, P.f_ext, cfg, r=r))
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2102_11026_b200.problem import build_problem
+from paper_2102_11026_b200 import rdsim
+from paper_2102_11026_b200.daereduce import ReducedState
+P = build_problem("cfg2", n_fc=4)
+r, rb, rdb = P.random_state()
+cfg = rdsim.SimConfig(dt=P.cfg.dt)
+st = ReducedState(rb, rdb, cfg.dt)
+phi = rdsim.residual(P.rm, P.model, st, P.f_ext, cfg, r=r)
+S = rdsim.system_jacobian(P.rm, P.model, st, P.f_ext, cfg, r=r)
+st0 = P.rest_state()
+nxt = rdsim.step(P.rm, P.model, st0, P.f_ext, rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=2))
+np.savez(sys.argv[2], phi=phi, S=S, r=nxt.r)
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"NLROM_ASYNC_CHAIN": "1"},
+    {"NLROM_LU_COLS": "1", "NLROM_MASS_LATE": "1"},
+    {"NLROM_BWD_CFG": "1", "NLROM_NO_WS_GEMM": "1"},
+    {"NLROM_NO_FUSED_MLP": "1", "NLROM_LU_ROWS": "1"},
+])
+def test_kernel_variants(cuda_ok, env, tmp_path):
+    """Opt-in kernel variants (selected by environment at context creation, hence a fresh
+    process) against the oracle: async cluster hand-off chain, column-cyclic LU, mass block on
+    the late branch, 16-CTA vhp clusters, cp.async output GEMM, unfused per-layer GEMMs."""
+    import os
+    import subprocess
+    import sys
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200.rdsim import SimConfig
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "v.npz")
+    e = dict(os.environ, **env)
+    subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root, out], env=e, check=True, timeout=600)
+    got = np.load(out)
+    P = build_problem("cfg2", n_fc=4)
+    S = oracle_sim(P)
+    r, rb, rdb = P.random_state()
+    oc = ocfg(SimConfig(dt=P.cfg.dt))
+    assert rel(got["phi"], ors.residual(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+    assert rel(got["S"], ors.system_jacobian(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+    st0 = P.rest_state()
+    ro, _, _, _ = ors.step(S, st0.r.copy(), st0.rdot.copy(), P.f_ext,
+                           ocfg(SimConfig(dt=P.cfg.dt, fixed_iters=2)))
+    assert np.abs(got["r"] - ro).max() <= 1e-10 * np.abs(ro).max()
