@@ -111,6 +111,9 @@ struct nlrom_ctx {
   // mass block on a side branch beside the weight net (default) or, with NLROM_MASS_LATE, beside
   // the vhp chain (measured slower: the 16-CTA clusters cannot co-schedule with it)
   bool mass_early = getenv("NLROM_MASS_LATE") == nullptr;
+  // 1 (default): forked after the cubature, beside the assembly; 0: beside the weight net (measured
+  // slower: it contends with the cubature for SMs)
+  int mass_pos = getenv("NLROM_MASS_POS") ? atoi(getenv("NLROM_MASS_POS")) : 1;
   DBuf cpR, cpFloc, cpFsum, cpCore, cpBlocks, cpCb, cpX, cpFcore;
   double cp_m_core = 0, cp_k_core = 0, cp_m_string = 0, cp_m_total = 0;
   cudaGraphExec_t gC[2] = {nullptr, nullptr};
@@ -363,8 +366,15 @@ void wnet_phase(nlrom_ctx* c) {
     ++gemm_launch_count;
     nsplit = 1;
   } else {
-    launch(c, k_gemv_splitk, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
-           (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
+    if (c->wchunk == 64)
+      launch(c, k_gemv_splitk_t<2>, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
+             (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wpart.p, c->n_sims);
+    else if (c->wchunk == 32)
+      launch(c, k_gemv_splitk_t<1>, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
+             (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wpart.p, c->n_sims);
+    else
+      launch(c, k_gemv_splitk, dim3(c->wsplit, c->n_sims), 256, 0, (const double*)c->W1.p, round_up(c->N, 2),
+             (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
   }
   const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + nsplit * c->wn) * 8;
   if (c->wn % 2 == 0 && 256 % c->wn == 0 && (c->n_sims == 1 || nsplit == 1)) {
@@ -456,9 +466,10 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
   bundle_forward(c, cfg.dt, cfg.drop_fict);
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
-  if (c->mass_early) mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
+  if (c->mass_early && c->mass_pos == 0) mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
   if (cfg.integration == 0) wnet_phase(c);
   cubature_phase(c, s, cfg.integration == 0, false);  // forces gathered per row by the assembly
+  if (c->mass_early && c->mass_pos == 1) mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
   assemble_phase(c, s, cfg.dt, cfg.drop_fict);
   if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));  // phi, S_base (and the mass block)
 }

@@ -117,6 +117,54 @@ __global__ void k_gemv_splitk(const double* __restrict__ A, int lda, const doubl
   }
 }
 
+// Same split-K GEMV with every load of a lane issued up front: CH k-values per lane (chunk =
+// 32 CH columns), 8 rows per warp, 8 interleaved shuffle trees.
+template <int CH>
+__global__ void __launch_bounds__(256) k_gemv_splitk_t(const double* __restrict__ A, int lda,
+                                                       const double* __restrict__ x, long long strideX, int M, int K,
+                                                       double* __restrict__ part, int n_sims) {
+  pdl_wait();
+  pdl_launch();
+  const int s = blockIdx.x, sim = blockIdx.y;
+  const int k0 = s * 32 * CH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const double* xs = x + (size_t)sim * strideX;
+  double xv[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int k = k0 + lane + 32 * c;
+    xv[c] = (k < K) ? xs[k] : 0.0;
+  }
+  for (int m0 = warp * 8; m0 < M; m0 += nw * 8) {
+    double a[8][CH];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int k = k0 + lane + 32 * c;
+        a[u][c] = (m0 + u < M && k < K) ? A[(size_t)(m0 + u) * lda + k] : 0.0;
+      }
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc[u] = 0.0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[u] = fma(a[u][c], xv[c], acc[u]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+    if (lane < 8 && m0 + lane < M) {
+      double v = acc[0];
+#pragma unroll
+      for (int u = 1; u < 8; ++u)
+        if (lane == u) v = acc[u];
+      part[((size_t)s * n_sims + sim) * M + m0 + lane] = v;
+    }
+  }
+}
+
 // Weight-net tail, grid (ceil(|C|/64), n_sims): every CTA rebuilds h1..h3 (tiny) and
 // evaluates 64 rows of the C-restricted last layer:
 //   h1 = sin(sum parts + b1), h2 = sin(W2 h1 + b2), h3 = sin(W3 h2 + b3),
@@ -208,9 +256,17 @@ __device__ __forceinline__ double wnet_row_tpr(const double* __restrict__ W, int
                                                int tpr) {
   const int per = wn / tpr;
   double acc = 0.0;
-  for (int i = 0; i < per; ++i) {
-    const int k = q + tpr * ((i + m) % per);  // rotated walk: rows of a warp hit different banks
-    acc = fma(W[(size_t)m * wn + k], hin[k], acc);
+  if ((per & (per - 1)) == 0) {
+    const int rot = m & (per - 1);
+    for (int i = 0; i < per; ++i) {
+      const int k = q + tpr * ((i + rot) & (per - 1));  // rotated walk: rows of a warp hit different banks
+      acc = fma(W[(size_t)m * wn + k], hin[k], acc);
+    }
+  } else {
+    for (int i = 0; i < per; ++i) {
+      const int k = q + tpr * ((i + m) % per);
+      acc = fma(W[(size_t)m * wn + k], hin[k], acc);
+    }
   }
   for (int o = tpr >> 1; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
