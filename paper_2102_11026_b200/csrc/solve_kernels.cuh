@@ -324,15 +324,17 @@ __global__ void k_reduce_cub(const double* __restrict__ part_f, const double* __
 }
 
 // --------------------------------------------------------------------------- LU
-// One CTA (256 threads = 16 x 16) per sim: Gaussian elimination with partial pivoting
-// on [S | -phi]. The matrix lives in shared memory; thread (ty, tx)
+// One CTA (256 threads = 16 x 16) per sim: elimination with partial pivoting on
+// [S | -phi | extra rhs]. The matrix lives in shared memory; thread (ty, tx)
 // owns the NB x NB elements (ty + 16a, tx + 16b), keeps them in registers and writes
 // them back after every update. Every warp finds the pivot itself (exact argmax of
-// |A[i][k]| over unused rows via integer warp reductions on the IEEE bits, lowest row
-// on ties), so a pivot step needs ONE barrier: within a step only unused rows and
-// columns > k are written while the pivot row and column k are read. Pivoting is
-// implicit (rows are marked used instead of swapped: same arithmetic as LU-pp).
-// Back substitution by warp 0 with shuffles. If `apply`, r += dr.
+// |A[i][k]| over unused rows via integer warp reductions on the IEEE bits, lowest row on
+// ties, as LAPACK idamax), so a pivot step needs ONE barrier: within a step only
+// columns > k of non-pivot rows are written while the pivot row and column k are read.
+// Pivoting is implicit (rows are marked used instead of swapped). Gauss-Jordan form: the
+// used rows are eliminated too, which costs no latency here (every thread updates its block
+// in parallel anyway) and turns the sequential back substitution into one division per
+// unknown. Same pivot sequence as LU-pp; results agree to roundoff. If `apply`, r += dr.
 // status[sim] = 1 on a zero pivot.
 // 1/p on the pivot critical path: MUFU reciprocal seed + two Newton steps (error <= 1 ulp;
 // the IEEE-rounded division costs ~3x the latency here). |p| is a partial pivot, never
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
 #pragma unroll
     for (int a = 0; a < NB; ++a) {
       const int i = ty + 16 * a;
-      act[a] = !is_used(i);
+      act[a] = (i < n) && (i != piv);  // Gauss-Jordan: every row but the pivot row is eliminated
       l[a] = M[i * LDF + k];
     }
 #pragma unroll
@@ -461,53 +463,19 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     if (tid == 0) status[sim] = 1;
     return;
   }
-  // back substitution: warp 0 for -phi (column n), warp w for extra right-hand side w
-  const int warp = tid >> 5;
-  if (warp <= nx) {
-    const int col = n + warp;
-    constexpr int NU = (D + 31) / 32;
-    double bv[NU];
-    const double* rowp[NU];  // physical U rows of this lane's unknowns, resolved once
-#pragma unroll
-    for (int u = 0; u < NU; ++u) {
-      const int t = lane + 32 * u;
-      rowp[u] = M + (t < n ? pivrow[t] : 0) * LDF;
-      bv[u] = (t < n) ? rowp[u][col] : 0.0;
+  // Gauss-Jordan: the pivot rows form a diagonal system, x_k = rhs[piv_k] / a[piv_k][k]
+  // (no sequential back substitution). Column n is -phi, columns n+1.. the extra right-hand sides.
+  for (int t = tid; t < n * (1 + nx); t += blockDim.x) {
+    const int kk = t % n, col = t / n;
+    const double x = M[pivrow[kk] * LDF + n + col] * rdiag[kk];
+    if (col == 0) {
+      dr[(size_t)sim * n + kk] = x;
+      if (apply) r[(size_t)sim * n + kk] += x;
+    } else {
+      xout[((size_t)sim * nx + col - 1) * n + kk] = x;
     }
-#pragma unroll 4
-    for (int t = n - 1; t >= 0; --t) {
-      const int owner = t & 31, slot = t >> 5;
-      const double rd = rdiag[t];
-      double uc[NU];
-#pragma unroll
-      for (int u = 0; u < NU; ++u) uc[u] = rowp[u][t];  // independent of the x chain
-      double bt = 0.0;
-#pragma unroll
-      for (int u = 0; u < NU; ++u)
-        if (u == slot) bt = bv[u];
-      bt = __shfl_sync(0xffffffffu, bt, owner);
-      const double xt = bt * rd;
-#pragma unroll
-      for (int u = 0; u < NU; ++u) {
-        const int tt = lane + 32 * u;
-        if (tt < t) bv[u] = fma(-uc[u], xt, bv[u]);
-        else if (tt == t) bv[u] = xt;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < NU; ++u) {
-      const int t = lane + 32 * u;
-      if (t < n) {
-        if (warp == 0) {
-          dr[(size_t)sim * n + t] = bv[u];
-          if (apply) r[(size_t)sim * n + t] += bv[u];
-        } else {
-          xout[((size_t)sim * nx + warp - 1) * n + t] = bv[u];
-        }
-      }
-    }
-    if (tid == 0) status[sim] = 0;
   }
+  if (tid == 0) status[sim] = 0;
 }
 
 // Column-cyclic variant for n <= 64 and n + 1 + nx <= 72 columns: warp w owns columns
