@@ -614,7 +614,7 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
   const int n = c->n;
   const double* Gt = add_vhp ? (const double*)c->Gt.p : nullptr;
   auto go = [&](auto kern) {
-    launch(c, kern, c->n_sims, 256, lu_smem_bytes(n + nx), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
+    launch(c, kern, c->n_sims, 256, lu_smem_bytes(n + nx, c->n_q), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
            c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt, c->n_p);
   };
   // k_lu_cols (column-cyclic, one producer warp per pivot step) is correct but slower than the

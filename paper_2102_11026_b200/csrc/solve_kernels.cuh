@@ -358,13 +358,15 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
   pdl_launch();
   constexpr int D = 16 * NB;           // covered rows / columns (n + 1 <= D)
   constexpr int LDF = D + 1;
-  extern __shared__ double M[];        // [D][LDF]
+  extern __shared__ double M[];        // [D][LDF] | vhp block [n_q][n_q]
   __shared__ int pivrow[D];
   __shared__ double rdiag[D];
   const int sim = blockIdx.x;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31;
   const double* Ss = S + (size_t)sim * n * n;
-  // stage [S | phi] into shared memory with async copies (one round trip for all elements)
+  const int nq = n - n_p;
+  double* Vs = M + D * LDF;            // vhp[k][i] = G_t[2k+1][i] (k_reduce_S without G_t built S_base)
+  // stage [S | phi | extra rhs] and the vhp block with async copies (one round trip for all)
   for (int idx = tid; idx < D * D; idx += 256) {
     const int i = idx / D, j = idx % D;
     double* dst = M + i * LDF + j;
@@ -373,6 +375,11 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     else if (i < n && j > n && j <= n + nx) cp_async8(dst, xrhs + ((size_t)sim * nx + (j - n - 1)) * n + i);
     else *dst = 0.0;
   }
+  if (Gt)
+    for (int idx = tid; idx < nq * nq; idx += 256) {
+      const int k = idx / nq, i = idx % nq;
+      cp_async8(Vs + idx, Gt + ((size_t)sim * 2 * nq + 2 * k + 1) * ldg + i);
+    }
   cp_async_all_wait();
   __syncthreads();
   double A[NB][NB];
@@ -383,17 +390,15 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
       const int i = ty + 16 * a, j = tx + 16 * b;
       double v = M[i * LDF + j];
       if (j == n) v = -v;  // rhs = -phi
-      // S = S_base + diag(0, vhp): vhp[i][k] = G_t[2k+1][i] (k_reduce_S without G_t built S_base)
-      if (Gt && i >= n_p && j >= n_p && i < n && j < n)
-        v += Gt[((size_t)sim * 2 * (n - n_p) + 2 * (j - n_p) + 1) * ldg + (i - n_p)];
+      if (Gt && i >= n_p && j >= n_p && i < n && j < n) v += Vs[(j - n_p) * nq + (i - n_p)];  // S_base + diag(0, vhp)
       A[a][b] = v;
     }
   __syncthreads();
+  // the shared copy holds the full matrix from here on (the first pivot row is read from it)
 #pragma unroll
   for (int a = 0; a < NB; ++a)
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-      if (tx + 16 * b == n) M[(ty + 16 * a) * LDF + n] = A[a][b];
+    for (int b = 0; b < NB; ++b) M[(ty + 16 * a) * LDF + tx + 16 * b] = A[a][b];
   // rows >= n are never pivots
   unsigned long long used_lo = 0ull, used_hi = 0ull;  // rows 0..63, 64..127
   for (int i = n; i < D; ++i) {
@@ -704,9 +709,10 @@ __global__ void __launch_bounds__(256) k_lu_cols(const double* __restrict__ S, c
 
 // n: unknowns + extra right-hand sides (D >= n + 1 columns incl. -phi)
 inline int lu_nb(int n) { return (n + 1 <= 64) ? 4 : (n + 1 <= 96) ? 6 : 8; }
-inline size_t lu_smem_bytes(int n) {
+// n: unknowns + extra rhs; nq: size of the vhp block staged beside the matrix
+inline size_t lu_smem_bytes(int n, int nq = 0) {
   const int D = 16 * lu_nb(n);
-  return (size_t)D * (D + 1) * 8;
+  return (size_t)D * (D + 1) * 8 + (size_t)nq * nq * 8;
 }
 
 // r = base + t * dr ; rdot = (r - r_bar)/dt ; elementwise product

@@ -355,3 +355,20 @@ def test_kernel_variants(cuda_ok, env, tmp_path):
     ro, _, _, _ = ors.step(S, st0.r.copy(), st0.rdot.copy(), P.f_ext,
                            ocfg(SimConfig(dt=P.cfg.dt, fixed_iters=2)))
     assert np.abs(got["r"] - ro).max() <= 1e-10 * np.abs(ro).max()
+
+
+@pytest.mark.parametrize("n_p", [1, 2])
+def test_step_small_linear_block(cuda_ok, n_p):
+    """Few linear modes: the first pivots fall in the nonlinear block, whose vhp term the LU adds
+    while staging (regression: the first pivot row must carry it)."""
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200 import rdsim
+    P = build_problem("tiny", n_p=n_p)
+    S = oracle_sim(P)
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=3)
+    r, rb, rdb = P.random_state()
+    from paper_2102_11026_b200.daereduce import ReducedState
+    st = ReducedState(rb, rdb, cfg.dt)
+    got = rdsim.step(P.rm, P.model, st, P.f_ext, cfg)
+    ro, _, _, _ = ors.step(S, rb.copy(), rdb.copy(), P.f_ext, ocfg(cfg))
+    assert np.abs(got.r - ro).max() <= 1e-10 * np.abs(ro).max()
