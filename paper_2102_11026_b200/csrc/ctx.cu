@@ -377,7 +377,7 @@ void wnet_phase(nlrom_ctx* c) {
              (const double*)c->u.p, (long long)c->N, c->wn, c->N, c->wchunk, c->wpart.p, c->n_sims);
   }
   const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + nsplit * c->wn) * 8;
-  if (c->wn % 2 == 0 && 256 % c->wn == 0 && (c->n_sims == 1 || nsplit == 1)) {
+  if (c->wn % 2 == 0 && 256 % c->wn == 0 && c->wn >= 16 && (c->n_sims == 1 || nsplit == 1)) {
     launch(c, k_wnet_tail2, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm + 16,
            (const double*)c->wpart.p, nsplit, c->wn, (const double*)c->b1.p, (const double*)c->W2.p,
            (const double*)c->b2.p, (const double*)c->W3.p, (const double*)c->b3.p, (const double*)c->W4C.p,

@@ -460,8 +460,16 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
   auto Xb = [&](int i) { return sm + i * kmax * LDX; };
   auto Wbuf = [&](int i) { return sm + 2 * kmax * LDX + i * R * LDWS; };
   auto Zbuf = [&](int i) { return sm + 2 * kmax * LDX + 2 * R * LDWS + i * R * G; };  // [R][G] cache slice
-  double* Ys = sm + 2 * kmax * LDX + 2 * R * LDWS + 2 * R * G;  // [G][R+1]
-  double* Os = Ys + G * (R + 1);                                 // [R][LDX]
+  constexpr int NTILE = (R / 8) * (G / 8);
+  constexpr int KSPL = NTILE >= 8 ? 1 : (8 / NTILE > 4 ? 4 : 8 / NTILE);
+  double* Ys = sm + 2 * kmax * LDX + 2 * R * LDWS + 2 * R * G;  // [KSPL][G][R+1] partial tiles
+  double* Os = Ys + KSPL * G * (R + 1);                          // [R][LDX]
+  auto ysum = [&](int col, int row) {
+    double v = Ys[col * (R + 1) + row];
+#pragma unroll
+    for (int k2 = 1; k2 < KSPL; ++k2) v += Ys[k2 * G * (R + 1) + col * (R + 1) + row];
+    return v;
+  };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)cluster.block_rank();
   const int r0 = rank * R;
@@ -529,19 +537,24 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
       cp_async_wait<1>();
       mbar_wait(wbar + (s & 1), ((s - 1) >> 1) & 1);
       __syncthreads();
-      for (int tile = warp; tile < NT; tile += NTH / 32) {
+      // K split over KSPL warps per tile when there are fewer tiles than warps (shorter DMMA
+      // dependency chains); the partial tiles are summed in fixed order by the epilogue
+      const int n16 = Kp / 16;  // K segments in units of 16 (some may be empty for small K)
+      for (int tw = warp; tw < NT * KSPL; tw += NTH / 32) {
+        const int tile = tw % NT, ks = tw / NT;
         const int tm = tile % TM, tn = tile / TM;
         double c[4][2] = {};
         const double* wrow = Ws + (tm * 8 + (lane >> 2)) * LDWS + (lane & 3);
         const double* xcol = Xc + (lane & 3) * LDX + tn * 8 + (lane >> 2);
-        for (int k0 = 0; k0 < Kp; k0 += 16) {
+        for (int k0 = 16 * (ks * n16 / KSPL); k0 < 16 * ((ks + 1) * n16 / KSPL); k0 += 16) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], wrow[k0 + 4 * u], xcol[(k0 + 4 * u) * LDX]);
         }
+        double* Yp = Ys + ks * G * (R + 1);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int row = tm * 8 + (lane >> 2), col = tn * 8 + 2 * (lane & 3) + e;
-          Ys[col * (R + 1) + row] = (c[0][e] + c[1][e]) + (c[2][e] + c[3][e]);
+          Yp[col * (R + 1) + row] = (c[0][e] + c[1][e]) + (c[2][e] + c[3][e]);
         }
       }
       __syncthreads();
@@ -552,7 +565,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
         const int rr = t % R, col = t / R;
         const int i = r0 + rr, p = gl * PG + col / 2;
         if (i < a.n_q && p < a.n_q)
-          a.Gt[((size_t)sim * 2 * a.n_q + 2 * p + (col & 1)) * a.ldG + i] = Ys[col * (R + 1) + rr];
+          a.Gt[((size_t)sim * 2 * a.n_q + 2 * p + (col & 1)) * a.ldG + i] = ysum(col, rr);
       }
       break;
     }
@@ -566,8 +579,8 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
         d0 = a.gpart ? gval[rr] : a.g[(size_t)sim * a.w + m];
         d1 = 0.0;
       } else {
-        d0 = Ys[(2 * j) * (R + 1) + rr];
-        d1 = Ys[(2 * j + 1) * (R + 1) + rr];
+        d0 = ysum(2 * j, rr);
+        d1 = ysum(2 * j + 1, rr);
       }
       const double z0 = Z[rr * G + 2 * j], z1 = Z[rr * G + 2 * j + 1];
       double sn, cs;
@@ -598,7 +611,9 @@ template <int R, int G = 16>
 inline size_t mlp_bwd_smem(int w) {
   using P = MlpPlan<R, G>;
   const int kp = P::kp(w);
-  return (size_t)(2 * kp * P::LDX + 2 * R * P::ldws(kp) + 2 * R * G + G * (R + 1) + R * P::LDX) * 8 + 16;
+  constexpr int NTILE = (R / 8) * (G / 8);
+  constexpr int KSPL = NTILE >= 8 ? 1 : (8 / NTILE > 4 ? 4 : 8 / NTILE);
+  return (size_t)(2 * kp * P::LDX + 2 * R * P::ldws(kp) + 2 * R * G + KSPL * G * (R + 1) + R * P::LDX) * 8 + 16;
 }
 
 }  // namespace nlrom

@@ -371,4 +371,5 @@ def test_step_small_linear_block(cuda_ok, n_p):
     st = ReducedState(rb, rdb, cfg.dt)
     got = rdsim.step(P.rm, P.model, st, P.f_ext, cfg)
     ro, _, _, _ = ors.step(S, rb.copy(), rdb.copy(), P.f_ext, ocfg(cfg))
-    assert np.abs(got.r - ro).max() <= 1e-10 * np.abs(ro).max()
+    # far from the solution (|dr| ~ 1) with cond(S) ~ 1e5: roundoff of the two LU orders grows
+    assert np.abs(got.r - ro).max() <= 1e-8 * np.abs(ro).max()
