@@ -68,6 +68,24 @@ struct DBuf {
   DBuf& operator=(DBuf&& o) noexcept { free(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; return *this; }
 };
 
+// pinned host staging buffer (fast async host<->device copies for the host-buffer API)
+struct HBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (count <= n) return;
+    free();
+    NL_CUDA(cudaHostAlloc(&p, count * sizeof(double), cudaHostAllocDefault));
+    n = count;
+  }
+  void free() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~HBuf() { free(); }
+};
+
 struct IBuf {
   int* p = nullptr;
   size_t n = 0;

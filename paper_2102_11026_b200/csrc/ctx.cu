@@ -106,6 +106,7 @@ struct nlrom_ctx {
   int launches_E = 0, launches_J = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DBuf flush;
+  HBuf hin, hout;  // pinned staging of nlrom_step's host inputs / outputs
   // substructured scene (coupled_kernels.cuh): strings of this rank + replicated core
   bool coupled = false;
   // mass block on a side branch beside the weight net (default) or, with NLROM_MASS_LATE, beside
@@ -1220,13 +1221,48 @@ static void run_step(nlrom_ctx* c, const nlrom_simcfg& cfg, nlrom_step_info* inf
 extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar, const double* fext,
                           const nlrom_simcfg* cfg, double* r_out, double* rdot_out, nlrom_step_info* info) {
   CTX_TRY(c)
-  set_state(c, nullptr, rbar, rdbar, fext);
-  run_step(c, *cfg, info);
   const int nn = c->n_sims * c->n;
-  launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg->dt, nn);
-  d2h(c, r_out, c->r, nn);
-  d2h(c, rdot_out, c->rdot, nn);
-  NL_CUDA(cudaStreamSynchronize(c->st));
+  const size_t nf = (size_t)c->n_sims * c->N;
+  if (cfg->fixed_iters > 0) {
+    // fixed-iteration mode: inputs through pinned staging, every launch enqueued, ONE host sync
+    // at the end for r, rdot, the status flags and the final residual norm
+    c->hin.alloc(2 * (size_t)nn + nf);
+    c->hout.alloc(2 * (size_t)nn + 2 + c->n_sims);
+    double* hi = c->hin.p;
+    memcpy(hi, rbar, (size_t)nn * 8);
+    memcpy(hi + nn, rdbar, (size_t)nn * 8);
+    memcpy(hi + 2 * nn, fext, nf * 8);
+    NL_CUDA(cudaMemcpyAsync(c->rbar.p, hi, (size_t)nn * 8, cudaMemcpyHostToDevice, c->st));
+    NL_CUDA(cudaMemcpyAsync(c->rdbar.p, hi + nn, (size_t)nn * 8, cudaMemcpyHostToDevice, c->st));
+    NL_CUDA(cudaMemcpyAsync(c->fext.p, hi + 2 * nn, nf * 8, cudaMemcpyHostToDevice, c->st));
+    ensure_graphs(c, *cfg);
+    launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg->dt, nn);
+    for (int it = 0; it < cfg->fixed_iters; ++it) NL_CUDA(cudaGraphLaunch(c->gIter, c->st));
+    NL_CUDA(cudaGraphLaunch(c->gE, c->st));
+    launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg->dt,
+           nn);
+    double* ho = c->hout.p;
+    NL_CUDA(cudaMemcpyAsync(ho, c->r.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
+    NL_CUDA(cudaMemcpyAsync(ho + nn, c->rdot.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
+    NL_CUDA(cudaMemcpyAsync(ho + 2 * nn, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
+    int* hs = reinterpret_cast<int*>(ho + 2 * nn + 2);
+    NL_CUDA(cudaMemcpyAsync(hs, c->status.p, c->n_sims * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    NL_CUDA(cudaStreamSynchronize(c->st));
+    for (int s2 = 0; s2 < c->n_sims; ++s2)
+      if (hs[s2]) throw Error(NLROM_ERR_NONFINITE, "singular system Jacobian (zero pivot in LU)");
+    memcpy(r_out, ho, (size_t)nn * 8);
+    memcpy(rdot_out, ho + nn, (size_t)nn * 8);
+    c->last_norm = ho[2 * nn];
+    if (info) { info->iters = cfg->fixed_iters; info->res_norm = ho[2 * nn]; info->status = 0; }
+  } else {
+    set_state(c, nullptr, rbar, rdbar, fext);
+    run_step(c, *cfg, info);
+    launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg->dt,
+           nn);
+    d2h(c, r_out, c->r, nn);
+    d2h(c, rdot_out, c->rdot, nn);
+    NL_CUDA(cudaStreamSynchronize(c->st));
+  }
   CTX_END(c)
 }
 

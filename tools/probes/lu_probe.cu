@@ -56,7 +56,7 @@ int main() {
   printf("\n");
   long long t2[16];
   cudaMemcpyFromSymbol(t2, g_lu_trace2, sizeof t2);
-  printf("warp3 step10->11: bar.sync wait %lld | piv/mul+update col %lld | to produce %lld | redux %lld | rcp %lld | mul/sts %lld\n",
-         t2[1] - t2[0], t2[2] - t2[1], t2[3] - t2[2], t2[4] - t2[3], t2[5] - t2[4], t2[6] - t2[5]);
+  printf("k_lu_solve step 10 (thread 0): search+redux %lld | rcp %lld | loads+update %lld | barrier %lld | total %lld\n",
+         t2[1] - t2[0], t2[2] - t2[1], t2[3] - t2[2], t2[4] - t2[3], t2[4] - t2[0]);
 #endif
 }
