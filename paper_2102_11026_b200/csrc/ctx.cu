@@ -393,6 +393,7 @@ void wnet_phase(nlrom_ctx* c) {
 void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true) {
   CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, weighted ? c->wC.p : nullptr, c->u.p, c->Jt.p,
             c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk, nullptr, nullptr};
+  a.early = weighted ? 1 : 0;  // the weight-net tail (producer) launches dependents only after its own wait
   size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162) * 8;
   launch(c, k_cubature, dim3(s.nchunk, c->n_sims), 256, smem, a);
   if (scatter)

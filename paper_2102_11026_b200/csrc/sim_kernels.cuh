@@ -367,6 +367,7 @@ struct CubArgs {
   int nchunk;
   double* Ke_out;          // optional (E, 144): w-scaled element stiffness
   double* fred_out;        // optional (E, n): per-element J~_e^T (w f_e)
+  int early = 0;           // 1: the producer grid is the weight net (J~, u complete at launch)
 };
 
 __device__ __forceinline__ void mat3_mul(const double* A, const double* B, double* C) {
@@ -376,9 +377,14 @@ __device__ __forceinline__ void mat3_mul(const double* A, const double* B, doubl
     for (int j = 0; j < 3; ++j) C[i * 3 + j] = A[i * 3] * B[j] + A[i * 3 + 1] * B[3 + j] + A[i * 3 + 2] * B[6 + j];
 }
 
+// Programmatic-launch overlap: everything that does not depend on the weight net (the DOF rows,
+// the J~ / u gathers, the element physics and G_e = K_e J~_e, all unweighted) runs BEFORE the
+// dependency wait, i.e. while the weight-net kernels still execute; the element weights scale
+// f_e and the G_e rows afterwards (the Gram is linear in w_e). Safe because the producer
+// (k_wnet_tail*) issues launch_dependents only after its own wait, so the output layer that
+// wrote J~ and u has completed when this grid starts.
 __global__ void k_cubature(CubArgs a) {
-  pdl_wait();
-  pdl_launch();
+  if (!a.early) pdl_wait();  // producer wrote J~ / u itself: wait before the gathers
   extern __shared__ double sh[];
   const int n = a.n;
   const int epc = a.epc;
@@ -446,7 +452,7 @@ __global__ void k_cubature(CubArgs a) {
 #pragma unroll
     for (int l = 0; l < 9; ++l) Di[l] = a.Dm_inv[(size_t)e * 9 + l];
     const double V = a.vol[e];
-    const double we = a.w ? a.w[(size_t)sim * a.n_elems + ei] : 1.0;
+    const double we = 1.0;  // weights applied after the dependency wait
     // G rows: g_i (i=1..3) = rows of Dm^-1, g_0 = -sum
     double G[12];
 #pragma unroll
@@ -485,7 +491,6 @@ __global__ void k_cubature(CubArgs a) {
       int i = lane / 3, aa = lane % 3;
       double f = V * (P[aa * 3] * G[i * 3] + P[aa * 3 + 1] * G[i * 3 + 1] + P[aa * 3 + 2] * G[i * 3 + 2]);
       Fs[el * 12 + lane] = we * f;
-      a.fe_w[((size_t)sim * a.n_elems + ei) * 12 + lane] = we * f;
       // stiffness column for DOF (jv, d) = lane: dF_ab = delta_ad g_jv[b]
       int jv = lane / 3, d = lane % 3;
       double dF[9];
@@ -517,25 +522,12 @@ __global__ void k_cubature(CubArgs a) {
         int ri = r / 3, ra = r % 3;
         double kv = V * (t1[ra * 3] * G[ri * 3] + t1[ra * 3 + 1] * G[ri * 3 + 1] + t1[ra * 3 + 2] * G[ri * 3 + 2]);
         Ks[el * 144 + r * 12 + lane] = we * kv;
-        if (a.Ke_out) a.Ke_out[(size_t)ei * 144 + r * 12 + lane] = we * kv;
       }
     }
   }
   __syncthreads();
-  if (!Jt) return;
-  if (a.fred_out) {
-    for (int idx = threadIdx.x; idx < epc * n; idx += blockDim.x) {
-      int el = idx / n, i = idx % n;
-      int ei = chunk * epc + el;
-      if (ei >= a.n_elems) continue;
-      double acc = 0.0;
-      for (int l = 0; l < 12; ++l) acc = fma(Js[(el * 12 + l) * ldp + i], Fs[el * 12 + l], acc);
-      a.fred_out[(size_t)ei * n + i] = acc;
-    }
-    return;
-  }
-  // G_e = (w K_e) J~_e   (12 x n): warp per (element, row), lanes over columns
-  {
+  // G_e = K_e J~_e (12 x n, unweighted): warp per (element, row), lanes over columns
+  if (Jt && !a.fred_out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int rr = warp; rr < epc * 12; rr += nw) {
       const int el = rr / 12;
@@ -551,6 +543,42 @@ __global__ void k_cubature(CubArgs a) {
         Gs[rr * ldp + j] = acc;
       }
     }
+  }
+  // ---- the weight net's output is needed from here on
+  pdl_wait();
+  pdl_launch();
+  __shared__ double wsh[64];
+  for (int el = threadIdx.x; el < epc; el += blockDim.x) {
+    const int ei = chunk * epc + el;
+    wsh[el] = (a.w && ei < a.n_elems) ? a.w[(size_t)sim * a.n_elems + ei] : 1.0;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < epc * 12; t += blockDim.x) {
+    const int el = t / 12, ei = chunk * epc + el;
+    Fs[t] *= wsh[el];
+    if (ei < a.n_elems) a.fe_w[((size_t)sim * a.n_elems + ei) * 12 + t % 12] = Fs[t];
+  }
+  if (a.Ke_out)
+    for (int t = threadIdx.x; t < epc * 144; t += blockDim.x) {
+      const int el = t / 144, ei = chunk * epc + el;
+      if (ei < a.n_elems) a.Ke_out[(size_t)ei * 144 + t % 144] = wsh[el] * Ks[t];
+    }
+  if (!Jt) return;
+  if (a.fred_out) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < epc * n; idx += blockDim.x) {
+      int el = idx / n, i = idx % n;
+      int ei = chunk * epc + el;
+      if (ei >= a.n_elems) continue;
+      double acc = 0.0;
+      for (int l = 0; l < 12; ++l) acc = fma(Js[(el * 12 + l) * ldp + i], Fs[el * 12 + l], acc);
+      a.fred_out[(size_t)ei * n + i] = acc;
+    }
+    return;
+  }
+  for (int t = threadIdx.x; t < epc * 12 * n; t += blockDim.x) {  // G_e rows scaled by w_e
+    const int rr = t / n, j = t % n;
+    Gs[rr * ldp + j] *= wsh[rr / 12];
   }
   __syncthreads();
   // partial K~ = J~_C^T (w K J~_C) over the chunk's rows on the DMMA pipe; partial f~ = J~_C^T (w f)
