@@ -594,8 +594,7 @@ bool fused_vhp_backward(nlrom_ctx* c) {
   if (!go(true)) return false;
   if (M % 2 == 0 && c->ldlast % 2 == 0 && M <= 512) {
     // 24-row chunks over ~280 CTAs; the chain's prologue sums the partials (no reduce launch)
-    static const int rows = getenv("NLROM_GEMV_ROWS") ? atoi(getenv("NLROM_GEMV_ROWS")) : 24;
-    const int nch = ceil_div(c->N, rows);
+    const int rows = 24, nch = ceil_div(c->N, rows);
     launch(c, k_gemv_t2, dim3(nch, c->n_sims), 256, 0, (const double*)c->Alast.p, c->ldlast, M,
            (const double*)c->a.p, c->N, rows, c->bpart.p, nch);
     a.gpart = c->bpart.p;

@@ -177,9 +177,11 @@ struct AsmAArgs {
   int drop_fict;
 };
 
+// Programmatic-launch overlap: the J~ . c dot products (J~, hvv: output layer; r, r_bar,
+// rdot_bar: state) run before the dependency wait -- the producer (k_cubature) launches
+// dependents only after its own wait, so the output layer has completed -- and only the
+// gathered element forces (cubature output) are read after it.
 __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
-  pdl_wait();
-  pdl_launch();
   __shared__ double cs[128];
   __shared__ double as[128];
   __shared__ double red[4][64];
@@ -200,6 +202,10 @@ __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
     if (rl < A.RC && row < A.N) {
       const double* Jr = Jsim + (size_t)row * A.ldjt;
       for (int j = h; j < n; j += 2) acc = fma(Jr[j], cs[j], acc);
+    }
+    pdl_wait();
+    pdl_launch();
+    if (rl < A.RC && row < A.N) {
       const double* fw = A.fe_w + (size_t)sim * A.n_elems * 12;
       for (int k = A.rowptr[row] + h; k < A.rowptr[row + 1]; k += 2) fs += fw[A.entries[k]];
     }
@@ -354,6 +360,8 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
                                                    int* __restrict__ status, const double* __restrict__ xrhs, int nx,
                                                    double* __restrict__ xout, const double* __restrict__ Gt, int ldg,
                                                    int n_p) {
+  // every input waits: in a captured graph the event edge from the side branch (S_base, phi)
+  // into this PDL launch is programmatic too, so nothing is complete before the wait
   pdl_wait();
   pdl_launch();
   constexpr int D = 16 * NB;           // covered rows / columns (n + 1 <= D)
