@@ -501,11 +501,12 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
   };
   // prologue: constants (weights of the first multiply, stage 1) before the dependency wait
   load_w(L1 - 1, 1);
+  // the forward caches were written by the jet chain, which has completed when this grid starts
+  // (the producer k_gemv_t2 launches dependents only after its own wait): load before ours
+  load_z(L1 - 1, 0);
   cp_async_commit();
   pdl_wait();
   pdl_launch();
-  load_z(L1 - 1, 0);
-  cp_async_commit();
   __shared__ double gsum[256];
   __shared__ double gval[32];
   if (a.gpart) {  // g rows of this CTA = fixed-order sum of the GEMV chunk partials
