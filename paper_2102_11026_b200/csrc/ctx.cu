@@ -249,7 +249,7 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
 using CfgOutC = GemmCfg<48, 128, 2, 4, 1, 32, 3>;
 // same tiling on the warp-specialised TMA pipeline (gemm_ws.cuh): 6 swizzled stages, one
 // producer warp; 13% faster on this shape (tools/probes/gemm_ws_probe.cu), bitwise identical
-using CfgOutWs = WsCfg<48, 128, 2, 4, 6>;
+using CfgOutWs = WsCfg<48, 128, 3, 4, 6>;  // 12 consumer warps (16 x 32 warp tiles): best of the probe
 
 void output_layer(nlrom_ctx* c) {
   GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->next, 0, 0};

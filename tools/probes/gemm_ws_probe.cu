@@ -61,9 +61,10 @@ void run(const char* name, int M, int K, int C) {
 }
 
 int main() {
-  run<GemmCfg<64, 128, 2, 4, 1, 16, 3>, WsCfg<64, 128, 2, 4, 4>>("batched 256x256x393k", 256, 256, 4096 * 96);
-  run<GemmCfg<64, 128, 2, 4, 1, 16, 3>, WsCfg<128, 128, 4, 2, 4>>("batched (ws 128x128)", 256, 256, 4096 * 96);
-  run<GemmCfg<48, 128, 2, 4, 1, 32, 3>, WsCfg<48, 128, 2, 4, 6>>("output 6720x256x124", 6720, 256, 124);
-  run<GemmCfg<48, 128, 2, 4, 1, 32, 3>, WsCfg<48, 128, 2, 4, 8>>("output (8 stages)", 6720, 256, 124);
+  run<GemmCfg<48, 128, 2, 4, 1, 32, 3>, WsCfg<48, 128, 2, 4, 6>>("output ws 2x4 (8 warps)", 6720, 256, 124);
+  run<GemmCfg<48, 128, 2, 4, 1, 32, 3>, WsCfg<48, 128, 2, 8, 6>>("output ws 2x8 (16 warps)", 6720, 256, 124);
+  run<GemmCfg<48, 128, 2, 4, 1, 32, 3>, WsCfg<48, 128, 1, 8, 6>>("output ws 1x8 (8 warps)", 6720, 256, 124);
+  run<GemmCfg<48, 128, 2, 4, 1, 32, 3>, WsCfg<48, 128, 3, 4, 6>>("output ws 3x4 (12 warps)", 6720, 256, 124);
+  run<GemmCfg<48, 128, 2, 4, 1, 32, 3>, WsCfg<48, 128, 6, 4, 6>>("output ws 6x4 (24 warps)", 6720, 256, 124);
   return 0;
 }
