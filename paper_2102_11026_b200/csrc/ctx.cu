@@ -234,7 +234,7 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
   s.row_ptr.upload(ptr.data(), ptr.size());
   s.entries.upload(ent.data(), ent.size());
   const int n = c->n;
-  s.epc = 4;  // 4 elements (48 DOF rows) per CTA: ~125 CTAs for |C| = 500, shorter per-CTA chains
+  s.epc = getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : 2;  // elements per CTA (2: 250 CTAs for |C| = 500)
   while (s.epc > 1 && (size_t)(2 * s.epc * 12 * gram_ld(n) + s.epc * 162) * 8 > 200 * 1024) s.epc /= 2;
   s.nchunk = std::max(1, ceil_div(std::max(s.n, 1), s.epc));
   s.fe_w.alloc((size_t)c->n_sims * std::max(s.n, 1) * 12);
