@@ -207,7 +207,8 @@ void choose_groups(int n_q, int width, bool batched, int& G, int& gps) {
   (void)width;
 }
 
-void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std::vector<int>& rows_host) {
+void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std::vector<int>& rows_host,
+               int epc) {
   s.n = (int)elems.size();
   s.elems.upload(elems.data(), elems.size());
   // CSR: unique rows -> (element slot * 12 + l)
@@ -234,7 +235,7 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
   s.row_ptr.upload(ptr.data(), ptr.size());
   s.entries.upload(ent.data(), ent.size());
   const int n = c->n;
-  s.epc = getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : 2;  // elements per CTA (2: 250 CTAs for |C| = 500)
+  s.epc = epc;
   while (s.epc > 1 && (size_t)(2 * s.epc * 12 * gram_ld(n) + s.epc * 162) * 8 > 200 * 1024) s.epc /= 2;
   s.nchunk = std::max(1, ceil_div(std::max(s.n, 1), s.epc));
   s.fe_w.alloc((size_t)c->n_sims * std::max(s.n, 1) * 12);
@@ -835,8 +836,10 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       upload(c->vol, d->vol, c->T);
       std::vector<int> cub(d->cub_elems, d->cub_elems + d->n_cub), all(c->T);
       for (int e = 0; e < c->T; ++e) all[e] = e;
-      build_set(c, c->setC, cub, rows);
-      build_set(c, c->setAll, all, rows);
+      // cubature set: 2 elements per CTA (250 CTAs for |C| = 500); the all-element set of the
+      // exact-sum mode (not the hot path): 8, keeping its per-chunk partials small
+      build_set(c, c->setC, cub, rows, getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : 2);
+      build_set(c, c->setAll, all, rows, 8);
     }
     // weight net (rows of the last layer restricted to C)
     {
