@@ -102,6 +102,8 @@ struct nlrom_ctx {
   int ldGt = 0;
   // graphs
   cudaGraphExec_t gE = nullptr, gJ = nullptr, gIter = nullptr;
+  cudaGraphExec_t gStep = nullptr;  // whole fixed-iteration step incl. pinned H2D / D2H (nlrom_step)
+  std::string step_key;
   std::string graph_key;
   int launches_E = 0, launches_J = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -685,7 +687,9 @@ void ensure_graphs(nlrom_ctx* c, const nlrom_simcfg& cfg) {
   if (c->gE) cudaGraphExecDestroy(c->gE);
   if (c->gJ) cudaGraphExecDestroy(c->gJ);
   if (c->gIter) cudaGraphExecDestroy(c->gIter);
-  c->gE = c->gJ = c->gIter = nullptr;
+  if (c->gStep) cudaGraphExecDestroy(c->gStep);
+  c->gE = c->gJ = c->gIter = c->gStep = nullptr;
+  c->step_key.clear();
   // eager warm-up (sets kernel attributes outside of capture)
   phase_E(c, cfg);
   phase_J(c, cfg, false);
@@ -958,6 +962,7 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->gE) cudaGraphExecDestroy(c->gE);
   if (c->gJ) cudaGraphExecDestroy(c->gJ);
   if (c->gIter) cudaGraphExecDestroy(c->gIter);
+  if (c->gStep) cudaGraphExecDestroy(c->gStep);
   for (auto g : c->gC)
     if (g) cudaGraphExecDestroy(g);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1235,21 +1240,37 @@ extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar,
     memcpy(hi, rbar, (size_t)nn * 8);
     memcpy(hi + nn, rdbar, (size_t)nn * 8);
     memcpy(hi + 2 * nn, fext, nf * 8);
-    NL_CUDA(cudaMemcpyAsync(c->rbar.p, hi, (size_t)nn * 8, cudaMemcpyHostToDevice, c->st));
-    NL_CUDA(cudaMemcpyAsync(c->rdbar.p, hi + nn, (size_t)nn * 8, cudaMemcpyHostToDevice, c->st));
-    NL_CUDA(cudaMemcpyAsync(c->fext.p, hi + 2 * nn, nf * 8, cudaMemcpyHostToDevice, c->st));
-    ensure_graphs(c, *cfg);
-    launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg->dt, nn);
-    for (int it = 0; it < cfg->fixed_iters; ++it) NL_CUDA(cudaGraphLaunch(c->gIter, c->st));
-    NL_CUDA(cudaGraphLaunch(c->gE, c->st));
-    launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg->dt,
-           nn);
     double* ho = c->hout.p;
-    NL_CUDA(cudaMemcpyAsync(ho, c->r.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
-    NL_CUDA(cudaMemcpyAsync(ho + nn, c->rdot.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
-    NL_CUDA(cudaMemcpyAsync(ho + 2 * nn, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
     int* hs = reinterpret_cast<int*>(ho + 2 * nn + 2);
-    NL_CUDA(cudaMemcpyAsync(hs, c->status.p, c->n_sims * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    ensure_graphs(c, *cfg);
+    char kb[96];
+    snprintf(kb, sizeof kb, "|%d|%p|%p", cfg->fixed_iters, (void*)hi, (void*)ho);
+    const std::string key = c->graph_key + kb;
+    if (!c->gStep || c->step_key != key) {
+      // the whole step as ONE graph: pinned H2D, predictor, the Newton iterations, the final
+      // residual, rdot and the pinned D2H of r, rdot, ||phi|| and the pivot status
+      if (c->gStep) cudaGraphExecDestroy(c->gStep);
+      c->gStep = capture(c, [&] {
+        NL_CUDA(cudaMemcpyAsync(c->rbar.p, hi, (size_t)nn * 8, cudaMemcpyHostToDevice, c->st));
+        NL_CUDA(cudaMemcpyAsync(c->rdbar.p, hi + nn, (size_t)nn * 8, cudaMemcpyHostToDevice, c->st));
+        NL_CUDA(cudaMemcpyAsync(c->fext.p, hi + 2 * nn, nf * 8, cudaMemcpyHostToDevice, c->st));
+        launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg->dt,
+               nn);
+        for (int it = 0; it < cfg->fixed_iters; ++it) {
+          phase_E(c, *cfg, false);
+          phase_J(c, *cfg, true, nullptr, 0, nullptr, true);
+        }
+        phase_E(c, *cfg);
+        launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p,
+               1.0 / cfg->dt, nn);
+        NL_CUDA(cudaMemcpyAsync(ho, c->r.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
+        NL_CUDA(cudaMemcpyAsync(ho + nn, c->rdot.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
+        NL_CUDA(cudaMemcpyAsync(ho + 2 * nn, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
+        NL_CUDA(cudaMemcpyAsync(hs, c->status.p, c->n_sims * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+      }, nullptr);
+      c->step_key = key;
+    }
+    NL_CUDA(cudaGraphLaunch(c->gStep, c->st));
     NL_CUDA(cudaStreamSynchronize(c->st));
     for (int s2 = 0; s2 < c->n_sims; ++s2)
       if (hs[s2]) throw Error(NLROM_ERR_NONFINITE, "singular system Jacobian (zero pivot in LU)");

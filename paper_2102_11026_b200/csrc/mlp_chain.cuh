@@ -25,10 +25,14 @@ constexpr int MLP_MAXL = 16;
 // Optional phase timestamps (tools/probes/chain_probe.cu): CTA (0,0) thread 0, per layer.
 #ifdef NLROM_CHAIN_TRACE
 __device__ long long g_chain_trace[MLP_MAXL][6];
+__device__ long long g_bwd_trace[MLP_MAXL + 1][6];
 #define CHAIN_MARK(l, p) \
   if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_chain_trace[l][p] = clock64();
+#define BWD_MARK(s, p) \
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_bwd_trace[s][p] = clock64();
 #else
 #define CHAIN_MARK(l, p)
+#define BWD_MARK(s, p)
 #endif
 
 struct MlpFwdArgs {
@@ -530,6 +534,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
     if (s + 1 <= L1 && s >= 1) load_w(l - 1, (s + 1) & 1);
     if (s + 1 <= L1 - 1) load_z(L1 - 1 - (s + 1) + 0, (s + 1) & 1);
     cp_async_commit();
+    BWD_MARK(s, 0);
     if (s >= 1) {
       double* Xc = Xb(s & 1);
       const double* Ws = Wbuf(s & 1);
@@ -538,6 +543,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
       cp_async_wait<1>();
       mbar_wait(wbar + (s & 1), ((s - 1) >> 1) & 1);
       __syncthreads();
+      BWD_MARK(s, 1);
       // K split over KSPL warps per tile when there are fewer tiles than warps (shorter DMMA
       // dependency chains); the partial tiles are summed in fixed order by the epilogue
       const int n16 = Kp / 16;  // K segments in units of 16 (some may be empty for small K)
@@ -559,6 +565,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
         }
       }
       __syncthreads();
+      BWD_MARK(s, 2);
     }
     if (s == L1) {
       // G = W_0^T Delta_0: rows i < n_q
@@ -591,6 +598,7 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
       Os[rr * LDX + 2 * j + 1] = fma(d0, -sn * z1, d1 * cs);
     }
     __syncthreads();
+    BWD_MARK(s, 3);
     {
       double* Xn = Xb((s + 1) & 1);
       constexpr int C2 = G / 2;
@@ -604,7 +612,9 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
         }
       }
     }
+    BWD_MARK(s, 4);
     cluster.sync();
+    BWD_MARK(s, 5);
   }
 }
 

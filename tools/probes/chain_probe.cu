@@ -102,5 +102,68 @@ int main() {
   };
   run(false);
   run(true);
+  // ---- vhp backward chain <32, 8, 8> on the caches of the forward run
+  {
+    constexpr int RB = 32, CSB = 8, GB = 8;
+    MlpBwdArgs b{};
+    std::vector<double> gh(w);
+    for (auto& x : gh) x = U(rng);
+    double* gd;
+    cudaMalloc(&gd, w * 8);
+    cudaMemcpy(gd, gh.data(), w * 8, cudaMemcpyHostToDevice);
+    b.g = gd; b.gpart = nullptr; b.L1 = L1; b.w = w; b.n_q = nq;
+    const int ldpb = 256 + 4;
+    for (int l = 0; l < L1; ++l) {
+      const int in = l ? w : nq;
+      std::vector<double> wtp((size_t)w * ldpb, 0.0);
+      std::vector<double> wl((size_t)w * in);
+      cudaMemcpy(wl.data(), a.W[l], wl.size() * 8, cudaMemcpyDeviceToHost);
+      for (int r = 0; r < w; ++r)
+        for (int k = 0; k < in; ++k) wtp[(size_t)k * ldpb + r] = wl[(size_t)r * in + k];
+      double* d;
+      cudaMalloc(&d, wtp.size() * 8);
+      cudaMemcpy(d, wtp.data(), wtp.size() * 8, cudaMemcpyHostToDevice);
+      b.WTp[l] = d;
+      b.cache[l] = a.cache[l];
+    }
+    b.ldpb = ldpb; b.ldc = w;
+    double* Gt;
+    cudaMalloc(&Gt, (size_t)2 * nq * w * 8);
+    b.Gt = Gt; b.ldG = w;
+    b.gpb = (nq + GB / 2 - 1) / (GB / 2);
+    const size_t smem = mlp_bwd_smem<RB, GB>(w);
+    cudaFuncSetAttribute(k_mlp_dual_bwd<RB, CSB, GB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CSB, b.gpb, 1);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CSB;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int it = 0; it < 5; ++it) cudaLaunchKernelEx(&cfg, k_mlp_dual_bwd<RB, CSB, GB>, b);
+    cudaEventRecord(e0);
+    for (int it = 0; it < 20; ++it) cudaLaunchKernelEx(&cfg, k_mlp_dual_bwd<RB, CSB, GB>, b);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("k_mlp_dual_bwd<32,8,8>: %.2f us per launch (smem %zu B) err=%s\n", ms / 20 * 1e3, smem,
+           cudaGetErrorString(cudaGetLastError()));
+    long long tr[MLP_MAXL + 1][6];
+    cudaMemcpyFromSymbol(tr, g_bwd_trace, sizeof tr);
+    printf("stage  wait   dmma  epilogue  bcast  barrier  total (cycles)\n");
+    for (int st = 1; st <= L1; ++st) {
+      long long prev = tr[st - 1][5];
+      printf("%5d %6lld %6lld %9lld %6lld %8lld %6lld\n", st, tr[st][1] - tr[st][0], tr[st][2] - tr[st][1],
+             tr[st][3] - tr[st][2], tr[st][4] - tr[st][3], tr[st][5] - tr[st][4], tr[st][5] - prev);
+    }
+  }
   return 0;
 }
