@@ -842,7 +842,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       for (int e = 0; e < c->T; ++e) all[e] = e;
       // cubature set: 2 elements per CTA (250 CTAs for |C| = 500); the all-element set of the
       // exact-sum mode (not the hot path): 8, keeping its per-chunk partials small
-      build_set(c, c->setC, cub, rows, getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : 2);
+      // many sims (batched): 8 elements per CTA keeps the per-chunk partials (and their reduction) small
+      const bool many = c->n_sims * (4 + 4 * c->n_q) >= 2048 || getenv("NLROM_BATCHED") != nullptr;
+      build_set(c, c->setC, cub, rows, getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : (many ? 8 : 2));
       build_set(c, c->setAll, all, rows, 8);
     }
     // weight net (rows of the last layer restricted to C)
