@@ -216,6 +216,11 @@ NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
 NLROM_API int nlrom_bench_prefix(nlrom_ctx* ctx, int n_iters, int flush_l2, int cap, float* ms, char* names,
                                  int names_len, int* n_launches);
 
+/* Test hook: fills the shared memory of every SM with NaN bit patterns (one resident
+ * max-shared-memory CTA per SM, synchronous), so that a later kernel reading shared memory it
+ * never wrote is caught deterministically by the parity tests. No context needed. */
+NLROM_API int nlrom_debug_poison_shared_memory(int device);
+
 /* The context's CUDA stream (cudaStream_t) -- every call above is ordered on it; a host
  * that interleaves its own collectives (NCCL) with the coupled phases below uses it. */
 NLROM_API int nlrom_stream(nlrom_ctx* ctx, void** stream);

@@ -27,7 +27,7 @@ EXPORTED = [
     "nlrom_bench_iterations", "nlrom_launches_per_iteration", "nlrom_element_forces",
     "nlrom_element_reduced_forces", "nlrom_bench_kernels", "nlrom_stream", "nlrom_coupled_setup",
     "nlrom_coupled_begin", "nlrom_coupled_eval", "nlrom_coupled_update", "nlrom_coupled_read",
-    "nlrom_coupled_launches", "nlrom_bench_prefix",
+    "nlrom_coupled_launches", "nlrom_bench_prefix", "nlrom_debug_poison_shared_memory",
 ]
 
 
@@ -109,6 +109,7 @@ def lib():
             "nlrom_coupled_launches": (C.c_int, [vp]),
             "nlrom_bench_prefix": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float), C.c_char_p,
                                              C.c_int, ip]),
+            "nlrom_debug_poison_shared_memory": (C.c_int, [C.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

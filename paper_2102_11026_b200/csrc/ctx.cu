@@ -302,7 +302,7 @@ bool launch_mlp_fwd(nlrom_ctx* c, const MlpFwdArgs& a) {
 }
 
 bool fused_hidden_forward(nlrom_ctx* c, double dt, int drop_fict) {
-  if (getenv("NLROM_NO_FUSED_MLP") || c->batched) return false;
+  if (getenv("NLROM_NO_FUSED_MLP") || getenv("NLROM_NO_FUSED_FWD") || c->batched) return false;
   const int L1 = c->L - 1, w = c->wL1;
   if (L1 < 1 || L1 > MLP_MAXL) return false;
   for (int l = 1; l <= L1; ++l)
@@ -565,7 +565,7 @@ bool launch_mlp_bwd(nlrom_ctx* c, MlpBwdArgs a, int dry) {
 }
 
 bool fused_vhp_backward(nlrom_ctx* c) {
-  if (getenv("NLROM_NO_FUSED_MLP") || c->next || c->batched) return false;
+  if (getenv("NLROM_NO_FUSED_MLP") || getenv("NLROM_NO_FUSED_BWD") || c->next || c->batched) return false;
   const int L1 = c->L - 1, w = c->wL1;
   if (L1 < 1 || L1 > MLP_MAXL) return false;
   for (int l = 1; l <= L1; ++l)
@@ -1317,6 +1317,30 @@ extern "C" int nlrom_step_device(nlrom_ctx* c, const double* rbar, const double*
 
 __global__ void k_flush(double* p, size_t n, double v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void k_poison_smem(int n) {
+  extern __shared__ double ps[];
+  const double nan = __longlong_as_double(0x7ff8dead0000beefLL);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ps[i] = nan;
+  __syncthreads();
+  if (threadIdx.x == 0 && ps[n - 1] == 0.0) ps[0] = 1.0;  // keep the stores
+}
+
+extern "C" int nlrom_debug_poison_shared_memory(int device) {
+  try {
+    NL_CUDA(cudaSetDevice(device));
+    int smem = 0, sms = 0;
+    NL_CUDA(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    NL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    NL_CUDA(cudaFuncSetAttribute(k_poison_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    for (int rep = 0; rep < 4; ++rep) k_poison_smem<<<sms * 2, 1024, smem>>>(smem / 8);
+    NL_CHECK_LAUNCH();
+    NL_CUDA(cudaDeviceSynchronize());
+    return NLROM_OK;
+  } catch (const Error& e) {
+    return e.code;
+  }
 }
 
 extern "C" int nlrom_bench_iterations(nlrom_ctx* c, int n_iters, int flush_l2, float* ms_total, float* ms_dom) {

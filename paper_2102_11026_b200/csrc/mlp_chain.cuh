@@ -126,11 +126,11 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
   }
   pdl_wait();
   pdl_launch();
-  // seed of this group: X[0][i][c], i < n_q; rows n_q .. kmax of both X buffers are zero
-  for (int t = tid; t < (kmax - a.n_q) * LDX; t += NTH) {
-    Xb(0)[a.n_q * LDX + t] = 0.0;
-    Xb(1)[a.n_q * LDX + t] = 0.0;
-  }
+  // seed of this group: X[0][i][c], i < n_q; rows n_q .. kmax of X[0] and rows w .. kmax of X[1]
+  // are zero (K padding). Rows < w of X[1] are NOT touched here: other CTAs of the cluster may
+  // already be broadcasting their layer-0 slices into them.
+  for (int t = tid; t < (kmax - a.n_q) * LDX; t += NTH) Xb(0)[a.n_q * LDX + t] = 0.0;
+  for (int t = tid; t < (kmax - a.w) * LDX; t += NTH) Xb(1)[a.w * LDX + t] = 0.0;
   for (int t = tid; t < a.n_q * G; t += NTH) {
     const int i = t / G, cl = t % G;
     const double* rs = a.r + (size_t)sim * a.n;
@@ -509,6 +509,13 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
   // (the producer k_gemv_t2 launches dependents only after its own wait): load before ours
   load_z(L1 - 1, 0);
   cp_async_commit();
+  // K padding rows w .. kmax of both X buffers: zero (the padded weight columns are zero, but
+  // stale shared memory may hold NaN / Inf bit patterns, and 0 * NaN = NaN). Remote CTAs only
+  // ever write rows < w.
+  for (int t = tid; t < (kmax - a.w) * LDX; t += NTH) {
+    Xb(0)[a.w * LDX + t] = 0.0;
+    Xb(1)[a.w * LDX + t] = 0.0;
+  }
   pdl_wait();
   pdl_launch();
   __shared__ double gsum[256];

@@ -373,3 +373,35 @@ def test_step_small_linear_block(cuda_ok, n_p):
     ro, _, _, _ = ors.step(S, rb.copy(), rdb.copy(), P.f_ext, ocfg(cfg))
     # far from the solution (|dr| ~ 1) with cond(S) ~ 1e5: roundoff of the two LU orders grows
     assert np.abs(got.r - ro).max() <= 1e-8 * np.abs(ro).max()
+
+
+@pytest.mark.parametrize("problem", ["cfg1", "tiny"])
+def test_stale_shared_memory(problem):
+    """Kernels must not read shared memory they never wrote: every SM's shared memory is
+    filled with NaN before each call (regression: the vhp chain's K-padding rows at w = 40)."""
+    from paper_2102_11026_b200 import _lib, rdsim
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200.session import Session
+    P = build_problem(problem)
+    S = oracle_sim(P)
+    L = _lib.lib()
+    poison = lambda: _lib.check(L.nlrom_debug_poison_shared_memory(0), lambda: b"poison")
+    ns = 3
+    sess = Session(P.rm, P.model, P.cm, n_sims=ns)
+    sess._ncub_cache = len(P.cm.C)
+    n = P.cfg.n_p + P.cfg.n_q
+    states = [P.random_state(seed=60 + i) for i in range(ns)]
+    r, rb, rdb = (np.concatenate([s[j] for s in states]) for j in range(3))
+    fext = np.tile(P.f_ext, ns)
+    cfg = rdsim.SimConfig(dt=P.cfg.dt)
+    poison()
+    Sg = sess.system_jacobian(r, rb, rdb, fext, cfg)
+    for i, (ri, rbi, rdbi) in enumerate(states):
+        assert rel(Sg[i], ors.system_jacobian(S, ri, (rbi, rdbi), P.f_ext, ocfg(cfg))) < 1e-11, i
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=2)
+    for k in range(2):
+        poison()
+        r1, rd1, _, _ = sess.step(rb, rdb, fext, cfg)
+        for i, (ri, rbi, rdbi) in enumerate(states):
+            ro, _, _, _ = ors.step(S, rbi, rdbi, P.f_ext, ocfg(cfg))
+            assert np.abs(r1.reshape(ns, n)[i] - ro).max() <= 1e-10 * np.abs(ro).max(), (k, i)
