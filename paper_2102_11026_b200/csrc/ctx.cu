@@ -19,6 +19,7 @@
 #include "epilogues.cuh"
 #include "sim_kernels.cuh"
 #include "solve_kernels.cuh"
+#include "lu_warp.cuh"
 #include "mlp_chain.cuh"
 #include "coupled_kernels.cuh"
 #include "gemm_ws.cuh"
@@ -628,6 +629,21 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
            c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt, c->n_p);
     return;
   }
+  // warp-register producer / consumer LU (lu_warp.cuh): bitwise identical results, but slower
+  // than the row-block kernel on B200 (issue-bound at one warp per scheduler: 34.8 vs 26.6 us
+  // at n = 60, tools/probes/lu_warp_probe.cu): opt-in only
+  static const bool warp_lu = getenv("NLROM_LU_WARP") != nullptr;
+  if (n <= LUW_MAXN && luw_warps(n, nx) <= 3 && warp_lu) {
+    const int nw = luw_warps(n, nx);
+    auto gow = [&](auto kern) {
+      launch(c, kern, c->n_sims, 256, luw_smem_bytes(nw, c->n_q), (const double*)c->S.p, (const double*)c->phi.p,
+             c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt, c->n_p);
+    };
+    if (nw == 1) gow(k_lu_warp<1>);
+    else if (nw == 2) gow(k_lu_warp<2>);
+    else gow(k_lu_warp<3>);
+    return;
+  }
   switch (lu_nb(n + nx)) {
     case 4: go(k_lu_solve<4>); break;
     case 6: go(k_lu_solve<6>); break;
@@ -946,6 +962,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_warp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     if (c->n + 4 > 128) throw Error(NLROM_ERR_ARG, "n_p + n_q must be <= 124");
     NL_CUDA(cudaDeviceSynchronize());
     *out = c;

@@ -330,11 +330,13 @@ np.savez(sys.argv[2], phi=phi, S=S, r=nxt.r)
     {"NLROM_LU_COLS": "1", "NLROM_MASS_LATE": "1"},
     {"NLROM_BWD_CFG": "1", "NLROM_NO_WS_GEMM": "1"},
     {"NLROM_NO_FUSED_MLP": "1", "NLROM_LU_ROWS": "1"},
+    {"NLROM_LU_WARP": "1"},
 ])
 def test_kernel_variants(cuda_ok, env, tmp_path):
     """Opt-in kernel variants (selected by environment at context creation, hence a fresh
     process) against the oracle: async cluster hand-off chain, column-cyclic LU, mass block on
-    the late branch, 16-CTA vhp clusters, cp.async output GEMM, unfused per-layer GEMMs."""
+    the late branch, 16-CTA vhp clusters, cp.async output GEMM, unfused per-layer GEMMs,
+    warp-register producer / consumer LU."""
     import os
     import subprocess
     import sys
