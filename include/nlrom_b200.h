@@ -251,6 +251,51 @@ NLROM_API int nlrom_coupled_read(nlrom_ctx* ctx, double dt, double* r, double* r
 /* kernel launches of one coupled Newton iteration (eval graph + update) */
 NLROM_API int nlrom_coupled_launches(nlrom_ctx* ctx);
 
+/* ---------------------------------------------------------------------------------------
+ * Full-space StVK implicit Euler (elastic.fullspace_step; SURVEY.md §8f
+ * rank 2: ground truth for trajectory error and the pose generator's integrator,
+ * posegen.generate_poses SPEC.md:395-403). One Newton solve per step of
+ *   M (v' - v) / dt + (alpha M + beta K(u')) v' + f_int(u') = f_ext,   u' = u + dt v',
+ * unknown v'; Newton matrix (1 + alpha dt) M + (beta dt + dt^2) K(u') (dK/du v' dropped:
+ * it changes the convergence rate only, not the solution); each linear system by Jacobi-
+ * preconditioned CG in one cooperative kernel (deterministic reductions). The mesh data are
+ * those of nlrom_model_desc (free-DOF numbering by vert_dof, Dirichlet by elimination). */
+typedef struct nlrom_fs nlrom_fs;
+
+typedef struct {
+  int n_verts, n_tets;
+  const int* tets;          /* (T,4)                                           */
+  const int* vert_dof;      /* (V,) free-vertex index or -1 if fixed           */
+  const double* Dm_inv;     /* (T,3,3) row-major                               */
+  const double* vol;        /* (T,)                                            */
+  const double* mass;       /* (N,) lumped, free DOFs                          */
+  double mu, lambda, alpha, beta;
+} nlrom_fs_desc;
+
+typedef struct {
+  double dt;
+  double newton_tol;        /* ||residual force||_2 <= newton_tol * max(1, ||f_ext||_2) */
+  int max_iters;            /* Newton iterations before NLROM_ERR_NEWTON       */
+  double cg_tol;            /* relative CG residual                            */
+  int cg_max_iters;
+} nlrom_fs_cfg;
+
+typedef struct {
+  int iters;                /* Newton iterations                               */
+  int cg_iters;             /* CG iterations, all Newton iterations            */
+  double res_norm;          /* final ||residual force||_2                      */
+  double energy;            /* StVK energy at u'                               */
+} nlrom_fs_info;
+
+NLROM_API int nlrom_fs_create(nlrom_fs** out, int device, const nlrom_fs_desc* desc);
+NLROM_API void nlrom_fs_destroy(nlrom_fs* fs);
+NLROM_API const char* nlrom_fs_last_error(const nlrom_fs* fs);
+/* (u, v) -> (u', v'), all (N,) */
+NLROM_API int nlrom_fs_step(nlrom_fs* fs, const double* u, const double* v, const double* f_ext,
+                            const nlrom_fs_cfg* cfg, double* u_out, double* v_out, nlrom_fs_info* info);
+/* StVK energy and internal force at u (f_int nullable) */
+NLROM_API int nlrom_fs_energy_force(nlrom_fs* fs, const double* u, double* energy, double* f_int);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,7 @@ EXPORTED = [
     "nlrom_element_reduced_forces", "nlrom_bench_kernels", "nlrom_stream", "nlrom_coupled_setup",
     "nlrom_coupled_begin", "nlrom_coupled_eval", "nlrom_coupled_update", "nlrom_coupled_read",
     "nlrom_coupled_launches", "nlrom_bench_prefix", "nlrom_debug_poison_shared_memory",
+    "nlrom_fs_create", "nlrom_fs_destroy", "nlrom_fs_last_error", "nlrom_fs_step", "nlrom_fs_energy_force",
 ]
 
 
@@ -59,6 +60,22 @@ class SimCfg(C.Structure):
 
 class StepInfo(C.Structure):
     _fields_ = [("iters", C.c_int), ("res_norm", C.c_double), ("status", C.c_int)]
+
+
+class FsDesc(C.Structure):
+    _fields_ = [("n_verts", C.c_int), ("n_tets", C.c_int), ("tets", C.POINTER(C.c_int)),
+                ("vert_dof", C.POINTER(C.c_int)), ("Dm_inv", C.POINTER(C.c_double)), ("vol", C.POINTER(C.c_double)),
+                ("mass", C.POINTER(C.c_double)), ("mu", C.c_double), ("lam", C.c_double), ("alpha", C.c_double),
+                ("beta", C.c_double)]
+
+
+class FsCfg(C.Structure):
+    _fields_ = [("dt", C.c_double), ("newton_tol", C.c_double), ("max_iters", C.c_int), ("cg_tol", C.c_double),
+                ("cg_max_iters", C.c_int)]
+
+
+class FsInfo(C.Structure):
+    _fields_ = [("iters", C.c_int), ("cg_iters", C.c_int), ("res_norm", C.c_double), ("energy", C.c_double)]
 
 
 _lib = None
@@ -110,6 +127,11 @@ def lib():
             "nlrom_bench_prefix": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float), C.c_char_p,
                                              C.c_int, ip]),
             "nlrom_debug_poison_shared_memory": (C.c_int, [C.c_int]),
+            "nlrom_fs_create": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(FsDesc)]),
+            "nlrom_fs_destroy": (None, [vp]),
+            "nlrom_fs_last_error": (C.c_char_p, [vp]),
+            "nlrom_fs_step": (C.c_int, [vp, dp, dp, dp, C.POINTER(FsCfg), dp, dp, C.POINTER(FsInfo)]),
+            "nlrom_fs_energy_force": (C.c_int, [vp, dp, dp, dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -82,6 +82,7 @@ class ElasticModel:
         self.vertex_mass = vm
         self.mass = np.repeat(vm[free], 3)
         self._fe = None
+        self._fs = None
 
     @property
     def n_tets(self):
@@ -156,6 +157,12 @@ def element_reduced_force(model: ElasticModel, rm, r, e):
     return out[0] if single else out
 
 
-def fullspace_step(*_a, **_k):
-    """Full-space implicit Euler is ranked "next"."""
-    raise NotImplementedError("fullspace_step is out of the round-1 hot-path scope (SURVEY.md §8f)")
+def fullspace_step(model: ElasticModel, u, v, f_ext, dt, cfg=None, return_info: bool = False):
+    """Implicit Euler in the full space: Newton solve of
+    M (v' - v)/dt + (alpha M + beta K(u')) v' + f_int(u') = f_ext with u' = u + dt v'.
+    GPU (csrc/fullspace.cu): element kernels, CSR assembly, cooperative Jacobi-PCG.
+    Returns (u', v') (and a FullspaceInfo if ``return_info``); raises
+    _lib.NewtonDivergence after ``cfg.max_iters`` Newton iterations."""
+    from .fullspace import session_for as _fs
+    uo, vo, info = _fs(model).step(u, v, f_ext, dt, cfg)
+    return (uo, vo, info) if return_info else (uo, vo)
