@@ -66,6 +66,12 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes ~0.1-0.3 s to start: wait for its first row, then keep only the
+            # rows sampled inside the timed region
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -286,6 +292,45 @@ def cpu_baseline(P, budget_s=12.0, max_iters=30):
                       f"system_jacobian with the 4n_q+2 reference passes + LU) at cfg2, median"}
 
 
+def fullspace_leg(args, rank, world):
+    """elastic.fullspace_step on the cfg2 mesh (N = 6720):
+    gravity from rest, wall clock per step through the public API (host arrays in and out),
+    beside one step of the scipy-direct oracle -- the ground-truth integrator the reduced step
+    replaces."""
+    import numpy as np
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200.fullspace import FullspaceConfig, FullspaceSession
+    P = build_problem("cfg2", n_fc=2, width=16)
+    fs = FullspaceSession(P.model)
+    cfg = FullspaceConfig()
+    u = v = np.zeros(P.model.N)
+    u, v, _ = fs.step(u, v, P.f_ext, P.cfg.dt, cfg)
+    ts, its, cgs = [], [], []
+    for _ in range(4):
+        t0 = time.perf_counter()
+        u, v, info = fs.step(u, v, P.f_ext, P.cfg.dt, cfg)
+        ts.append(time.perf_counter() - t0)
+        its.append(info.iters)
+        cgs.append(info.cg_iters)
+    out = {"workload": "cfg2 mesh (10290 tets, N = 6720), StVK implicit Euler, gravity, dt = 1/60",
+           "ms_per_step": barrier_max(world, 1e3 * sorted(ts)[len(ts) // 2]),
+           "newton_iters": its, "pcg_iters": cgs}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = fullspace_cpu_baseline(P, u, v)
+    return out
+
+
+def fullspace_cpu_baseline(P, u, v):
+    """cpu_baseline of the full-space leg: one step of the scipy-direct oracle on the host."""
+    from oracle import elastic as oe, fullspace as ofs
+    c = P.cfg
+    om = oe.OModel(P.data["verts"], P.data["tets"], P.data["fixed"], c.young, c.poisson, c.density, c.alpha)
+    t0 = time.perf_counter()
+    ofs.fullspace_step(om, u, v, P.f_ext, c.dt)
+    return {"value": 1e3 * (time.perf_counter() - t0), "unit": "ms per step", "kind": "port",
+            "sample": "1 step of oracle/fullspace.py (numpy + scipy spsolve) at the same state"}
+
+
 def run_reference(args):
     rank, world, local = dist_setup(0)
     if rank != 0:
@@ -375,6 +420,10 @@ def run_ours(args):
     if not args.no_coupled:
         coupled = coupled_leg(args, rank, world)
 
+    fullspace = None
+    if not args.no_fullspace:
+        fullspace = fullspace_leg(args, rank, world)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(P)
@@ -393,6 +442,7 @@ def run_ours(args):
             "roofline": roof,
             "batched_cfg5": batched,
             "coupled_cfg4": coupled,
+            "fullspace_cfg2": fullspace,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "hz_at_3_iters": 1000.0 / (3 * value),
@@ -414,6 +464,7 @@ def main():
     ap.add_argument("--batched-sims", type=int, default=4096)
     ap.add_argument("--no-coupled", action="store_true", help="skip the cfg4 320-string coupled leg")
     ap.add_argument("--strings", type=int, default=320)
+    ap.add_argument("--no-fullspace", action="store_true", help="skip the full-space implicit Euler leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -228,7 +228,10 @@ struct PcgArgs {
   double* relres;
 };
 
-// block-wide sum (256 threads), fixed order; result in every thread
+constexpr int PCG_NTH = 1024;  // 32 warps per block: rows of the latency-bound SpMV in flight
+constexpr int PCG_NW = PCG_NTH / 32;
+
+// block-wide sum, fixed order; result in every thread
 __device__ __forceinline__ double pcg_block_sum(double v, double* red) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -237,7 +240,7 @@ __device__ __forceinline__ double pcg_block_sum(double v, double* red) {
   __syncthreads();
   double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) s += red[w];
+  for (int w = 0; w < PCG_NW; ++w) s += red[w];
   return s;
 }
 
@@ -250,25 +253,32 @@ __device__ __forceinline__ double pcg_grid_sum(const double* part, int k, int nb
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   __syncthreads();
-  if (threadIdx.x == 0) red[8] = v;
+  if (threadIdx.x == 0) red[PCG_NW] = v;
   __syncthreads();
-  return red[8];
+  return red[PCG_NW];
 }
 
-__global__ void __launch_bounds__(256) k_fs_pcg(PcgArgs a) {
+// Two grid-wide syncs per iteration: the direction update p = z + beta p_prev is not a phase of
+// its own -- the SpMV forms it on the fly for every column it reads (the owner block stores it
+// for its rows in the other buffer of p), with exactly the same expression, so all blocks see
+// the same p bits.
+__device__ __forceinline__ double pcg_dir(double z, double beta, double pprev) { return fma(beta, pprev, z); }
+
+__global__ void __launch_bounds__(PCG_NTH) k_fs_pcg(PcgArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[9];
+  __shared__ double red[PCG_NW + 1];
   const int nb = gridDim.x, blk = blockIdx.x, tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int per = (a.N + nb - 1) / nb;
   const int r0 = min(a.N, blk * per), r1 = min(a.N, r0 + per);
+  double* P[2] = {a.p, a.Ap + a.N};  // direction buffers (Ap has room for 2N)
   double lrz = 0.0, lbb = 0.0;
   for (int i = r0 + tid; i < r1; i += blockDim.x) {
     const double bi = a.b[i], zi = a.dinv[i] * bi;
     a.x[i] = 0.0;
     a.r[i] = bi;
     a.z[i] = zi;
-    a.p[i] = zi;
+    P[1][i] = 0.0;  // p_prev of iteration 0 (beta = 0)
     lrz += bi * zi;
     lbb += bi * bi;
   }
@@ -282,19 +292,26 @@ __global__ void __launch_bounds__(256) k_fs_pcg(PcgArgs a) {
   double rz = pcg_grid_sum(a.part, 0, nb, red);
   const double bb = pcg_grid_sum(a.part, 1, nb, red);
   const double thr = a.tol * a.tol * bb;
-  double rr = bb;
+  double rr = bb, beta = 0.0;
   int it = 0;
   while (bb > 0.0 && it < a.maxit) {
-    // Ap = A p (warp per row), partial p . Ap
+    double* pc = P[it & 1];
+    const double* pp = P[(it + 1) & 1];
+    // Ap = A p with p = z + beta p_prev formed per column read (warp per row), partial p . Ap
     double lpap = 0.0;
-    for (int i = r0 + warp; i < r1; i += 8) {
+    for (int i = r0 + warp; i < r1; i += PCG_NW) {
       double s = 0.0;
-      for (int k = a.rp[i] + lane; k < a.rp[i + 1]; k += 32) s = fma(a.A[k], __ldcg(a.p + a.col[k]), s);
+      for (int k = a.rp[i] + lane; k < a.rp[i + 1]; k += 32) {
+        const int c = a.col[k];
+        s = fma(a.A[k], pcg_dir(__ldcg(a.z + c), beta, __ldcg(pp + c)), s);
+      }
 #pragma unroll
       for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) {
+        const double pi = pcg_dir(__ldcg(a.z + i), beta, __ldcg(pp + i));
+        pc[i] = pi;
         a.Ap[i] = s;
-        lpap += __ldcg(a.p + i) * s;
+        lpap += pi * s;
       }
     }
     lpap = pcg_block_sum(lpap, red);
@@ -304,9 +321,8 @@ __global__ void __launch_bounds__(256) k_fs_pcg(PcgArgs a) {
     const double alpha = rz / pap;
     double lrz2 = 0.0, lrr = 0.0;
     for (int i = r0 + tid; i < r1; i += blockDim.x) {
-      const double pi = a.p[i];
-      a.x[i] += alpha * pi;
-      const double ri = a.r[i] - alpha * a.Ap[i];
+      a.x[i] += alpha * __ldcg(pc + i);
+      const double ri = a.r[i] - alpha * __ldcg(a.Ap + i);
       a.r[i] = ri;
       const double zi = a.dinv[i] * ri;
       a.z[i] = zi;
@@ -324,10 +340,8 @@ __global__ void __launch_bounds__(256) k_fs_pcg(PcgArgs a) {
     rr = pcg_grid_sum(a.part, 1, nb, red);
     ++it;
     if (!(rr > thr)) break;  // converged (or NaN: stop, the host sees it)
-    const double beta = rz2 / rz;
+    beta = rz2 / rz;
     rz = rz2;
-    for (int i = r0 + tid; i < r1; i += blockDim.x) a.p[i] = a.z[i] + beta * a.p[i];
-    grid.sync();
   }
   if (blk == 0 && tid == 0) {
     *a.iters = it;
@@ -494,6 +508,7 @@ extern "C" int nlrom_fs_create(nlrom_fs** out, int device, const nlrom_fs_desc* 
     for (DBuf* bf : {&f->u, &f->v, &f->x, &f->up, &f->fext, &f->b, &f->dinv, &f->fint, &f->cg_x, &f->cg_r, &f->cg_z,
                      &f->cg_p, &f->cg_Ap})
       bf->alloc(N);
+    f->cg_Ap.alloc((size_t)2 * N);  // Ap | second direction buffer
     f->fe.alloc((size_t)T * 12);
     f->Ke.alloc((size_t)T * 144);
     f->epart.alloc((T + 7) / 8);
@@ -505,9 +520,11 @@ extern "C" int nlrom_fs_create(nlrom_fs** out, int device, const nlrom_fs_desc* 
     // cooperative PCG grid: one block per SM (co-residency required by grid.sync)
     int sms = 0, occ = 0;
     NL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    NL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fs_pcg, 256, 0));
+    NL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fs_pcg, PCG_NTH, 0));
     if (occ < 1) throw Error(NLROM_ERR_CUDA, "k_fs_pcg cannot be resident");
+    // one 1024-thread block per SM (tools/bench_fullspace.py: 37..296 blocks all within 10%)
     f->pcg_blocks = std::max(1, std::min(sms, (N + 31) / 32));
+    if (const char* env = getenv("NLROM_FS_BLOCKS")) f->pcg_blocks = std::max(1, std::min(sms * occ, atoi(env)));
     f->cg_part.alloc((size_t)f->pcg_blocks * 4);
     NL_CUDA(cudaDeviceSynchronize());
     *out = f;
@@ -599,7 +616,7 @@ extern "C" int nlrom_fs_step(nlrom_fs* f, const double* u, const double* v, cons
     PcgArgs pa{f->rp.p, f->col.p, f->Hv.p, f->dinv.p, f->b.p, f->cg_x.p, f->cg_r.p, f->cg_z.p, f->cg_p.p,
                f->cg_Ap.p, f->cg_part.p, N, cfg->cg_tol, cfg->cg_max_iters, f->iters.p, f->relres.p};
     void* kargs[] = {&pa};
-    NL_CUDA(cudaLaunchCooperativeKernel((const void*)k_fs_pcg, dim3(f->pcg_blocks), dim3(256), kargs, 0, f->st));
+    NL_CUDA(cudaLaunchCooperativeKernel((const void*)k_fs_pcg, dim3(f->pcg_blocks), dim3(PCG_NTH), kargs, 0, f->st));
     int cit = 0;
     NL_CUDA(cudaMemcpyAsync(&cit, f->iters.p, 4, cudaMemcpyDeviceToHost, f->st));
     k_fs_axpy<<<g1, 256, 0, f->st>>>(f->x.p, f->x.p, f->cg_x.p, 1.0, N);  // v' += dv
