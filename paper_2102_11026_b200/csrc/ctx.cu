@@ -61,6 +61,9 @@ struct nlrom_ctx {
   int device = 0;
   cudaStream_t st = nullptr, st2 = nullptr;
   cudaEvent_t evFork = nullptr, evJoin = nullptr, evFork2 = nullptr, evJoin2 = nullptr;
+  cudaEvent_t evWf = nullptr, evW = nullptr;  // early weight net: fork after the hidden chain, join before the cubature
+  DBuf wA1;        // weight-net layer 1 folded onto the decoder: [W1 P W_L | W1 U | W1 P b_L] (wn x wA1ld)
+  int wA1ld = 0;
   std::string err;
   double last_norm = 0.0;
   int N = 0, n_p = 0, n_q = 0, n = 0, L = 0, n_sims = 1, T = 0, V = 0;
@@ -394,10 +397,12 @@ void wnet_phase(nlrom_ctx* c) {
          (const double*)c->b3.p, (const double*)c->W4C.p, (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
 }
 
-void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true) {
+void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true, bool early = true) {
   CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, weighted ? c->wC.p : nullptr, c->u.p, c->Jt.p,
             c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk, nullptr, nullptr};
-  a.early = weighted ? 1 : 0;  // the weight-net tail (producer) launches dependents only after its own wait
+  // early: the weight-net tail (the only producer) launches dependents only after its own wait,
+  // so J~ / u are complete at launch; not when the output layer itself is a direct producer
+  a.early = (weighted && early) ? 1 : 0;
   size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162) * 8;
   launch(c, k_cubature, dim3(s.nchunk, c->n_sims), 256, smem, a);
   if (scatter)
@@ -469,12 +474,42 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 }
 
 // join_side = false leaves the phi / S_base branch open for phase_J (one-graph Newton iteration)
+// Early weight net: the net's layer 1 is folded onto the hidden chain's output (k_wnet_head), so
+// head + tail run on a side branch concurrently with the output layer instead of after it.
+bool early_wnet_ok(nlrom_ctx* c) {
+  static const bool off = getenv("NLROM_WNET_LATE") != nullptr;
+  return !off && c->wA1.p && !c->batched && c->wn >= 16 && c->wn % 2 == 0 && 256 % c->wn == 0 &&
+         c->wL1 + c->n_p + 1 <= 1024 && c->n_cub > 0;
+}
+
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
-  bundle_forward(c, cfg.dt, cfg.drop_fict);
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
+  bool early_w = cfg.integration == 0 && early_wnet_ok(c) && fused_hidden_forward(c, cfg.dt, cfg.drop_fict);
+  if (early_w) {
+    NL_CUDA(cudaEventRecord(c->evWf, c->st));
+    NL_CUDA(cudaStreamWaitEvent(c->st2, c->evWf, 0));
+    std::swap(c->st, c->st2);
+    launch(c, k_wnet_head, c->n_sims, 256, 0, (const double*)c->H[c->L - 2].p, c->ldH[c->L - 2], c->Cc,
+           (const double*)c->r.p, c->n, c->n_p, c->wL1, (const double*)c->wA1.p, c->wA1ld, c->wn, c->wpart.p);
+    const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + c->wn) * 8;
+    launch(c, k_wnet_tail2, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm + 16,
+           (const double*)c->wpart.p, 1, c->wn, (const double*)c->b1.p, (const double*)c->W2.p,
+           (const double*)c->b2.p, (const double*)c->W3.p, (const double*)c->b3.p, (const double*)c->W4C.p,
+           (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
+    std::swap(c->st, c->st2);
+    NL_CUDA(cudaEventRecord(c->evW, c->st2));
+    output_layer(c);
+  } else {
+    bundle_forward(c, cfg.dt, cfg.drop_fict);
+  }
   if (c->mass_early && c->mass_pos == 0) mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
-  if (cfg.integration == 0) wnet_phase(c);
-  cubature_phase(c, s, cfg.integration == 0, false);  // forces gathered per row by the assembly
+  if (early_w) {
+    NL_CUDA(cudaStreamWaitEvent(c->st, c->evW, 0));
+    cubature_phase(c, s, true, false, /*early=*/false);
+  } else {
+    if (cfg.integration == 0) wnet_phase(c);
+    cubature_phase(c, s, cfg.integration == 0, false);  // forces gathered per row by the assembly
+  }
   if (c->mass_early && c->mass_pos == 1) mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
   assemble_phase(c, s, cfg.dt, cfg.drop_fict);
   if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));  // phi, S_base (and the mass block)
@@ -763,6 +798,8 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreateWithFlags(&c->evFork2, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreateWithFlags(&c->evJoin2, cudaEventDisableTiming));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evWf, cudaEventDisableTiming));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evW, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreate(&c->ev0));
     NL_CUDA(cudaEventCreate(&c->ev1));
     c->n_sims = d->n_sims > 0 ? d->n_sims : 1;
@@ -805,6 +842,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         upload(c->WTp[l], wtp.data(), wtp.size());
       }
     }
+    std::vector<double> PWL_host, PbL_host;  // P W_L (N x w), P b_L (N): also fold the weight net's layer 1
     // last layer fused with the filter: D = P (W_L h + b_L) = (P W_L) h + P b_L with
     // P = I - U U^T folded into the weights once at upload (no filter GEMM per iteration).
     const double* WL = d->W[L - 1];
@@ -813,7 +851,11 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->next = 0;
     c->ldlast = round_up(w, 2);
     {
-      std::vector<double> ATh((size_t)n_p * w, 0.0), Utb(n_p, 0.0), Pbh(N), A((size_t)N * w);
+      std::vector<double>& Pbh = PbL_host;
+      std::vector<double>& A = PWL_host;
+      Pbh.assign(N, 0.0);
+      A.assign((size_t)N * w, 0.0);
+      std::vector<double> ATh((size_t)n_p * w, 0.0), Utb(n_p, 0.0);
       for (int r = 0; r < N; ++r)
         for (int j = 0; j < n_p; ++j) {
           const double ur = d->U[(size_t)r * n_p + j];
@@ -883,6 +925,26 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       }
       upload(c->W4C, w4.data(), w4.size());
       upload(c->b4C, b4.data(), b4.size());
+      // layer 1 of the weight net on u = U p + P (W_L h + b_L) folded onto the
+      // last hidden activation h and p: W1 u = (W1 P W_L) h + (W1 U) p + W1 P b_L, a wn x (w + n_p + 1)
+      // matrix formed once -- the weight net then needs only the hidden chain, not the output layer
+      if (!PWL_host.empty()) {
+        const int wL = c->wL1;
+        c->wA1ld = round_up(wL + n_p + 1, 2);
+        std::vector<double> F((size_t)wn * c->wA1ld, 0.0);
+        for (int o = 0; o < wn; ++o) {
+          double* Fo = F.data() + (size_t)o * c->wA1ld;
+          const double* W1o = d->wnet_W[0] + (size_t)o * N;
+          for (int r = 0; r < N; ++r) {
+            const double wv = W1o[r];
+            const double* Ar = PWL_host.data() + (size_t)r * wL;
+            for (int k = 0; k < wL; ++k) Fo[k] += wv * Ar[k];
+            for (int j = 0; j < n_p; ++j) Fo[wL + j] += wv * d->U[(size_t)r * n_p + j];
+            Fo[wL + n_p] += wv * PbL_host[r];
+          }
+        }
+        upload(c->wA1, F.data(), F.size());
+      }
       c->wchunk = round_up(std::max(32, ceil_div(N, 148)), 32);
       c->wsplit = ceil_div(N, c->wchunk);
       c->wpart.alloc((size_t)c->wsplit * c->n_sims * wn);
@@ -994,6 +1056,8 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->evJoin) cudaEventDestroy(c->evJoin);
   if (c->evFork2) cudaEventDestroy(c->evFork2);
   if (c->evJoin2) cudaEventDestroy(c->evJoin2);
+  if (c->evWf) cudaEventDestroy(c->evWf);
+  if (c->evW) cudaEventDestroy(c->evW);
   delete c;
 }
 

@@ -272,6 +272,33 @@ __device__ __forceinline__ double wnet_row_tpr(const double* __restrict__ W, int
   return acc;
 }
 
+// Weight-net layer 1 from the decoder's last hidden activation (folded weights, see the upload
+// in ctx.cu): part[sim][m] = sum_k F[m][k] x[k], x = [h (w) | p (n_p) | 1]; h is the base jet
+// column of the hidden chain's output (compact column sim * cs). Runs on a side branch while the
+// output layer executes; k_wnet_tail2 (n_split = 1) adds b1 and finishes the net.
+__global__ void __launch_bounds__(256) k_wnet_head(const double* __restrict__ H, int ldH, int cs,
+                                                   const double* __restrict__ r, int n, int n_p, int w,
+                                                   const double* __restrict__ F, int ldF, int wn,
+                                                   double* __restrict__ part) {
+  __shared__ double x[1024];
+  const int sim = blockIdx.x, tid = threadIdx.x;
+  const int K = w + n_p + 1;
+  pdl_wait();
+  pdl_launch();
+  for (int k = tid; k < K; k += blockDim.x)
+    x[k] = k < w ? H[(size_t)sim * cs * ldH + k] : (k < w + n_p ? r[(size_t)sim * n + (k - w)] : 1.0);
+  __syncthreads();
+  const int tpr = blockDim.x / wn;  // threads per output row (wn divides 256)
+  const int m = tid / tpr, q = tid % tpr;
+  double acc = 0.0;
+  if (m < wn) {
+    const double* Fm = F + (size_t)m * ldF;
+    for (int k = q; k < K; k += tpr) acc = fma(Fm[k], x[k], acc);
+  }
+  for (int o = tpr >> 1; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (m < wn && q == 0) part[(size_t)sim * wn + m] = acc;
+}
+
 __global__ void __launch_bounds__(256) k_wnet_tail2(const double* __restrict__ part, int n_split, int wn,
                                                     const double* __restrict__ b1, const double* __restrict__ W2,
                                                     const double* __restrict__ b2, const double* __restrict__ W3,
