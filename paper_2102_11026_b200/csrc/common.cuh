@@ -32,7 +32,26 @@ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 constexpr int kNoBudget = 1 << 30;
 inline int& launch_budget() { static int b = kNoBudget; return b; }
 inline std::vector<const void*>& launch_log() { static std::vector<const void*> v; return v; }
+// Timing experiments only: NLROM_DEBUG_SKIP=name1,name2 drops every launch whose kernel name
+// contains one of the substrings (results are then wrong; used to find the critical path).
+inline bool launch_skipped(const void* fn) {
+  static const char* env = getenv("NLROM_DEBUG_SKIP");
+  if (!env || !*env) return false;
+  const char* name = nullptr;
+  if (cudaFuncGetName(&name, fn) != cudaSuccess || !name) return false;
+  std::string list(env), nm(name);
+  size_t pos = 0;
+  while (pos <= list.size()) {
+    size_t e = list.find(',', pos);
+    if (e == std::string::npos) e = list.size();
+    const std::string tok = list.substr(pos, e - pos);
+    if (!tok.empty() && nm.find(tok) != std::string::npos) return true;
+    pos = e + 1;
+  }
+  return false;
+}
 inline bool launch_gate(const void* fn) {
+  if (launch_skipped(fn)) return false;
   int& b = launch_budget();
   if (b >= kNoBudget) return true;
   if (b <= 0) return false;

@@ -96,6 +96,8 @@ struct nlrom_ctx {
   DBuf u, value, hvv, Jt, dJ;
   // assembly / solve
   int rpc = 128, nchA = 0;
+  int nchAa = 0, nphi = 0;     // k_assemble_a chunks (32 rows) when it also forms the vhp seed; partPhi chunks
+  bool agemv = false;          // the last assemble_phase produced the vhp-chain seed partials
   int rpcM = 128, nchM = 0;  // row chunking of the mass block (finer: more CTAs for its Gram)
   int s_ctas = getenv("NLROM_S_CTAS") ? atoi(getenv("NLROM_S_CTAS")) : 1 << 20;  // side-branch S reduction CTAs
   DBuf a, partA, partPhi, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
@@ -447,12 +449,23 @@ void mass_block_fork(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 
 // a and the J~^T a partials on the critical path; phi = sum of partials and S_base = mass block
 // + dt^2 K~ (no vhp) on the side branch (after the mass block), joined where they are consumed.
+bool fused_vhp_backward(nlrom_ctx* c, bool check_only);
+
 void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
+  c->agemv = false;
+  c->nphi = c->nchA;
   if (c->rpc <= 128 && c->n <= 128) {
+    // with the fused vhp chain: 32-row chunks that also form the chain's seed (P W_L)^T a
+    const bool g = fused_vhp_backward(c, true) && c->wL1 <= 256 && c->ldlast % 2 == 0 &&
+                   !getenv("NLROM_SEPARATE_GEMV");
+    const int rc = g ? ASMA_GROWS : c->rpc, nch = g ? c->nchAa : c->nchA;
     AsmAArgs A{c->Jt.p, c->ldjt, c->mass.p, c->hvv.p, c->fext.p, c->r.p, c->rbar.p, c->rdbar.p,
                s.rowptr_full.p, s.entries.p, s.fe_w.p, std::max(s.n, 1), c->a.p, c->partPhi.p,
-               c->N, c->n, c->rpc, c->nchA, dt, c->alpha, drop_fict};
-    launch(c, k_assemble_a, dim3(c->nchA, c->n_sims), 256, 0, A);
+               c->N, c->n, rc, nch, dt, c->alpha, drop_fict,
+               (const double*)c->Alast.p, c->ldlast, c->wL1, g ? c->bpart.p : nullptr};
+    launch(c, k_assemble_a, dim3(nch, c->n_sims), 256, 0, A);
+    c->agemv = g;
+    c->nphi = nch;
   } else {
     launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
            (const int*)s.row_ptr.p, (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N,
@@ -462,7 +475,7 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   NL_CUDA(cudaEventRecord(c->evFork2, c->st));
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evFork2, 0));
   std::swap(c->st, c->st2);
-  launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nchA, c->n,
+  launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nphi, c->n,
          c->phi.p, c->norm.p);
   if (!c->mass_early) mass_block_launch(c, s, dt, drop_fict);  // mass block, overlapping the vhp chain
   const int n = c->n;
@@ -479,7 +492,7 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 bool early_wnet_ok(nlrom_ctx* c) {
   static const bool off = getenv("NLROM_WNET_LATE") != nullptr;
   return !off && c->wA1.p && !c->batched && c->wn >= 16 && c->wn % 2 == 0 && 256 % c->wn == 0 &&
-         c->wL1 + c->n_p + 1 <= 1024 && c->n_cub > 0;
+         c->wL1 + c->n_p + 1 <= 1024 && c->n_cub > 0 && wnet_head_smem(c->wn, c->wA1ld) <= 220 * 1024;
 }
 
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
@@ -489,7 +502,7 @@ void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
     NL_CUDA(cudaEventRecord(c->evWf, c->st));
     NL_CUDA(cudaStreamWaitEvent(c->st2, c->evWf, 0));
     std::swap(c->st, c->st2);
-    launch(c, k_wnet_head, c->n_sims, 256, 0, (const double*)c->H[c->L - 2].p, c->ldH[c->L - 2], c->Cc,
+    launch(c, k_wnet_head, c->n_sims, 256, wnet_head_smem(c->wn, c->wA1ld), (const double*)c->H[c->L - 2].p, c->ldH[c->L - 2], c->Cc,
            (const double*)c->r.p, c->n, c->n_p, c->wL1, (const double*)c->wA1.p, c->wA1ld, c->wn, c->wpart.p);
     const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + c->wn) * 8;
     launch(c, k_wnet_tail2, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm + 16,
@@ -600,7 +613,8 @@ bool launch_mlp_bwd(nlrom_ctx* c, MlpBwdArgs a, int dry) {
   return true;
 }
 
-bool fused_vhp_backward(nlrom_ctx* c) {
+// check_only: report whether the fused chain applies (nothing launched)
+bool fused_vhp_backward(nlrom_ctx* c, bool check_only) {
   if (getenv("NLROM_NO_FUSED_MLP") || getenv("NLROM_NO_FUSED_BWD") || c->next || c->batched) return false;
   const int L1 = c->L - 1, w = c->wL1;
   if (L1 < 1 || L1 > MLP_MAXL) return false;
@@ -631,7 +645,12 @@ bool fused_vhp_backward(nlrom_ctx* c) {
     return false;
   };
   if (!go(true)) return false;
-  if (M % 2 == 0 && c->ldlast % 2 == 0 && M <= 512) {
+  if (check_only) return true;
+  if (c->agemv) {
+    // seed partials already formed by k_assemble_a (32-row chunks)
+    a.gpart = c->bpart.p;
+    a.gnch = c->nchAa;
+  } else if (M % 2 == 0 && c->ldlast % 2 == 0 && M <= 512) {
     // 24-row chunks over ~280 CTAs; the chain's prologue sums the partials (no reduce launch)
     const int rows = 24, nch = ceil_div(c->N, rows);
     launch(c, k_gemv_t2, dim3(nch, c->n_sims), 256, 0, (const double*)c->Alast.p, c->ldlast, M,
@@ -689,7 +708,7 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
 // side_open: phase E left its phi / S_base branch unjoined (captured in the same graph)
 void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply, const double* xrhs = nullptr, int nx = 0,
              double* xout = nullptr, bool side_open = false) {
-  if (!fused_vhp_backward(c))
+  if (!fused_vhp_backward(c, false))
     decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
   if (side_open) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));  // S_base, phi from phase E's branch
   launch_lu(c, apply, xrhs, nx, xout, true);  // S = S_base + diag(0, vhp) while staging
@@ -991,7 +1010,8 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     const int n = c->n, S = c->n_sims;
     c->a.alloc((size_t)S * N);
     c->partA.alloc((size_t)S * std::max(c->nchA, c->nchM) * n * n);
-    c->partPhi.alloc((size_t)S * c->nchA * n);
+    c->nchAa = ceil_div(N, ASMA_GROWS);
+    c->partPhi.alloc((size_t)S * std::max(c->nchA, c->nchAa) * n);
     c->phi.alloc((size_t)S * n);
     c->norm.alloc(S);
     c->S.alloc((size_t)S * n * n);
@@ -1024,6 +1044,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_wnet_head, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_warp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1481,7 +1502,7 @@ extern "C" int nlrom_bench_kernels(nlrom_ctx* c, int n_iters, int flush_l2, floa
         break;
       case 1: output_layer(c); break;
       case 2:
-        if (!fused_vhp_backward(c))
+        if (!fused_vhp_backward(c, false))
           decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
         break;
       default: {

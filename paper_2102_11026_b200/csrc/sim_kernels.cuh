@@ -275,26 +275,47 @@ __device__ __forceinline__ double wnet_row_tpr(const double* __restrict__ W, int
 // Weight-net layer 1 from the decoder's last hidden activation (folded weights, see the upload
 // in ctx.cu): part[sim][m] = sum_k F[m][k] x[k], x = [h (w) | p (n_p) | 1]; h is the base jet
 // column of the hidden chain's output (compact column sim * cs). Runs on a side branch while the
-// output layer executes; k_wnet_tail2 (n_split = 1) adds b1 and finishes the net.
+// output layer executes; k_wnet_tail2 (n_split = 1) adds b1 and finishes the net. The folded
+// matrix (wn x ldF, constant) lands in shared memory by one TMA bulk copy issued BEFORE the
+// dependency wait, i.e. while the hidden chain still runs.
+inline size_t wnet_head_smem(int wn, int ldF) { return (size_t)wn * ldF * 8 + 1024 * 8 + 16; }
+
 __global__ void __launch_bounds__(256) k_wnet_head(const double* __restrict__ H, int ldH, int cs,
                                                    const double* __restrict__ r, int n, int n_p, int w,
                                                    const double* __restrict__ F, int ldF, int wn,
                                                    double* __restrict__ part) {
-  __shared__ double x[1024];
+  extern __shared__ __align__(16) double hs[];
+  double* Fs = hs;                   // [wn][ldF]
+  double* x = Fs + (size_t)wn * ldF;  // [<= 1024]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(x + 1024);
   const int sim = blockIdx.x, tid = threadIdx.x;
   const int K = w + n_p + 1;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = (uint32_t)(wn * ldF * 8);
+    mbar_expect_tx(bar, bytes);
+    tma_g2s(Fs, F, bytes, bar);
+  }
   pdl_wait();
   pdl_launch();
   for (int k = tid; k < K; k += blockDim.x)
     x[k] = k < w ? H[(size_t)sim * cs * ldH + k] : (k < w + n_p ? r[(size_t)sim * n + (k - w)] : 1.0);
   __syncthreads();
+  mbar_wait(bar, 0);
   const int tpr = blockDim.x / wn;  // threads per output row (wn divides 256)
   const int m = tid / tpr, q = tid % tpr;
-  double acc = 0.0;
+  double a0 = 0.0, a1 = 0.0;
   if (m < wn) {
-    const double* Fm = F + (size_t)m * ldF;
-    for (int k = q; k < K; k += tpr) acc = fma(Fm[k], x[k], acc);
+    const double* Fm = Fs + (size_t)m * ldF;
+    int k = q;
+    for (; k + tpr < K; k += 2 * tpr) {
+      a0 = fma(Fm[k], x[k], a0);
+      a1 = fma(Fm[k + tpr], x[k + tpr], a1);
+    }
+    if (k < K) a0 = fma(Fm[k], x[k], a0);
   }
+  double acc = a0 + a1;
   for (int o = tpr >> 1; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (m < wn && q == 0) part[(size_t)sim * wn + m] = acc;
 }

@@ -175,12 +175,19 @@ struct AsmAArgs {
   int N, n, RC, nchunk;
   double dt, alpha;
   int drop_fict;
+  // optional, fused (P W_L)^T a for the vhp chain: gpart[sim][chunk][M] = sum_rows PW[row][:] a_row
+  const double* PW; int ldPW, M;
+  double* gpart;
 };
 
 // Programmatic-launch overlap: the J~ . c dot products (J~, hvv: output layer; r, r_bar,
 // rdot_bar: state) run before the dependency wait -- the producer (k_cubature) launches
 // dependents only after its own wait, so the output layer has completed -- and only the
 // gathered element forces (cubature output) are read after it.
+// With A.gpart (RC <= 32, M <= 256): the seed of the vhp chain, (P W_L)^T a, is accumulated here
+// per chunk (the chain's prologue sums the chunk partials): each thread owns one column of P W_L
+// and loads its RC entries (constants) before the dependency wait.
+constexpr int ASMA_GROWS = 32;
 __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
   __shared__ double cs[128];
   __shared__ double as[128];
@@ -188,6 +195,15 @@ __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
   const int chunk = blockIdx.x, sim = blockIdx.y, tid = threadIdx.x;
   const int n = A.n;
   const double ah = A.alpha * A.dt;
+  double pw[ASMA_GROWS];
+  const bool gcol = A.gpart && tid < A.M;
+  if (A.gpart) {
+#pragma unroll
+    for (int rl = 0; rl < ASMA_GROWS; ++rl) {
+      const int row = chunk * A.RC + rl;
+      pw[rl] = (gcol && rl < A.RC && row < A.N) ? A.PW[(size_t)row * A.ldPW + tid] : 0.0;
+    }
+  }
   for (int i = tid; i < n; i += blockDim.x) {
     const size_t o = (size_t)sim * n + i;
     cs[i] = (1.0 + ah) * (A.r[o] - A.rbar[o]) - A.dt * A.rdbar[o];
@@ -224,6 +240,15 @@ __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
     }
   }
   __syncthreads();
+  if (A.gpart) {
+    double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+    for (int rl = 0; rl < ASMA_GROWS; rl += 2) {
+      g0 = fma(pw[rl], as[rl], g0);
+      g1 = fma(pw[rl + 1], as[rl + 1], g1);
+    }
+    if (gcol) A.gpart[((size_t)sim * A.nchunk + chunk) * A.M + tid] = g0 + g1;
+  }
   const int q = tid >> 6, jl = tid & 63;
   for (int j0 = 0; j0 < n; j0 += 64) {
     const int j = j0 + jl;
