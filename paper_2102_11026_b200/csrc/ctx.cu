@@ -59,9 +59,11 @@ int gemm_launch_count = 0;
 
 struct nlrom_ctx {
   int device = 0;
-  cudaStream_t st = nullptr, st2 = nullptr;
+  cudaStream_t st = nullptr, st2 = nullptr, st3 = nullptr;
   cudaEvent_t evFork = nullptr, evJoin = nullptr, evFork2 = nullptr, evJoin2 = nullptr;
   cudaEvent_t evWf = nullptr, evW = nullptr;  // early weight net: fork after the hidden chain, join before the cubature
+  cudaEvent_t evK = nullptr, evM = nullptr;    // split cubature: stiffness branch fork; mass block (st3) done
+  cudaEvent_t evP = nullptr;                   // phi reduced (st3)
   DBuf wA1;        // weight-net layer 1 folded onto the decoder: [W1 P W_L | W1 U | W1 P b_L] (wn x wA1ld)
   int wA1ld = 0;
   std::string err;
@@ -83,6 +85,7 @@ struct nlrom_ctx {
   DBuf Dm_inv, vol;
   double mu = 0, lam = 0, alpha = 0;
   CubSet setC, setAll;
+  CubSet setCF;  // split phase E: the cubature set chunked for the force-only launch (2 elements per CTA)
   // wnet
   int wn = 0, n_cub = 0;
   DBuf W1, b1, W2, b2, W3, b3, W4C, b4C;
@@ -399,9 +402,12 @@ void wnet_phase(nlrom_ctx* c) {
          (const double*)c->b3.p, (const double*)c->W4C.p, (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
 }
 
-void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true, bool early = true) {
-  CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, weighted ? c->wC.p : nullptr, c->u.p, c->Jt.p,
-            c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk, nullptr, nullptr};
+// part: 0 forces + stiffness, 1 weighted element forces only (fe_w), 2 stiffness / Gram only
+void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true, bool early = true, int part = 0) {
+  CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, weighted ? c->wC.p : nullptr, c->u.p,
+            part == 1 ? nullptr : c->Jt.p, c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p,
+            s.part_K.p, s.nchunk, nullptr, nullptr};
+  a.skip_fe = part == 2 ? 1 : 0;
   // early: the weight-net tail (the only producer) launches dependents only after its own wait,
   // so J~ / u are complete at launch; not when the output layer itself is a direct producer
   a.early = (weighted && early) ? 1 : 0;
@@ -495,9 +501,86 @@ bool early_wnet_ok(nlrom_ctx* c) {
          c->wL1 + c->n_p + 1 <= 1024 && c->n_cub > 0 && wnet_head_smem(c->wn, c->wA1ld) <= 220 * 1024;
 }
 
+// Split phase E (early weight net + mass block on st3 + cubature split into a force-only launch
+// on the critical path and the stiffness / Gram launch on a side branch):
+//   st : jet chain -> output layer -> [wait W] -> k_cubature(forces) -> k_assemble_a
+//   st2: wnet head -> tail (W) -> [wait K] k_cubature(stiffness) -> [wait M] k_reduce_S
+//   st3: [after the output layer] k_assemble_mass (M) -> [wait A] k_reduce_phi (P)
+//   (st2 and st3 joined before the LU)
+void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s) {
+  auto on = [&](cudaStream_t& other, auto fn) {
+    std::swap(c->st, other);
+    fn();
+    std::swap(c->st, other);
+  };
+  NL_CUDA(cudaEventRecord(c->evWf, c->st));
+  NL_CUDA(cudaStreamWaitEvent(c->st2, c->evWf, 0));
+  on(c->st2, [&] {
+    launch(c, k_wnet_head, c->n_sims, 256, wnet_head_smem(c->wn, c->wA1ld), (const double*)c->H[c->L - 2].p,
+           c->ldH[c->L - 2], c->Cc, (const double*)c->r.p, c->n, c->n_p, c->wL1, (const double*)c->wA1.p, c->wA1ld,
+           c->wn, c->wpart.p);
+    const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + c->wn) * 8;
+    launch(c, k_wnet_tail2, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm + 16,
+           (const double*)c->wpart.p, 1, c->wn, (const double*)c->b1.p, (const double*)c->W2.p,
+           (const double*)c->b2.p, (const double*)c->W3.p, (const double*)c->b3.p, (const double*)c->W4C.p,
+           (const double*)c->b4C.p, c->n_cub, c->wC.p, c->n_sims);
+  });
+  NL_CUDA(cudaEventRecord(c->evW, c->st2));
+  output_layer(c);
+  NL_CUDA(cudaEventRecord(c->evFork, c->st));
+  NL_CUDA(cudaStreamWaitEvent(c->st3, c->evFork, 0));
+  on(c->st3, [&] { mass_block_launch(c, s, cfg.dt, cfg.drop_fict); });
+  NL_CUDA(cudaEventRecord(c->evM, c->st3));
+  NL_CUDA(cudaStreamWaitEvent(c->st, c->evW, 0));
+  NL_CUDA(cudaEventRecord(c->evK, c->st));
+  NL_CUDA(cudaStreamWaitEvent(c->st2, c->evK, 0));
+  on(c->st2, [&] { cubature_phase(c, s, true, false, false, 2); });
+  CubSet& sf = c->setCF.n ? c->setCF : s;
+  cubature_phase(c, sf, true, false, false, 1);
+  // a (+ the vhp seed partials) on the critical path; phi and S_base on st2
+  c->agemv = false;
+  const bool g = fused_vhp_backward(c, true) && c->wL1 <= 256 && c->ldlast % 2 == 0 && !getenv("NLROM_SEPARATE_GEMV");
+  const int rc = g ? ASMA_GROWS : c->rpc, nch = g ? c->nchAa : c->nchA;
+  AsmAArgs A{c->Jt.p, c->ldjt, c->mass.p, c->hvv.p, c->fext.p, c->r.p, c->rbar.p, c->rdbar.p,
+             sf.rowptr_full.p, sf.entries.p, sf.fe_w.p, std::max(sf.n, 1), c->a.p, c->partPhi.p,
+             c->N, c->n, rc, nch, cfg.dt, c->alpha, cfg.drop_fict,
+             (const double*)c->Alast.p, c->ldlast, c->wL1, g ? c->bpart.p : nullptr};
+  launch(c, k_assemble_a, dim3(nch, c->n_sims), 256, 0, A);
+  c->agemv = g;
+  c->nphi = nch;
+  // phi on st3 (after the mass block), S_base on st2 (after the stiffness launch and the mass
+  // block): the two reductions run concurrently; evJoin2 covers both
+  NL_CUDA(cudaEventRecord(c->evFork2, c->st));
+  NL_CUDA(cudaStreamWaitEvent(c->st3, c->evFork2, 0));
+  on(c->st3, [&] {
+    launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nphi, c->n,
+           c->phi.p, c->norm.p);
+  });
+  NL_CUDA(cudaEventRecord(c->evP, c->st3));
+  NL_CUDA(cudaStreamWaitEvent(c->st2, c->evM, 0));  // the mass block partials
+  on(c->st2, [&] {
+    const int n = c->n;
+    const int sblocks = std::min(ceil_div(n * n, 32), c->s_ctas);
+    launch(c, k_reduce_S, dim3(sblocks, c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
+           (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
+  });
+  NL_CUDA(cudaStreamWaitEvent(c->st2, c->evP, 0));
+  NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));
+}
+
+bool split_phase_ok(nlrom_ctx* c) {
+  static const bool off = getenv("NLROM_NO_SPLIT_E") != nullptr;
+  return !off && c->mass_early && c->rpc <= 128 && c->n <= 128;
+}
+
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   bool early_w = cfg.integration == 0 && early_wnet_ok(c) && fused_hidden_forward(c, cfg.dt, cfg.drop_fict);
+  if (early_w && split_phase_ok(c)) {
+    phase_E_split(c, cfg, s);
+    if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));
+    return;
+  }
   if (early_w) {
     NL_CUDA(cudaEventRecord(c->evWf, c->st));
     NL_CUDA(cudaStreamWaitEvent(c->st2, c->evWf, 0));
@@ -813,12 +896,16 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->device = device;
     NL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     NL_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    NL_CUDA(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
     NL_CUDA(cudaEventCreateWithFlags(&c->evFork, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreateWithFlags(&c->evJoin, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreateWithFlags(&c->evFork2, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreateWithFlags(&c->evJoin2, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreateWithFlags(&c->evWf, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreateWithFlags(&c->evW, cudaEventDisableTiming));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evK, cudaEventDisableTiming));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evM, cudaEventDisableTiming));
+    NL_CUDA(cudaEventCreateWithFlags(&c->evP, cudaEventDisableTiming));
     NL_CUDA(cudaEventCreate(&c->ev0));
     NL_CUDA(cudaEventCreate(&c->ev1));
     c->n_sims = d->n_sims > 0 ? d->n_sims : 1;
@@ -921,7 +1008,12 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       // exact-sum mode (not the hot path): 8, keeping its per-chunk partials small
       // many sims (batched): 8 elements per CTA keeps the per-chunk partials (and their reduction) small
       const bool many = c->n_sims * (4 + 4 * c->n_q) >= 2048 || getenv("NLROM_BATCHED") != nullptr;
-      build_set(c, c->setC, cub, rows, getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : (many ? 8 : 2));
+      // split phase E (default): the stiffness / Gram launch is off the critical path, where fewer,
+      // longer chunks win (12 elements per CTA: fewer K~ partials to reduce); the force-only launch
+      // on the critical path keeps 2 per CTA (setCF)
+      const bool split = getenv("NLROM_NO_SPLIT_E") == nullptr && !many;
+      build_set(c, c->setC, cub, rows, getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : (many ? 8 : split ? 12 : 2));
+      if (split) build_set(c, c->setCF, cub, rows, getenv("NLROM_EPCF") ? atoi(getenv("NLROM_EPCF")) : 6);
       build_set(c, c->setAll, all, rows, 8);
     }
     // weight net (rows of the last layer restricted to C)
@@ -1073,12 +1165,16 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->st) cudaStreamDestroy(c->st);
   if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->st3) cudaStreamDestroy(c->st3);
   if (c->evFork) cudaEventDestroy(c->evFork);
   if (c->evJoin) cudaEventDestroy(c->evJoin);
   if (c->evFork2) cudaEventDestroy(c->evFork2);
   if (c->evJoin2) cudaEventDestroy(c->evJoin2);
   if (c->evWf) cudaEventDestroy(c->evWf);
   if (c->evW) cudaEventDestroy(c->evW);
+  if (c->evK) cudaEventDestroy(c->evK);
+  if (c->evM) cudaEventDestroy(c->evM);
+  if (c->evP) cudaEventDestroy(c->evP);
   delete c;
 }
 

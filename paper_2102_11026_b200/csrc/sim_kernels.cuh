@@ -416,6 +416,7 @@ struct CubArgs {
   double* Ke_out;          // optional (E, 144): w-scaled element stiffness
   double* fred_out;        // optional (E, n): per-element J~_e^T (w f_e)
   int early = 0;           // 1: the producer grid is the weight net (J~, u complete at launch)
+  int skip_fe = 0;         // 1: do not write fe_w (a concurrent force-only launch owns it)
 };
 
 __device__ __forceinline__ void mat3_mul(const double* A, const double* B, double* C) {
@@ -539,6 +540,7 @@ __global__ void k_cubature(CubArgs a) {
       int i = lane / 3, aa = lane % 3;
       double f = V * (P[aa * 3] * G[i * 3] + P[aa * 3 + 1] * G[i * 3 + 1] + P[aa * 3 + 2] * G[i * 3 + 2]);
       Fs[el * 12 + lane] = we * f;
+      if (!Jt && !a.Ke_out) continue;  // force-only launch: no element stiffness
       // stiffness column for DOF (jv, d) = lane: dF_ab = delta_ad g_jv[b]
       int jv = lane / 3, d = lane % 3;
       double dF[9];
@@ -604,7 +606,7 @@ __global__ void k_cubature(CubArgs a) {
   for (int t = threadIdx.x; t < epc * 12; t += blockDim.x) {
     const int el = t / 12, ei = chunk * epc + el;
     Fs[t] *= wsh[el];
-    if (ei < a.n_elems) a.fe_w[((size_t)sim * a.n_elems + ei) * 12 + t % 12] = Fs[t];
+    if (ei < a.n_elems && !a.skip_fe) a.fe_w[((size_t)sim * a.n_elems + ei) * 12 + t % 12] = Fs[t];
   }
   if (a.Ke_out)
     for (int t = threadIdx.x; t < epc * 144; t += blockDim.x) {
