@@ -379,6 +379,10 @@ __device__ __forceinline__ double recip_fast(double p) {
   return fma(r, e, r);
 }
 
+#ifdef LU_CYCLES
+__device__ long long g_lu_cycles[2];  // tools/probes/lu_warp_probe.cu: cycles of the pivot loop
+#endif
+
 template <int NB>
 __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, const double* __restrict__ phi,
                                                    double* __restrict__ dr, double* __restrict__ r, int n, int apply,
@@ -443,6 +447,9 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
   };
   bool bad = false;
   __syncthreads();
+#ifdef LU_CYCLES
+  if (tid == 0) g_lu_cycles[0] = clock64();
+#endif
   for (int k = 0; k < n; ++k) {
     // every warp: argmax over the column (rows lane + 32u)
     double best = -1.0;
@@ -497,6 +504,9 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
     }
     __syncthreads();
   }
+#ifdef LU_CYCLES
+  if (tid == 0) g_lu_cycles[1] = clock64();
+#endif
   if (bad) {
     if (tid == 0) status[sim] = 1;
     return;

@@ -49,6 +49,11 @@ int main(int argc, char** argv) {
       k_lu_solve<4><<<1, 256, lu_smem_bytes(n)>>>(dS, dphi, ddr, dr, n, 0, st, nullptr, 0, nullptr, nullptr, 0, 0);
     }, 200);
     cudaMemcpy(x_ref.data(), ddr, n * 8, cudaMemcpyDeviceToHost);
+#ifdef LU_CYCLES
+    long long cyc[2];
+    cudaMemcpyFromSymbol(cyc, g_lu_cycles, sizeof cyc);
+    printf("n=%2d  k_lu_solve pivot loop %lld cycles (%.0f per step)\n", n, cyc[1] - cyc[0], (double)(cyc[1] - cyc[0]) / n);
+#endif
     cudaMemset(ddr, 0, n * 8);
     const int nw = luw_warps(n, 0);
     const size_t sm = luw_smem_bytes(nw, 0);
