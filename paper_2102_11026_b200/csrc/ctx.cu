@@ -20,6 +20,7 @@
 #include "sim_kernels.cuh"
 #include "solve_kernels.cuh"
 #include "lu_warp.cuh"
+#include "lu_split.cuh"
 #include "mlp_chain.cuh"
 #include "coupled_kernels.cuh"
 #include "gemm_ws.cuh"
@@ -101,6 +102,11 @@ struct nlrom_ctx {
   int rpc = 128, nchA = 0;
   int nchAa = 0, nphi = 0;     // k_assemble_a chunks (32 rows) when it also forms the vhp seed; partPhi chunks
   bool agemv = false;          // the last assemble_phase produced the vhp-chain seed partials
+  // split LU (lu_split.cuh): front n_p pivot steps on a side branch, back steps after the vhp
+  DBuf luF, luRd;
+  IBuf luPiv, luFlag;
+  int luFC = 0;
+  bool lu_front_done = false;
   int rpcM = 128, nchM = 0;  // row chunking of the mass block (finer: more CTAs for its Gram)
   int s_ctas = getenv("NLROM_S_CTAS") ? atoi(getenv("NLROM_S_CTAS")) : 1 << 20;  // side-branch S reduction CTAs
   DBuf a, partA, partPhi, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
@@ -507,7 +513,47 @@ bool early_wnet_ok(nlrom_ctx* c) {
 //   st2: wnet head -> tail (W) -> [wait K] k_cubature(stiffness) -> [wait M] k_reduce_S
 //   st3: [after the output layer] k_assemble_mass (M) -> [wait A] k_reduce_phi (P)
 //   (st2 and st3 joined before the LU)
-void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s) {
+// Opt-in (NLROM_LU_SPLIT=1): correct (tests, tools/probes/lu_split_probe.cu: 1.5e-14 vs the
+// one-shot LU) but slower at cfg2 so far -- the front (30 steps on 96 columns, ~990 cycles per
+// step) cannot start before S_base, which the stiffness Gram and its reduction deliver only ~10 us
+// before the vhp chain ends, so the side branch becomes the critical path (0.138 vs 0.129 ms).
+bool lu_split_ok(nlrom_ctx* c) {
+  static const bool on = getenv("NLROM_LU_SPLIT") != nullptr;
+  return on && !c->coupled && c->n <= 64 && c->n_p >= 1 && c->luFC > 0 && c->luFC <= 128 &&
+         c->n_q + 1 <= 64;
+}
+
+template <int NBC>
+void launch_front_t(nlrom_ctx* c) {
+  LuSplitArgs a{c->n, c->n_p, 0, c->luFC, (const double*)c->S.p, (const double*)c->phi.p, nullptr, c->luF.p,
+                c->luPiv.p, c->luRd.p, c->luFlag.p, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr};
+  launch(c, k_lu_front<NBC>, c->n_sims, 256, LuSplitPlan<NBC>::bytes(0), a);
+}
+
+void launch_lu_front(nlrom_ctx* c) {
+  const int nb = (c->luFC + 15) / 16;
+  if (nb <= 2) launch_front_t<2>(c);
+  else if (nb <= 4) launch_front_t<4>(c);
+  else if (nb <= 6) launch_front_t<6>(c);
+  else launch_front_t<8>(c);
+}
+
+template <int NBC>
+void launch_back_t(nlrom_ctx* c, bool apply) {
+  LuSplitArgs a{c->n, c->n_p, 0, c->luFC, nullptr, nullptr, nullptr, c->luF.p, c->luPiv.p, c->luRd.p, c->luFlag.p,
+                (const double*)c->Gt.p, c->ldGt, c->dr.p, c->r.p, apply ? 1 : 0, c->status.p, nullptr};
+  launch(c, k_lu_back<NBC>, c->n_sims, 256, LuSplitPlan<NBC>::bytes(c->n_q), a);
+}
+
+void launch_lu_back(nlrom_ctx* c, bool apply) {
+  const int nb = (c->n_q + 1 + 15) / 16;
+  if (nb <= 1) launch_back_t<1>(c, apply);
+  else if (nb <= 2) launch_back_t<2>(c, apply);
+  else if (nb <= 3) launch_back_t<3>(c, apply);
+  else launch_back_t<4>(c, apply);
+}
+
+void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s, bool front) {
   auto on = [&](cudaStream_t& other, auto fn) {
     std::swap(c->st, other);
     fn();
@@ -565,6 +611,11 @@ void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s) {
            (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
   });
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evP, 0));
+  if (front) {
+    // the first n_p pivot steps of the Newton solve need S_base and phi only (lu_split.cuh)
+    on(c->st2, [&] { launch_lu_front(c); });
+    c->lu_front_done = true;
+  }
   NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));
 }
 
@@ -576,8 +627,10 @@ bool split_phase_ok(nlrom_ctx* c) {
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   bool early_w = cfg.integration == 0 && early_wnet_ok(c) && fused_hidden_forward(c, cfg.dt, cfg.drop_fict);
+  c->lu_front_done = false;
   if (early_w && split_phase_ok(c)) {
-    phase_E_split(c, cfg, s);
+    // the LU front only in the one-graph Newton iteration (join_side = false: phase_J follows)
+    phase_E_split(c, cfg, s, !join_side && lu_split_ok(c));
     if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));
     return;
   }
@@ -754,6 +807,12 @@ bool fused_vhp_backward(nlrom_ctx* c, bool check_only) {
 void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 0, double* xout = nullptr,
                bool add_vhp = false) {
   const int n = c->n;
+  if (c->lu_front_done && nx == 0 && add_vhp) {
+    launch_lu_back(c, apply);  // the front ran on phase E's side branch
+    c->lu_front_done = false;
+    return;
+  }
+  c->lu_front_done = false;
   const double* Gt = add_vhp ? (const double*)c->Gt.p : nullptr;
   auto go = [&](auto kern) {
     launch(c, kern, c->n_sims, 256, lu_smem_bytes(n + nx, c->n_q), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
@@ -1103,6 +1162,13 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->a.alloc((size_t)S * N);
     c->partA.alloc((size_t)S * std::max(c->nchA, c->nchM) * n * n);
     c->nchAa = ceil_div(N, ASMA_GROWS);
+    if (n <= 64) {
+      c->luFC = n + 1 + c->n_q;
+      c->luF.alloc((size_t)S * n * c->luFC);
+      c->luRd.alloc((size_t)S * n);
+      c->luPiv.alloc((size_t)S * n);
+      c->luFlag.alloc(S);
+    }
     c->partPhi.alloc((size_t)S * std::max(c->nchA, c->nchAa) * n);
     c->phi.alloc((size_t)S * n);
     c->norm.alloc(S);
@@ -1137,6 +1203,14 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_head, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_front<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_front<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_front<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_front<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_back<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_back<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_back<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_back<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_warp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

@@ -329,6 +329,7 @@ np.savez(sys.argv[2], phi=phi, S=S, r=nxt.r)
     {"NLROM_ASYNC_CHAIN": "1", "NLROM_SEPARATE_GEMV": "1"},
     {"NLROM_LU_COLS": "1", "NLROM_MASS_LATE": "1"},
     {"NLROM_BWD_CFG": "1", "NLROM_NO_WS_GEMM": "1"},
+    {"NLROM_LU_SPLIT": "1"},
     {"NLROM_NO_FUSED_MLP": "1", "NLROM_LU_ROWS": "1"},
     {"NLROM_LU_WARP": "1", "NLROM_WNET_LATE": "1"},
 ])
