@@ -247,6 +247,15 @@ def batched_leg(args, rank, world):
     _, fp64 = peaks()
     stage_ms = s.bench_kernels(3, flush_l2=True)
     roof = decoder_roofline(P, stage_ms, ns, fp64)
+    cub_ms, cub_bytes = s.bench_cubature(5, flush_l2=True)
+    pk, _ = peaks()
+    hbm = pk.get("hbm_gbs")
+    cub_gbs = cub_bytes / (cub_ms * 1e-3) / 1e9
+    cub_roof = {"bound": "hbm", "kernel": "k_cubature (all %d local sims, |C| elements each)" % ns,
+                "achieved": cub_gbs, "peak": hbm, "unit": "GB/s", "frac": (cub_gbs / hbm) if hbm else None,
+                "traffic": None, "kernel_ms": cub_ms, "algorithmic_bytes_per_launch": cub_bytes,
+                "algorithmic_def": "SURVEY.md 8d B_cub = |C| (96 n + 200) + 8 (n + n^2) per sim",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "absent"}
     launches = s.launches_per_iteration()
     del s
     return {"workload": "cfg5: %d independent sims (10-layer w256 DAE, n_q=20, n_p=10, N=960, |C|=100), "
@@ -254,7 +263,7 @@ def batched_leg(args, rank, world):
             "scaling": "strong (total sims fixed)", "ms_per_iteration": ms,
             "sim_iterations_per_s": total * 1e3 / ms, "iterations": iters,
             "l2": "flushed between timed iterations", "decoder_roofline_rank0": roof,
-            "gpu_launches_per_iteration": launches}
+            "cubature_roofline_rank0": cub_roof, "gpu_launches_per_iteration": launches}
 
 
 # --------------------------------------------------------------------------- CPU arms

@@ -206,6 +206,12 @@ NLROM_API int nlrom_bench_iterations(nlrom_ctx* ctx, int n_iters, int flush_l2, 
  * ms4[3] LU solve. Used by bench.py to pick and time the dominant kernel. */
 NLROM_API int nlrom_bench_kernels(nlrom_ctx* ctx, int n_iters, int flush_l2, float* ms4);
 
+/* Device time of one cubature launch over the context's cubature set (weighted element forces,
+ * stiffness, reduced-force / reduced-stiffness partials) for all sims, L2 flushed before each
+ * launch, averaged over n_iters; *bytes = the algorithmic bytes of that launch (SURVEY.md 8d
+ * B_cub per sim x n_sims). bench.py reports *bytes / *ms against the HBM peak. */
+NLROM_API int nlrom_bench_cubature(nlrom_ctx* ctx, int n_iters, int flush_l2, float* ms, double* bytes);
+
 /* Number of kernel launches of one Newton iteration (for bench "gpu_launches"). */
 NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
 

@@ -50,7 +50,8 @@ struct CubSet {
   IBuf row_ids, row_ptr, entries;
   IBuf rowptr_full;  // (N + 1) CSR over all free-DOF rows (same entries), gathered by k_assemble_a
   int n_rows = 0;
-  int epc = 1, nchunk = 0;
+  int epc = 1, nchunk = 0;  // elements per chunk; partials per sim (CTAs along x)
+  int nech = 0, cpc = 1;     // element chunks; element chunks per CTA (nchunk = ceil(nech / cpc))
   DBuf fe_w, part_f, part_K, f;
 };
 
@@ -254,7 +255,18 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
   const int n = c->n;
   s.epc = epc;
   while (s.epc > 1 && (size_t)(2 * s.epc * 12 * gram_ld(n) + s.epc * 162) * 8 > 200 * 1024) s.epc /= 2;
-  s.nchunk = std::max(1, ceil_div(std::max(s.n, 1), s.epc));
+  s.nech = std::max(1, ceil_div(std::max(s.n, 1), s.epc));
+  // Many sims: a CTA walks several element chunks of its sim and accumulates the Gram in shared
+  // memory, so the partial K~ traffic (n^2 doubles per CTA, written and re-read by the
+  // reduction) shrinks by cpc; keep >= ~2 waves of 3 CTAs per SM.
+  s.cpc = 1;
+  if (c->n_sims > 1 && n <= 256 &&
+      (size_t)(2 * s.epc * 12 * gram_ld(n) + s.epc * 162 + n * n + n) * 8 <= 200 * 1024) {
+    const long long ctas = (long long)c->n_sims * s.nech;
+    s.cpc = (int)std::max(1LL, std::min<long long>(s.nech, ctas / (148 * 3 * 2)));
+    if (getenv("NLROM_CPC")) s.cpc = std::max(1, std::min(s.nech, atoi(getenv("NLROM_CPC"))));
+  }
+  s.nchunk = ceil_div(s.nech, s.cpc);
   s.fe_w.alloc((size_t)c->n_sims * std::max(s.n, 1) * 12);
   s.part_f.alloc((size_t)c->n_sims * s.nchunk * n);
   s.part_K.alloc((size_t)c->n_sims * s.nchunk * n * n);
@@ -414,11 +426,14 @@ void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true,
             part == 1 ? nullptr : c->Jt.p, c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p,
             s.part_K.p, s.nchunk, nullptr, nullptr};
   a.skip_fe = part == 2 ? 1 : 0;
+  a.cpc = part == 1 ? 1 : s.cpc;  // the force-only launch writes no partials: one chunk per CTA
   // early: the weight-net tail (the only producer) launches dependents only after its own wait,
   // so J~ / u are complete at launch; not when the output layer itself is a direct producer
   a.early = (weighted && early) ? 1 : 0;
-  size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162) * 8;
-  launch(c, k_cubature, dim3(s.nchunk, c->n_sims), 256, smem, a);
+  size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162 + (a.cpc > 1 ? c->n * c->n + c->n : 0)) * 8;
+  // many sims: 3 resident CTAs per SM (80 registers) when the shared memory allows it
+  const bool three = c->n_sims > 1 && smem <= 74 * 1024 && !getenv("NLROM_CUB_MINB2");
+  launch(c, three ? k_cubature<3> : k_cubature<2>, dim3(a.cpc > 1 ? s.nchunk : s.nech, c->n_sims), 256, smem, a);
   if (scatter)
   launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
          (const int*)s.row_ptr.p, (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N,
@@ -1194,7 +1209,8 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->ldGt = round_up(n_q, 2);
     c->Gt.alloc((size_t)S * 2 * n_q * c->ldGt);
     // kernel attributes for large dynamic shared memory
-    NL_CUDA(cudaFuncSetAttribute(k_cubature, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_cubature<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_cubature<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1702,6 +1718,41 @@ extern "C" int nlrom_bench_kernels(nlrom_ctx* c, int n_iters, int flush_l2, floa
   CTX_END(c)
 }
 
+// Device time of one cubature launch (the context's cubature set: weighted element forces,
+// element stiffness, G_e = w_e K_e J~_e and the J~_C^T G / J~_C^T f partials, the kernel of the
+// batched step), L2 flushed before each launch; *bytes = SURVEY.md 8d's algorithmic bytes
+// B_cub = |C| (96 n + 200) + 8 (n + n^2) per sim, times n_sims.
+extern "C" int nlrom_bench_cubature(nlrom_ctx* c, int n_iters, int flush_l2, float* ms, double* bytes) {
+  CTX_TRY(c)
+  if (c->graph_key.empty()) throw Error(NLROM_ERR_ARG, "run nlrom_step first (captures the graphs)");
+  if (flush_l2 && !c->flush.p) c->flush.alloc((size_t)32 << 20);
+  int integ = 0;
+  {
+    double dt;
+    int drop;
+    sscanf(c->graph_key.c_str(), "%lf|%d|%d", &dt, &drop, &integ);
+  }
+  CubSet& s = integ == 1 ? c->setAll : c->setC;
+  float acc = 0.f;
+  for (int i = 0; i < n_iters; ++i) {
+    if (flush_l2) {
+      k_flush<<<1184, 256, 0, c->st>>>(c->flush.p, c->flush.n, (double)i);
+      NL_CHECK_LAUNCH();
+    }
+    NL_CUDA(cudaEventRecord(c->ev0, c->st));
+    cubature_phase(c, s, integ == 0, false, false, 0);
+    NL_CUDA(cudaEventRecord(c->ev1, c->st));
+    NL_CUDA(cudaEventSynchronize(c->ev1));
+    float t = 0.f;
+    NL_CUDA(cudaEventElapsedTime(&t, c->ev0, c->ev1));
+    acc += t;
+  }
+  *ms = acc / std::max(1, n_iters);
+  const double n = c->n;
+  *bytes = (double)c->n_sims * ((double)s.n * (96.0 * n + 200.0) + 8.0 * (n + n * n));
+  CTX_END(c)
+}
+
 extern "C" int nlrom_launches_per_iteration(nlrom_ctx* c) { return c ? c->launches_E + c->launches_J : 0; }
 
 // Prefix-graph timing: for k = 1 .. n, capture the first k launches of one Newton iteration
@@ -1779,7 +1830,7 @@ extern "C" int nlrom_element_forces(nlrom_ctx* c, const double* u, int want_K, d
             c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p, s.part_K.p, s.nchunk,
             want_K ? Ke.p : nullptr, nullptr};
   size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162) * 8;
-  launch(c, k_cubature, dim3(s.nchunk, 1), 256, smem, a);
+  launch(c, k_cubature<2>, dim3(s.nech, 1), 256, smem, a);  // force-only: no partials
   launch(c, k_scatter_rows, grid1((long long)s.n_rows), 256, 0, (const int*)s.row_ids.p, (const int*)s.row_ptr.p,
          (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N, 1);
   d2h(c, f_int, s.f, c->N);
@@ -1802,7 +1853,7 @@ extern "C" int nlrom_element_reduced_forces(nlrom_ctx* c, const double* r, const
   CubArgs a{de.p, n_elems, c->elem_rows.p, c->Dm_inv.p, c->vol.p, nullptr, c->u.p, c->Jt.p,
             c->N, c->n, c->ldjt, c->mu, c->lam, epc, few.p, pf.p, pK.p, nch, nullptr, fo.p};
   size_t smem = (size_t)(2 * epc * 12 * gram_ld(c->n) + epc * 162) * 8;
-  launch(c, k_cubature, dim3(nch, 1), 256, smem, a);
+  launch(c, k_cubature<2>, dim3(nch, 1), 256, smem, a);
   d2h(c, out, fo, (size_t)n_elems * c->n);
   NL_CUDA(cudaStreamSynchronize(c->st));
   CTX_END(c)

@@ -417,6 +417,9 @@ struct CubArgs {
   double* fred_out;        // optional (E, n): per-element J~_e^T (w f_e)
   int early = 0;           // 1: the producer grid is the weight net (J~, u complete at launch)
   int skip_fe = 0;         // 1: do not write fe_w (a concurrent force-only launch owns it)
+  int cpc = 1;             // element chunks per CTA: the Gram accumulates in shared memory over
+                           // cpc chunks and each CTA writes ONE partial (nchunk = partials per
+                           // sim); > 1 only with J~ and without fred_out
 };
 
 __device__ __forceinline__ void mat3_mul(const double* A, const double* B, double* C) {
@@ -432,7 +435,8 @@ __device__ __forceinline__ void mat3_mul(const double* A, const double* B, doubl
 // f_e and the G_e rows afterwards (the Gram is linear in w_e). Safe because the producer
 // (k_wnet_tail*) issues launch_dependents only after its own wait, so the output layer that
 // wrote J~ and u has completed when this grid starts.
-__global__ void k_cubature(CubArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
   if (!a.early) pdl_wait();  // producer wrote J~ / u itself: wait before the gathers
   extern __shared__ double sh[];
   const int n = a.n;
@@ -442,13 +446,21 @@ __global__ void k_cubature(CubArgs a) {
   double* Gs = Js + (size_t)epc * 12 * ldp;  // [epc*12][ldp]  (w K J)
   double* Ks = Gs + (size_t)epc * 12 * ldp;  // [epc][12][12]
   double* Fs = Ks + (size_t)epc * 144;     // [epc][12]
-  const int chunk = blockIdx.x, sim = blockIdx.y;
+  const int sim = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const double* u = a.u + (size_t)sim * a.N;
   const double* Jt = a.Jt ? a.Jt + (size_t)sim * a.N * a.ldjt : nullptr;
+  int* Rw = reinterpret_cast<int*>(Fs + (size_t)epc * 12);  // [epc][12]
+  double* Kacc = reinterpret_cast<double*>(Rw + epc * 12);  // [n][n] + [n] (K~, f~ partials) when cpc > 1
+  __shared__ double wsh[64];
+  for (int ck = 0; ck < a.cpc; ++ck) {
+  const int chunk = blockIdx.x * a.cpc + ck;  // element chunk
+  if (ck > 0) {
+    if (chunk * epc >= a.n_elems) break;      // uniform over the CTA
+    __syncthreads();                          // the previous chunk's Gram read Js / Gs / Fs
+  }
 
   // stage the chunk's 12 DOF rows per element, then gather the J~ rows (independent loads)
-  int* Rw = reinterpret_cast<int*>(Fs + (size_t)epc * 12);  // [epc][12]
   for (int idx = threadIdx.x; idx < epc * 12; idx += blockDim.x) {
     const int ei = chunk * epc + idx / 12;
     int row = -1;
@@ -461,15 +473,23 @@ __global__ void k_cubature(CubArgs a) {
   __syncthreads();
   {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int rr = warp; Jt && rr < epc * 12; rr += nw) {  // warp per J~ row: no div / mod
-      const int row = Rw[rr];
-      double* dst = Js + rr * ldp;
-      if ((a.ldjt & 1) == 0 && (ldp & 1) == 0) {  // 16-byte chunks (both pitches even)
-        for (int j = 2 * lane; j < n; j += 64) {
+    if (Jt && (a.ldjt & 1) == 0 && (ldp & 1) == 0) {  // 16-byte chunks (both pitches even)
+      // n <= 32: a half-warp per J~ row (two rows per warp instruction), else a warp per row
+      const int half = n <= 32 ? 1 : 0;
+      const int sub = half ? lane >> 4 : 0, sl = half ? lane & 15 : lane, step = half ? 32 : 64;
+      for (int rr = (warp << half) + sub; rr < epc * 12; rr += nw << half) {
+        const int row = Rw[rr];
+        double* dst = Js + rr * ldp;
+        for (int j = 2 * sl; j < n; j += step) {
           if (row >= 0) cp_async16(dst + j, Jt + (size_t)row * a.ldjt + j, true);
           else dst[j] = dst[j + 1] = 0.0;
         }
-      } else {
+      }
+    } else
+    for (int rr = warp; Jt && rr < epc * 12; rr += nw) {  // warp per J~ row: no div / mod
+      const int row = Rw[rr];
+      double* dst = Js + rr * ldp;
+      {
         for (int j = lane; j < n; j += 32) {
           if (row >= 0) cp_async8(dst + j, Jt + (size_t)row * a.ldjt + j);
           else dst[j] = 0.0;
@@ -501,7 +521,7 @@ __global__ void k_cubature(CubArgs a) {
 #pragma unroll
     for (int l = 0; l < 9; ++l) Di[l] = a.Dm_inv[(size_t)e * 9 + l];
     const double V = a.vol[e];
-    const double we = 1.0;  // weights applied after the dependency wait
+    const double we = 1.0;  // weights applied after the dependency wait (row weights of the Gram)
     // G rows: g_i (i=1..3) = rows of Dm^-1, g_0 = -sum
     double G[12];
 #pragma unroll
@@ -537,17 +557,24 @@ __global__ void k_cubature(CubArgs a) {
     double P[9];
     mat3_mul(F, S, P);
     if (lane < 12) {
-      int i = lane / 3, aa = lane % 3;
-      double f = V * (P[aa * 3] * G[i * 3] + P[aa * 3 + 1] * G[i * 3 + 1] + P[aa * 3 + 2] * G[i * 3 + 2]);
+      const int i = lane / 3, aa = lane % 3;
+      // row i of G and row aa of P by selects (no dynamically indexed local arrays)
+      double gi[3], pa[3];
+#pragma unroll
+      for (int y = 0; y < 3; ++y) {
+        gi[y] = i == 0 ? G[y] : i == 1 ? G[3 + y] : i == 2 ? G[6 + y] : G[9 + y];
+        pa[y] = aa == 0 ? P[y] : aa == 1 ? P[3 + y] : P[6 + y];
+      }
+      double f = V * (pa[0] * gi[0] + pa[1] * gi[1] + pa[2] * gi[2]);
       Fs[el * 12 + lane] = we * f;
       if (!Jt && !a.Ke_out) continue;  // force-only launch: no element stiffness
-      // stiffness column for DOF (jv, d) = lane: dF_ab = delta_ad g_jv[b]
-      int jv = lane / 3, d = lane % 3;
+      // stiffness column for DOF (jv, d) = (i, aa) = lane: dF_ab = delta_ad g_jv[b]
+      const int d = aa;
       double dF[9];
 #pragma unroll
       for (int x = 0; x < 3; ++x)
 #pragma unroll
-        for (int y = 0; y < 3; ++y) dF[x * 3 + y] = (x == d) ? G[jv * 3 + y] : 0.0;
+        for (int y = 0; y < 3; ++y) dF[x * 3 + y] = (x == d) ? gi[y] : 0.0;
       double dE[9];
 #pragma unroll
       for (int x = 0; x < 3; ++x)
@@ -576,37 +603,26 @@ __global__ void k_cubature(CubArgs a) {
     }
   }
   __syncthreads();
-  // G_e = K_e J~_e (12 x n, unweighted): warp per (element, row), lanes over columns
-  if (Jt && !a.fred_out) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int rr = warp; rr < epc * 12; rr += nw) {
-      const int el = rr / 12;
-      const double* Kr = Ks + rr * 12;  // = el * 144 + (rr % 12) * 12
-      const double* Je = Js + (size_t)el * 12 * ldp;
-      double kr[12];
-#pragma unroll
-      for (int c = 0; c < 12; ++c) kr[c] = Kr[c];
-      for (int j = lane; j < n; j += 32) {
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < 12; ++c) acc = fma(kr[c], Je[c * ldp + j], acc);
-        Gs[rr * ldp + j] = acc;
-      }
-    }
-  }
+  // G_e = K_e J~_e (12 x n, unweighted) on the DMMA pipe
+  if (Jt && !a.fred_out) ke_j_dmma(Ks, Js, Gs, ldp, epc, n);
   // ---- the weight net's output is needed from here on
   pdl_wait();
   pdl_launch();
-  __shared__ double wsh[64];
   for (int el = threadIdx.x; el < epc; el += blockDim.x) {
     const int ei = chunk * epc + el;
     wsh[el] = (a.w && ei < a.n_elems) ? a.w[(size_t)sim * a.n_elems + ei] : 1.0;
   }
   __syncthreads();
+  const bool gram = Jt && !a.fred_out;
   for (int t = threadIdx.x; t < epc * 12; t += blockDim.x) {
     const int el = t / 12, ei = chunk * epc + el;
-    Fs[t] *= wsh[el];
-    if (ei < a.n_elems && !a.skip_fe) a.fe_w[((size_t)sim * a.n_elems + ei) * 12 + t % 12] = Fs[t];
+    const double f = Fs[t], v = f * wsh[el];
+    Fs[t] = v;
+    if (gram) {  // padding columns: n carries f_e, n + 1 the Gram's row weight w_e
+      Gs[t * ldp + n] = f;
+      Gs[t * ldp + n + 1] = wsh[el];
+    }
+    if (ei < a.n_elems && !a.skip_fe) a.fe_w[((size_t)sim * a.n_elems + ei) * 12 + t % 12] = v;
   }
   if (a.Ke_out)
     for (int t = threadIdx.x; t < epc * 144; t += blockDim.x) {
@@ -626,20 +642,22 @@ __global__ void k_cubature(CubArgs a) {
     }
     return;
   }
-  for (int t = threadIdx.x; t < epc * 12 * n; t += blockDim.x) {  // G_e rows scaled by w_e
-    const int rr = t / n, j = t % n;
-    Gs[rr * ldp + j] *= wsh[rr / 12];
-  }
   __syncthreads();
-  // partial K~ = J~_C^T (w K J~_C) over the chunk's rows on the DMMA pipe; partial f~ = J~_C^T (w f)
-  double* pK = a.part_K + ((size_t)sim * a.nchunk + chunk) * n * n;
+  // partial K~ = J~_C^T diag(w) (K J~_C) and f~ = J~_C^T diag(w) f over the chunk's rows, one
+  // row-weighted DMMA Gram
   const int R = epc * 12;
-  gram_dmma(Js, ldp, Gs, ldp, R, n, n, pK, n);
-  double* pf = a.part_f + ((size_t)sim * a.nchunk + chunk) * n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double acc = 0.0;
-    for (int rr = 0; rr < R; ++rr) acc = fma(Js[rr * ldp + i], Fs[rr], acc);
-    pf[i] = acc;
+  if (a.cpc == 1)
+    gram_dmma_kf(Js, ldp, Gs, ldp, R, n, a.part_K + ((size_t)sim * a.nchunk + blockIdx.x) * n * n, n,
+                 a.part_f + ((size_t)sim * a.nchunk + blockIdx.x) * n, false);
+  else
+    gram_dmma_kf(Js, ldp, Gs, ldp, R, n, Kacc, n, Kacc + n * n, ck > 0);  // warp-owned tiles: no race
+  }  // chunks of this CTA
+  if (a.cpc > 1) {
+    __syncthreads();
+    double* pK = a.part_K + ((size_t)sim * a.nchunk + blockIdx.x) * n * n;
+    double* pf = a.part_f + ((size_t)sim * a.nchunk + blockIdx.x) * n;
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) pK[t] = Kacc[t];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) pf[t] = Kacc[n * n + t];
   }
 }
 

@@ -215,6 +215,12 @@ class Session:
         self._chk(self._L.nlrom_bench_kernels(self._h, int(n_iters), int(flush_l2), out))
         return list(out)
 
+    def bench_cubature(self, n_iters, flush_l2=True):
+        """(device ms, algorithmic bytes) of one cubature launch over all sims."""
+        ms, by = C.c_float(), C.c_double()
+        self._chk(self._L.nlrom_bench_cubature(self._h, int(n_iters), int(flush_l2), C.byref(ms), C.byref(by)))
+        return ms.value, by.value
+
     def bench_prefix(self, n_iters=50, flush_l2=True, cap=64):
         """[(kernel name, marginal in-graph ms)] for the launches of one Newton iteration."""
         ms = (C.c_float * cap)()
