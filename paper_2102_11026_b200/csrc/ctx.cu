@@ -46,6 +46,8 @@ using CfgBig = GemmCfg<64, 128, 2, 4, 1, 16, 3>;
 
 struct CubSet {
   IBuf elems;
+  IBuf rows_g;       // (n, 12) DOF rows of the set's elements, gathered once (no id indirection)
+  DBuf Dm_g, vol_g;  // (n, 9) Dm^-1 and (n) volumes of the set's elements
   int n = 0;
   IBuf row_ids, row_ptr, entries;
   IBuf rowptr_full;  // (N + 1) CSR over all free-DOF rows (same entries), gathered by k_assemble_a
@@ -225,10 +227,24 @@ void choose_groups(int n_q, int width, bool batched, int& G, int& gps) {
   (void)width;
 }
 
+void upload(DBuf& d, const double* h, size_t n);
+
 void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std::vector<int>& rows_host,
-               int epc) {
+               int epc, const double* Dm_host, const double* vol_host) {
   s.n = (int)elems.size();
   s.elems.upload(elems.data(), elems.size());
+  {
+    std::vector<int> rg((size_t)std::max(s.n, 1) * 12, -1);
+    std::vector<double> dg((size_t)std::max(s.n, 1) * 9, 0.0), vg((size_t)std::max(s.n, 1), 0.0);
+    for (int i = 0; i < s.n; ++i) {
+      for (int l = 0; l < 12; ++l) rg[(size_t)i * 12 + l] = rows_host[(size_t)elems[i] * 12 + l];
+      for (int l = 0; l < 9; ++l) dg[(size_t)i * 9 + l] = Dm_host[(size_t)elems[i] * 9 + l];
+      vg[i] = vol_host[elems[i]];
+    }
+    s.rows_g.upload(rg.data(), rg.size());
+    upload(s.Dm_g, dg.data(), dg.size());
+    upload(s.vol_g, vg.data(), vg.size());
+  }
   // CSR: unique rows -> (element slot * 12 + l)
   std::map<int, std::vector<int>> m;
   for (int i = 0; i < s.n; ++i)
@@ -426,6 +442,9 @@ void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true,
             part == 1 ? nullptr : c->Jt.p, c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p,
             s.part_K.p, s.nchunk, nullptr, nullptr};
   a.skip_fe = part == 2 ? 1 : 0;
+  a.rows_g = s.rows_g.p;
+  a.Dm_g = s.Dm_g.p;
+  a.vol_g = s.vol_g.p;
   a.cpc = part == 1 ? 1 : s.cpc;  // the force-only launch writes no partials: one chunk per CTA
   // early: the weight-net tail (the only producer) launches dependents only after its own wait,
   // so J~ / u are complete at launch; not when the output layer itself is a direct producer
@@ -1086,9 +1105,11 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       // longer chunks win (12 elements per CTA: fewer K~ partials to reduce); the force-only launch
       // on the critical path keeps 2 per CTA (setCF)
       const bool split = getenv("NLROM_NO_SPLIT_E") == nullptr && !many;
-      build_set(c, c->setC, cub, rows, getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : (many ? 8 : split ? 12 : 2));
-      if (split) build_set(c, c->setCF, cub, rows, getenv("NLROM_EPCF") ? atoi(getenv("NLROM_EPCF")) : 6);
-      build_set(c, c->setAll, all, rows, 8);
+      build_set(c, c->setC, cub, rows, getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : (many ? 8 : split ? 12 : 2),
+                d->Dm_inv, d->vol);
+      if (split)
+        build_set(c, c->setCF, cub, rows, getenv("NLROM_EPCF") ? atoi(getenv("NLROM_EPCF")) : 6, d->Dm_inv, d->vol);
+      build_set(c, c->setAll, all, rows, 8, d->Dm_inv, d->vol);
     }
     // weight net (rows of the last layer restricted to C)
     {

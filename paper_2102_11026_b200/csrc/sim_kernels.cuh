@@ -417,6 +417,9 @@ struct CubArgs {
   double* fred_out;        // optional (E, n): per-element J~_e^T (w f_e)
   int early = 0;           // 1: the producer grid is the weight net (J~, u complete at launch)
   int skip_fe = 0;         // 1: do not write fe_w (a concurrent force-only launch owns it)
+  const int* rows_g = nullptr;     // optional (n_elems, 12) set-gathered DOF rows
+  const double* Dm_g = nullptr;    // optional (n_elems, 9) set-gathered Dm^-1
+  const double* vol_g = nullptr;   // optional (n_elems) set-gathered volumes
   int cpc = 1;             // element chunks per CTA: the Gram accumulates in shared memory over
                            // cpc chunks and each CTA writes ONE partial (nchunk = partials per
                            // sim); > 1 only with J~ and without fred_out
@@ -453,6 +456,8 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
   int* Rw = reinterpret_cast<int*>(Fs + (size_t)epc * 12);  // [epc][12]
   double* Kacc = reinterpret_cast<double*>(Rw + epc * 12);  // [n][n] + [n] (K~, f~ partials) when cpc > 1
   __shared__ double wsh[64];
+  const bool pref = a.rows_g != nullptr && epc * 12 <= (int)blockDim.x;
+  int nxt = -1;
   for (int ck = 0; ck < a.cpc; ++ck) {
   const int chunk = blockIdx.x * a.cpc + ck;  // element chunk
   if (ck > 0) {
@@ -460,7 +465,16 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     __syncthreads();                          // the previous chunk's Gram read Js / Gs / Fs
   }
 
-  // stage the chunk's 12 DOF rows per element, then gather the J~ rows (independent loads)
+  // stage the chunk's 12 DOF rows per element, then gather the J~ rows (independent loads).
+  // Set-gathered rows: held in a register one chunk ahead (loaded while the previous chunk
+  // computes), so a chunk starts without a global round trip.
+  if (pref) {
+    if (ck == 0 && threadIdx.x < epc * 12) {
+      const int ei = chunk * epc + threadIdx.x / 12;
+      nxt = ei < a.n_elems ? a.rows_g[(size_t)chunk * epc * 12 + threadIdx.x] : -1;
+    }
+    if (threadIdx.x < epc * 12) Rw[threadIdx.x] = nxt;
+  } else
   for (int idx = threadIdx.x; idx < epc * 12; idx += blockDim.x) {
     const int ei = chunk * epc + idx / 12;
     int row = -1;
@@ -497,6 +511,10 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
       }
     }
   }
+  if (pref && ck + 1 < a.cpc && threadIdx.x < epc * 12) {  // next chunk's rows, in flight during this one
+    const int ei = (chunk + 1) * epc + threadIdx.x / 12;
+    nxt = ei < a.n_elems ? a.rows_g[(size_t)(chunk + 1) * epc * 12 + threadIdx.x] : -1;
+  }
   cp_async_all_wait();
   // element physics, one warp per element
   for (int el = warp; el < epc; el += nw) {
@@ -508,7 +526,9 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
       }
       continue;
     }
-    int e = a.elems ? a.elems[ei] : ei;
+    const int e = a.Dm_g ? ei : (a.elems ? a.elems[ei] : ei);  // index into Dm / vol
+    const double* Dm = a.Dm_g ? a.Dm_g : a.Dm_inv;
+    const double* vl = a.vol_g ? a.vol_g : a.vol;
     double ue = 0.0;
     if (lane < 12) {
       const int row = Rw[el * 12 + lane];
@@ -519,8 +539,8 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     for (int l = 0; l < 12; ++l) uv[l] = __shfl_sync(0xffffffffu, ue, l);
     double Di[9];
 #pragma unroll
-    for (int l = 0; l < 9; ++l) Di[l] = a.Dm_inv[(size_t)e * 9 + l];
-    const double V = a.vol[e];
+    for (int l = 0; l < 9; ++l) Di[l] = Dm[(size_t)e * 9 + l];
+    const double V = vl[e];
     const double we = 1.0;  // weights applied after the dependency wait (row weights of the Gram)
     // G rows: g_i (i=1..3) = rows of Dm^-1, g_0 = -sum
     double G[12];
@@ -602,9 +622,6 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
       }
     }
   }
-  __syncthreads();
-  // G_e = K_e J~_e (12 x n, unweighted) on the DMMA pipe
-  if (Jt && !a.fred_out) ke_j_dmma(Ks, Js, Gs, ldp, epc, n);
   // ---- the weight net's output is needed from here on
   pdl_wait();
   pdl_launch();
@@ -612,16 +629,15 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     const int ei = chunk * epc + el;
     wsh[el] = (a.w && ei < a.n_elems) ? a.w[(size_t)sim * a.n_elems + ei] : 1.0;
   }
-  __syncthreads();
+  __syncthreads();  // physics done (Ks, Fs), weights staged
   const bool gram = Jt && !a.fred_out;
+  // G_e = w_e K_e J~_e (12 x n) on the DMMA pipe
+  if (gram) ke_j_dmma(Ks, Js, Gs, ldp, epc, n, wsh);
   for (int t = threadIdx.x; t < epc * 12; t += blockDim.x) {
     const int el = t / 12, ei = chunk * epc + el;
-    const double f = Fs[t], v = f * wsh[el];
+    const double v = Fs[t] * wsh[el];
     Fs[t] = v;
-    if (gram) {  // padding columns: n carries f_e, n + 1 the Gram's row weight w_e
-      Gs[t * ldp + n] = f;
-      Gs[t * ldp + n + 1] = wsh[el];
-    }
+    if (gram) Gs[t * ldp + n] = v;  // padding column n carries w f into the Gram
     if (ei < a.n_elems && !a.skip_fe) a.fe_w[((size_t)sim * a.n_elems + ei) * 12 + t % 12] = v;
   }
   if (a.Ke_out)
@@ -643,8 +659,7 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     return;
   }
   __syncthreads();
-  // partial K~ = J~_C^T diag(w) (K J~_C) and f~ = J~_C^T diag(w) f over the chunk's rows, one
-  // row-weighted DMMA Gram
+  // partial K~ = J~_C^T (w K J~_C) and f~ = J~_C^T (w f) over the chunk's rows, one DMMA Gram
   const int R = epc * 12;
   if (a.cpc == 1)
     gram_dmma_kf(Js, ldp, Gs, ldp, R, n, a.part_K + ((size_t)sim * a.nchunk + blockIdx.x) * n * n, n,
