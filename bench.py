@@ -256,6 +256,14 @@ def batched_leg(args, rank, world):
                 "traffic": None, "kernel_ms": cub_ms, "algorithmic_bytes_per_launch": cub_bytes,
                 "algorithmic_def": "SURVEY.md 8d B_cub = |C| (96 n + 200) + 8 (n + n^2) per sim",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "absent"}
+    # ~(24 n^2 + 312 n + 3000) flop per element: 10.7 flop/B at cfg5, above the
+    # fp64 ridge (37 TFLOP/s / 6.55 TB/s = 5.7 flop/B), so the fp64 pipe, not HBM, bounds it
+    n_c = P.cm.C.size if hasattr(P.cm.C, "size") else len(P.cm.C)
+    cub_flops = ns * n_c * (24.0 * n * n + 312.0 * n + 3000.0)
+    cub_roof["fp64_view"] = {"bound": "tensor", "achieved": cub_flops / (cub_ms * 1e-3) / 1e12, "peak": fp64,
+                             "unit": "TFLOP/s", "frac": (cub_flops / (cub_ms * 1e-3) / 1e12 / fp64) if fp64 else None,
+                             "algorithmic_flops_per_launch": cub_flops,
+                             "min_time_ms_at_fp64_peak": (cub_flops / (fp64 * 1e12) * 1e3) if fp64 else None}
     launches = s.launches_per_iteration()
     del s
     return {"workload": "cfg5: %d independent sims (10-layer w256 DAE, n_q=20, n_p=10, N=960, |C|=100), "

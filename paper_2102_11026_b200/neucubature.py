@@ -4,7 +4,8 @@
 elements); ``cubature_integrate`` runs the fused device kernel: wnet restricted to
 the rows of C, per-element StVK force / stiffness for e in C, projection by the
 element's 12 rows of J~ and the weighted sums.
-Selection-net / alternating training / greedy NNLS are offline.
+Selection net, alternating training and the greedy NNLS baseline (offline, SURVEY.md §8f
+rank 3) are in ``cubature_train`` and re-exported here under the SPEC names.
 """
 
 from __future__ import annotations
@@ -57,13 +58,10 @@ def select_topk(C, s, K):
     return np.asarray(C + add, dtype=np.int32)
 
 
-def train_alternating(*_a, **_k):
-    raise NotImplementedError("neural cubature training is offline (SURVEY.md §8f rank 3)")
-
-
-def greedy_cubature(*_a, **_k):
-    raise NotImplementedError("greedy NNLS cubature is offline (SURVEY.md §8f rank 3)")
-
-
-def snet_forward(*_a, **_k):
-    raise NotImplementedError("the GCN selection net is offline training (SURVEY.md §8f rank 3)")
+# Offline training and the greedy baseline live in cubature_train.py.
+def __getattr__(name):
+    if name in ("train_alternating", "greedy_cubature", "snet_forward", "nnls", "build_train_set",
+                "cubature_error", "CubatureTrainSet", "SelectionNet", "mesh_graph", "farthest_point_elements"):
+        from . import cubature_train
+        return getattr(cubature_train, name)
+    raise AttributeError(name)

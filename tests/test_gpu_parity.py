@@ -408,3 +408,22 @@ def test_stale_shared_memory(problem):
         for i, (ri, rbi, rdbi) in enumerate(states):
             ro, _, _, _ = ors.step(S, rbi, rdbi, P.f_ext, ocfg(cfg))
             assert np.abs(r1.reshape(ns, n)[i] - ro).max() <= 1e-10 * np.abs(ro).max(), (k, i)
+
+
+# ------------------------------------------------------------------ neural-cubature training set
+def test_build_train_set(cfg1):
+    """Per-element reduced forces of all elements at training poses (GPU k_cubature, per-element
+    projection) vs the oracle restatement."""
+    from oracle import cubature_train as oct_
+    from paper_2102_11026_b200 import cubature_train as ct
+    P, S = cfg1
+    rng = np.random.default_rng(11)
+    rs = rng.uniform(-0.3, 0.3, (3, P.cfg.n_p + P.cfg.n_q))
+    ts = ct.build_train_set(P.rm, P.model, rs)
+    f, F, u = oct_.train_arrays(S.model, S.rm, rs)
+    assert ts.F.shape == F.shape
+    for s in range(3):
+        assert rel(ts.F[s], F[s]) < 1e-11 and rel(ts.f[s], f[s]) < 1e-11 and rel(ts.u[s], u[s]) < 1e-12
+    C, w = ct.greedy_cubature(P.rm, P.model, ts, 10)
+    Co, wo = oct_.greedy(f, F, 10)
+    assert list(C) == list(Co) and np.allclose(w, wo, rtol=1e-7, atol=1e-10)
