@@ -212,6 +212,12 @@ NLROM_API int nlrom_bench_kernels(nlrom_ctx* ctx, int n_iters, int flush_l2, flo
  * B_cub per sim x n_sims). bench.py reports *bytes / *ms against the HBM peak. */
 NLROM_API int nlrom_bench_cubature(nlrom_ctx* ctx, int n_iters, int flush_l2, float* ms, double* bytes);
 
+/* Neural-cubature training set (Eq. 18): for each of n_poses
+ * poses rs (n_poses x n, row-major) the per-element reduced forces J~_e(r)^T f_e(u(r)) of ALL
+ * T elements into F_out (n_poses x T x n) and, if u_out != NULL, u(r) into u_out (n_poses x N).
+ * Replaces per-pose calls of elastic.element_reduced_force over all elements. */
+NLROM_API int nlrom_train_forces(nlrom_ctx* ctx, const double* rs, int n_poses, double* F_out, double* u_out);
+
 /* Number of kernel launches of one Newton iteration (for bench "gpu_launches"). */
 NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
 

@@ -25,7 +25,7 @@ EXPORTED = [
     "nlrom_system_jacobian", "nlrom_delta_j", "nlrom_fictitious_force", "nlrom_wnet_forward",
     "nlrom_cubature_integrate", "nlrom_full_displacement", "nlrom_jtilde", "nlrom_step", "nlrom_step_device",
     "nlrom_bench_iterations", "nlrom_launches_per_iteration", "nlrom_element_forces",
-    "nlrom_element_reduced_forces", "nlrom_bench_kernels", "nlrom_bench_cubature", "nlrom_stream", "nlrom_coupled_setup",
+    "nlrom_element_reduced_forces", "nlrom_bench_kernels", "nlrom_bench_cubature", "nlrom_train_forces", "nlrom_stream", "nlrom_coupled_setup",
     "nlrom_coupled_begin", "nlrom_coupled_eval", "nlrom_coupled_update", "nlrom_coupled_read",
     "nlrom_coupled_launches", "nlrom_bench_prefix", "nlrom_debug_poison_shared_memory",
     "nlrom_fs_create", "nlrom_fs_destroy", "nlrom_fs_last_error", "nlrom_fs_step", "nlrom_fs_energy_force",
@@ -116,6 +116,7 @@ def lib():
             "nlrom_launches_per_iteration": (C.c_int, [vp]),
             "nlrom_bench_kernels": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
             "nlrom_bench_cubature": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float), dp]),
+            "nlrom_train_forces": (C.c_int, [vp, dp, C.c_int, dp, dp]),
             "nlrom_element_forces": (C.c_int, [vp, dp, C.c_int, dp, dp]),
             "nlrom_element_reduced_forces": (C.c_int, [vp, dp, ip, C.c_int, dp]),
             "nlrom_stream": (C.c_int, [vp, C.POINTER(vp)]),

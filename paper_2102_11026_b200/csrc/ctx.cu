@@ -1880,6 +1880,31 @@ extern "C" int nlrom_element_reduced_forces(nlrom_ctx* c, const double* r, const
   CTX_END(c)
 }
 
+// Training-set builder: per-element reduced forces of ALL elements at
+// n_poses poses, buffers allocated once, one decoder bundle + one cubature launch per pose.
+extern "C" int nlrom_train_forces(nlrom_ctx* c, const double* rs, int n_poses, double* F_out, double* u_out) {
+  CTX_TRY(c)
+  if (n_poses <= 0) return NLROM_OK;
+  CubSet& s = c->setAll;
+  const int T = c->T, n = c->n, epc = s.epc, nch = ceil_div(T, epc);
+  DBuf few((size_t)T * 12), pf((size_t)nch * n), pK((size_t)nch * n * n), fo((size_t)T * n);
+  CubArgs a{nullptr, T, c->elem_rows.p, c->Dm_inv.p, c->vol.p, nullptr, c->u.p, c->Jt.p,
+            c->N, n, c->ldjt, c->mu, c->lam, epc, few.p, pf.p, pK.p, nch, nullptr, fo.p};
+  a.rows_g = s.rows_g.p;
+  a.Dm_g = s.Dm_g.p;
+  a.vol_g = s.vol_g.p;
+  const size_t smem = (size_t)(2 * epc * 12 * gram_ld(n) + epc * 162) * 8;
+  for (int k = 0; k < n_poses; ++k) {
+    const double* r = rs + (size_t)k * n;
+    bundle_only(c, r + c->n_p, nullptr, nullptr, 1.0, 0, r);
+    launch(c, k_cubature<2>, dim3(nch, 1), 256, smem, a);
+    d2h(c, F_out + (size_t)k * T * n, fo, (size_t)T * n);
+    if (u_out) d2h(c, u_out + (size_t)k * c->N, c->u, c->N);
+  }
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
 // =========================================================================== substructured scene
 // this context's sims are strings [lo, hi) of a scene of k_total strings
 // on a translating core; the host drives one Newton iteration as

@@ -58,13 +58,9 @@ class CubatureTrainSet:
 def build_train_set(rm, model, rs) -> CubatureTrainSet:
     """Per-element reduced forces of every element at every pose r_s, on the GPU (one decoder
     bundle + one cubature launch over all T elements per pose). f~(r_s) = sum_e f~_e(r_s)."""
-    from .daereduce import full_displacement
     from .session import session_for
     rs = np.atleast_2d(np.asarray(rs, dtype=np.float64))
-    s = session_for(rm, model)
-    all_e = np.arange(model.n_tets, dtype=np.int32)
-    F = np.stack([s.element_reduced_forces(r, all_e) for r in rs])
-    u = np.stack([full_displacement(rm, r) for r in rs])
+    F, u = session_for(rm, model).train_forces(rs)  # nlrom_train_forces
     return CubatureTrainSet(rs.copy(), F.sum(axis=1), F, u)
 
 
@@ -282,11 +278,14 @@ def _select_topk(C, s, K):
 
 def train_alternating(rm, model, ts: CubatureTrainSet, K: int = 5, rounds: int = 10, *, wnet=None,
                       snet: SelectionNet | None = None, n_init: int = 5, epochs: int = 15, lr: float = 1e-3,
-                      seed: int = 0, device=None, return_log: bool = False):
+                      seed: int = 0, device=None, return_log: bool = False, nnls_init: bool = True,
+                      new_row_scale: float = 1e-2):
     """Fig. 4: C <- farthest-point samples; per round train W for ``epochs`` on L_W, compute the
     residuals fbar (Eq. 18), train S for ``epochs`` on L_S (W frozen), add the K best-scoring
-    non-members (select_topk). Both nets warm-start across rounds (§6.3). Returns a
-    CubatureModel (C, trained wnet, snet, K) [and a TrainLog]."""
+    non-members (select_topk). Both nets warm-start across rounds (§6.3). With
+    ``nnls_init`` every newly added element's output starts at its fixed-weight NNLS value
+    (bias sqrt(w_e), weight row scaled by ``new_row_scale``). Returns a CubatureModel
+    (C, trained wnet, snet, K) [and a TrainLog]."""
     import torch
     from .densenet import make_wnet
     from .neucubature import CubatureModel
@@ -307,8 +306,11 @@ def train_alternating(rm, model, ts: CubatureTrainSet, K: int = 5, rounds: int =
     snet = snet or SelectionNet.init(seed)
     Sp = [torch.tensor(p, dtype=dt, device=dev, requires_grad=True) for p in snet.params()]
     U = torch.as_tensor(ts.u, dtype=dt, device=dev)
-    F = torch.as_tensor(ts.F, dtype=dt, device=dev)
-    f = torch.as_tensor(ts.f, dtype=dt, device=dev)
+    # losses on per-pose normalised forces (every pose weighs equally, as in the Table 2 metric)
+    fs = np.maximum(np.linalg.norm(ts.f, axis=1), 1e-300)
+    F = torch.as_tensor(ts.F / fs[:, None, None], dtype=dt, device=dev)
+    f = torch.as_tensor(ts.f / fs[:, None], dtype=dt, device=dev)
+    A_np, b_np = _stacked(ts)
     X = torch.as_tensor(vertex_displacements(graph, ts.u), dtype=dt, device=dev)
 
     def w_all():
@@ -332,7 +334,20 @@ def train_alternating(rm, model, ts: CubatureTrainSet, K: int = 5, rounds: int =
         a = torch.clamp((fbar * g).sum(1) / torch.clamp((g * g).sum(1), min=1e-300), min=0.0)
         return torch.linalg.norm(fbar - a[:, None] * g, dim=1).mean()
 
+    def seed_new(C, new):
+        """Newly added members start from the fixed-weight NNLS fit on C: output bias
+        sqrt(w_e), output row scaled by ``new_row_scale`` (W then learns the pose dependence)."""
+        if not nnls_init or not len(new):
+            return
+        w, _ = nnls(A_np[np.asarray(C)].T, b_np)
+        pos = {int(e): i for i, e in enumerate(C)}
+        with torch.no_grad():
+            for e in new:
+                bp[-1][int(e)] = float(np.sqrt(w[pos[int(e)]]))
+                Wp[-1][int(e)] *= new_row_scale
+
     C = farthest_point_elements(model, n_init, seed)
+    seed_new(C, list(C))
     log = TrainLog()
     optW = torch.optim.Adam(Wp + bp, lr=lr)
     optS = torch.optim.Adam(Sp, lr=lr)
@@ -360,7 +375,9 @@ def train_alternating(rm, model, ts: CubatureTrainSet, K: int = 5, rounds: int =
         with torch.no_grad():
             log.loss_s.append(float(loss_s(fbar)))
             s_mean = _snet_torch(torch, graph, Sp, X).mean(0).cpu().numpy()
+        C_old = set(int(e) for e in C)
         C = _select_topk(C, s_mean, K)
+        seed_new(C, [e for e in C if int(e) not in C_old])
         log.sizes.append(int(len(C)))
     Ws = [W.detach().cpu().numpy() for W in Wp]
     bs = [b.detach().cpu().numpy() for b in bp]

@@ -166,6 +166,15 @@ class Session:
                                                        _lib.dptr(out)))
         return out
 
+    def train_forces(self, rs):
+        """(F (S, T, n), u (S, N)): per-element reduced forces of all elements at poses rs."""
+        rs = np.ascontiguousarray(np.atleast_2d(rs), dtype=np.float64)
+        S = rs.shape[0]
+        F = np.empty((S, self.T, self.n))
+        u = np.empty((S, self.N))
+        self._chk(self._L.nlrom_train_forces(self._h, _lib.dptr(rs), S, _lib.dptr(F), _lib.dptr(u)))
+        return F, u
+
     # ------------------------------------------------------------------ rdsim
     def _state(self, r_bar, rdot_bar, f_ext):
         S = self.n_sims

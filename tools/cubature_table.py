@@ -22,8 +22,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", default="cfg1")
-    ap.add_argument("--train", type=int, default=40)
-    ap.add_argument("--test", type=int, default=20)
+    ap.add_argument("--train", type=int, default=200)
+    ap.add_argument("--test", type=int, default=50)
     ap.add_argument("--sizes", type=int, nargs="+", default=[10, 20, 50])
     ap.add_argument("--K", type=int, nargs="+", default=[5, 10])
     ap.add_argument("--epochs", type=int, default=15)
