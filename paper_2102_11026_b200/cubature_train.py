@@ -279,6 +279,7 @@ def _select_topk(C, s, K):
 def train_alternating(rm, model, ts: CubatureTrainSet, K: int = 5, rounds: int = 10, *, wnet=None,
                       snet: SelectionNet | None = None, n_init: int = 5, epochs: int = 15, lr: float = 1e-3,
                       seed: int = 0, device=None, return_log: bool = False, nnls_init: bool = True,
+                      epochs_s: int | None = None,
                       new_row_scale: float = 1e-2):
     """Fig. 4: C <- farthest-point samples; per round train W for ``epochs`` on L_W, compute the
     residuals fbar (Eq. 18), train S for ``epochs`` on L_S (W frozen), add the K best-scoring
@@ -365,7 +366,7 @@ def train_alternating(rm, model, ts: CubatureTrainSet, K: int = 5, rounds: int =
             fbar = f - torch.einsum("st,stn->sn", wC, F)
             log.loss_w.append(float(Lw))
             log.errors.append(float((torch.linalg.norm(fbar, dim=1) / torch.linalg.norm(f, dim=1)).mean()))
-        for _ in range(epochs):
+        for _ in range(epochs if epochs_s is None else epochs_s):
             optS.zero_grad()
             L = loss_s(fbar)
             if not torch.isfinite(L):
