@@ -219,15 +219,19 @@ def test_trajectory_100_steps(cfg1, integ):
 
 
 # ------------------------------------------------------------------ independent sims in one context
-@pytest.mark.parametrize("batched", [False, True])
+@pytest.mark.parametrize("batched", [False, True, "cpc"])
 def test_multi_sim(cfg1, batched, monkeypatch):
     """n_sims independent simulations through one context == the single-sim oracle per sim.
-    batched=True forces the big-tile per-layer GEMM path used for thousands of sims (cfg5)."""
+    batched=True forces the big-tile per-layer GEMM path used for thousands of sims (cfg5);
+    "cpc" additionally makes each cubature CTA walk 4 element chunks of its sim (shared-memory
+    Gram accumulation, prefetched rows, the 3-CTA/SM kernel) as at cfg5 scale."""
     from paper_2102_11026_b200 import rdsim
     from paper_2102_11026_b200.session import Session
     P, S = cfg1
     if batched:
         monkeypatch.setenv("NLROM_BATCHED", "1")
+    if batched == "cpc":
+        monkeypatch.setenv("NLROM_CPC", "4")
     ns = 3
     sess = Session(P.rm, P.model, P.cm, n_sims=ns)
     sess._ncub_cache = len(P.cm.C)
