@@ -251,9 +251,16 @@ def batched_leg(args, rank, world):
     pk, _ = peaks()
     hbm = pk.get("hbm_gbs")
     cub_gbs = cub_bytes / (cub_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        if ns == 4096:  # the captured configuration
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "dominant_traffic.json")))[
+                "k_cubature_cfg5"]["dram_bytes_per_launch"]
+    except Exception:
+        pass
     cub_roof = {"bound": "hbm", "kernel": "k_cubature (all %d local sims, |C| elements each)" % ns,
                 "achieved": cub_gbs, "peak": hbm, "unit": "GB/s", "frac": (cub_gbs / hbm) if hbm else None,
-                "traffic": None, "kernel_ms": cub_ms, "algorithmic_bytes_per_launch": cub_bytes,
+                "traffic": traffic, "kernel_ms": cub_ms, "algorithmic_bytes_per_launch": cub_bytes,
                 "algorithmic_def": "SURVEY.md 8d B_cub = |C| (96 n + 200) + 8 (n + n^2) per sim",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "absent"}
     # ~(24 n^2 + 312 n + 3000) flop per element: 10.7 flop/B at cfg5, above the
