@@ -699,8 +699,9 @@ void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
 }
 
 // vhp backward: dual (NS = 2) passes, cache written by the bundle forward.
+// dcache: the caches hold sin'(z) as duals (the fused bundle's forward), not z.
 void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int npass_per_sim, std::vector<DBuf>& caches,
-                      std::vector<int>& ldcs, DBuf& D0, DBuf& D1, DBuf& Gout, int ldG) {
+                      std::vector<int>& ldcs, DBuf& D0, DBuf& D1, DBuf& Gout, int ldG, bool dcache = false) {
   const int ncols = c->n_sims * npass_per_sim * NS;
   const int M = c->wL1 + c->next;
   if (c->batched && c->AlastT.p && !c->next) {
@@ -720,6 +721,9 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
     if (mc)
       launch(c, k_bwd_delta<2, 1>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->next, (const double*)c->AT.p,
              (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
+    else if (dcache)
+      launch(c, k_bwd_delta<2, 2>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->next, (const double*)c->AT.p,
+             (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
     else
       launch(c, k_bwd_delta<2, 0>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->next, (const double*)c->AT.p,
              (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
@@ -734,6 +738,10 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
     GemmArgs g{c->WT[l].p, cur->p, c->ldWT[l], ldcs[l], c->widths[l], ncols, c->widths[l + 1], 0, 0};
     if (NS == 2) {
       if (mc) launch_gemm<CfgBwd>(g, EpiBwdAct<2, ACT_SIN_MC>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
+      else if (dcache && c->batched)
+        launch_gemm<CfgBig>(g, EpiBwdAct<2, ACT_DSIN_MD>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
+      else if (dcache)
+        launch_gemm<CfgBwd>(g, EpiBwdAct<2, ACT_DSIN_MD>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
       else if (c->batched) launch_gemm<CfgBig>(g, EpiBwdAct<2, ACT_SIN_MD>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
       else launch_gemm<CfgBwd>(g, EpiBwdAct<2, ACT_SIN_MD>{nxt->p, ldcs[l - 1], 0, caches[l - 1].p}, c->st);
     } else {
@@ -885,7 +893,7 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
 void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply, const double* xrhs = nullptr, int nx = 0,
              double* xout = nullptr, bool side_open = false) {
   if (!fused_vhp_backward(c, false))
-    decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
+    decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt, true);
   if (side_open) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));  // S_base, phi from phase E's branch
   launch_lu(c, apply, xrhs, nx, xout, true);  // S = S_base + diag(0, vhp) while staging
 }
@@ -1710,7 +1718,7 @@ extern "C" int nlrom_bench_kernels(nlrom_ctx* c, int n_iters, int flush_l2, floa
       case 1: output_layer(c); break;
       case 2:
         if (!fused_vhp_backward(c, false))
-          decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt);
+          decoder_backward(c, c->a.p, 2, false, c->n_q, c->cache, c->ldc, c->Delta0, c->Delta1, c->Gt, c->ldGt, true);
         break;
       default: {
         const int n = c->n;

@@ -5,7 +5,7 @@
 
 namespace nlrom {
 
-enum ActKind { ACT_NONE = 0, ACT_SIN_MC = 1, ACT_SIN_MD = 2, ACT_SQUARE_MC = 3 };
+enum ActKind { ACT_NONE = 0, ACT_SIN_MC = 1, ACT_SIN_MD = 2, ACT_SQUARE_MC = 3, ACT_DSIN_MD = 4 };
 
 // Activation over passes of N = 2^order adjacent slot columns.
 //  ACT_SIN_MC    : true multicomplex sin (mcx.py:63-100)
@@ -84,6 +84,9 @@ struct EpiBwdAct {
         mc_sincos<N>(z, sn, f);
       } else if constexpr (ACT == ACT_SIN_MD) {
         md_sincos<N>(z, nullptr, f);
+      } else if constexpr (ACT == ACT_DSIN_MD) {  // the bundle cache already holds sin'(z) as a dual
+#pragma unroll
+        for (int s = 0; s < N; ++s) f[s] = z[s];
       } else if constexpr (ACT == ACT_SQUARE_MC) {
 #pragma unroll
         for (int s = 0; s < N; ++s) f[s] = 2.0 * z[s];
@@ -91,7 +94,7 @@ struct EpiBwdAct {
 #pragma unroll
         for (int s = 0; s < N; ++s) f[s] = (s == 0) ? 1.0 : 0.0;
       }
-      if constexpr (ACT == ACT_SIN_MD) md_mul<N>(d, f, o); else mc_mul<N>(d, f, o);
+      if constexpr (ACT == ACT_SIN_MD || ACT == ACT_DSIN_MD) md_mul<N>(d, f, o); else mc_mul<N>(d, f, o);
 #pragma unroll
       for (int s = 0; s < N; ++s) Yz[(size_t)(cbase + s) * ldy + m] = o[s];
     }
@@ -151,9 +154,9 @@ struct EpiJet {
         const size_t col = compact ? (size_t)(sim * cs + 4 + 4 * kg) : (size_t)(cg + 4 + 4 * k);
 #pragma unroll
         for (int s = 0; s < 4; ++s) Yz[(col + s) * ldy + m] = yo[s];
-        if (Cz && kg < n_q) {
-          Cz[(size_t)(2 * kg) * ldcache + m] = z[0];
-          Cz[(size_t)(2 * kg + 1) * ldcache + m] = y[0];
+        if (Cz && kg < n_q) {  // sin'(z0 + y0 e) = cos z0 - sin z0 y0 e (dual), for the vhp backward
+          Cz[(size_t)(2 * kg) * ldcache + m] = jc.c1;
+          Cz[(size_t)(2 * kg + 1) * ldcache + m] = jc.ns * y[0];
         }
       }
     }

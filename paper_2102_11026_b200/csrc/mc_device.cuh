@@ -119,6 +119,7 @@ __device__ __forceinline__ void md_sincos(const double* z, double* s, double* c)
 // sin(z + t y) = sin z + t cos(z) y.
 struct JetCos {
   double c1, cs, css, cr;  // cos(z) coefficients
+  double ns;               // -sin(z0)
 };
 
 __device__ __forceinline__ void jet_sin_base(const double z[4], double out[4], JetCos& jc) {
@@ -129,6 +130,7 @@ __device__ __forceinline__ void jet_sin_base(const double z[4], double out[4], J
   out[2] = C0 * z[2] - 0.5 * S0 * z[1] * z[1];
   out[3] = C0 * z[3];
   jc.c1 = C0;
+  jc.ns = -S0;
   jc.cs = -S0 * z[1];
   jc.css = -S0 * z[2] - 0.5 * C0 * z[1] * z[1];
   jc.cr = -S0 * z[3];

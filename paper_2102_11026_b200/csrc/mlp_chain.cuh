@@ -199,8 +199,8 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
         for (int s = 0; s < 4; ++s) y[s] = Ys[(4 + 4 * k + s) * (R + 1) + rr];
         if (kg < a.n_q) {
           double* Cz = a.cache[l] + (size_t)sim * 2 * a.n_q * a.ldc;
-          Cz[(size_t)(2 * kg) * a.ldc + m] = z[0];
-          Cz[(size_t)(2 * kg + 1) * a.ldc + m] = y[0];
+          Cz[(size_t)(2 * kg) * a.ldc + m] = jc.c1;  // sin'(z) as a dual: cos z0, -sin z0 y0
+          Cz[(size_t)(2 * kg + 1) * a.ldc + m] = jc.ns * y[0];
         }
         jet_tangent(jc, y, o);
         col = 4 + 4 * k;
@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd_async(MlpFwdArgs a) {
         for (int s4 = 0; s4 < 4; ++s4) y[s4] = Ys[(4 + 4 * k + s4) * (R + 1) + rr];
         if (kg < a.n_q) {
           double* Cz = a.cache[l] + (size_t)sim * 2 * a.n_q * a.ldc;
-          Cz[(size_t)(2 * kg) * a.ldc + m] = z[0];
-          Cz[(size_t)(2 * kg + 1) * a.ldc + m] = y[0];
+          Cz[(size_t)(2 * kg) * a.ldc + m] = jc.c1;  // sin'(z) as a dual: cos z0, -sin z0 y0
+          Cz[(size_t)(2 * kg + 1) * a.ldc + m] = jc.ns * y[0];
         }
         jet_tangent(jc, y, o);
         col = 4 + 4 * k;
@@ -597,12 +597,11 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
         d0 = ysum(2 * j, rr);
         d1 = ysum(2 * j + 1, rr);
       }
-      const double z0 = Z[rr * G + 2 * j], z1 = Z[rr * G + 2 * j + 1];
-      double sn, cs;
-      sincos(z0, &sn, &cs);
-      // dual cos(z0 + z1 e) = cos z0 - sin z0 z1 e ; (d0 + d1 e)(f0 + f1 e) = d0 f0 + (d0 f1 + d1 f0) e
-      Os[rr * LDX + 2 * j] = d0 * cs;
-      Os[rr * LDX + 2 * j + 1] = fma(d0, -sn * z1, d1 * cs);
+      // the cache holds sin'(z) = cos(z0 + z1 e) = f0 + f1 e (formed by the forward's epilogue);
+      // (d0 + d1 e)(f0 + f1 e) = d0 f0 + (d0 f1 + d1 f0) e
+      const double f0 = Z[rr * G + 2 * j], f1 = Z[rr * G + 2 * j + 1];
+      Os[rr * LDX + 2 * j] = d0 * f0;
+      Os[rr * LDX + 2 * j + 1] = fma(d0, f1, d1 * f0);
     }
     __syncthreads();
     BWD_MARK(s, 3);

@@ -877,7 +877,8 @@ __global__ void k_reduce_cols(const double* __restrict__ part, int nchunk, int M
 
 // g = y[:w] + A_T^T y[w:]  (A_T = U^T W_L: the filter's adjoint folded into the last layer),
 // Delta[p*NS + s][i] = (g_i * act'(z_{L-1}))[s] in the arithmetic of the passes
-// (NS = 1 real; 2 dual (MC = 0) or complex (MC = 1)). grid (ceil(w/32), n_sims), block 256.
+// (NS = 1 real; 2 dual (MC = 0) or complex (MC = 1)); MC = 2: z already holds act'(z) as a dual
+// (the fused bundle's cache). grid (ceil(w/32), n_sims), block 256.
 template <int NS, int MC>
 __global__ void k_bwd_delta(const double* __restrict__ y, int w, int n_p, const double* __restrict__ AT,
                             const double* __restrict__ zc, int ldz, int npass, double* __restrict__ Delta) {
@@ -915,8 +916,14 @@ __global__ void k_bwd_delta(const double* __restrict__ y, int w, int n_p, const 
     double z[NS], f[NS], s[NS];
 #pragma unroll
     for (int q = 0; q < NS; ++q) z[q] = Z[(size_t)(p * NS + q) * ldz + i];
-    if (MC) mc_sincos<NS>(z, s, f);
-    else md_sincos<NS>(z, s, f);
+    if (MC == 2) {  // bundle cache: sin'(z) already formed by the forward
+#pragma unroll
+      for (int q = 0; q < NS; ++q) f[q] = z[q];
+    } else if (MC) {
+      mc_sincos<NS>(z, s, f);
+    } else {
+      md_sincos<NS>(z, s, f);
+    }
 #pragma unroll
     for (int q = 0; q < NS; ++q) D[(size_t)(p * NS + q) * ldz + i] = g[il] * f[q];
   }
