@@ -375,9 +375,10 @@ bool fused_hidden_forward(nlrom_ctx* c, double dt, int drop_fict) {
   return false;
 }
 
-void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
+// with_output = false: hidden layers only (stage timing of nlrom_bench_kernels).
+void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = true) {
   if (fused_hidden_forward(c, dt, drop_fict)) {
-    output_layer(c);
+    if (with_output) output_layer(c);
     return;
   }
   const int ncols = c->n_sims * c->Cb;
@@ -401,7 +402,7 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict) {
     EpiStore e{c->H[c->L - 2].p + c->wL1, c->ldlast, 0, nullptr, 1, nullptr};
     hid_gemm(c->G, g, e, c->st);
   }
-  output_layer(c);
+  if (with_output) output_layer(c);
 }
 
 void wnet_phase(nlrom_ctx* c) {
@@ -705,9 +706,27 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
   const int ncols = c->n_sims * npass_per_sim * NS;
   const int M = c->wL1 + c->next;
   if (c->batched && c->AlastT.p && !c->next) {
-    // y (n_sims x w) = a (n_sims x N) (P W_L): one GEMM for all sims
-    GemmArgs g{c->AlastT.p, a_vec, c->ldAT, c->N, M, c->n_sims, c->N, 0, 0};
-    launch_gemm<CfgBig>(g, EpiStore{c->ybuf.p, M, 0, nullptr, 1, nullptr}, c->st);
+    // y (n_sims x w) = a (n_sims x N) (P W_L): one GEMM for all sims. Few output tiles (K = N
+    // long): split K over blockIdx.z into [sim][split][M] partials, then a fixed-order reduction.
+    const int tiles = ceil_div(M, CfgBig::BM) * ceil_div(c->n_sims, CfgBig::BN);
+    int split = 1;
+    for (int sp : {16, 12, 10, 8, 6, 5, 4, 3, 2})
+      if (tiles * sp <= 2 * 148 * 2 && c->N % sp == 0 && (c->N / sp) % 2 == 0 && c->N / sp >= 64 &&
+          (size_t)c->n_sims * sp * M <= c->bpart.n) {
+        split = sp;
+        break;
+      }
+    if (tiles >= 148 || getenv("NLROM_NO_SPLITK")) split = 1;
+    if (split == 1) {
+      GemmArgs g{c->AlastT.p, a_vec, c->ldAT, c->N, M, c->n_sims, c->N, 0, 0};
+      launch_gemm<CfgBig>(g, EpiStore{c->ybuf.p, M, 0, nullptr, 1, nullptr}, c->st);
+    } else {
+      const int Kc = c->N / split;
+      GemmArgs g{c->AlastT.p, a_vec, c->ldAT, c->N, M, c->n_sims, Kc, Kc, Kc};
+      launch_gemm<CfgBig>(g, EpiStore{c->bpart.p, split * M, M, nullptr, 1, nullptr}, c->st, split);
+      launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->bpart.p, split, M,
+             c->ybuf.p);
+    }
     ++gemm_launch_count;
   } else {
     launch(c, k_gemv_t, dim3(c->bnch, c->n_sims), 128, 0, (const double*)c->Alast.p, c->ldlast, M, a_vec, c->N,
@@ -1713,7 +1732,7 @@ extern "C" int nlrom_bench_kernels(nlrom_ctx* c, int n_iters, int flush_l2, floa
   auto stage = [&](int which) {
     switch (which) {
       case 0:
-        if (!fused_hidden_forward(c, dt, 0)) bundle_forward(c, dt, 0);
+        if (!fused_hidden_forward(c, dt, 0)) bundle_forward(c, dt, 0, false);  // hidden layers only
         break;
       case 1: output_layer(c); break;
       case 2:

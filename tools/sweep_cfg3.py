@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--nq", type=int, nargs="+", default=[5, 10, 20, 30, 48, 64])
     ap.add_argument("--depth", type=int, nargs="+", default=[4, 8, 12, 16])
     ap.add_argument("--iters", type=int, default=100)
+    ap.add_argument("--sims", type=int, default=1, help="independent sims per context (throughput mode)")
     args = ap.parse_args()
     from paper_2102_11026_b200.problem import build_problem
     from paper_2102_11026_b200 import rdsim
@@ -27,19 +28,25 @@ def main():
     for L in args.depth:
         for nq in args.nq:
             P = build_problem("cfg2", n_q=nq, n_fc=L)
-            s = Session(P.rm, P.model, P.cm)
-            r, rb, rdb = P.random_state()
-            s.step(rb, rdb, P.f_ext, rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=1))
+            ns = args.sims
+            s = Session(P.rm, P.model, P.cm, n_sims=ns)
+            st_ = [P.random_state(seed=4 + i) for i in range(ns)]
+            import numpy as np
+            rb = np.concatenate([x[1] for x in st_]) * (0.1 if ns > 1 else 1.0)
+            rdb = np.concatenate([x[2] for x in st_]) * (0.1 if ns > 1 else 1.0)
+            s.step(rb, rdb, np.tile(P.f_ext, ns), rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=1))
             s.bench_iterations(5)
             tot, _ = s.bench_iterations(args.iters)
             st = s.bench_kernels(max(10, args.iters // 4))
-            roof = bench.decoder_roofline(P, st, 1, fp64)
-            print(json.dumps({"n_q": nq, "depth": L, "ms_per_iteration": tot / args.iters,
+            roof = bench.decoder_roofline(P, st, ns, fp64)
+            print(json.dumps({"n_q": nq, "depth": L, "n_sims": ns, "ms_per_iteration": tot / args.iters,
+                              "sim_iterations_per_s": ns * 1e3 / (tot / args.iters),
                               "hz_3_iters": 1000.0 / (3 * tot / args.iters),
                               "decoder_ms": roof["kernel_ms"], "lu_ms": st[3],
                               "F_dec_gflop": roof["algorithmic_flops_per_launch"] / 1e9,
                               "decoder_tflops_alg": roof["achieved"], "frac_alg": roof["frac"],
-                              "executed_frac": roof["executed_frac"], "launches": s.launches_per_iteration()}),
+                              "executed_frac": roof["executed_frac"], "executed_tflops": roof["executed_tflops"],
+                              "stages_ms": roof["stages_ms"], "launches": s.launches_per_iteration()}),
                   flush=True)
             del s
 
