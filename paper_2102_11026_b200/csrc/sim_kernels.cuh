@@ -516,31 +516,29 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     nxt = ei < a.n_elems ? a.rows_g[(size_t)(chunk + 1) * epc * 12 + threadIdx.x] : -1;
   }
   cp_async_all_wait();
-  // element physics, one warp per element
-  for (int el = warp; el < epc; el += nw) {
-    int ei = chunk * epc + el;
-    if (ei >= a.n_elems) {
-      if (lane < 12) {
-        Fs[el * 12 + lane] = 0.0;
-        for (int r = 0; r < 12; ++r) Ks[el * 144 + r * 12 + lane] = 0.0;
-      }
-      continue;
-    }
-    const int e = a.Dm_g ? ei : (a.elems ? a.elems[ei] : ei);  // index into Dm / vol
+  // element physics: two elements per warp (one per half-warp; lanes 0..11 of a half own the
+  // element's 12 DOFs). A padding element (past the set) gets V = 0 and Dm^-1 = 0, so its force
+  // and stiffness come out exactly zero without divergent control flow around the shuffles.
+  const int hw = lane >> 4, hl = lane & 15;
+  for (int el0 = 2 * warp; el0 < epc; el0 += 2 * nw) {
+    const int el = el0 + hw;
+    const int ei = chunk * epc + el;
+    const bool valid = el < epc && ei < a.n_elems;
+    const int e = !valid ? 0 : a.Dm_g ? ei : (a.elems ? a.elems[ei] : ei);  // index into Dm / vol
     const double* Dm = a.Dm_g ? a.Dm_g : a.Dm_inv;
     const double* vl = a.vol_g ? a.vol_g : a.vol;
     double ue = 0.0;
-    if (lane < 12) {
-      const int row = Rw[el * 12 + lane];
+    if (valid && hl < 12) {
+      const int row = Rw[el * 12 + hl];
       ue = row >= 0 ? u[row] : 0.0;
     }
     double uv[12];
 #pragma unroll
-    for (int l = 0; l < 12; ++l) uv[l] = __shfl_sync(0xffffffffu, ue, l);
+    for (int l = 0; l < 12; ++l) uv[l] = __shfl_sync(0xffffffffu, ue, l, 16);
     double Di[9];
 #pragma unroll
-    for (int l = 0; l < 9; ++l) Di[l] = Dm[(size_t)e * 9 + l];
-    const double V = vl[e];
+    for (int l = 0; l < 9; ++l) Di[l] = valid ? Dm[(size_t)e * 9 + l] : 0.0;
+    const double V = valid ? vl[e] : 0.0;
     const double we = 1.0;  // weights applied after the dependency wait (row weights of the Gram)
     // G rows: g_i (i=1..3) = rows of Dm^-1, g_0 = -sum
     double G[12];
@@ -576,8 +574,8 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     S[8] += a.lam * trE;
     double P[9];
     mat3_mul(F, S, P);
-    if (lane < 12) {
-      const int i = lane / 3, aa = lane % 3;
+    if (hl < 12 && el < epc) {
+      const int i = hl / 3, aa = hl % 3;
       // row i of G and row aa of P by selects (no dynamically indexed local arrays)
       double gi[3], pa[3];
 #pragma unroll
@@ -586,9 +584,9 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
         pa[y] = aa == 0 ? P[y] : aa == 1 ? P[3 + y] : P[6 + y];
       }
       double f = V * (pa[0] * gi[0] + pa[1] * gi[1] + pa[2] * gi[2]);
-      Fs[el * 12 + lane] = we * f;
+      Fs[el * 12 + hl] = we * f;
       if (!Jt && !a.Ke_out) continue;  // force-only launch: no element stiffness
-      // stiffness column for DOF (jv, d) = (i, aa) = lane: dF_ab = delta_ad g_jv[b]
+      // stiffness column for DOF (jv, d) = (i, aa) = hl: dF_ab = delta_ad g_jv[b]
       const int d = aa;
       double dF[9];
 #pragma unroll
@@ -618,7 +616,7 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
       for (int r = 0; r < 12; ++r) {
         int ri = r / 3, ra = r % 3;
         double kv = V * (t1[ra * 3] * G[ri * 3] + t1[ra * 3 + 1] * G[ri * 3 + 1] + t1[ra * 3 + 2] * G[ri * 3 + 2]);
-        Ks[el * 144 + r * 12 + lane] = we * kv;
+        Ks[el * 144 + r * 12 + hl] = we * kv;
       }
     }
   }
