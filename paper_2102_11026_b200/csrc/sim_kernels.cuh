@@ -456,7 +456,13 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
   int* Rw = reinterpret_cast<int*>(Fs + (size_t)epc * 12);  // [epc][12]
   double* Kacc = reinterpret_cast<double*>(Rw + epc * 12);  // [n][n] + [n] (K~, f~ partials) when cpc > 1
   __shared__ double wsh[64];
+  __shared__ uint64_t gbar;  // J~ row gather by TMA bulk copies (one mbarrier phase per chunk)
   const bool pref = a.rows_g != nullptr && epc * 12 <= (int)blockDim.x;
+  const bool bulk = pref && Jt && (a.ldjt & 1) == 0 && (ldp & 1) == 0;
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(&gbar, 1);
+    fence_mbar_init();
+  }
   int nxt = -1;
   for (int ck = 0; ck < a.cpc; ++ck) {
   const int chunk = blockIdx.x * a.cpc + ck;  // element chunk
@@ -484,8 +490,22 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     }
     Rw[idx] = row;
   }
-  __syncthreads();
-  {
+  const int nrows = __syncthreads_count(bulk && threadIdx.x < epc * 12 && nxt >= 0);
+  if (bulk) {
+    // one TMA bulk copy per valid J~ row (issued by the row's owner thread; even n so the size
+    // is a multiple of 16 bytes), fixed-DOF rows zero-filled; lands while the physics runs
+    const uint32_t B = (uint32_t)((n + 1) & ~1) * 8u;
+    if (threadIdx.x == 0) mbar_expect_tx(&gbar, (uint32_t)nrows * B);
+    if (threadIdx.x < epc * 12) {
+      double* dst = Js + threadIdx.x * ldp;
+      if (nxt >= 0) {
+        fence_proxy_async();
+        tma_g2s(dst, Jt + (size_t)nxt * a.ldjt, B, &gbar);
+      } else {
+        for (int j = 0; j < n; ++j) dst[j] = 0.0;
+      }
+    }
+  } else {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     if (Jt && (a.ldjt & 1) == 0 && (ldp & 1) == 0) {  // 16-byte chunks (both pitches even)
       // n <= 32: a half-warp per J~ row (two rows per warp instruction), else a warp per row
@@ -515,7 +535,6 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     const int ei = (chunk + 1) * epc + threadIdx.x / 12;
     nxt = ei < a.n_elems ? a.rows_g[(size_t)(chunk + 1) * epc * 12 + threadIdx.x] : -1;
   }
-  cp_async_all_wait();
   // element physics: two elements per warp (one per half-warp; lanes 0..11 of a half own the
   // element's 12 DOFs). A padding element (past the set) gets V = 0 and Dm^-1 = 0, so its force
   // and stiffness come out exactly zero without divergent control flow around the shuffles.
@@ -627,7 +646,9 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
     const int ei = chunk * epc + el;
     wsh[el] = (a.w && ei < a.n_elems) ? a.w[(size_t)sim * a.n_elems + ei] : 1.0;
   }
-  __syncthreads();  // physics done (Ks, Fs), weights staged
+  if (bulk) mbar_wait_cta(&gbar, (uint32_t)(ck & 1));  // the J~ rows of this chunk
+  else cp_async_all_wait();
+  __syncthreads();  // physics done (Ks, Fs), weights staged, J~ rows landed
   const bool gram = Jt && !a.fred_out;
   // G_e = w_e K_e J~_e (12 x n) on the DMMA pipe
   if (gram) ke_j_dmma(Ks, Js, Gs, ldp, epc, n, wsh);
