@@ -296,13 +296,28 @@ using CfgOutC = GemmCfg<48, 128, 2, 4, 1, 32, 3>;
 // same tiling on the warp-specialised TMA pipeline (gemm_ws.cuh): 6 swizzled stages, one
 // producer warp; 13% faster on this shape (tools/probes/gemm_ws_probe.cu), bitwise identical
 using CfgOutWs = WsCfg<48, 128, 3, 4, 6>;  // 12 consumer warps (16 x 32 warp tiles): best of the probe
+// <= 64 output columns (one sim at n_q <= 31: 2 + 2 n_q columns): half-width tiles, so no DMMA
+// work is spent on padding columns
+// (24 x 64 tiles: 280 CTAs, ~2 per SM: 7.9 us in the cfg2 graph vs 12.1 us for 48 x 128 over the
+// same 62 columns and 16.4 us for 48 x 64; NLROM_OUT_TILE selects 0: 48x128, 1: 48x64, 3: 16x64)
+using CfgOutWs64 = WsCfg<48, 64, 3, 2, 6>;
+using CfgOutWs64b = WsCfg<24, 64, 3, 2, 6>;
+using CfgOutWs64c = WsCfg<16, 64, 2, 2, 6>;
+using CfgOutWs64d = WsCfg<8, 64, 1, 2, 6>;
 
 void output_layer(nlrom_ctx* c) {
   GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->next, 0, 0};
   EpiJetOutC e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
                c->n_p, c->n_q};
   if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
-  else if (c->ldlast % 2 == 0 && !getenv("NLROM_NO_WS_GEMM")) launch_gemm_ws<CfgOutWs>(g, e, c->st);
+  else if (c->ldlast % 2 == 0 && !getenv("NLROM_NO_WS_GEMM")) {
+    static const int tile = getenv("NLROM_OUT_TILE") ? atoi(getenv("NLROM_OUT_TILE")) : 3;
+    if (g.C <= 64 && tile == 1) launch_gemm_ws<CfgOutWs64>(g, e, c->st);
+    else if (g.C <= 64 && tile == 2) launch_gemm_ws<CfgOutWs64b>(g, e, c->st);
+    else if (g.C <= 64 && tile == 3) launch_gemm_ws<CfgOutWs64c>(g, e, c->st);
+    else if (g.C <= 64 && tile == 4) launch_gemm_ws<CfgOutWs64d>(g, e, c->st);
+    else launch_gemm_ws<CfgOutWs>(g, e, c->st);
+  }
   else launch_gemm<CfgOutC>(g, e, c->st);
   ++gemm_launch_count;
 }
@@ -1184,8 +1199,8 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       c->wC.alloc((size_t)c->n_sims * std::max(1, c->n_cub));
     }
     // bundle buffers
-    c->Cc = 4 + 4 * n_q;  // compact (de-replicated) columns per sim
-    c->batched = c->n_sims * c->Cc >= 2048 || getenv("NLROM_BATCHED") != nullptr;
+    c->Cc = 2 + 2 * n_q;  // output-layer columns per sim: [D_1, 2 D_ss | (D_t, 2 D_tss + D_tr) x n_q]
+    c->batched = c->n_sims * (4 + 4 * n_q) >= 2048 || getenv("NLROM_BATCHED") != nullptr;
     choose_groups(n_q, w, c->batched, c->G, c->gps);
     c->Cb = c->G * c->gps;
     c->ldq = round_up(n_q, 2);

@@ -116,11 +116,11 @@ struct EpiJet {
   int group;          // columns per group (BN is a multiple of it)
   int gps;            // groups per simulation
   int n_q;            // tangent directions per simulation
-  int compact;        // 1: write the de-replicated layout [base | n_q tangents] per sim (next layer is linear)
+  int compact;        // 1: write the output layout per sim (next layer is linear): [h_1, 2 h_ss | (h_t, 2 h_tss + h_tr) x n_q]
   __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
     double* Yz = Y + (size_t)t.z * strideY;
     const int nk = (group - 4) / 4;           // tangents per group
-    const int cs = 4 + 4 * n_q;               // compact columns per sim
+    const int cs = 2 + 2 * n_q;               // output-layout columns per sim
     const int ngt = t.bn / group;             // groups in this tile
     for (int i = tid; i < t.bm * ngt; i += nt) {
       const int gt = i / t.bm, ml = i % t.bm;
@@ -141,8 +141,8 @@ struct EpiJet {
 #pragma unroll
         for (int s = 0; s < 4; ++s) Yz[(size_t)(cg + s) * ldy + m] = o[s];
       } else if (gl == 0) {
-#pragma unroll
-        for (int s = 0; s < 4; ++s) Yz[(size_t)(sim * cs + s) * ldy + m] = o[s];
+        Yz[(size_t)(sim * cs) * ldy + m] = o[0];
+        Yz[(size_t)(sim * cs + 1) * ldy + m] = 2.0 * o[2];
       }
       for (int k = 0; k < nk; ++k) {
         const int kg = gl * nk + k;           // tangent index within the simulation
@@ -151,9 +151,15 @@ struct EpiJet {
 #pragma unroll
         for (int s = 0; s < 4; ++s) y[s] = cs0[(4 + 4 * k + s) * t.ldc];
         jet_tangent(jc, y, yo);
-        const size_t col = compact ? (size_t)(sim * cs + 4 + 4 * kg) : (size_t)(cg + 4 + 4 * k);
+        if (compact) {
+          const size_t col = (size_t)(sim * cs + 2 + 2 * kg);
+          Yz[col * ldy + m] = yo[0];
+          Yz[(col + 1) * ldy + m] = fma(2.0, yo[2], yo[3]);
+        } else {
+          const size_t col = (size_t)(cg + 4 + 4 * k);
 #pragma unroll
-        for (int s = 0; s < 4; ++s) Yz[(col + s) * ldy + m] = yo[s];
+          for (int s = 0; s < 4; ++s) Yz[(col + s) * ldy + m] = yo[s];
+        }
         if (Cz && kg < n_q) {  // sin'(z0 + y0 e) = cos z0 - sin z0 y0 e (dual), for the vhp backward
           Cz[(size_t)(2 * kg) * ldcache + m] = jc.c1;
           Cz[(size_t)(2 * kg + 1) * ldcache + m] = jc.ns * y[0];
@@ -177,16 +183,16 @@ struct EpiJetOutC {
   int ldjt, lddj, n_p, n_q;
   __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
     const int N = g.M;
-    const int cs = 4 + 4 * n_q;
-    const int ngrp = t.bn / 4;
+    const int cs = 2 + 2 * n_q;  // per sim: [D_1, 2 D_ss | (D_t, 2 D_tss + D_tr) x n_q] (combined upstream)
+    const int ngrp = t.bn / 2;
     for (int i = tid; i < t.bm * ngrp; i += nt) {
       const int q = i / t.bm, ml = i % t.bm;
       const int m = t.m0 + ml;
-      const int c = t.c0 + 4 * q;
+      const int c = t.c0 + 2 * q;
       if (m >= N || c >= g.C) continue;
       const int sim = c / cs, rem = c % cs;
       const size_t sv = (size_t)sim * N + m;
-      const double* col = t.Cs + (4 * q) * t.ldc + ml;
+      const double* col = t.Cs + (2 * q) * t.ldc + ml;
       if (rem == 0) {
         const double d1 = col[0] + bias[m];
         double up = 0.0;
@@ -195,11 +201,11 @@ struct EpiJetOutC {
         for (int k = 0; k < n_p; ++k) up = fma(Ur[k], pz[k], up);
         u[sv] = up + d1;
         value[sv] = d1;
-        hvv[sv] = 2.0 * col[2 * t.ldc];
+        hvv[sv] = col[t.ldc];
       } else {
-        const int kg = (rem - 4) >> 2;
+        const int kg = (rem - 2) >> 1;
         Jt[sv * ldjt + n_p + kg] = col[0];
-        dJ[sv * lddj + kg] = 2.0 * col[2 * t.ldc] + col[3 * t.ldc];
+        dJ[sv * lddj + kg] = col[t.ldc];
       }
     }
   }

@@ -54,7 +54,7 @@ struct MlpFwdArgs {
   // outputs
   double* cache[MLP_MAXL];  // vhp caches: (n_sims * 2 n_q) x ldc per layer
   int ldc;
-  double* Hout;  // compact activation of the last hidden layer: (n_sims * (4 + 4 n_q)) x ldH
+  double* Hout;  // last hidden layer in the output layout: (n_sims * (2 + 2 n_q)) x ldH
   int ldH;
   int G, gps;
 };
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
   const int gg = blockIdx.y;                 // global group = sim * gps + gl
   const int sim = gg / a.gps, gl = gg % a.gps;
   const int nk = (G - 4) / 4;
-  const int cs = 4 + 4 * a.n_q;
+  const int cs = 2 + 2 * a.n_q;  // output-layer columns per sim (see EpiJetOutC)
 
   // weight + bias slices land by ONE TMA bulk copy each (padded global layout), on a
   // per-buffer mbarrier; issued one layer ahead by thread 0
@@ -209,10 +209,12 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
         // compact layout for the linear output layer: base once per sim, tangents by index
         if (unit == 0 && gl == 0) {
 #pragma unroll
-          for (int s = 0; s < 4; ++s) a.Hout[(size_t)(sim * cs + s) * a.ldH + m] = o[s];
+          a.Hout[(size_t)(sim * cs) * a.ldH + m] = o[0];            // value slot
+          a.Hout[(size_t)(sim * cs + 1) * a.ldH + m] = 2.0 * o[2];  // 2 h_ss -> hvv
         } else if (unit > 0 && kg < a.n_q) {
 #pragma unroll
-          for (int s = 0; s < 4; ++s) a.Hout[(size_t)(sim * cs + 4 + 4 * kg + s) * a.ldH + m] = o[s];
+          a.Hout[(size_t)(sim * cs + 2 + 2 * kg) * a.ldH + m] = o[0];                     // h_t -> J
+          a.Hout[(size_t)(sim * cs + 3 + 2 * kg) * a.ldH + m] = fma(2.0, o[2], o[3]);  // 2 h_tss + h_tr -> dJ
         }
       } else {
 #pragma unroll
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd_async(MlpFwdArgs a) {
   const int gg = blockIdx.y;
   const int sim = gg / a.gps, gl = gg % a.gps;
   const int nk = (G - 4) / 4;
-  const int cs = 4 + 4 * a.n_q;
+  const int cs = 2 + 2 * a.n_q;  // output-layer columns per sim (see EpiJetOutC)
   constexpr uint32_t SLICE = R * G * 8;  // bytes one source delivers per layer
 
   auto issue_weights = [&](int l) {  // one thread: layer l's weight + bias slices -> buffer l & 1
@@ -402,10 +404,12 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd_async(MlpFwdArgs a) {
       if (last) {
         if (unit == 0 && gl == 0) {
 #pragma unroll
-          for (int s4 = 0; s4 < 4; ++s4) a.Hout[(size_t)(sim * cs + s4) * a.ldH + m] = o[s4];
+          a.Hout[(size_t)(sim * cs) * a.ldH + m] = o[0];
+          a.Hout[(size_t)(sim * cs + 1) * a.ldH + m] = 2.0 * o[2];
         } else if (unit > 0 && kg < a.n_q) {
 #pragma unroll
-          for (int s4 = 0; s4 < 4; ++s4) a.Hout[(size_t)(sim * cs + 4 + 4 * kg + s4) * a.ldH + m] = o[s4];
+          a.Hout[(size_t)(sim * cs + 2 + 2 * kg) * a.ldH + m] = o[0];
+          a.Hout[(size_t)(sim * cs + 3 + 2 * kg) * a.ldH + m] = fma(2.0, o[2], o[3]);
         }
       } else {
         const uint32_t la = xn_base + (uint32_t)(((r0 + rr) * LDX + col) * 8);
