@@ -148,7 +148,7 @@ def decoder_flops(P, n_sims=1):
     F = (18 * n_q + 6) * (2.0 * mac + 4.0 * N * n_p)
     G, gps = jet_groups(n_q, n_sims * (4 + 4 * n_q) >= 2048)
     hid_cols = gps * G                               # grouped jet columns through the sin layers
-    out_cols = 4 + 4 * n_q                           # compact columns through the output layer
+    out_cols = 2 + 2 * n_q                           # [D_1, 2 D_ss | (D_t, 2 D_tss + D_tr) x n_q] per sim
     executed = 2.0 * hid_cols * hidden_mac + 2.0 * out_cols * N * w + 2.0 * N * w + 2.0 * (2 * n_q) * hidden_mac
     return F, executed
 
