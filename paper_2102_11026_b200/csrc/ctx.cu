@@ -21,6 +21,7 @@
 #include "solve_kernels.cuh"
 #include "lu_warp.cuh"
 #include "lu_split.cuh"
+#include "lu_rank2.cuh"
 #include "mlp_chain.cuh"
 #include "coupled_kernels.cuh"
 #include "gemm_ws.cuh"
@@ -916,6 +917,18 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
     else gow(k_lu_warp<3>);
     return;
   }
+  // two pivot steps per barrier (lu_rank2.cuh): bitwise identical, but slower on B200 (53.5 vs
+  // 25.7 us in the cfg2 graph: the two dependent argmax + reciprocal chains per double step cost
+  // more than the barrier they save; tools/lu_rank2_check.py): opt-in only
+  static const bool rank2 = getenv("NLROM_LU_RANK2") != nullptr;
+  if (rank2) {
+    switch (lu_nb(n + nx)) {
+      case 4: go(k_lu_solve2<4>); break;
+      case 6: go(k_lu_solve2<6>); break;
+      default: go(k_lu_solve2<8>); break;
+    }
+    return;
+  }
   switch (lu_nb(n + nx)) {
     case 4: go(k_lu_solve<4>); break;
     case 6: go(k_lu_solve<6>); break;
@@ -1281,6 +1294,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_solve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_solve2<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_solve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_head, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_front<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_front<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

@@ -337,7 +337,7 @@ np.savez(sys.argv[2], phi=phi, S=S, r=nxt.r)
     {"NLROM_NO_FUSED_MLP": "1", "NLROM_LU_ROWS": "1"},
     {"NLROM_LU_WARP": "1", "NLROM_WNET_LATE": "1"},
     {"NLROM_OUT_TILE": "0", "NLROM_NO_SPLITK": "1"},
-    {"NLROM_OUT_TILE": "2", "NLROM_CUB_MINB2": "1"},
+    {"NLROM_OUT_TILE": "2", "NLROM_CUB_MINB2": "1", "NLROM_LU_RANK2": "1"},
 ])
 def test_kernel_variants(cuda_ok, env, tmp_path):
     """Opt-in kernel variants (selected by environment at context creation, hence a fresh
