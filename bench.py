@@ -146,10 +146,12 @@ def decoder_flops(P, n_sims=1):
     mac = sum(a * b for a, b in zip(widths[:-1], widths[1:]))
     hidden_mac = mac - w * N
     F = (18 * n_q + 6) * (2.0 * mac + 4.0 * N * n_p)
-    G, gps = jet_groups(n_q, n_sims * (4 + 4 * n_q) >= 2048)
+    batched = n_sims * (4 + 4 * n_q) >= 2048
+    G, gps = jet_groups(n_q, batched)
     hid_cols = gps * G                               # grouped jet columns through the sin layers
     out_cols = 2 + 2 * n_q                           # [D_1, 2 D_ss | (D_t, 2 D_tss + D_tr) x n_q] per sim
-    executed = 2.0 * hid_cols * hidden_mac + 2.0 * out_cols * N * w + 2.0 * N * w + 2.0 * (2 * n_q) * hidden_mac
+    bwd_cols = (1 + n_q) if batched else 2 * n_q     # vhp backward: shared real part when batched
+    executed = 2.0 * hid_cols * hidden_mac + 2.0 * out_cols * N * w + 2.0 * N * w + 2.0 * bwd_cols * hidden_mac
     return F, executed
 
 

@@ -752,6 +752,26 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
   }
   const int l_top = c->L - 2;
   dim3 gd(ceil_div(c->wL1, 32), c->n_sims);
+  const int P1 = 1 + npass_per_sim;
+  if (NS == 2 && !mc && dcache && c->batched && P1 <= CfgBig::BN && !getenv("NLROM_NO_SHARED_REAL")) {
+    // shared real part (EpiBwdShared): 1 + npass columns per sim instead of 2 npass, tiles of
+    // whole sims
+    const int cstep = (CfgBig::BN / P1) * P1, ncs = c->n_sims * P1;
+    launch(c, k_bwd_delta_sh, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->next, (const double*)c->AT.p,
+           (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
+    DBuf* cur = &D0;
+    DBuf* nxt = &D1;
+    for (int l = c->L - 2; l >= 1; --l) {
+      GemmArgs g{c->WT[l].p, cur->p, c->ldWT[l], ldcs[l], c->widths[l], ncs, c->widths[l + 1], 0, 0, cstep};
+      launch_gemm<CfgBig>(g, EpiBwdShared{nxt->p, ldcs[l - 1], caches[l - 1].p, npass_per_sim}, c->st);
+      ++gemm_launch_count;
+      std::swap(cur, nxt);
+    }
+    GemmArgs g{c->WT[0].p, cur->p, c->ldWT[0], ldcs[0], c->widths[0], ncs, c->widths[1], 0, 0, cstep};
+    launch_gemm<CfgBig>(g, EpiStoreShared{Gout.p, ldG, npass_per_sim}, c->st);
+    ++gemm_launch_count;
+    return;
+  }
   if (NS == 2) {
     if (mc)
       launch(c, k_bwd_delta<2, 1>, gd, 256, 0, (const double*)c->ybuf.p, c->wL1, c->next, (const double*)c->AT.p,

@@ -101,6 +101,59 @@ struct EpiBwdAct {
   }
 };
 
+// vhp backward of the fused bundle at many sims with the real part shared: the real part of the
+// dual cotangent is the same for every pass of a sim, so a sim's columns are [real | dual_1 ..
+// dual_npass] (1 + npass instead of 2 npass). Tiles hold whole sims (GemmArgs.cstep), so the real
+// column's product is in the same Cs tile: o0 = d0 f0, o_k = fma(d1_k, f0, d0 f1_k) (md_mul<2>
+// order, bitwise equal to EpiBwdAct<2, ACT_DSIN_MD>). cache: per sim 2 npass columns (f0, f1_k).
+struct EpiBwdShared {
+  double* Y;
+  int ldy;
+  const double* fcache;
+  int npass;
+  __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
+    const int P1 = 1 + npass;
+    for (int i = tid; i < t.bm * t.bn; i += nt) {
+      const int cl = i / t.bm, ml = i % t.bm;
+      const int c = t.c0 + cl, m = t.m0 + ml;
+      if (m >= g.M || c >= g.C) continue;
+      const int sim = c / P1, s = c % P1;
+      const double d0 = t.Cs[(cl - s) * t.ldc + ml];
+      const double* F = fcache + (size_t)sim * 2 * npass * ldy;
+      const double f0 = F[m];
+      if (s == 0) {
+        Y[(size_t)c * ldy + m] = d0 * f0;
+      } else {
+        const double f1 = F[(size_t)(2 * (s - 1) + 1) * ldy + m];
+        Y[(size_t)c * ldy + m] = fma(t.Cs[cl * t.ldc + ml], f0, d0 * f1);
+      }
+    }
+  }
+};
+
+// Last layer of the shared-real vhp backward: column (sim, 0) -> G_t[sim][2k] for every k,
+// column (sim, 1 + k) -> G_t[sim][2k + 1] (the reference vhp layout).
+struct EpiStoreShared {
+  double* Y;
+  int ldy;
+  int npass;
+  __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
+    const int P1 = 1 + npass;
+    for (int i = tid; i < t.bm * t.bn; i += nt) {
+      const int cl = i / t.bm, ml = i % t.bm;
+      const int c = t.c0 + cl, m = t.m0 + ml;
+      if (m >= g.M || c >= g.C) continue;
+      const int sim = c / P1, s = c % P1;
+      const double v = t.Cs[cl * t.ldc + ml];
+      double* G = Y + (size_t)sim * 2 * npass * ldy + m;
+      if (s == 0)
+        for (int k = 0; k < npass; ++k) G[(size_t)(2 * k) * ldy] = v;
+      else
+        G[(size_t)(2 * (s - 1) + 1) * ldy] = v;
+    }
+  }
+};
+
 // Hidden layer of the fused Newton bundle: tiles of G = BN columns laid out as
 // [base jet (1, s, s^2, r) | nk tangents x (t, ts, ts^2, tr)], see mc_device.cuh.
 // Writes the activated jet, and (optional) the dual cache for the vhp backward in

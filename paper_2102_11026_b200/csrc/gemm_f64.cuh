@@ -26,6 +26,8 @@ struct GemmArgs {
   int lda, ldb;
   int M, C, K;      // K must be even; lda, ldb even; base pointers 16B aligned
   long long strideA, strideB;  // per blockIdx.z (batched), in doubles
+  int cstep = 0;    // column tiles start every cstep columns (<= BN; 0: BN) -- tiles that hold whole
+                    // column groups (the epilogue sees t.bn = cstep columns)
 };
 
 struct Tile {
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(Cfg::NT) gemm_tn_kernel(GemmArgs g, Epi epi) {
   const int wk = warp / (Cfg::WM * Cfg::WN);
   const int wmn = warp % (Cfg::WM * Cfg::WN);
   const int wm = wmn % Cfg::WM, wn = wmn / Cfg::WM;
-  const int m0 = blockIdx.x * Cfg::BM, c0 = blockIdx.y * Cfg::BN;
+  const int m0 = blockIdx.x * Cfg::BM, c0 = blockIdx.y * (g.cstep ? g.cstep : Cfg::BN);
   const double* A = g.A + (size_t)blockIdx.z * g.strideA;
   const double* B = g.B + (size_t)blockIdx.z * g.strideB;
 
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(Cfg::NT) gemm_tn_kernel(GemmArgs g, Epi epi) {
     }
     __syncthreads();
   }
-  Tile t{Cs, Cfg::LDC, m0, c0, Cfg::BM, Cfg::BN, (int)blockIdx.z};
+  Tile t{Cs, Cfg::LDC, m0, c0, Cfg::BM, g.cstep ? g.cstep : Cfg::BN, (int)blockIdx.z};
   epi(t, g, tid, Cfg::NT);
 }
 
@@ -203,7 +205,7 @@ void launch_gemm(const GemmArgs& g, const Epi& epi, cudaStream_t st, int batch =
   }
   if (!launch_gate((const void*)gemm_tn_kernel<Cfg, Epi>)) return;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ceil_div(g.M, Cfg::BM), ceil_div(g.C, Cfg::BN), batch);
+  cfg.gridDim = dim3(ceil_div(g.M, Cfg::BM), ceil_div(g.C, g.cstep ? g.cstep : Cfg::BN), batch);
   cfg.blockDim = dim3(Cfg::NT);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = st;

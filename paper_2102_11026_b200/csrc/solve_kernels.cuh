@@ -879,6 +879,44 @@ __global__ void k_reduce_cols(const double* __restrict__ part, int nchunk, int M
 // Delta[p*NS + s][i] = (g_i * act'(z_{L-1}))[s] in the arithmetic of the passes
 // (NS = 1 real; 2 dual (MC = 0) or complex (MC = 1)); MC = 2: z already holds act'(z) as a dual
 // (the fused bundle's cache). grid (ceil(w/32), n_sims), block 256.
+// Shared-real layout (EpiBwdShared): per sim [g f0 | g f1_1 .. g f1_npass] from the sin'(z) cache.
+__global__ void k_bwd_delta_sh(const double* __restrict__ y, int w, int n_p, const double* __restrict__ AT,
+                               const double* __restrict__ zc, int ldz, int npass, double* __restrict__ Delta) {
+  pdl_wait();
+  pdl_launch();
+  __shared__ double g[32];
+  const int sim = blockIdx.y;
+  const int i0 = blockIdx.x * 32;
+  const int M = w + n_p;
+  const double* ys = y + (size_t)sim * M;
+  {
+    __shared__ double gp[8][32];
+    const int il = threadIdx.x & 31, w8 = threadIdx.x >> 5;
+    const int i = i0 + il;
+    double acc = 0.0;
+    if (i < w)
+      for (int j = w8; j < n_p; j += 8) acc = fma(AT[(size_t)j * w + i], ys[w + j], acc);
+    gp[w8][il] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double s = (i < w) ? ys[i] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += gp[q][il];
+      g[il] = s;
+    }
+  }
+  __syncthreads();
+  const double* Z = zc + (size_t)sim * npass * 2 * ldz;
+  double* D = Delta + (size_t)sim * (npass + 1) * ldz;
+  for (int t = threadIdx.x; t < (npass + 1) * 32; t += blockDim.x) {
+    const int il = t & 31, s = t >> 5;
+    const int i = i0 + il;
+    if (i >= w) continue;
+    const double f = s == 0 ? Z[i] : Z[(size_t)(2 * (s - 1) + 1) * ldz + i];
+    D[(size_t)s * ldz + i] = g[il] * f;
+  }
+}
+
 template <int NS, int MC>
 __global__ void k_bwd_delta(const double* __restrict__ y, int w, int n_p, const double* __restrict__ AT,
                             const double* __restrict__ zc, int ldz, int npass, double* __restrict__ Delta) {

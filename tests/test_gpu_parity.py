@@ -219,7 +219,7 @@ def test_trajectory_100_steps(cfg1, integ):
 
 
 # ------------------------------------------------------------------ independent sims in one context
-@pytest.mark.parametrize("batched", [False, True, "cpc"])
+@pytest.mark.parametrize("batched", [False, True, "cpc", "noshare"])
 def test_multi_sim(cfg1, batched, monkeypatch):
     """n_sims independent simulations through one context == the single-sim oracle per sim.
     batched=True forces the big-tile per-layer GEMM path used for thousands of sims (cfg5);
@@ -232,6 +232,8 @@ def test_multi_sim(cfg1, batched, monkeypatch):
         monkeypatch.setenv("NLROM_BATCHED", "1")
     if batched == "cpc":
         monkeypatch.setenv("NLROM_CPC", "4")
+    if batched == "noshare":  # batched vhp backward with 2 npass dual columns (no shared real part)
+        monkeypatch.setenv("NLROM_NO_SHARED_REAL", "1")
     ns = 3
     sess = Session(P.rm, P.model, P.cm, n_sims=ns)
     sess._ncub_cache = len(P.cm.C)
