@@ -753,7 +753,11 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
   const int l_top = c->L - 2;
   dim3 gd(ceil_div(c->wL1, 32), c->n_sims);
   const int P1 = 1 + npass_per_sim;
-  if (NS == 2 && !mc && dcache && c->batched && P1 <= CfgBig::BN && !getenv("NLROM_NO_SHARED_REAL")) {
+  // shared real part only when the GEMMs are throughput-bound (>= 4 waves of CTAs in the 2 npass
+  // layout): with few CTAs (cfg4: 25 per layer) fewer, longer tiles are slower (0.92 vs 0.85 ms)
+  const long long ctas2 = (long long)ceil_div(c->n_sims * 2 * npass_per_sim, CfgBig::BN) * ceil_div(c->wL1, CfgBig::BM);
+  if (NS == 2 && !mc && dcache && c->batched && P1 <= CfgBig::BN &&
+      (ctas2 >= 4 * 148 || getenv("NLROM_SHARED_REAL")) && !getenv("NLROM_NO_SHARED_REAL")) {
     // shared real part (EpiBwdShared): 1 + npass columns per sim instead of 2 npass, tiles of
     // whole sims
     const int cstep = (CfgBig::BN / P1) * P1, ncs = c->n_sims * P1;

@@ -230,10 +230,11 @@ def test_multi_sim(cfg1, batched, monkeypatch):
     P, S = cfg1
     if batched:
         monkeypatch.setenv("NLROM_BATCHED", "1")
-    if batched == "cpc":
+    if batched == "cpc":  # + the shared-real vhp backward (default only at >= 4 waves of CTAs)
         monkeypatch.setenv("NLROM_CPC", "4")
+        monkeypatch.setenv("NLROM_SHARED_REAL", "1")
     if batched == "noshare":  # batched vhp backward with 2 npass dual columns (no shared real part)
-        monkeypatch.setenv("NLROM_NO_SHARED_REAL", "1")
+        monkeypatch.setenv("NLROM_NO_SHARED_REAL", "1")  # (the default at 3 sims anyway)
     ns = 3
     sess = Session(P.rm, P.model, P.cm, n_sims=ns)
     sess._ncub_cache = len(P.cm.C)
