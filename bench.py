@@ -150,7 +150,9 @@ def decoder_flops(P, n_sims=1):
     G, gps = jet_groups(n_q, batched)
     hid_cols = gps * G                               # grouped jet columns through the sin layers
     out_cols = 2 + 2 * n_q                           # [D_1, 2 D_ss | (D_t, 2 D_tss + D_tr) x n_q] per sim
-    bwd_cols = (1 + n_q) if batched else 2 * n_q     # vhp backward: shared real part when batched
+    ctas2 = -(-(n_sims * 2 * n_q) // 128) * -(-w // 64)
+    shared = batched and ctas2 >= 4 * 148            # mirror of ctx.cu decoder_backward
+    bwd_cols = (1 + n_q) if shared else 2 * n_q      # vhp backward: shared real part at >= 4 waves
     executed = 2.0 * hid_cols * hidden_mac + 2.0 * out_cols * N * w + 2.0 * N * w + 2.0 * bwd_cols * hidden_mac
     return F, executed
 
