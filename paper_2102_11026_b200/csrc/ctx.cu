@@ -173,6 +173,16 @@ int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL
 // ---------------------------------------------------------------- GEMM dispatch
 template <class Epi>
 void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st, bool big = false) {
+  // big-tile hidden layers on the warp-specialised TMA pipeline (16 consumer warps, 4 stages):
+  // cfg5 hidden layers 14.76 -> 14.51 ms; NLROM_HID_WS=0 selects the cp.async CfgBig kernel,
+  // 2 an 8-consumer-warp variant (slower: 15.84 ms)
+  static const int hid_ws = getenv("NLROM_HID_WS") ? atoi(getenv("NLROM_HID_WS")) : 1;
+  if (big && 128 % G == 0 && hid_ws && g.K % 16 == 0 && g.lda % 2 == 0 && g.ldb % 2 == 0) {
+    if (hid_ws == 1) launch_gemm_ws<WsCfg<64, 128, 4, 4, 4>>(g, e, st);
+    else launch_gemm_ws<WsCfg<64, 128, 2, 4, 4>>(g, e, st);
+    ++gemm_launch_count;
+    return;
+  }
   if (big && 128 % G == 0) {
     launch_gemm<CfgBig>(g, e, st);
     ++gemm_launch_count;

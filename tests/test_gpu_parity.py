@@ -235,6 +235,7 @@ def test_multi_sim(cfg1, batched, monkeypatch):
         monkeypatch.setenv("NLROM_SHARED_REAL", "1")
     if batched == "noshare":  # batched vhp backward with 2 npass dual columns (no shared real part)
         monkeypatch.setenv("NLROM_NO_SHARED_REAL", "1")  # (the default at 3 sims anyway)
+        monkeypatch.setenv("NLROM_HID_WS", "0")  # + the cp.async big-tile hidden layers
     ns = 3
     sess = Session(P.rm, P.model, P.cm, n_sims=ns)
     sess._ncub_cache = len(P.cm.C)
