@@ -320,7 +320,13 @@ void output_layer(nlrom_ctx* c) {
   GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->next, 0, 0};
   EpiJetOutC e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
                c->n_p, c->n_q};
-  if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
+  // batched output layer on the warp-specialised pipeline: measured slower at cfg5 (3.38 / 3.39 ms
+  // vs 3.06 ms for CfgBig: the EpiJetOutC scatter dominates the tile), opt-in only
+  static const int out_ws = getenv("NLROM_OUT_BIG_WS") ? atoi(getenv("NLROM_OUT_BIG_WS")) : 0;
+  if (c->batched && out_ws && c->ldlast % 2 == 0 && (c->wL1 + c->next) % 16 == 0) {
+    if (out_ws == 1) launch_gemm_ws<WsCfg<64, 128, 4, 4, 4>>(g, e, c->st);
+    else launch_gemm_ws<WsCfg<48, 128, 3, 4, 6>>(g, e, c->st);
+  } else if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
   else if (c->ldlast % 2 == 0 && !getenv("NLROM_NO_WS_GEMM")) {
     static const int tile = getenv("NLROM_OUT_TILE") ? atoi(getenv("NLROM_OUT_TILE")) : 3;
     if (g.C <= 64 && tile == 1) launch_gemm_ws<CfgOutWs64>(g, e, c->st);
