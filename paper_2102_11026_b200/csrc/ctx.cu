@@ -783,7 +783,13 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
     DBuf* nxt = &D1;
     for (int l = c->L - 2; l >= 1; --l) {
       GemmArgs g{c->WT[l].p, cur->p, c->ldWT[l], ldcs[l], c->widths[l], ncs, c->widths[l + 1], 0, 0, cstep};
-      launch_gemm<CfgBig>(g, EpiBwdShared{nxt->p, ldcs[l - 1], caches[l - 1].p, npass_per_sim}, c->st);
+      // warp-specialised TMA pipeline with sim-aligned column tiles: cfg5 vhp 5.14 -> 4.77 ms
+      static const int bwd_ws = getenv("NLROM_BWD_WS") ? atoi(getenv("NLROM_BWD_WS")) : 1;
+      if (bwd_ws && c->widths[l + 1] % 16 == 0 && c->ldWT[l] % 2 == 0 && ldcs[l] % 2 == 0)
+        launch_gemm_ws<WsCfg<64, 128, 4, 4, 4>>(g, EpiBwdShared{nxt->p, ldcs[l - 1], caches[l - 1].p, npass_per_sim},
+                                                c->st);
+      else
+        launch_gemm<CfgBig>(g, EpiBwdShared{nxt->p, ldcs[l - 1], caches[l - 1].p, npass_per_sim}, c->st);
       ++gemm_launch_count;
       std::swap(cur, nxt);
     }

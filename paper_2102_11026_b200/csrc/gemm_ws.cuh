@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(Cfg::NT) gemm_ws_kernel(const __grid_constant_
       bool waited = false;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int tm = t % tiles_m, tc = (t / tiles_m) % tiles_c, tz = t / (tiles_m * tiles_c);
-        const int m0 = tm * Cfg::BM, c0 = tc * Cfg::BN;
+        const int m0 = tm * Cfg::BM, c0 = tc * (g.cstep ? g.cstep : Cfg::BN);
         int kt = 0;
         if (!waited) {
           // weight tiles of the first stages do not depend on the producer kernel: request
@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(Cfg::NT) gemm_ws_kernel(const __grid_constant_
           Cs[cc * Cfg::LDC + mm] = acc[i][j][e];
         }
     named_bar_sync(1, Cfg::NC);
-    Tile tile{Cs, Cfg::LDC, tm * Cfg::BM, tc * Cfg::BN, Cfg::BM, Cfg::BN, tz};
+    const int cs = g.cstep ? g.cstep : Cfg::BN;
+    Tile tile{Cs, Cfg::LDC, tm * Cfg::BM, tc * cs, Cfg::BM, cs, tz};
     epi(tile, g, tid, Cfg::NC);
   }
 }
@@ -209,7 +210,7 @@ void launch_gemm_ws(const GemmArgs& g, const Epi& epi, cudaStream_t st, int batc
   }
   const CUtensorMap tA = make_tile_map(g.A, g.K, g.M, g.lda, batch, g.strideA, Cfg::BM);
   const CUtensorMap tB = make_tile_map(g.B, g.K, g.C, g.ldb, batch, g.strideB, Cfg::BN);
-  const int tiles_m = ceil_div(g.M, Cfg::BM), tiles_c = ceil_div(g.C, Cfg::BN);
+  const int tiles_m = ceil_div(g.M, Cfg::BM), tiles_c = ceil_div(g.C, g.cstep ? g.cstep : Cfg::BN);
   const int ntiles = tiles_m * tiles_c * batch;
   int occ = 0;
   NL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_ws_kernel<Cfg, Epi>, Cfg::NT, Cfg::SMEM_BYTES));

@@ -219,7 +219,7 @@ def test_trajectory_100_steps(cfg1, integ):
 
 
 # ------------------------------------------------------------------ independent sims in one context
-@pytest.mark.parametrize("batched", [False, True, "cpc", "noshare"])
+@pytest.mark.parametrize("batched", [False, True, "cpc", "noshare", "sharedcp"])
 def test_multi_sim(cfg1, batched, monkeypatch):
     """n_sims independent simulations through one context == the single-sim oracle per sim.
     batched=True forces the big-tile per-layer GEMM path used for thousands of sims (cfg5);
@@ -233,6 +233,9 @@ def test_multi_sim(cfg1, batched, monkeypatch):
     if batched == "cpc":  # + the shared-real vhp backward (default only at >= 4 waves of CTAs)
         monkeypatch.setenv("NLROM_CPC", "4")
         monkeypatch.setenv("NLROM_SHARED_REAL", "1")
+    if batched == "sharedcp":  # shared-real vhp backward on the cp.async GEMM
+        monkeypatch.setenv("NLROM_SHARED_REAL", "1")
+        monkeypatch.setenv("NLROM_BWD_WS", "0")
     if batched == "noshare":  # batched vhp backward with 2 npass dual columns (no shared real part)
         monkeypatch.setenv("NLROM_NO_SHARED_REAL", "1")  # (the default at 3 sims anyway)
         monkeypatch.setenv("NLROM_HID_WS", "0")  # + the cp.async big-tile hidden layers
