@@ -112,6 +112,7 @@ struct nlrom_ctx {
   int luFC = 0;
   bool lu_front_done = false;
   int rpcM = 128, nchM = 0;  // row chunking of the mass block (finer: more CTAs for its Gram)
+  int cpmM = 1;              // mass-block row chunks per CTA (nchM = partials per sim)
   int s_ctas = getenv("NLROM_S_CTAS") ? atoi(getenv("NLROM_S_CTAS")) : 1 << 20;  // side-branch S reduction CTAs
   DBuf a, partA, partPhi, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
   IBuf status;
@@ -504,14 +505,15 @@ void assemble_launch(nlrom_ctx* c, CubSet& s, double dt, int drop_fict, int mode
 // it runs on a side stream (a parallel graph branch) while the weight net, the cubature and
 // the a-vector -- the critical path -- run on the main stream.
 size_t mass_smem(nlrom_ctx* c) {
-  return (size_t)(2 * c->rpcM * c->ldjt + c->rpcM * c->lddj + c->rpcM) * 8 + 16;
+  return (size_t)(2 * c->rpcM * c->ldjt + c->rpcM * c->lddj + c->rpcM) * 8 + 16 +
+         (c->cpmM > 1 ? (size_t)c->n * c->n * 8 : 0);
 }
 
 void mass_block_launch(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   if (c->rpcM != c->rpc || (c->ldjt == gram_ld(c->n) && c->lddj % 2 == 0 && mass_smem(c) <= 220 * 1024)) {
     launch(c, k_assemble_mass, dim3(c->nchM, c->n_sims), 256, mass_smem(c), (const double*)c->Jt.p, c->ldjt,
            (const double*)c->dJ.p, c->lddj, (const double*)c->mass.p, c->N, c->n, c->n_p, c->rpcM, c->nchM,
-           c->alpha * dt, c->partA.p);
+           c->alpha * dt, c->partA.p, c->cpmM);
   } else {
     assemble_launch(c, s, dt, drop_fict, 1);
   }
@@ -1295,6 +1297,14 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       while (c->rpcM > 16 && mass_smem(c) > 200 * 1024) c->rpcM /= 2;
     }
     c->nchM = ceil_div(N, c->rpcM);
+    if (c->ldjt == gram_ld(c->n) && c->lddj % 2 == 0 && c->n_sims > 1 && !getenv("NLROM_NO_CPM")) {
+      // many sims: a CTA walks several row chunks of its sim (>= ~2 waves of 2 CTAs per SM)
+      const int rows_ch = c->nchM;
+      c->cpmM = (int)std::max(1LL, std::min<long long>(rows_ch, (long long)c->n_sims * rows_ch / (148 * 2 * 2)));
+      if (getenv("NLROM_CPM")) c->cpmM = std::max(1, std::min(rows_ch, atoi(getenv("NLROM_CPM"))));
+      if (mass_smem(c) > 200 * 1024) c->cpmM = 1;
+      c->nchM = ceil_div(rows_ch, c->cpmM);
+    }
     const int n = c->n, S = c->n_sims;
     c->a.alloc((size_t)S * N);
     c->partA.alloc((size_t)S * std::max(c->nchA, c->nchM) * n * n);

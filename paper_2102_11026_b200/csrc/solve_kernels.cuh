@@ -113,14 +113,18 @@ __global__ void k_assemble(AsmArgs A) {
   if (A.mode != 1) gram_dmma(Js, ldp, Rs + n, ldp, RC, n, 1, Pp, 1);
 }
 
-// Mass block of the system matrix for one chunk of RC rows (the side-branch half of the
-// assembly, mode 1 of k_assemble): partA[chunk] = J~_rows^T M [(1+ah) U, (1+ah) J + dJ]_rows.
-// J~ rows (global pitch ldjt == the Gram panel pitch), dJ rows and the masses land by three TMA
-// bulk copies; the Gram product runs on the DMMA pipe.
+// Mass block of the system matrix for chunks of RC rows (the side-branch half of the assembly,
+// mode 1 of k_assemble): partA[p] = sum over the CTA's cpm row chunks of
+// J~_rows^T M [(1+ah) U, (1+ah) J + dJ]_rows. J~ rows (global pitch ldjt == the Gram panel pitch),
+// dJ rows and the masses land by three TMA bulk copies per chunk (one mbarrier phase each); the
+// Gram product runs on the DMMA pipe. cpm > 1 (many sims): the Gram accumulates in shared
+// memory and each CTA writes one partial (nchunk = partials per sim), so the partial traffic and
+// its reduction shrink by cpm.
 __global__ void __launch_bounds__(256) k_assemble_mass(const double* __restrict__ Jt, int ldjt,
                                                        const double* __restrict__ dJ, int lddj,
                                                        const double* __restrict__ mass, int N, int n, int n_p,
-                                                       int RC, int nchunk, double ah, double* __restrict__ part) {
+                                                       int RC, int nchunk, double ah, double* __restrict__ part,
+                                                       int cpm) {
   pdl_wait();
   pdl_launch();
   extern __shared__ __align__(16) double sh[];
@@ -130,32 +134,48 @@ __global__ void __launch_bounds__(256) k_assemble_mass(const double* __restrict_
   double* Ds = Rs + (size_t)RC * ldp;  // [RC][lddj]
   double* ms = Ds + (size_t)RC * lddj; // [RC]
   uint64_t* bar = reinterpret_cast<uint64_t*>(ms + RC);
-  const int chunk = blockIdx.x, sim = blockIdx.y, tid = threadIdx.x;
-  const int row0 = chunk * RC, nrow = min(RC, N - row0);
+  double* Kacc = reinterpret_cast<double*>(bar + 2);  // [n][n] when cpm > 1
+  const int sim = blockIdx.y, tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    const uint32_t bj = (uint32_t)(nrow * ldjt * 8), bd = (uint32_t)(nrow * lddj * 8), bm = (uint32_t)(nrow * 8);
-    mbar_expect_tx(bar, bj + bd + (nrow % 2 == 0 ? bm : 0));
-    tma_g2s(Js, Jt + ((size_t)sim * N + row0) * ldjt, bj, bar);
-    tma_g2s(Ds, dJ + ((size_t)sim * N + row0) * lddj, bd, bar);
-    if (nrow % 2 == 0) tma_g2s(ms, mass + row0, bm, bar);
   }
-  if (nrow % 2 != 0)
-    for (int i = tid; i < nrow; i += blockDim.x) ms[i] = mass[row0 + i];
-  for (int t = tid; t < (RC - nrow) * ldp; t += blockDim.x) {  // zero tail rows of the last chunk
-    Js[(size_t)nrow * ldp + t] = 0.0;
-    Rs[(size_t)nrow * ldp + t] = 0.0;
+  for (int ck = 0; ck < cpm; ++ck) {
+    const int chunk = blockIdx.x * cpm + ck;
+    const int row0 = chunk * RC;
+    if (row0 >= N) break;  // uniform over the CTA
+    const int nrow = min(RC, N - row0);
+    __syncthreads();  // barrier init visible; the previous chunk's Gram is done with Js / Rs
+    if (tid == 0) {
+      fence_proxy_async();
+      const uint32_t bj = (uint32_t)(nrow * ldjt * 8), bd = (uint32_t)(nrow * lddj * 8), bm = (uint32_t)(nrow * 8);
+      mbar_expect_tx(bar, bj + bd + (nrow % 2 == 0 ? bm : 0));
+      tma_g2s(Js, Jt + ((size_t)sim * N + row0) * ldjt, bj, bar);
+      tma_g2s(Ds, dJ + ((size_t)sim * N + row0) * lddj, bd, bar);
+      if (nrow % 2 == 0) tma_g2s(ms, mass + row0, bm, bar);
+    }
+    if (nrow % 2 != 0)
+      for (int i = tid; i < nrow; i += blockDim.x) ms[i] = mass[row0 + i];
+    for (int t = tid; t < (RC - nrow) * ldp; t += blockDim.x) {  // zero tail rows of the last chunk
+      Js[(size_t)nrow * ldp + t] = 0.0;
+      Rs[(size_t)nrow * ldp + t] = 0.0;
+    }
+    __syncthreads();
+    mbar_wait(bar, (uint32_t)(ck & 1));
+    for (int t = tid; t < nrow * n; t += blockDim.x) {
+      const int rl = t / n, j = t % n;
+      const double dj = (j >= n_p) ? Ds[rl * lddj + (j - n_p)] : 0.0;
+      Rs[rl * ldp + j] = ((1.0 + ah) * Js[rl * ldp + j] + dj) * ms[rl];
+    }
+    __syncthreads();
+    if (cpm == 1) gram_dmma(Js, ldp, Rs, ldp, RC, n, n, part + ((size_t)sim * nchunk + blockIdx.x) * n * n, n);
+    else gram_dmma(Js, ldp, Rs, ldp, RC, n, n, Kacc, n, ck > 0);  // warp-owned tiles: no race
   }
-  __syncthreads();
-  mbar_wait(bar, 0);
-  for (int t = tid; t < nrow * n; t += blockDim.x) {
-    const int rl = t / n, j = t % n;
-    const double dj = (j >= n_p) ? Ds[rl * lddj + (j - n_p)] : 0.0;
-    Rs[rl * ldp + j] = ((1.0 + ah) * Js[rl * ldp + j] + dj) * ms[rl];
+  if (cpm > 1) {
+    __syncthreads();
+    double* P = part + ((size_t)sim * nchunk + blockIdx.x) * n * n;
+    for (int t = tid; t < n * n; t += blockDim.x) P[t] = Kacc[t];
   }
-  __syncthreads();
-  gram_dmma(Js, ldp, Rs, ldp, RC, n, n, part + ((size_t)sim * nchunk + chunk) * n * n, n);
 }
 
 // The critical-path half of the assembly for one chunk of RC <= 128 rows, with the weighted

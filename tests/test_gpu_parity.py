@@ -233,6 +233,7 @@ def test_multi_sim(cfg1, batched, monkeypatch):
     if batched == "cpc":  # + the shared-real vhp backward (default only at >= 4 waves of CTAs)
         monkeypatch.setenv("NLROM_CPC", "4")
         monkeypatch.setenv("NLROM_SHARED_REAL", "1")
+        monkeypatch.setenv("NLROM_CPM", "4")  # mass block: 4 row chunks per CTA
     if batched == "sharedcp":  # shared-real vhp backward on the cp.async GEMM
         monkeypatch.setenv("NLROM_SHARED_REAL", "1")
         monkeypatch.setenv("NLROM_BWD_WS", "0")
