@@ -977,6 +977,17 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
     }
     return;
   }
+  // look-ahead pivot search (k_lu_la): bitwise identical, slower in the cfg2 graph (38.8 vs
+  // 30.7 us, tools/lu_rank2_check.py NLROM_LU_LA): opt-in only
+  static const bool lookahead = getenv("NLROM_LU_LA") != nullptr;
+  if (lookahead) {
+    switch (lu_nb(n + nx)) {
+      case 4: go(k_lu_la<4>); break;
+      case 6: go(k_lu_la<6>); break;
+      default: go(k_lu_la<8>); break;
+    }
+    return;
+  }
   switch (lu_nb(n + nx)) {
     case 4: go(k_lu_solve<4>); break;
     case 6: go(k_lu_solve<6>); break;
@@ -1348,6 +1359,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_la<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_la<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_la<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

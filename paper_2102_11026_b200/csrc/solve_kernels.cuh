@@ -546,6 +546,201 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
   if (tid == 0) status[sim] = 0;
 }
 
+// Look-ahead form of k_lu_solve (same arithmetic, same pivots, bitwise equal results): the
+// pivot search and reciprocal of step k + 1 run before step k's barrier on a register copy of
+// column k + 1 that every warp updates itself, so the barrier -> argmax -> 1/p -> update chain
+// of the row-block kernel loses its argmax and 1/p legs. Column k + 1 as of step k - 1 is read
+// from a double-buffered side copy (nxt) written by its owners, never from M, which the owners
+// overwrite during step k.
+template <int NB>
+__global__ void __launch_bounds__(256) k_lu_la(const double* __restrict__ S, const double* __restrict__ phi,
+                                                   double* __restrict__ dr, double* __restrict__ r, int n, int apply,
+                                                   int* __restrict__ status, const double* __restrict__ xrhs, int nx,
+                                                   double* __restrict__ xout, const double* __restrict__ Gt, int ldg,
+                                                   int n_p) {
+  // every input waits: in a captured graph the event edge from the side branch (S_base, phi)
+  // into this PDL launch is programmatic too, so nothing is complete before the wait
+  pdl_wait();
+  pdl_launch();
+  constexpr int D = 16 * NB;           // covered rows / columns (n + 1 <= D)
+  constexpr int LDF = D + 1;
+  extern __shared__ double M[];        // [D][LDF] | vhp block [n_q][n_q]
+  __shared__ int pivrow[D];
+  __shared__ double rdiag[D];
+  __shared__ double nxt[2][D];          // column k + 1 as of the end of step k - 1 (slot (k + 1) & 1)
+  const int sim = blockIdx.x;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31;
+  const double* Ss = S + (size_t)sim * n * n;
+  const int nq = n - n_p;
+  double* Vs = M + D * LDF;            // vhp[k][i] = G_t[2k+1][i] (k_reduce_S without G_t built S_base)
+  // stage [S | phi | extra rhs] and the vhp block with async copies (one round trip for all)
+  for (int idx = tid; idx < D * D; idx += 256) {
+    const int i = idx / D, j = idx % D;
+    double* dst = M + i * LDF + j;
+    if (i < n && j < n) cp_async8(dst, Ss + (size_t)i * n + j);
+    else if (i < n && j == n) cp_async8(dst, phi + (size_t)sim * n + i);
+    else if (i < n && j > n && j <= n + nx) cp_async8(dst, xrhs + ((size_t)sim * nx + (j - n - 1)) * n + i);
+    else *dst = 0.0;
+  }
+  if (Gt)
+    for (int idx = tid; idx < nq * nq; idx += 256) {
+      const int k = idx / nq, i = idx % nq;
+      cp_async8(Vs + idx, Gt + ((size_t)sim * 2 * nq + 2 * k + 1) * ldg + i);
+    }
+  cp_async_all_wait();
+  __syncthreads();
+  double A[NB][NB];
+#pragma unroll
+  for (int a = 0; a < NB; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int i = ty + 16 * a, j = tx + 16 * b;
+      double v = M[i * LDF + j];
+      if (j == n) v = -v;  // rhs = -phi
+      if (Gt && i >= n_p && j >= n_p && i < n && j < n) v += Vs[(j - n_p) * nq + (i - n_p)];  // S_base + diag(0, vhp)
+      A[a][b] = v;
+    }
+  __syncthreads();
+  // the shared copy holds the full matrix from here on (the first pivot row is read from it)
+#pragma unroll
+  for (int a = 0; a < NB; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      M[(ty + 16 * a) * LDF + tx + 16 * b] = A[a][b];
+      if (tx + 16 * b == 1) nxt[1][ty + 16 * a] = A[a][b];
+    }
+  // rows >= n are never pivots
+  unsigned long long used_lo = 0ull, used_hi = 0ull;  // rows 0..63, 64..127
+  for (int i = n; i < D; ++i) {
+    if (i < 64) used_lo |= 1ull << i;
+    else used_hi |= 1ull << (i - 64);
+  }
+  auto is_used = [&](int i) -> bool {
+    return i < 64 ? ((used_lo >> i) & 1ull) : ((used_hi >> (i - 64)) & 1ull);
+  };
+  bool bad = false;
+  __syncthreads();
+#ifdef LU_CYCLES
+  if (tid == 0) g_lu_cycles[0] = clock64();
+#endif
+  // argmax of |c| over the unused rows lane + 32u (LAPACK idamax ties: lowest row); the pivot
+  // value comes back from its owner lane, bitwise the element the row-block update stores
+  constexpr int U = D / 32;
+  auto find_pivot = [&](const double (&c)[U], int& piv, double& pv) -> bool {
+    double best = -1.0;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = lane + 32 * u;
+      if (!is_used(i)) {
+        const double v = fabs(c[u]);
+        if (v > best) { best = v; bi = i; }
+      }
+    }
+    const unsigned long long key = (best >= 0.0) ? (unsigned long long)__double_as_longlong(best) : 0ull;
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    piv = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)bi : 0x7fffffffu);
+    if (!(mhi | mlo) || piv >= n) return false;
+    double sel = c[0];
+#pragma unroll
+    for (int u = 1; u < U; ++u)
+      if ((piv >> 5) == u) sel = c[u];
+    pv = __shfl_sync(0xffffffffu, sel, piv & 31);
+    if (piv < 64) used_lo |= 1ull << piv;
+    else used_hi |= 1ull << (piv - 64);
+    return true;
+  };
+  double c0[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) c0[u] = M[(lane + 32 * u) * LDF];
+  int piv;
+  double rp;
+  {
+    double pv;
+    if (n > 0 && !find_pivot(c0, piv, pv)) bad = true;
+    else rp = recip_fast(pv);
+  }
+  for (int k = 0; k < n && !bad; ++k) {
+    // step k's pivot (piv, rp) and column k (c0) were found during step k - 1: every warp
+    // updates column k + 1 for its rows itself (the same fma the row-block owners do) and
+    // searches step k + 1's pivot before the barrier instead of after it
+    if (tid == 0) {
+      pivrow[k] = piv;
+      rdiag[k] = rp;
+    }
+    const bool ahead = k + 1 < n;
+    const double* prow = M + piv * LDF;
+    double pr[NB], l[NB], c1[U];
+    bool act[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) pr[b] = prow[tx + 16 * b];
+#pragma unroll
+    for (int a = 0; a < NB; ++a) {
+      const int i = ty + 16 * a;
+      act[a] = (i < n) && (i != piv);  // Gauss-Jordan: every row but the pivot row is eliminated
+      l[a] = M[i * LDF + k];
+    }
+    const double p1 = ahead ? prow[k + 1] : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) c1[u] = nxt[(k + 1) & 1][lane + 32 * u];
+    // step k + 1's pivot chain first: the trailing update below is independent of it and
+    // fills the REDUX / shuffle / reciprocal latencies
+    int piv_n = piv;
+    double rp_n = rp;
+    if (ahead) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = lane + 32 * u;
+        if (i < n && i != piv) c1[u] = fma(-(c0[u] * rp), p1, c1[u]);
+        c0[u] = c1[u];
+      }
+      double pv;
+      if (!find_pivot(c0, piv_n, pv)) { bad = true; break; }
+      rp_n = recip_fast(pv);
+    }
+#pragma unroll
+    for (int a = 0; a < NB; ++a) {
+      const int i = ty + 16 * a;
+      const double la = l[a] * rp;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (NB > 4 && 16 * b + 15 <= k) continue;  // column block already eliminated (uniform)
+        const int j = tx + 16 * b;
+        if (act[a] && j > k) {
+          A[a][b] = fma(-la, pr[b], A[a][b]);
+          M[i * LDF + j] = A[a][b];
+        }
+        if (j == k + 2) nxt[k & 1][i] = A[a][b];
+      }
+    }
+    piv = piv_n;
+    rp = rp_n;
+    __syncthreads();
+  }
+#ifdef LU_CYCLES
+  if (tid == 0) g_lu_cycles[1] = clock64();
+#endif
+  if (bad) {
+    if (tid == 0) status[sim] = 1;
+    return;
+  }
+  // Gauss-Jordan: the pivot rows form a diagonal system, x_k = rhs[piv_k] / a[piv_k][k]
+  // (no sequential back substitution). Column n is -phi, columns n+1.. the extra right-hand sides.
+  for (int t = tid; t < n * (1 + nx); t += blockDim.x) {
+    const int kk = t % n, col = t / n;
+    const double x = M[pivrow[kk] * LDF + n + col] * rdiag[kk];
+    if (col == 0) {
+      dr[(size_t)sim * n + kk] = x;
+      if (apply) r[(size_t)sim * n + kk] += x;
+    } else {
+      xout[((size_t)sim * nx + col - 1) * n + kk] = x;
+    }
+  }
+  if (tid == 0) status[sim] = 0;
+}
+
 // Column-cyclic variant for n <= 64 and n + 1 + nx <= 72 columns: warp w owns columns
 // w, w + 8, ...; lane holds rows lane and lane + 32 of them in registers. Pivot step k is
 // produced by ONE warp (the owner of column k: pivot search with REDUX, reciprocal,

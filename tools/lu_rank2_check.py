@@ -1,5 +1,6 @@
-"""Bitwise comparison of the rank-2 LU (NLROM_LU_RANK2=1, csrc/lu_rank2.cuh) with the default
-row-block LU over 3 fixed-iteration steps on several configs (fresh process per variant)."""
+"""Bitwise comparison of an opt-in LU variant with the default row-block LU over 3
+fixed-iteration steps on several configs (fresh process per variant). Variant = the env switch
+in argv[1]: NLROM_LU_RANK2 (csrc/lu_rank2.cuh, the default) or NLROM_LU_LA (k_lu_la)."""
 import os, sys, subprocess, numpy as np
 root = "/root/repo" if os.path.exists("/root/repo") else os.environ["GRAFT_REPO_ROOT"]
 code = r'''
@@ -17,10 +18,11 @@ for name, kw in [("cfg2", {}), ("cfg1", {}), ("cfg2", {"n_q": 31}), ("cfg2", {"n
     out[name + str(kw)] = st.r
 np.savez(sys.argv[2], **{k.replace(" ", ""): v for k, v in out.items()})
 '''
+VAR = sys.argv[1] if len(sys.argv) > 1 else "NLROM_LU_RANK2"
 res = {}
 for env in ("0", "1"):
     e = dict(os.environ)
-    if env == "1": e["NLROM_LU_RANK2"] = "1"
+    if env == "1": e[VAR] = "1"
     f = f"/tmp/lu_{env}.npz"
     subprocess.run([sys.executable, "-c", code, root, f], env=e, check=True)
     res[env] = np.load(f)
