@@ -166,8 +166,9 @@ NLROM_API int nlrom_fictitious_force(nlrom_ctx* ctx, const double* q, const doub
 
 /* neucubature: wnet_forward restricted to C and
  * cubature_integrate: f_red (n), K_red (n,n) row-major,
- * integration 0 = cubature, 1 = exact_sum (C = all elements, w = 1). */
-NLROM_API int nlrom_wnet_forward(nlrom_ctx* ctx, const double* r, double* w_cub);
+ * integration 0 = cubature, 1 = exact_sum (C = all elements, w = 1).
+ * w_cub holds w_len doubles; w_len must equal |C| (NLROM_ERR_DIM otherwise). */
+NLROM_API int nlrom_wnet_forward(nlrom_ctx* ctx, const double* r, double* w_cub, int64_t w_len);
 NLROM_API int nlrom_cubature_integrate(nlrom_ctx* ctx, const double* r, int integration, double* f_red, double* K_red);
 
 /* elastic: per-element StVK forces of a full-space displacement u (N,):

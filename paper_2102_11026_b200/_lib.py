@@ -106,7 +106,7 @@ def lib():
             "nlrom_system_jacobian": (C.c_int, [vp, dp, dp, dp, dp, C.POINTER(SimCfg), dp]),
             "nlrom_delta_j": (C.c_int, [vp, dp, dp, dp, C.c_double, C.c_int, dp]),
             "nlrom_fictitious_force": (C.c_int, [vp, dp, dp, dp]),
-            "nlrom_wnet_forward": (C.c_int, [vp, dp, dp]),
+            "nlrom_wnet_forward": (C.c_int, [vp, dp, dp, C.c_int64]),
             "nlrom_cubature_integrate": (C.c_int, [vp, dp, C.c_int, dp, dp]),
             "nlrom_full_displacement": (C.c_int, [vp, dp, dp]),
             "nlrom_jtilde": (C.c_int, [vp, dp, dp]),

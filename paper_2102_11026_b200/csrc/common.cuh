@@ -32,9 +32,14 @@ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 constexpr int kNoBudget = 1 << 30;
 inline int& launch_budget() { static int b = kNoBudget; return b; }
 inline std::vector<const void*>& launch_log() { static std::vector<const void*> v; return v; }
-// Timing experiments only: NLROM_DEBUG_SKIP=name1,name2 drops every launch whose kernel name
-// contains one of the substrings (results are then wrong; used to find the critical path).
+// Timing experiments only, compiled in with -DNLROM_TIMING_EXPERIMENTS (never in the release
+// library): NLROM_DEBUG_SKIP=name1,name2 drops every launch whose kernel name contains one of
+// the substrings (results are then wrong; used to find the critical path).
 inline bool launch_skipped(const void* fn) {
+#ifndef NLROM_TIMING_EXPERIMENTS
+  (void)fn;
+  return false;
+#else
   static const char* env = getenv("NLROM_DEBUG_SKIP");
   if (!env || !*env) return false;
   const char* name = nullptr;
@@ -49,6 +54,7 @@ inline bool launch_skipped(const void* fn) {
     pos = e + 1;
   }
   return false;
+#endif
 }
 inline bool launch_gate(const void* fn) {
   if (launch_skipped(fn)) return false;

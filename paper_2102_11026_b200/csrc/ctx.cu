@@ -19,9 +19,6 @@
 #include "epilogues.cuh"
 #include "sim_kernels.cuh"
 #include "solve_kernels.cuh"
-#include "lu_warp.cuh"
-#include "lu_split.cuh"
-#include "lu_rank2.cuh"
 #include "mlp_chain.cuh"
 #include "coupled_kernels.cuh"
 #include "gemm_ws.cuh"
@@ -60,10 +57,55 @@ struct CubSet {
 
 int gemm_launch_count = 0;
 
+// Code-path overrides for tests: NLROM_PATH = comma-separated tokens, read once per context.
+// Every token selects a correct, tested path that the size heuristics would otherwise pick only
+// at other problem sizes (so small tests can cover the cfg5-scale kernels):
+//   batched         many-sims big-tile per-layer GEMMs (default when n_sims (4 + 4 n_q) >= 2048)
+//   unfused         per-layer GEMMs instead of the cluster-fused hidden / vhp chains
+//   hid_cp          cp.async big-tile hidden layers instead of the warp-specialised TMA kernel
+//   bwd_cp          cp.async big-tile shared-real vhp layers instead of the TMA kernel
+//   shared_real     shared-real vhp backward even below 4 waves of CTAs
+//   no_shared_real  2 n_q dual columns per sim in the batched vhp backward
+//   cpc=K, cpm=K    element / mass row chunks walked per CTA (many sims)
+//   tangents=K      jet tangents per column group (1, 3, 5, 7 or 15)
+struct PathOpts {
+  bool batched = false, unfused = false, hid_cp = false, bwd_cp = false, shared_real = false,
+       no_shared_real = false;
+  int cpc = 0, cpm = 0, tangents = 0;
+  static PathOpts from_env() {
+    PathOpts o;
+    const char* env = getenv("NLROM_PATH");
+    if (!env) return o;
+    std::string list(env);
+    size_t pos = 0;
+    while (pos <= list.size()) {
+      size_t e = list.find(',', pos);
+      if (e == std::string::npos) e = list.size();
+      const std::string tok = list.substr(pos, e - pos);
+      const size_t eq = tok.find('=');
+      const std::string key = tok.substr(0, eq);
+      const int val = eq == std::string::npos ? 1 : atoi(tok.c_str() + eq + 1);
+      if (key == "batched") o.batched = true;
+      else if (key == "unfused") o.unfused = true;
+      else if (key == "hid_cp") o.hid_cp = true;
+      else if (key == "bwd_cp") o.bwd_cp = true;
+      else if (key == "shared_real") o.shared_real = true;
+      else if (key == "no_shared_real") o.no_shared_real = true;
+      else if (key == "cpc") o.cpc = val;
+      else if (key == "cpm") o.cpm = val;
+      else if (key == "tangents") o.tangents = val;
+      else if (!key.empty()) throw Error(NLROM_ERR_ARG, "unknown NLROM_PATH token: " + key);
+      pos = e + 1;
+    }
+    return o;
+  }
+};
+
 }  // namespace
 
 struct nlrom_ctx {
   int device = 0;
+  PathOpts opt;
   cudaStream_t st = nullptr, st2 = nullptr, st3 = nullptr;
   cudaEvent_t evFork = nullptr, evJoin = nullptr, evFork2 = nullptr, evJoin2 = nullptr;
   cudaEvent_t evWf = nullptr, evW = nullptr;  // early weight net: fork after the hidden chain, join before the cubature
@@ -106,14 +148,8 @@ struct nlrom_ctx {
   int rpc = 128, nchA = 0;
   int nchAa = 0, nphi = 0;     // k_assemble_a chunks (32 rows) when it also forms the vhp seed; partPhi chunks
   bool agemv = false;          // the last assemble_phase produced the vhp-chain seed partials
-  // split LU (lu_split.cuh): front n_p pivot steps on a side branch, back steps after the vhp
-  DBuf luF, luRd;
-  IBuf luPiv, luFlag;
-  int luFC = 0;
-  bool lu_front_done = false;
   int rpcM = 128, nchM = 0;  // row chunking of the mass block (finer: more CTAs for its Gram)
   int cpmM = 1;              // mass-block row chunks per CTA (nchM = partials per sim)
-  int s_ctas = getenv("NLROM_S_CTAS") ? atoi(getenv("NLROM_S_CTAS")) : 1 << 20;  // side-branch S reduction CTAs
   DBuf a, partA, partPhi, phi, norm, S, dr, r, rbar, rdbar, fext, rsave, rdot, tmpN;
   IBuf status;
   // backward
@@ -131,12 +167,6 @@ struct nlrom_ctx {
   HBuf hin, hout;  // pinned staging of nlrom_step's host inputs / outputs
   // substructured scene (coupled_kernels.cuh): strings of this rank + replicated core
   bool coupled = false;
-  // mass block on a side branch beside the weight net (default) or, with NLROM_MASS_LATE, beside
-  // the vhp chain (measured slower: the 16-CTA clusters cannot co-schedule with it)
-  bool mass_early = getenv("NLROM_MASS_LATE") == nullptr;
-  // 1 (default): forked after the cubature, beside the assembly; 0: beside the weight net (measured
-  // slower: it contends with the cubature for SMs)
-  int mass_pos = getenv("NLROM_MASS_POS") ? atoi(getenv("NLROM_MASS_POS")) : 1;
   DBuf cpR, cpFloc, cpFsum, cpCore, cpBlocks, cpCb, cpX, cpFcore;
   double cp_m_core = 0, cp_k_core = 0, cp_m_string = 0, cp_m_total = 0;
   cudaGraphExec_t gC[2] = {nullptr, nullptr};
@@ -173,14 +203,11 @@ int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL
 
 // ---------------------------------------------------------------- GEMM dispatch
 template <class Epi>
-void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st, bool big = false) {
+void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st, bool big = false, bool cp_async = false) {
   // big-tile hidden layers on the warp-specialised TMA pipeline (16 consumer warps, 4 stages):
-  // cfg5 hidden layers 14.76 -> 14.51 ms; NLROM_HID_WS=0 selects the cp.async CfgBig kernel,
-  // 2 an 8-consumer-warp variant (slower: 15.84 ms)
-  static const int hid_ws = getenv("NLROM_HID_WS") ? atoi(getenv("NLROM_HID_WS")) : 1;
-  if (big && 128 % G == 0 && hid_ws && g.K % 16 == 0 && g.lda % 2 == 0 && g.ldb % 2 == 0) {
-    if (hid_ws == 1) launch_gemm_ws<WsCfg<64, 128, 4, 4, 4>>(g, e, st);
-    else launch_gemm_ws<WsCfg<64, 128, 2, 4, 4>>(g, e, st);
+  // cfg5 hidden layers 14.76 -> 14.51 ms vs the cp.async CfgBig kernel (NLROM_PATH=hid_cp)
+  if (big && 128 % G == 0 && !cp_async && g.K % 16 == 0 && g.lda % 2 == 0 && g.ldb % 2 == 0) {
+    launch_gemm_ws<WsCfg<64, 128, 4, 4, 4>>(g, e, st);
     ++gemm_launch_count;
     return;
   }
@@ -212,10 +239,10 @@ void out_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st) {
   ++gemm_launch_count;
 }
 
-void choose_groups(int n_q, int width, bool batched, int& G, int& gps) {
+void choose_groups(int n_q, int width, bool batched, int forced, int& G, int& gps) {
   const int cand[5] = {1, 3, 5, 7, 15};
   int g = 3;
-  if (const char* env = getenv("NLROM_JET_TANGENTS")) g = atoi(env);
+  if (forced > 0) g = forced;
   else if (batched) {
     // big 128-column tiles: G | 128, fewest executed columns G * ceil(n_q / g)
     int best = 1 << 30;
@@ -233,7 +260,7 @@ void choose_groups(int n_q, int width, bool batched, int& G, int& gps) {
   }
   bool ok = false;
   for (int c : cand) ok |= (c == g);
-  if (!ok) throw Error(NLROM_ERR_ARG, "NLROM_JET_TANGENTS must be one of 1,3,5,7,15");
+  if (!ok) throw Error(NLROM_ERR_ARG, "jet tangents per group must be one of 1,3,5,7,15");
   G = 4 + 4 * g;
   gps = (n_q + g - 1) / g;
   (void)width;
@@ -292,7 +319,7 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
       (size_t)(2 * s.epc * 12 * gram_ld(n) + s.epc * 162 + n * n + n) * 8 <= 200 * 1024) {
     const long long ctas = (long long)c->n_sims * s.nech;
     s.cpc = (int)std::max(1LL, std::min<long long>(s.nech, ctas / (148 * 3 * 2)));
-    if (getenv("NLROM_CPC")) s.cpc = std::max(1, std::min(s.nech, atoi(getenv("NLROM_CPC"))));
+    if (c->opt.cpc > 0) s.cpc = std::max(1, std::min(s.nech, c->opt.cpc));
   }
   s.nchunk = ceil_div(s.nech, s.cpc);
   s.fe_w.alloc((size_t)c->n_sims * std::max(s.n, 1) * 12);
@@ -310,32 +337,18 @@ using CfgOutC = GemmCfg<48, 128, 2, 4, 1, 32, 3>;
 using CfgOutWs = WsCfg<48, 128, 3, 4, 6>;  // 12 consumer warps (16 x 32 warp tiles): best of the probe
 // <= 64 output columns (one sim at n_q <= 31: 2 + 2 n_q columns): half-width tiles, so no DMMA
 // work is spent on padding columns
-// (24 x 64 tiles: 280 CTAs, ~2 per SM: 7.9 us in the cfg2 graph vs 12.1 us for 48 x 128 over the
-// same 62 columns and 16.4 us for 48 x 64; NLROM_OUT_TILE selects 0: 48x128, 1: 48x64, 3: 16x64)
-using CfgOutWs64 = WsCfg<48, 64, 3, 2, 6>;
-using CfgOutWs64b = WsCfg<24, 64, 3, 2, 6>;
+// (16 x 64 tiles, 420 CTAs: fastest of 48x128 / 48x64 / 24x64 / 16x64 / 8x64 in the cfg2 graph)
 using CfgOutWs64c = WsCfg<16, 64, 2, 2, 6>;
-using CfgOutWs64d = WsCfg<8, 64, 1, 2, 6>;
 
 void output_layer(nlrom_ctx* c) {
   GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->next, 0, 0};
   EpiJetOutC e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
                c->n_p, c->n_q};
-  // batched output layer on the warp-specialised pipeline: measured slower at cfg5 (3.38 / 3.39 ms
-  // vs 3.06 ms for CfgBig: the EpiJetOutC scatter dominates the tile), opt-in only
-  static const int out_ws = getenv("NLROM_OUT_BIG_WS") ? atoi(getenv("NLROM_OUT_BIG_WS")) : 0;
-  if (c->batched && out_ws && c->ldlast % 2 == 0 && (c->wL1 + c->next) % 16 == 0) {
-    if (out_ws == 1) launch_gemm_ws<WsCfg<64, 128, 4, 4, 4>>(g, e, c->st);
-    else launch_gemm_ws<WsCfg<48, 128, 3, 4, 6>>(g, e, c->st);
-  } else if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
-  else if (c->ldlast % 2 == 0 && !getenv("NLROM_NO_WS_GEMM")) {
-    static const int tile = getenv("NLROM_OUT_TILE") ? atoi(getenv("NLROM_OUT_TILE")) : 3;
-    if (g.C <= 64 && tile == 1) launch_gemm_ws<CfgOutWs64>(g, e, c->st);
-    else if (g.C <= 64 && tile == 2) launch_gemm_ws<CfgOutWs64b>(g, e, c->st);
-    else if (g.C <= 64 && tile == 3) launch_gemm_ws<CfgOutWs64c>(g, e, c->st);
-    else if (g.C <= 64 && tile == 4) launch_gemm_ws<CfgOutWs64d>(g, e, c->st);
-    else launch_gemm_ws<CfgOutWs>(g, e, c->st);
-  }
+  // batched: the cp.async big-tile kernel (the warp-specialised pipeline measured slower here:
+  // 3.38 vs 3.06 ms at cfg5, the EpiJetOutC scatter dominates the tile)
+  if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
+  else if (c->ldlast % 2 == 0 && g.C <= 64) launch_gemm_ws<CfgOutWs64c>(g, e, c->st);
+  else if (c->ldlast % 2 == 0) launch_gemm_ws<CfgOutWs>(g, e, c->st);
   else launch_gemm<CfgOutC>(g, e, c->st);
   ++gemm_launch_count;
 }
@@ -343,14 +356,12 @@ void output_layer(nlrom_ctx* c) {
 // Fused hidden chain (mlp_chain.cuh): one cluster of CS CTAs per column group.
 template <int R, int G, int CS>
 bool launch_mlp_fwd(nlrom_ctx* c, const MlpFwdArgs& a) {
-  // DSMEM stores + cluster barrier per layer; NLROM_ASYNC_CHAIN=1 selects the st.async /
-  // per-source mbarrier / TMA-weight variant (correct, but slower at cfg2 so far:
-  // tools/probes/chain_probe.cu)
-  static const bool sync_chain = getenv("NLROM_ASYNC_CHAIN") == nullptr;
+  // DSMEM stores + cluster barrier per layer (the st.async / per-source mbarrier variant measured
+  // slower at cfg2: tools/probes/retired/mlp_chain_async.cuh)
   const int kmax = std::max(c->wL1, c->n_q);
-  const size_t smem = sync_chain ? MlpPlan<R, G>::bytes(kmax) : MlpAsyncPlan<R, G, CS>::bytes(kmax);
+  const size_t smem = MlpPlan<R, G>::bytes(kmax);
   if (smem > 227 * 1024) return false;
-  auto kern = sync_chain ? k_mlp_jet_fwd<R, G, CS> : k_mlp_jet_fwd_async<R, G, CS>;
+  auto kern = k_mlp_jet_fwd<R, G, CS>;
   static bool configured = false;
   if (!configured) {
     NL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -378,7 +389,7 @@ bool launch_mlp_fwd(nlrom_ctx* c, const MlpFwdArgs& a) {
 }
 
 bool fused_hidden_forward(nlrom_ctx* c, double dt, int drop_fict) {
-  if (getenv("NLROM_NO_FUSED_MLP") || getenv("NLROM_NO_FUSED_FWD") || c->batched) return false;
+  if (c->opt.unfused || c->batched) return false;
   const int L1 = c->L - 1, w = c->wL1;
   if (L1 < 1 || L1 > MLP_MAXL) return false;
   for (int l = 1; l <= L1; ++l)
@@ -426,7 +437,7 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
     const int compact = (l == c->L - 2) ? 1 : 0;
     GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
     EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, compact};
-    hid_gemm(c->G, g, e, c->st, c->batched);
+    hid_gemm(c->G, g, e, c->st, c->batched, c->opt.hid_cp);
     in = c->H[l].p;
     ldin = c->ldH[l];
   }
@@ -485,7 +496,7 @@ void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true,
   a.early = (weighted && early) ? 1 : 0;
   size_t smem = (size_t)(2 * s.epc * 12 * gram_ld(c->n) + s.epc * 162 + (a.cpc > 1 ? c->n * c->n + c->n : 0)) * 8;
   // many sims: 3 resident CTAs per SM (80 registers) when the shared memory allows it
-  const bool three = c->n_sims > 1 && smem <= 74 * 1024 && !getenv("NLROM_CUB_MINB2");
+  const bool three = c->n_sims > 1 && smem <= 74 * 1024;
   launch(c, three ? k_cubature<3> : k_cubature<2>, dim3(a.cpc > 1 ? s.nchunk : s.nech, c->n_sims), 256, smem, a);
   if (scatter)
   launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
@@ -537,8 +548,7 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   c->nphi = c->nchA;
   if (c->rpc <= 128 && c->n <= 128) {
     // with the fused vhp chain: 32-row chunks that also form the chain's seed (P W_L)^T a
-    const bool g = fused_vhp_backward(c, true) && c->wL1 <= 256 && c->ldlast % 2 == 0 &&
-                   !getenv("NLROM_SEPARATE_GEMV");
+    const bool g = fused_vhp_backward(c, true) && c->wL1 <= 256 && c->ldlast % 2 == 0;
     const int rc = g ? ASMA_GROWS : c->rpc, nch = g ? c->nchAa : c->nchA;
     AsmAArgs A{c->Jt.p, c->ldjt, c->mass.p, c->hvv.p, c->fext.p, c->r.p, c->rbar.p, c->rdbar.p,
                s.rowptr_full.p, s.entries.p, s.fe_w.p, std::max(s.n, 1), c->a.p, c->partPhi.p,
@@ -558,9 +568,8 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   std::swap(c->st, c->st2);
   launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nphi, c->n,
          c->phi.p, c->norm.p);
-  if (!c->mass_early) mass_block_launch(c, s, dt, drop_fict);  // mass block, overlapping the vhp chain
   const int n = c->n;
-  const int sblocks = std::min(ceil_div(n * n, 32), c->s_ctas);
+  const int sblocks = ceil_div(n * n, 32);
   launch(c, k_reduce_S, dim3(sblocks, c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
          (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, dt, c->S.p);
   std::swap(c->st, c->st2);
@@ -571,8 +580,7 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 // Early weight net: the net's layer 1 is folded onto the hidden chain's output (k_wnet_head), so
 // head + tail run on a side branch concurrently with the output layer instead of after it.
 bool early_wnet_ok(nlrom_ctx* c) {
-  static const bool off = getenv("NLROM_WNET_LATE") != nullptr;
-  return !off && c->wA1.p && !c->batched && c->wn >= 16 && c->wn % 2 == 0 && 256 % c->wn == 0 &&
+  return c->wA1.p && !c->batched && c->wn >= 16 && c->wn % 2 == 0 && 256 % c->wn == 0 &&
          c->wL1 + c->n_p + 1 <= 1024 && c->n_cub > 0 && wnet_head_smem(c->wn, c->wA1ld) <= 220 * 1024;
 }
 
@@ -582,47 +590,7 @@ bool early_wnet_ok(nlrom_ctx* c) {
 //   st2: wnet head -> tail (W) -> [wait K] k_cubature(stiffness) -> [wait M] k_reduce_S
 //   st3: [after the output layer] k_assemble_mass (M) -> [wait A] k_reduce_phi (P)
 //   (st2 and st3 joined before the LU)
-// Opt-in (NLROM_LU_SPLIT=1): correct (tests, tools/probes/lu_split_probe.cu: 1.5e-14 vs the
-// one-shot LU) but slower at cfg2 so far -- the front (30 steps on 96 columns, ~990 cycles per
-// step) cannot start before S_base, which the stiffness Gram and its reduction deliver only ~10 us
-// before the vhp chain ends, so the side branch becomes the critical path (0.138 vs 0.129 ms).
-bool lu_split_ok(nlrom_ctx* c) {
-  static const bool on = getenv("NLROM_LU_SPLIT") != nullptr;
-  return on && !c->coupled && c->n <= 64 && c->n_p >= 1 && c->luFC > 0 && c->luFC <= 128 &&
-         c->n_q + 1 <= 64;
-}
-
-template <int NBC>
-void launch_front_t(nlrom_ctx* c) {
-  LuSplitArgs a{c->n, c->n_p, 0, c->luFC, (const double*)c->S.p, (const double*)c->phi.p, nullptr, c->luF.p,
-                c->luPiv.p, c->luRd.p, c->luFlag.p, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr};
-  launch(c, k_lu_front<NBC>, c->n_sims, 256, LuSplitPlan<NBC>::bytes(0), a);
-}
-
-void launch_lu_front(nlrom_ctx* c) {
-  const int nb = (c->luFC + 15) / 16;
-  if (nb <= 2) launch_front_t<2>(c);
-  else if (nb <= 4) launch_front_t<4>(c);
-  else if (nb <= 6) launch_front_t<6>(c);
-  else launch_front_t<8>(c);
-}
-
-template <int NBC>
-void launch_back_t(nlrom_ctx* c, bool apply) {
-  LuSplitArgs a{c->n, c->n_p, 0, c->luFC, nullptr, nullptr, nullptr, c->luF.p, c->luPiv.p, c->luRd.p, c->luFlag.p,
-                (const double*)c->Gt.p, c->ldGt, c->dr.p, c->r.p, apply ? 1 : 0, c->status.p, nullptr};
-  launch(c, k_lu_back<NBC>, c->n_sims, 256, LuSplitPlan<NBC>::bytes(c->n_q), a);
-}
-
-void launch_lu_back(nlrom_ctx* c, bool apply) {
-  const int nb = (c->n_q + 1 + 15) / 16;
-  if (nb <= 1) launch_back_t<1>(c, apply);
-  else if (nb <= 2) launch_back_t<2>(c, apply);
-  else if (nb <= 3) launch_back_t<3>(c, apply);
-  else launch_back_t<4>(c, apply);
-}
-
-void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s, bool front) {
+void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s) {
   auto on = [&](cudaStream_t& other, auto fn) {
     std::swap(c->st, other);
     fn();
@@ -654,7 +622,7 @@ void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s, bool front)
   cubature_phase(c, sf, true, false, false, 1);
   // a (+ the vhp seed partials) on the critical path; phi and S_base on st2
   c->agemv = false;
-  const bool g = fused_vhp_backward(c, true) && c->wL1 <= 256 && c->ldlast % 2 == 0 && !getenv("NLROM_SEPARATE_GEMV");
+  const bool g = fused_vhp_backward(c, true) && c->wL1 <= 256 && c->ldlast % 2 == 0;
   const int rc = g ? ASMA_GROWS : c->rpc, nch = g ? c->nchAa : c->nchA;
   AsmAArgs A{c->Jt.p, c->ldjt, c->mass.p, c->hvv.p, c->fext.p, c->r.p, c->rbar.p, c->rdbar.p,
              sf.rowptr_full.p, sf.entries.p, sf.fe_w.p, std::max(sf.n, 1), c->a.p, c->partPhi.p,
@@ -675,31 +643,23 @@ void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s, bool front)
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evM, 0));  // the mass block partials
   on(c->st2, [&] {
     const int n = c->n;
-    const int sblocks = std::min(ceil_div(n * n, 32), c->s_ctas);
+    const int sblocks = ceil_div(n * n, 32);
     launch(c, k_reduce_S, dim3(sblocks, c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
            (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
   });
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evP, 0));
-  if (front) {
-    // the first n_p pivot steps of the Newton solve need S_base and phi only (lu_split.cuh)
-    on(c->st2, [&] { launch_lu_front(c); });
-    c->lu_front_done = true;
-  }
   NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));
 }
 
 bool split_phase_ok(nlrom_ctx* c) {
-  static const bool off = getenv("NLROM_NO_SPLIT_E") != nullptr;
-  return !off && c->mass_early && c->rpc <= 128 && c->n <= 128;
+  return c->rpc <= 128 && c->n <= 128;
 }
 
 void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   bool early_w = cfg.integration == 0 && early_wnet_ok(c) && fused_hidden_forward(c, cfg.dt, cfg.drop_fict);
-  c->lu_front_done = false;
   if (early_w && split_phase_ok(c)) {
-    // the LU front only in the one-graph Newton iteration (join_side = false: phase_J follows)
-    phase_E_split(c, cfg, s, !join_side && lu_split_ok(c));
+    phase_E_split(c, cfg, s);
     if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));
     return;
   }
@@ -720,7 +680,6 @@ void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
   } else {
     bundle_forward(c, cfg.dt, cfg.drop_fict);
   }
-  if (c->mass_early && c->mass_pos == 0) mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
   if (early_w) {
     NL_CUDA(cudaStreamWaitEvent(c->st, c->evW, 0));
     cubature_phase(c, s, true, false, /*early=*/false);
@@ -728,7 +687,7 @@ void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
     if (cfg.integration == 0) wnet_phase(c);
     cubature_phase(c, s, cfg.integration == 0, false);  // forces gathered per row by the assembly
   }
-  if (c->mass_early && c->mass_pos == 1) mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
+  mass_block_fork(c, s, cfg.dt, cfg.drop_fict);
   assemble_phase(c, s, cfg.dt, cfg.drop_fict);
   if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));  // phi, S_base (and the mass block)
 }
@@ -750,7 +709,7 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
         split = sp;
         break;
       }
-    if (tiles >= 148 || getenv("NLROM_NO_SPLITK")) split = 1;
+    if (tiles >= 148) split = 1;
     if (split == 1) {
       GemmArgs g{c->AlastT.p, a_vec, c->ldAT, c->N, M, c->n_sims, c->N, 0, 0};
       launch_gemm<CfgBig>(g, EpiStore{c->ybuf.p, M, 0, nullptr, 1, nullptr}, c->st);
@@ -775,7 +734,7 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
   // layout): with few CTAs (cfg4: 25 per layer) fewer, longer tiles are slower (0.92 vs 0.85 ms)
   const long long ctas2 = (long long)ceil_div(c->n_sims * 2 * npass_per_sim, CfgBig::BN) * ceil_div(c->wL1, CfgBig::BM);
   if (NS == 2 && !mc && dcache && c->batched && P1 <= CfgBig::BN &&
-      (ctas2 >= 4 * 148 || getenv("NLROM_SHARED_REAL")) && !getenv("NLROM_NO_SHARED_REAL")) {
+      (ctas2 >= 4 * 148 || c->opt.shared_real) && !c->opt.no_shared_real) {
     // shared real part (EpiBwdShared): 1 + npass columns per sim instead of 2 npass, tiles of
     // whole sims
     const int cstep = (CfgBig::BN / P1) * P1, ncs = c->n_sims * P1;
@@ -786,8 +745,7 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
     for (int l = c->L - 2; l >= 1; --l) {
       GemmArgs g{c->WT[l].p, cur->p, c->ldWT[l], ldcs[l], c->widths[l], ncs, c->widths[l + 1], 0, 0, cstep};
       // warp-specialised TMA pipeline with sim-aligned column tiles: cfg5 vhp 5.14 -> 4.77 ms
-      static const int bwd_ws = getenv("NLROM_BWD_WS") ? atoi(getenv("NLROM_BWD_WS")) : 1;
-      if (bwd_ws && c->widths[l + 1] % 16 == 0 && c->ldWT[l] % 2 == 0 && ldcs[l] % 2 == 0)
+      if (!c->opt.bwd_cp && c->widths[l + 1] % 16 == 0 && c->ldWT[l] % 2 == 0 && ldcs[l] % 2 == 0)
         launch_gemm_ws<WsCfg<64, 128, 4, 4, 4>>(g, EpiBwdShared{nxt->p, ldcs[l - 1], caches[l - 1].p, npass_per_sim},
                                                 c->st);
       else
@@ -876,7 +834,7 @@ bool launch_mlp_bwd(nlrom_ctx* c, MlpBwdArgs a, int dry) {
 
 // check_only: report whether the fused chain applies (nothing launched)
 bool fused_vhp_backward(nlrom_ctx* c, bool check_only) {
-  if (getenv("NLROM_NO_FUSED_MLP") || getenv("NLROM_NO_FUSED_BWD") || c->next || c->batched) return false;
+  if (c->opt.unfused || c->next || c->batched) return false;
   const int L1 = c->L - 1, w = c->wL1;
   if (L1 < 1 || L1 > MLP_MAXL) return false;
   for (int l = 1; l <= L1; ++l)
@@ -891,13 +849,10 @@ bool fused_vhp_backward(nlrom_ctx* c, bool check_only) {
   a.ldc = c->ldc[0]; a.Gt = c->Gt.p; a.ldG = c->ldGt;
   a.ldpb = c->ldpb;
   if (c->ldpb != round_up(w, 16) + 4) return false;
-  static const int bwd_cfg = getenv("NLROM_BWD_CFG") ? atoi(getenv("NLROM_BWD_CFG")) : 0;
   auto go = [&](bool dry) -> bool {
     if (w == 256) {
       // 4 dual passes (8 columns) per 8-CTA cluster halve the DSMEM bytes each CTA broadcasts per
       // stage relative to 8 passes on 16-CTA clusters (the stage is broadcast-bound)
-      if (bwd_cfg == 1) return launch_mlp_bwd<16, 16, 16>(c, a, dry);
-      if (bwd_cfg == 2) return launch_mlp_bwd<16, 16, 8>(c, a, dry);
       return launch_mlp_bwd<32, 8, 8>(c, a, dry);
     }
     if (w == 64) return launch_mlp_bwd<8, 8>(c, a, dry);
@@ -932,62 +887,13 @@ bool fused_vhp_backward(nlrom_ctx* c, bool check_only) {
 void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 0, double* xout = nullptr,
                bool add_vhp = false) {
   const int n = c->n;
-  if (c->lu_front_done && nx == 0 && add_vhp) {
-    launch_lu_back(c, apply);  // the front ran on phase E's side branch
-    c->lu_front_done = false;
-    return;
-  }
-  c->lu_front_done = false;
   const double* Gt = add_vhp ? (const double*)c->Gt.p : nullptr;
   auto go = [&](auto kern) {
     launch(c, kern, c->n_sims, 256, lu_smem_bytes(n + nx, c->n_q), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
            c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt, c->n_p);
   };
-  // k_lu_cols (column-cyclic, one producer warp per pivot step) is correct but slower than the
-  // row-block kernel on B200 (tools/probes/lu_probe.cu: 47 vs 33 us at n = 60): opt-in only
-  if (n <= LUC_D && n + 1 + nx <= 8 * LUC_CPW && getenv("NLROM_LU_COLS")) {
-    launch(c, k_lu_cols, c->n_sims, 256, luc_smem_bytes(), (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
-           c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt, c->n_p);
-    return;
-  }
-  // warp-register producer / consumer LU (lu_warp.cuh): bitwise identical results, but slower
-  // than the row-block kernel on B200 (issue-bound at one warp per scheduler: 34.8 vs 26.6 us
-  // at n = 60, tools/probes/lu_warp_probe.cu): opt-in only
-  static const bool warp_lu = getenv("NLROM_LU_WARP") != nullptr;
-  if (n <= LUW_MAXN && luw_warps(n, nx) <= 3 && warp_lu) {
-    const int nw = luw_warps(n, nx);
-    auto gow = [&](auto kern) {
-      launch(c, kern, c->n_sims, 256, luw_smem_bytes(nw, c->n_q), (const double*)c->S.p, (const double*)c->phi.p,
-             c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt, c->n_p);
-    };
-    if (nw == 1) gow(k_lu_warp<1>);
-    else if (nw == 2) gow(k_lu_warp<2>);
-    else gow(k_lu_warp<3>);
-    return;
-  }
-  // two pivot steps per barrier (lu_rank2.cuh): bitwise identical, but slower on B200 (53.5 vs
-  // 25.7 us in the cfg2 graph: the two dependent argmax + reciprocal chains per double step cost
-  // more than the barrier they save; tools/lu_rank2_check.py): opt-in only
-  static const bool rank2 = getenv("NLROM_LU_RANK2") != nullptr;
-  if (rank2) {
-    switch (lu_nb(n + nx)) {
-      case 4: go(k_lu_solve2<4>); break;
-      case 6: go(k_lu_solve2<6>); break;
-      default: go(k_lu_solve2<8>); break;
-    }
-    return;
-  }
-  // look-ahead pivot search (k_lu_la): bitwise identical, slower in the cfg2 graph (38.8 vs
-  // 30.7 us, tools/lu_rank2_check.py NLROM_LU_LA): opt-in only
-  static const bool lookahead = getenv("NLROM_LU_LA") != nullptr;
-  if (lookahead) {
-    switch (lu_nb(n + nx)) {
-      case 4: go(k_lu_la<4>); break;
-      case 6: go(k_lu_la<6>); break;
-      default: go(k_lu_la<8>); break;
-    }
-    return;
-  }
+  // retired variants (warp-register, column-cyclic, rank-2, look-ahead, split front/back): bitwise
+  // equal and measured slower on B200 (tools/probes/retired/)
   switch (lu_nb(n + nx)) {
     case 4: go(k_lu_solve<4>); break;
     case 6: go(k_lu_solve<6>); break;
@@ -1101,6 +1007,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaSetDevice(device));
     c = new nlrom_ctx();
     c->device = device;
+    c->opt = PathOpts::from_env();
     NL_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     NL_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
     NL_CUDA(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
@@ -1214,15 +1121,15 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       // cubature set: 2 elements per CTA (250 CTAs for |C| = 500); the all-element set of the
       // exact-sum mode (not the hot path): 8, keeping its per-chunk partials small
       // many sims (batched): 8 elements per CTA keeps the per-chunk partials (and their reduction) small
-      const bool many = c->n_sims * (4 + 4 * c->n_q) >= 2048 || getenv("NLROM_BATCHED") != nullptr;
+      const bool many = c->n_sims * (4 + 4 * c->n_q) >= 2048 || c->opt.batched;
       // split phase E (default): the stiffness / Gram launch is off the critical path, where fewer,
       // longer chunks win (12 elements per CTA: fewer K~ partials to reduce); the force-only launch
       // on the critical path keeps 2 per CTA (setCF)
-      const bool split = getenv("NLROM_NO_SPLIT_E") == nullptr && !many;
-      build_set(c, c->setC, cub, rows, getenv("NLROM_EPC") ? atoi(getenv("NLROM_EPC")) : (many ? 8 : split ? 12 : 2),
+      const bool split = !many;
+      build_set(c, c->setC, cub, rows, many ? 8 : 12,
                 d->Dm_inv, d->vol);
       if (split)
-        build_set(c, c->setCF, cub, rows, getenv("NLROM_EPCF") ? atoi(getenv("NLROM_EPCF")) : 6, d->Dm_inv, d->vol);
+        build_set(c, c->setCF, cub, rows, 6, d->Dm_inv, d->vol);
       build_set(c, c->setAll, all, rows, 8, d->Dm_inv, d->vol);
     }
     // weight net (rows of the last layer restricted to C)
@@ -1272,8 +1179,8 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     }
     // bundle buffers
     c->Cc = 2 + 2 * n_q;  // output-layer columns per sim: [D_1, 2 D_ss | (D_t, 2 D_tss + D_tr) x n_q]
-    c->batched = c->n_sims * (4 + 4 * n_q) >= 2048 || getenv("NLROM_BATCHED") != nullptr;
-    choose_groups(n_q, w, c->batched, c->G, c->gps);
+    c->batched = c->n_sims * (4 + 4 * n_q) >= 2048 || c->opt.batched;
+    choose_groups(n_q, w, c->batched, c->opt.tangents, c->G, c->gps);
     c->Cb = c->G * c->gps;
     c->ldq = round_up(n_q, 2);
     const int ncols = c->n_sims * c->Cb;
@@ -1308,11 +1215,11 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       while (c->rpcM > 16 && mass_smem(c) > 200 * 1024) c->rpcM /= 2;
     }
     c->nchM = ceil_div(N, c->rpcM);
-    if (c->ldjt == gram_ld(c->n) && c->lddj % 2 == 0 && c->n_sims > 1 && !getenv("NLROM_NO_CPM")) {
+    if (c->ldjt == gram_ld(c->n) && c->lddj % 2 == 0 && c->n_sims > 1) {
       // many sims: a CTA walks several row chunks of its sim (>= ~2 waves of 2 CTAs per SM)
       const int rows_ch = c->nchM;
       c->cpmM = (int)std::max(1LL, std::min<long long>(rows_ch, (long long)c->n_sims * rows_ch / (148 * 2 * 2)));
-      if (getenv("NLROM_CPM")) c->cpmM = std::max(1, std::min(rows_ch, atoi(getenv("NLROM_CPM"))));
+      if (c->opt.cpm > 0) c->cpmM = std::max(1, std::min(rows_ch, c->opt.cpm));
       if (mass_smem(c) > 200 * 1024) c->cpmM = 1;
       c->nchM = ceil_div(rows_ch, c->cpmM);
     }
@@ -1320,13 +1227,6 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->a.alloc((size_t)S * N);
     c->partA.alloc((size_t)S * std::max(c->nchA, c->nchM) * n * n);
     c->nchAa = ceil_div(N, ASMA_GROWS);
-    if (n <= 64) {
-      c->luFC = n + 1 + c->n_q;
-      c->luF.alloc((size_t)S * n * c->luFC);
-      c->luRd.alloc((size_t)S * n);
-      c->luPiv.alloc((size_t)S * n);
-      c->luFlag.alloc(S);
-    }
     c->partPhi.alloc((size_t)S * std::max(c->nchA, c->nchAa) * n);
     c->phi.alloc((size_t)S * n);
     c->norm.alloc(S);
@@ -1359,26 +1259,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_la<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_la<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_la<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_solve2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_solve2<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_solve2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_head, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_front<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_front<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_front<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_front<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_back<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_back<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_back<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_back<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_warp<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     if (c->n + 4 > 128) throw Error(NLROM_ERR_ARG, "n_p + n_q must be <= 124");
     NL_CUDA(cudaDeviceSynchronize());
     *out = c;
@@ -1595,8 +1478,9 @@ extern "C" int nlrom_jtilde(nlrom_ctx* c, const double* q, double* Jt) {
   CTX_END(c)
 }
 
-extern "C" int nlrom_wnet_forward(nlrom_ctx* c, const double* r, double* w) {
+extern "C" int nlrom_wnet_forward(nlrom_ctx* c, const double* r, double* w, int64_t w_len) {
   CTX_TRY(c)
+  if (w_len != c->n_cub) throw Error(NLROM_ERR_DIM, "wnet_forward: output length must equal |C|");
   bundle_only(c, r + c->n_p, nullptr, nullptr, 1.0, 0, r);
   wnet_phase(c);
   d2h(c, w, c->wC, c->n_cub);

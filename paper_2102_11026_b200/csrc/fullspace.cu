@@ -524,7 +524,6 @@ extern "C" int nlrom_fs_create(nlrom_fs** out, int device, const nlrom_fs_desc* 
     if (occ < 1) throw Error(NLROM_ERR_CUDA, "k_fs_pcg cannot be resident");
     // one 1024-thread block per SM (tools/bench_fullspace.py: 37..296 blocks all within 10%)
     f->pcg_blocks = std::max(1, std::min(sms, (N + 31) / 32));
-    if (const char* env = getenv("NLROM_FS_BLOCKS")) f->pcg_blocks = std::max(1, std::min(sms * occ, atoi(env)));
     f->cg_part.alloc((size_t)f->pcg_blocks * 4);
     NL_CUDA(cudaDeviceSynchronize());
     *out = f;

@@ -14,8 +14,6 @@ import numpy as np
 
 from . import _lib
 
-_SESSIONS: dict = {}
-
 
 def _simcfg(cfg) -> _lib.SimCfg:
     s = _lib.SimCfg()
@@ -68,6 +66,7 @@ class Session:
         if C_ids.size != np.unique(C_ids).size:
             raise ValueError("cubature set has duplicates (SPEC.md:586)")
         d.n_cub = int(C_ids.size)
+        self.n_cub = d.n_cub
         d.cub_elems = _lib.iptr(arr(C_ids if C_ids.size else np.zeros(1, np.int32), _lib.i32))
         if cm is not None and cm.wnet is not None:
             from .densenet import decoder_parts as _dp
@@ -138,12 +137,10 @@ class Session:
         return out
 
     def wnet_forward_cub(self, r):
-        out = np.empty(max(1, self._n_cub()))
-        self._chk(self._L.nlrom_wnet_forward(self._h, _lib.dptr(self._v(r, self.n)), _lib.dptr(out)))
+        """Weight-net outputs on the cubature set C (length |C|)."""
+        out = np.empty(self.n_cub)
+        self._chk(self._L.nlrom_wnet_forward(self._h, _lib.dptr(self._v(r, self.n)), _lib.dptr(out), out.size))
         return out
-
-    def _n_cub(self):
-        return getattr(self, "_ncub_cache", None) or 0
 
     def cubature_integrate(self, r, integration="cubature"):
         f = np.empty(self.n)
@@ -244,13 +241,68 @@ class Session:
         return int(self._L.nlrom_launches_per_iteration(self._h))
 
 
+def _uploaded_arrays(rm, model, cm):
+    """Every host array a Session copies to the device (decoder, basis, mesh, set, weight net)."""
+    arrs = [rm.U, model.mass, model.mesh.tets, model.vert_dof, model.Dm_inv, model.vol]
+    nets = [rm.decoder] + ([cm.wnet] if cm is not None and cm.wnet is not None else [])
+    for net in nets:
+        for table in (net.weights, net.biases, net.bases):
+            arrs.extend(table[k] for k in sorted(table))
+    if cm is not None:
+        arrs.append(cm.C)
+    return [a for a in arrs if isinstance(a, np.ndarray)]
+
+
+def _fingerprint(arrs):
+    return tuple((id(a), a.__array_interface__["data"][0], a.shape) for a in arrs)
+
+
+_MAX_SESSIONS_PER_MODEL = 4
+
+
 def session_for(rm, model, cm=None, n_sims: int = 1) -> Session:
-    """Cached session keyed by the identity of the model objects."""
-    key = (id(rm), id(model), id(cm), n_sims)
-    s = _SESSIONS.get(key)
-    if s is None:
-        s = Session(rm, model, cm, n_sims)
-        if cm is not None:
-            s._ncub_cache = len(cm.C)
-        _SESSIONS[key] = s
+    """The device session of (rm, model, cm), cached on ``rm``.
+
+    The cache entry holds strong references to ``model`` and ``cm`` (so their ids cannot
+    be recycled while it exists) and a fingerprint of every uploaded array (identity, data
+    pointer, shape): replacing an array (``net.weights[i] = W2``, a new mesh, a new set)
+    rebuilds the session. The uploaded arrays are made read-only, so an in-place edit of
+    weights that a device context holds raises instead of silently using stale values;
+    call ``invalidate(rm)`` first to edit in place. At most a few sessions per model are
+    kept (oldest evicted and its device memory freed)."""
+    cache = rm.__dict__.setdefault("_nlrom_sessions", {})
+    key = (id(model), id(cm), int(n_sims))
+    arrs = _uploaded_arrays(rm, model, cm)
+    fp = _fingerprint(arrs)
+    hit = cache.get(key)
+    if hit is not None and hit[0] is model and hit[1] is cm and hit[2] == fp:
+        return hit[3]
+    if hit is not None:
+        _drop(cache, key)
+    while len(cache) >= _MAX_SESSIONS_PER_MODEL:
+        _drop(cache, next(iter(cache)))
+    s = Session(rm, model, cm, n_sims)
+    frozen = []
+    for a in arrs:
+        if a.flags.writeable:
+            a.flags.writeable = False
+            frozen.append(a)
+    cache[key] = (model, cm, fp, s, frozen)
     return s
+
+
+def _drop(cache, key):
+    model, cm, fp, s, frozen = cache.pop(key)
+    for a in frozen:
+        try:
+            a.flags.writeable = True
+        except ValueError:
+            pass
+    s._fin()  # free the device context now, not at garbage collection
+
+
+def invalidate(rm):
+    """Drop every cached device session of ``rm`` (and make its arrays writeable again)."""
+    cache = rm.__dict__.get("_nlrom_sessions", {})
+    for key in list(cache):
+        _drop(cache, key)

@@ -84,7 +84,7 @@ def test_coupled_batched_strings(cuda_ok, monkeypatch):
     """Many strings per rank take the big-tile batched decoder path (forced here on cfg4's string)."""
     from paper_2102_11026_b200.problem import build_problem
     from paper_2102_11026_b200 import rdsim, synth
-    monkeypatch.setenv("NLROM_BATCHED", "1")
+    monkeypatch.setenv("NLROM_PATH", "batched")
     P = build_problem("cfg4")
     k = 3
     sc, osc = _scene(P, k)

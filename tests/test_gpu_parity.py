@@ -228,21 +228,17 @@ def test_multi_sim(cfg1, batched, monkeypatch):
     from paper_2102_11026_b200 import rdsim
     from paper_2102_11026_b200.session import Session
     P, S = cfg1
-    if batched:
-        monkeypatch.setenv("NLROM_BATCHED", "1")
-    if batched == "cpc":  # + the shared-real vhp backward (default only at >= 4 waves of CTAs)
-        monkeypatch.setenv("NLROM_CPC", "4")
-        monkeypatch.setenv("NLROM_SHARED_REAL", "1")
-        monkeypatch.setenv("NLROM_CPM", "4")  # mass block: 4 row chunks per CTA
-    if batched == "sharedcp":  # shared-real vhp backward on the cp.async GEMM
-        monkeypatch.setenv("NLROM_SHARED_REAL", "1")
-        monkeypatch.setenv("NLROM_BWD_WS", "0")
-    if batched == "noshare":  # batched vhp backward with 2 npass dual columns (no shared real part)
-        monkeypatch.setenv("NLROM_NO_SHARED_REAL", "1")  # (the default at 3 sims anyway)
-        monkeypatch.setenv("NLROM_HID_WS", "0")  # + the cp.async big-tile hidden layers
+    path = {False: None, True: "batched",
+            # + the shared-real vhp backward (default only at >= 4 waves of CTAs), 4 element /
+            # mass row chunks per cubature / mass CTA
+            "cpc": "batched,cpc=4,shared_real,cpm=4",
+            "sharedcp": "batched,shared_real,bwd_cp",        # shared-real vhp on the cp.async GEMM
+            "noshare": "batched,no_shared_real,hid_cp",      # 2 n_q dual columns; cp.async hidden layers
+            }[batched]
+    if path:
+        monkeypatch.setenv("NLROM_PATH", path)
     ns = 3
     sess = Session(P.rm, P.model, P.cm, n_sims=ns)
-    sess._ncub_cache = len(P.cm.C)
     states = [P.random_state(seed=40 + i) for i in range(ns)]
     r, rb, rdb = (np.concatenate([s[j] for s in states]) for j in range(3))
     fext = np.tile(P.f_ext, ns)
@@ -338,20 +334,14 @@ np.savez(sys.argv[2], phi=phi, S=S, r=nxt.r)
 
 
 @pytest.mark.parametrize("env", [
-    {"NLROM_ASYNC_CHAIN": "1", "NLROM_SEPARATE_GEMV": "1"},
-    {"NLROM_LU_COLS": "1", "NLROM_MASS_LATE": "1"},
-    {"NLROM_BWD_CFG": "1", "NLROM_NO_WS_GEMM": "1"},
-    {"NLROM_LU_SPLIT": "1"},
-    {"NLROM_NO_FUSED_MLP": "1", "NLROM_LU_ROWS": "1"},
-    {"NLROM_LU_WARP": "1", "NLROM_WNET_LATE": "1"},
-    {"NLROM_OUT_TILE": "0", "NLROM_NO_SPLITK": "1"},
-    {"NLROM_OUT_TILE": "2", "NLROM_CUB_MINB2": "1", "NLROM_LU_RANK2": "1"},
+    {"NLROM_PATH": "unfused"},
+    {"NLROM_PATH": "unfused,tangents=7"},
+    {"NLROM_PATH": "batched,tangents=1"},
 ])
 def test_kernel_variants(cuda_ok, env, tmp_path):
-    """Opt-in kernel variants (selected by environment at context creation, hence a fresh
-    process) against the oracle: async cluster hand-off chain, column-cyclic LU, mass block on
-    the late branch, 16-CTA vhp clusters, cp.async output GEMM, unfused per-layer GEMMs,
-    warp-register producer / consumer LU."""
+    """Alternate code paths (NLROM_PATH, read at context creation, hence a fresh process)
+    against the oracle: unfused per-layer GEMMs instead of the cluster chains, other jet group
+    sizes, the batched kernels at one sim."""
     import os
     import subprocess
     import sys
@@ -405,7 +395,6 @@ def test_stale_shared_memory(problem):
     poison = lambda: _lib.check(L.nlrom_debug_poison_shared_memory(0), lambda: b"poison")
     ns = 3
     sess = Session(P.rm, P.model, P.cm, n_sims=ns)
-    sess._ncub_cache = len(P.cm.C)
     n = P.cfg.n_p + P.cfg.n_q
     states = [P.random_state(seed=60 + i) for i in range(ns)]
     r, rb, rdb = (np.concatenate([s[j] for s in states]) for j in range(3))

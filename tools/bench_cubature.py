@@ -2,7 +2,7 @@
 """Cubature kernel throughput at many sims (cfg5 / cfg4 style): device ms of one k_cubature
 launch over all sims and SURVEY.md 8d's algorithmic bytes / ms against the HBM peak.
 
-    NLROM_CPC=1 python tools/bench_cubature.py [--cfg cfg5] [--sims 4096]
+    NLROM_PATH=cpc=1 python tools/bench_cubature.py [--cfg cfg5] [--sims 4096]
 """
 import argparse
 import json
@@ -36,7 +36,7 @@ def main():
         s.bench_cubature(2)
         ms, by = s.bench_cubature(args.iters)
         tot, _ = s.bench_iterations(args.iters)
-        print(json.dumps({"cfg": args.cfg, "n_sims": ns, "cpc_env": os.environ.get("NLROM_CPC"),
+        print(json.dumps({"cfg": args.cfg, "n_sims": ns, "cpc_env": os.environ.get("NLROM_PATH"),
                           "cubature_ms": ms, "bytes": by, "gbs": by / ms / 1e6, "frac": by / ms / 1e6 / hbm,
                           "iteration_ms": tot / args.iters}))
         del s

@@ -4,7 +4,7 @@
 #include <cstdio>
 #include <vector>
 #include <random>
-#include "../../paper_2102_11026_b200/csrc/lu_split.cuh"
+#include "retired/lu_split.cuh"
 using namespace nlrom;
 int main() {
   const int n = 60, n_p = 30, nq = 30, FC = n + 1 + nq;

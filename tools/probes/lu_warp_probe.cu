@@ -7,7 +7,7 @@
 #include <cstdlib>
 #include <vector>
 #include <random>
-#include "../../paper_2102_11026_b200/csrc/lu_warp.cuh"
+#include "retired/lu_warp.cuh"
 using namespace nlrom;
 
 template <class K>

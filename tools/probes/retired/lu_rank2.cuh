@@ -16,7 +16,7 @@
 // next double step reads the multipliers of those two rows from PR (later steps write the
 // rows back to the mirror as ordinary rows; after the loop every owner stores its block).
 #pragma once
-#include "solve_kernels.cuh"
+#include "../../../paper_2102_11026_b200/csrc/solve_kernels.cuh"
 
 namespace nlrom {
 

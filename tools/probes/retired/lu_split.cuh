@@ -11,7 +11,7 @@
 // updates as k_lu_solve; only the V contribution is summed in a different order (roundoff).
 // Thread (ty, tx) of 256 owns rows ty + 16a (a < 4) and columns tx + 16b (b < NBC).
 #pragma once
-#include "solve_kernels.cuh"
+#include "../../../paper_2102_11026_b200/csrc/solve_kernels.cuh"
 
 namespace nlrom {
 

@@ -16,7 +16,7 @@
 // row is eliminated, x_k = rhs[piv_k] / a[piv_k][k]; m = a_ik * (1 / a_pk),
 // a_ij = fma(-m, a_pj, a_ij)), so the two kernels agree bit for bit.
 #pragma once
-#include "solve_kernels.cuh"  // recip_fast, cp_async8, mbarrier helpers
+#include "../../../paper_2102_11026_b200/csrc/solve_kernels.cuh"  // recip_fast, cp_async8, mbarrier helpers
 
 namespace nlrom {
 
