@@ -13,8 +13,12 @@ backprop, LU with partial pivoting, r += dr -- one CUDA-graph replay.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1: launched by torch.distributed.run; cfg2 is a single mesh that does not shard
-(SURVEY.md §8e "replicas only"), so every rank runs an independent replica.
+N > 1: one process per GPU. Under torch.distributed.run the ranks come from the environment;
+`bench.py --gpus N` without WORLD_SIZE launches torch.distributed.run itself. cfg2 is a single
+mesh that does not shard (SURVEY.md §8e "replicas only"): every rank runs an independent
+replica, `value` is the per-replica ms per Newton iteration (max over ranks) and the aggregate
+iteration rate of all replicas is reported beside it. The cfg5 leg (4096 independent sims)
+shards sims over the ranks; the cfg4 leg shards strings and does one allreduce per iteration.
 """
 
 from __future__ import annotations
@@ -22,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -34,6 +39,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ms per implicit Newton step (DAE J/H/3rd-order + cubature) at 10-layer DAE"
 WORKLOAD = "cfg2: 10-layer w256 sin DAE, n_q=30, n_p=30, 10290-tet mesh (N=6720), |C|=500 wnet cubature, fp64"
+
+
+def config_dict(world):
+    """The `config` object of BOTH arms (identical for the same N)."""
+    return {"workload": WORKLOAD,
+            "step": "one Newton iteration (fixed-iteration mode: E + J + LU-pp + r += dr)",
+            "l2": "flushed (256 MB write) before every timed replay, outside the timed events",
+            "replicas": world,
+            "parallelism": (f"replicas x{world} (cfg2 does not shard, SURVEY.md §8e)" if world > 1
+                            else "single GPU")}
 
 
 def peaks():
@@ -51,7 +66,7 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms while the GPU is loaded."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -66,8 +81,6 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
-            # nvidia-smi takes ~0.1-0.3 s to start: wait for its first row, then keep only the
-            # rows sampled inside the timed region
             t0 = time.time()
             while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
                 time.sleep(0.005)
@@ -101,14 +114,37 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def dist_setup(n_gpus):
+# --------------------------------------------------------------------------- process topology
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: run N ranks through torch.distributed.run."""
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+               NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def dist_setup(backend):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if n_gpus > 0 else "gloo")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")        # communicator lines show nRanks
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
     return rank, world, local
 
 
@@ -158,23 +194,27 @@ def decoder_flops(P, n_sims=1):
 
 
 def decoder_roofline(P, stage_ms, n_sims, fp64):
+    """Roofline of the decoder bundle (hidden jet chain + output layer + vhp backward chain).
+    `achieved` counts the flops the kernels EXECUTE (the fp64 tensor pipe's real work);
+    the §8d algorithmic figure of the reference pass structure is reported separately as the
+    work the collapsed bundle replaces (it is not a pipe fraction)."""
     F, ex = decoder_flops(P, n_sims)
     dec_ms = stage_ms[0] + stage_ms[1] + stage_ms[2]
-    achieved = F * n_sims / (dec_ms * 1e-3) / 1e12
     executed = ex * n_sims / (dec_ms * 1e-3) / 1e12
+    algorithmic = F * n_sims / (dec_ms * 1e-3) / 1e12
     return {"bound": "tensor",
-            "kernel": "decoder bundle: k_mlp_jet_fwd (hidden jet chain) + output GEMM (EpiJetOutC) + "
-                      "k_gemv_t/k_mlp_dual_bwd (vhp backprop chain), fp64 DMMA",
-            "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
-            "frac": (achieved / fp64) if fp64 else None, "traffic": None,
+            "kernel": "decoder bundle: hidden jet layers + output GEMM (EpiJetOutC) + vhp backprop layers, fp64 DMMA",
+            "achieved": executed, "peak": fp64, "unit": "TFLOP/s",
+            "frac": (executed / fp64) if fp64 else None, "traffic": None,
             "peak_source": "profiles/fp64_peak.json: measured DMMA.8x8x4 fp64 (MEASURED_PEAKS.json has no fp64 entry)",
-            "kernel_ms": dec_ms, "algorithmic_flops_per_launch": F * n_sims,
-            "algorithmic_def": "SURVEY.md §8d F_dec = (18 n_q+6)(2 sum in*out + 4 N n_p) per sim (reference pass structure)",
-            "executed_flops_per_launch": ex * n_sims, "executed_tflops": executed,
-            "executed_frac": (executed / fp64) if fp64 else None,
-            "stages_ms": {"k_mlp_jet_fwd": stage_ms[0], "output_gemm": stage_ms[1], "vhp_bwd": stage_ms[2]}}
+            "kernel_ms": dec_ms, "executed_flops_per_launch": ex * n_sims,
+            "algorithmic": {"flops_per_launch": F * n_sims, "tflops_equivalent": algorithmic,
+                            "def": "SURVEY.md §8d F_dec = (18 n_q+6)(2 sum in*out + 4 N n_p) per sim: the "
+                                   "reference's 4 n_q + 2 passes; the jet bundle executes fewer columns"},
+            "stages_ms": {"hidden_jet": stage_ms[0], "output_gemm": stage_ms[1], "vhp_bwd": stage_ms[2]}}
 
 
+# --------------------------------------------------------------------------- extra legs
 def coupled_leg(args, rank, world):
     """cfg4: the 320-string puffer ball, strings sharded over the ranks, the core
     replicated; per Newton iteration one graph per rank + ONE allreduce of 16 doubles (NCCL on
@@ -224,30 +264,31 @@ def coupled_leg(args, rank, world):
 
 def batched_leg(args, rank, world):
     """cfg5: 4096 independent 10-layer DAE sims, sharded over the ranks with
-    no data-path collective; one graph replay = one Newton iteration of every local sim."""
+    no data-path collective (sim ranges of paper_2102_11026_b200.shard); one graph replay = one
+    Newton iteration of every local sim."""
     import torch
     from paper_2102_11026_b200.problem import build_problem
     from paper_2102_11026_b200 import rdsim
-    from paper_2102_11026_b200.session import Session
+    from paper_2102_11026_b200.shard import SimShard
     P = build_problem("cfg5")
     total = args.batched_sims
-    lo, hi = rank * total // world, (rank + 1) * total // world
-    ns = hi - lo
+    sh = SimShard(P.rm, P.model, P.cm, total, rank, world)
+    ns = sh.n_local
     n = P.cfg.n_p + P.cfg.n_q
-    rng = np.random.default_rng(4 + lo)
+    rng = np.random.default_rng(4 + sh.lo)
     rb = rng.uniform(-0.05, 0.05, ns * n)
     rdb = rng.uniform(-0.1, 0.1, ns * n)
-    s = Session(P.rm, P.model, P.cm, n_sims=ns)
+    s = sh.session
     cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=1)
     s.step(rb, rdb, np.tile(P.f_ext, ns), cfg)
     iters = 10
-    s.bench_iterations(3, flush_l2=True)
+    s.bench_replays(3, flush_l2=True)
     barrier(world)
     torch.cuda.synchronize()
-    tot, _ = s.bench_iterations(iters, flush_l2=True)
+    each = s.bench_replays(iters, flush_l2=True)
     torch.cuda.synchronize()
     barrier(world)
-    ms = barrier_max(world, tot / iters)
+    ms = barrier_max(world, float(each.mean()))
     _, fp64 = peaks()
     stage_ms = s.bench_kernels(3, flush_l2=True)
     roof = decoder_roofline(P, stage_ms, ns, fp64)
@@ -276,48 +317,14 @@ def batched_leg(args, rank, world):
                              "algorithmic_flops_per_launch": cub_flops,
                              "min_time_ms_at_fp64_peak": (cub_flops / (fp64 * 1e12) * 1e3) if fp64 else None}
     launches = s.launches_per_iteration()
-    del s
+    del s, sh
     return {"workload": "cfg5: %d independent sims (10-layer w256 DAE, n_q=20, n_p=10, N=960, |C|=100), "
                         "%d per GPU, no per-iteration collective" % (total, ns),
             "scaling": "strong (total sims fixed)", "ms_per_iteration": ms,
+            "ms_per_iteration_median_rank0": float(np.median(each)),
             "sim_iterations_per_s": total * 1e3 / ms, "iterations": iters,
             "l2": "flushed between timed iterations", "decoder_roofline_rank0": roof,
             "cubature_roofline_rank0": cub_roof, "gpu_launches_per_iteration": launches}
-
-
-# --------------------------------------------------------------------------- CPU arms
-def oracle_iteration_runner(P):
-    """One Newton iteration of the reference algorithm (numpy fp64 restatement of SPEC
-    rdsim: residual + analytic system Jacobian with the reference pass structure + LU)."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import scipy.linalg
-    from helpers import oracle_sim
-    from oracle import rdsim as ors
-    S = oracle_sim(P)
-    r, rb, rdb = P.random_state()
-    oc = ors.OSimConfig(dt=P.cfg.dt)
-    state = (rb, rdb)
-    cur = {"r": r.copy()}
-
-    def one():
-        phi = ors.residual(S, cur["r"], state, P.f_ext, oc)
-        J = ors.system_jacobian(S, cur["r"], state, P.f_ext, oc)
-        cur["r"] = cur["r"] + scipy.linalg.lu_solve(scipy.linalg.lu_factor(J), -phi)
-    return one
-
-
-def cpu_baseline(P, budget_s=12.0, max_iters=30):
-    one = oracle_iteration_runner(P)
-    one()  # warm-up
-    times = []
-    t_end = time.perf_counter() + budget_s
-    while len(times) < max_iters and (len(times) < 3 or time.perf_counter() < t_end):
-        t0 = time.perf_counter()
-        one()
-        times.append(time.perf_counter() - t0)
-    return {"value": 1e3 * float(np.median(times)), "unit": "ms", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{len(times)} Newton iterations of the numpy-fp64 oracle (SPEC rdsim residual + "
-                      f"system_jacobian with the 4n_q+2 reference passes + LU) at cfg2, median"}
 
 
 def fullspace_leg(args, rank, world):
@@ -325,7 +332,6 @@ def fullspace_leg(args, rank, world):
     gravity from rest, wall clock per step through the public API (host arrays in and out),
     beside one step of the scipy-direct oracle -- the ground-truth integrator the reduced step
     replaces."""
-    import numpy as np
     from paper_2102_11026_b200.problem import build_problem
     from paper_2102_11026_b200.fullspace import FullspaceConfig, FullspaceSession
     P = build_problem("cfg2", n_fc=2, width=16)
@@ -359,36 +365,157 @@ def fullspace_cpu_baseline(P, u, v):
             "sample": "1 step of oracle/fullspace.py (numpy + scipy spsolve) at the same state"}
 
 
+# --------------------------------------------------------------------------- CPU arms (oracle = checker / baseline)
+def blas_threads(n):
+    """Pin the host BLAS pool to n threads (torchrun exports OMP_NUM_THREADS=1); returns the
+    thread count the pools actually report."""
+    from threadpoolctl import threadpool_info, threadpool_limits
+    threadpool_limits(limits=n)
+    info = threadpool_info()
+    return max([d.get("num_threads", 1) for d in info] or [1])
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_iteration_runner(P):
+    """One Newton iteration of the reference algorithm (numpy fp64 restatement of SPEC
+    rdsim: residual + analytic system Jacobian with the reference pass structure + LU)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import scipy.linalg
+    from helpers import oracle_sim
+    from oracle import rdsim as ors
+    S = oracle_sim(P)
+    r, rb, rdb = P.random_state()
+    oc = ors.OSimConfig(dt=P.cfg.dt)
+    state = (rb, rdb)
+    cur = {"r": r.copy()}
+
+    def one():
+        phi = ors.residual(S, cur["r"], state, P.f_ext, oc)
+        J = ors.system_jacobian(S, cur["r"], state, P.f_ext, oc)
+        cur["r"] = cur["r"] + scipy.linalg.lu_solve(scipy.linalg.lu_factor(J), -phi)
+    return one
+
+
+def timed_oracle(one, n_min, budget_s):
+    one()  # warm-up
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while len(times) < n_min or (time.perf_counter() < t_end and len(times) < 30):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_baseline(P, budget_s=10.0):
+    """The oracle on the box's host cores: all cores (the reported baseline) and 1 thread (the
+    paper's single-core convention)."""
+    one = oracle_iteration_runner(P)
+    cores = blas_threads(host_cores())
+    times = timed_oracle(one, 3, budget_s)
+    t1 = blas_threads(1)
+    times1 = timed_oracle(one, 2, budget_s / 2)
+    blas_threads(host_cores())
+    return {"value": 1e3 * float(np.median(times)), "unit": "ms", "cores": cores, "kind": "port",
+            "cpu": cpu_model(),
+            "sample": f"{len(times)} Newton iterations of the numpy-fp64 oracle (SPEC rdsim residual + "
+                      f"system_jacobian with the 4n_q+2 reference passes + LU) at cfg2, median",
+            "single_thread": {"value": 1e3 * float(np.median(times1)), "unit": "ms", "cores": t1,
+                              "sample": f"{len(times1)} iterations, median"}}
+
+
+def parity_check(s, P, r_start, rb, rdb, iters=3):
+    """The exact benchmarked graph vs the oracle (checker): from the iterate the timed region
+    started at, `iters` replays of the one-iteration graph against `iters` oracle Newton
+    iterations. Norm-relative max error of phi at each iterate and of r after
+    each update."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import scipy.linalg
+    from helpers import oracle_sim
+    from oracle import rdsim as ors
+    S = oracle_sim(P)
+    oc = ors.OSimConfig(dt=P.cfg.dt)
+    s.set_iterate(r_start)
+    ro = r_start.copy()
+    err_r = err_phi = 0.0
+    for _ in range(iters):
+        s.iterate(1)
+        rg, phig, _ = s.get_iterate()
+        phio = ors.residual(S, ro, (rb, rdb), P.f_ext, oc)
+        J = ors.system_jacobian(S, ro, (rb, rdb), P.f_ext, oc)
+        ro = ro + scipy.linalg.lu_solve(scipy.linalg.lu_factor(J), -phio)
+        err_phi = max(err_phi, float(np.abs(phig - phio).max() / np.abs(phio).max()))
+        err_r = max(err_r, float(np.abs(rg - ro).max() / np.abs(ro).max()))
+    return {"iterations": iters, "max_rel_err_r": err_r, "max_rel_err_phi": err_phi, "tol": 1e-10,
+            "ok": bool(err_r <= 1e-10 and err_phi <= 1e-10),
+            "def": "||x - x_oracle||_inf / ||x_oracle||_inf; the timed graph replayed from the timed "
+                   "region's start iterate vs oracle/rdsim.py fixed Newton iterations"}
+
+
 def run_reference(args):
-    rank, world, local = dist_setup(0)
+    """Reference arm: the reference algorithm's CPU implementation (the oracle port; the
+    reference ships no executable code above mcx) on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     from paper_2102_11026_b200.problem import build_problem
+    cores = blas_threads(host_cores())
     P = build_problem("cfg2")
     one = oracle_iteration_runner(P)
     for _ in range(args.warmup):
         one()
-    t0 = time.perf_counter()
+    times = []
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         one()
-    ms = 1e3 * (time.perf_counter() - t0) / args.steps
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8d)",
-        "config": {"workload": WORKLOAD, "parallelism": "host cores (numpy/OpenBLAS threads)"},
-        "cpu_baseline": {"value": ms, "unit": "ms", "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{args.steps} Newton iterations of the oracle at cfg2 (mean)"},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random-init weights, SURVEY.md §8d)",
+        "config": config_dict(world),
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port", "cpu": cpu_model(),
+                         "sample": f"{args.steps} Newton iterations of the numpy-fp64 oracle at cfg2 (mean), "
+                                   f"BLAS pool pinned to {cores} threads"},
+        "ms_median": 1e3 * float(np.median(times)),
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
 # --------------------------------------------------------------------------- GPU arm
+def load_gpu(s, seconds):
+    """Keep the GPU busy with flushed replays for `seconds` (clock sampling window)."""
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        s.bench_replays(50, flush_l2=True)
+
+
 def run_ours(args):
-    rank, world, local = dist_setup(args.gpus)
-    os.environ["NLROM_DEVICE"] = str(local)
     import torch
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py --impl ours needs a CUDA device (the product path has no CPU fallback)")
+    rank, world, local = dist_setup("nccl")
+    os.environ["NLROM_DEVICE"] = str(local)
     torch.cuda.set_device(local)
+    barrier(world)   # creates the NCCL communicator (NCCL_DEBUG=INFO prints nRanks)
     from paper_2102_11026_b200.problem import build_problem
     from paper_2102_11026_b200 import rdsim
     from paper_2102_11026_b200.session import session_for
@@ -396,17 +523,21 @@ def run_ours(args):
     s = session_for(P.rm, P.model, P.cm)
     r, rb, rdb = P.random_state(seed=4 + rank)
     cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=1)
-    s.step(rb, rdb, P.f_ext, cfg)              # captures the graphs, sets the state
-    s.bench_iterations(max(args.warmup, 3), flush_l2=True)
+    s.step(rb, rdb, P.f_ext, cfg)              # captures the graphs, sets r_bar / rdot_bar / f_ext
+    r_start, _, _ = s.get_iterate()
+    s.bench_replays(max(args.warmup, 3), flush_l2=True)
+    s.set_iterate(r_start)
 
-    barrier(world)
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ms_total, ms_dom = s.bench_iterations(args.steps, flush_l2=True)
-    torch.cuda.synchronize()
-    barrier(world)
-    ms_iter = barrier_max(world, ms_total / args.steps)
-    value = ms_iter / world  # whole-job: world * steps iterations in the max-over-ranks device time
+        load_gpu(s, 0.5)                       # clocks are sampled under the same load
+        s.set_iterate(r_start)
+        barrier(world)
+        torch.cuda.synchronize()
+        each = s.bench_replays(args.steps, flush_l2=True)
+        torch.cuda.synchronize()
+        barrier(world)
+        load_gpu(s, 0.5)
+    ms_iter = barrier_max(world, float(each.mean()))
 
     # e2e through the public API (rdsim.step, host buffers, H2D/D2H inside), 3 fixed iterations/step
     from paper_2102_11026_b200.daereduce import ReducedState
@@ -419,21 +550,26 @@ def run_ours(args):
     t0 = time.perf_counter()
     for _ in range(n_e2e):
         st = rdsim.step(P.rm, P.model, st, P.f_ext, cfg3)
-    e2e_ms = barrier_max(world, 1e3 * (time.perf_counter() - t0) / (n_e2e * 3)) / world
+    e2e_ms = barrier_max(world, 1e3 * (time.perf_counter() - t0) / (n_e2e * 3))
     n = P.cfg.n_p + P.cfg.n_q
     h2d = (2 * n + P.model.N) * 8
     d2h = 2 * n * 8 + 8
 
-    # roofline: every stage timed live with CUDA events on the context stream (L2 flushed
-    # before each launch). The decoder bundle (hidden jet chain + output layer + vhp
-    # backward chain) is the dominant unit (>= 60% of the step); its algorithmic work is
-    # SURVEY.md §8d F_dec = (18 n_q + 6)(2 sum_l in_l out_l + 4 N n_p) per sim, the
-    # reference's pass structure. Executed flops of the collapsed passes are reported beside it.
+    # roofline: stages timed live with CUDA events on the context stream (L2 flushed before each
+    # launch); in-graph share of the decoder bundle from the prefix-graph profile
     pk, fp64 = peaks()
     stage_ms = s.bench_kernels(max(20, args.steps // 4), flush_l2=True)
     roof = decoder_roofline(P, stage_ms, 1, fp64)
-    roof["share_of_step"] = roof["kernel_ms"] / ms_iter
-    roof["lu_ms"] = stage_ms[3]
+    roof["share_of_step_isolated"] = roof["kernel_ms"] / ms_iter
+    roof["lu_ms_isolated"] = stage_ms[3]
+    try:
+        marg, _ = s.bench_prefix(n_iters=20, flush_l2=True)
+        dec_names = ("k_mlp_jet_fwd", "gemm_ws_kernel", "gemm_tn_kernel", "k_mlp_dual_bwd", "k_gemv_t2")
+        in_graph = sum(v for nm, v in marg if any(k in nm for k in dec_names))
+        roof["share_of_step_in_graph"] = in_graph / max(sum(v for _, v in marg), 1e-9)
+        roof["in_graph_marginal_ms"] = {nm.split("(")[0][:60]: round(v, 5) for nm, v in marg}
+    except Exception as e:  # profiling aid only
+        roof["share_of_step_in_graph"] = f"unavailable: {e}"
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "dominant_traffic.json")))
         roof["traffic"] = sum(tr.get(k, {}).get("dram_bytes_per_launch", 0) for k in
@@ -441,44 +577,46 @@ def run_ours(args):
     except Exception:
         pass
 
-    batched = None
-    if not args.no_batched:
-        batched = batched_leg(args, rank, world)
-    coupled = None
-    if not args.no_coupled:
-        coupled = coupled_leg(args, rank, world)
+    batched = None if args.no_batched else batched_leg(args, rank, world)
+    coupled = None if args.no_coupled else coupled_leg(args, rank, world)
+    fullspace = None if args.no_fullspace else fullspace_leg(args, rank, world)
 
-    fullspace = None
-    if not args.no_fullspace:
-        fullspace = fullspace_leg(args, rank, world)
+    cpu = parity = None
+    if rank == 0:
+        parity = parity_check(s, P, r_start, rb, rdb)
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(P)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(P)
-
+    line = None
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
+            "metric": METRIC, "value": ms_iter, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_iter, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random-init weights, SURVEY.md §8d)",
-            "config": {"workload": WORKLOAD, "newton": "fixed-iteration mode, 1 graph replay per step",
-                       "l2": "flushed between timed iterations (256 MB write)", "global_sims": world,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "config": config_dict(world),
+            "timing": {"mean_ms": float(each.mean()), "median_ms": float(np.median(each)),
+                       "p90_ms": float(np.percentile(each, 90)), "min_ms": float(each.min()), "replays": len(each),
+                       "how": "CUDA events around each graph replay on the context stream, max over ranks of "
+                              "the mean"},
+            "aggregate": {"newton_iterations_per_s": world * 1e3 / ms_iter,
+                          "def": "all replicas' iterations per second (each replica at value ms per iteration)"},
             "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d * 1, "d2h_bytes_per_step": d2h,
-                    "how": "nlrom.rdsim.step (host numpy in/out), fixed_iters=3, wall clock / 3"},
+                    "how": "nlrom.rdsim.step (host numpy in/out), fixed_iters=3, wall clock / 3, max over ranks"},
             "gpu_launches": s.launches_per_iteration() * args.steps,
             "roofline": roof,
+            "parity": parity,
             "batched_cfg5": batched,
             "coupled_cfg4": coupled,
             "fullspace_cfg2": fullspace,
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
-            "hz_at_3_iters": 1000.0 / (3 * value),
+            "clocks": dict(clk.summary(), window="0.5 s load + timed replays + 0.5 s load"),
+            "hz_at_3_iters": 1000.0 / (3 * ms_iter),
         }
-        print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
 
 
 def main():
@@ -494,8 +632,12 @@ def main():
     ap.add_argument("--strings", type=int, default=320)
     ap.add_argument("--no-fullspace", action="store_true", help="skip the full-space implicit Euler leg")
     args = ap.parse_args()
+    if os.environ.get("NLROM_DEBUG_SKIP"):
+        raise SystemExit("bench.py refuses to run with NLROM_DEBUG_SKIP set (kernels would be dropped)")
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

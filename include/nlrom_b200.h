@@ -202,6 +202,23 @@ NLROM_API int nlrom_step_device(nlrom_ctx* ctx, const double* r_bar, const doubl
  * iteration. */
 NLROM_API int nlrom_bench_iterations(nlrom_ctx* ctx, int n_iters, int flush_l2, float* ms_total, float* ms_dominant);
 
+/* Per-replay timing for bench.py: replays the captured one-Newton-iteration graph n_iters
+ * times at the current device state (set by nlrom_step* / nlrom_set_iterate), each bracketed
+ * by CUDA events on the graph's stream, L2 flushed (256 MB write) before each replay outside
+ * the events if flush_l2; ms_each[i] = device ms of replay i. */
+NLROM_API int nlrom_bench_replays(nlrom_ctx* ctx, int n_iters, int flush_l2, float* ms_each);
+
+/* The benchmarked graph without timing: n_iters replays of one fixed Newton iteration
+ * (E at r, J, LU, r += dr) on the current device state. With nlrom_get_iterate /
+ * nlrom_set_iterate this lets bench.py and tests check the exact timed graph against the
+ * oracle (r after each iteration, phi at the iterate the iteration started from). */
+NLROM_API int nlrom_iterate(nlrom_ctx* ctx, int n_iters);
+/* r (n_sims x n) of the current iterate; phi (n_sims x n) and ||phi||_2 (n_sims) as evaluated
+ * by the last E phase (any of the pointers may be NULL). */
+NLROM_API int nlrom_get_iterate(nlrom_ctx* ctx, double* r, double* phi, double* norm);
+/* Overwrite the current iterate r (n_sims x n); r_bar, rdot_bar, f_ext stay as set. */
+NLROM_API int nlrom_set_iterate(nlrom_ctx* ctx, const double* r);
+
 /* Device time per stage (CUDA events on the context stream, averaged over n_iters):
  * ms4[0] hidden jet chain, ms4[1] decoder output layer, ms4[2] vhp backward chain,
  * ms4[3] LU solve. Used by bench.py to pick and time the dominant kernel. */

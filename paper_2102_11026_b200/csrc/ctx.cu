@@ -1706,6 +1706,59 @@ extern "C" int nlrom_bench_iterations(nlrom_ctx* c, int n_iters, int flush_l2, f
   CTX_END(c)
 }
 
+extern "C" int nlrom_bench_replays(nlrom_ctx* c, int n_iters, int flush_l2, float* ms_each) {
+  CTX_TRY(c)
+  if (c->graph_key.empty()) throw Error(NLROM_ERR_ARG, "run nlrom_step first (captures the graphs)");
+  if (n_iters <= 0 || !ms_each) throw Error(NLROM_ERR_ARG, "n_iters > 0 and ms_each required");
+  if (flush_l2 && !c->flush.p) c->flush.alloc((size_t)32 << 20);  // 256 MB > 126 MB L2
+  std::vector<cudaEvent_t> ev(2 * (size_t)n_iters);
+  for (auto& e : ev) NL_CUDA(cudaEventCreate(&e));
+  try {
+    for (int i = 0; i < n_iters; ++i) {
+      if (flush_l2) {
+        k_flush<<<1184, 256, 0, c->st>>>(c->flush.p, c->flush.n, (double)i);
+        NL_CHECK_LAUNCH();
+      }
+      NL_CUDA(cudaEventRecord(ev[2 * i], c->st));
+      NL_CUDA(cudaGraphLaunch(c->gIter, c->st));
+      NL_CUDA(cudaEventRecord(ev[2 * i + 1], c->st));
+    }
+    NL_CUDA(cudaStreamSynchronize(c->st));
+    for (int i = 0; i < n_iters; ++i) NL_CUDA(cudaEventElapsedTime(&ms_each[i], ev[2 * i], ev[2 * i + 1]));
+  } catch (...) {
+    for (auto& e : ev) cudaEventDestroy(e);
+    throw;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  CTX_END(c)
+}
+
+extern "C" int nlrom_iterate(nlrom_ctx* c, int n_iters) {
+  CTX_TRY(c)
+  if (c->graph_key.empty()) throw Error(NLROM_ERR_ARG, "run nlrom_step first (captures the graphs)");
+  for (int i = 0; i < n_iters; ++i) NL_CUDA(cudaGraphLaunch(c->gIter, c->st));
+  check_status(c);
+  CTX_END(c)
+}
+
+extern "C" int nlrom_get_iterate(nlrom_ctx* c, double* r, double* phi, double* norm) {
+  CTX_TRY(c)
+  const size_t nn = (size_t)c->n_sims * c->n;
+  if (r) d2h(c, r, c->r, nn);
+  if (phi) d2h(c, phi, c->phi, nn);
+  if (norm) d2h(c, norm, c->norm, c->n_sims);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
+extern "C" int nlrom_set_iterate(nlrom_ctx* c, const double* r) {
+  CTX_TRY(c)
+  if (!r) throw Error(NLROM_ERR_ARG, "null argument");
+  h2d(c, c->r, r, (size_t)c->n_sims * c->n);
+  NL_CUDA(cudaStreamSynchronize(c->st));
+  CTX_END(c)
+}
+
 // Per-stage device time (CUDA events on the context stream, L2 optionally flushed before
 // each launch), averaged over n_iters: [0] hidden jet chain (fused cluster kernel),
 // [1] decoder output layer, [2] vhp backward chain, [3] LU solve.

@@ -215,6 +215,26 @@ class Session:
         self._chk(self._L.nlrom_bench_iterations(self._h, int(n_iters), int(flush_l2), C.byref(tot), C.byref(dom)))
         return tot.value, dom.value
 
+    def bench_replays(self, n_iters, flush_l2=True):
+        """Device ms of each of n_iters replays of the one-Newton-iteration graph."""
+        out = (C.c_float * int(n_iters))()
+        self._chk(self._L.nlrom_bench_replays(self._h, int(n_iters), int(flush_l2), out))
+        return np.array(out[:], dtype=float)
+
+    def iterate(self, n_iters=1):
+        """n_iters replays of the benchmarked one-Newton-iteration graph (no timing)."""
+        self._chk(self._L.nlrom_iterate(self._h, int(n_iters)))
+
+    def get_iterate(self):
+        """(r, phi at the iterate the last E phase evaluated, ||phi||_2) per sim, flattened."""
+        nn = self.n_sims * self.n
+        r, phi, nrm = np.empty(nn), np.empty(nn), np.empty(self.n_sims)
+        self._chk(self._L.nlrom_get_iterate(self._h, _lib.dptr(r), _lib.dptr(phi), _lib.dptr(nrm)))
+        return r, phi, nrm
+
+    def set_iterate(self, r):
+        self._chk(self._L.nlrom_set_iterate(self._h, _lib.dptr(self._v(r, self.n_sims * self.n))))
+
     def bench_kernels(self, n_iters, flush_l2=True):
         """Device ms per launch of [hidden jet chain, output layer, vhp backward chain, LU]."""
         out = (C.c_float * 4)()
