@@ -521,10 +521,22 @@ def run_ours(args):
     from paper_2102_11026_b200.session import session_for
     P = build_problem("cfg2")
     s = session_for(P.rm, P.model, P.cm)
-    r, rb, rdb = P.random_state(seed=4 + rank)
+    n = P.cfg.n_p + P.cfg.n_q
+    # a physically evolving state: 5 timesteps under gravity from rest (3 Newton iterations
+    # each), so the timed Newton iterations converge as in a simulation (an arbitrary random
+    # state makes undamped fixed-iteration Newton diverge and feeds sin / cos garbage)
+    rb, rdb = np.zeros(n), np.zeros(n)
+    for _ in range(5):
+        rb, rdb, _, _ = s.step(rb, rdb, P.f_ext, rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=3))
     cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=1)
-    s.step(rb, rdb, P.f_ext, cfg)              # captures the graphs, sets r_bar / rdot_bar / f_ext
-    r_start, _, _ = s.get_iterate()
+
+    def arm():
+        """(Re)load the benchmark state: r_bar, rdot_bar, f_ext and the iterate the timed
+        region starts from (other API calls below move the context's state)."""
+        s.step(rb, rdb, P.f_ext, cfg)          # captures the graphs on first use
+        return s.get_iterate()[0]
+
+    r_start = arm()
     s.bench_replays(max(args.warmup, 3), flush_l2=True)
     s.set_iterate(r_start)
 
@@ -551,7 +563,6 @@ def run_ours(args):
     for _ in range(n_e2e):
         st = rdsim.step(P.rm, P.model, st, P.f_ext, cfg3)
     e2e_ms = barrier_max(world, 1e3 * (time.perf_counter() - t0) / (n_e2e * 3))
-    n = P.cfg.n_p + P.cfg.n_q
     h2d = (2 * n + P.model.N) * 8
     d2h = 2 * n * 8 + 8
 
@@ -583,6 +594,7 @@ def run_ours(args):
 
     cpu = parity = None
     if rank == 0:
+        arm()
         parity = parity_check(s, P, r_start, rb, rdb)
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(P)

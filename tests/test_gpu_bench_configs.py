@@ -29,17 +29,17 @@ def cfg2(cuda_ok):
 
 def test_cfg2_ten_steps_three_iterations(cfg2):
     from paper_2102_11026_b200 import rdsim
-    from paper_2102_11026_b200.daereduce import ReducedState
     P, S = cfg2
-    _, rb, rdb = P.random_state()
+    # gravity from rest (a random state makes un-damped fixed-iteration Newton diverge, which
+    # amplifies roundoff chaotically: not a parity test)
     cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=3)
-    st = ReducedState(rb, rdb, cfg.dt)
-    ro, rdo = rb.copy(), rdb.copy()
+    st = P.rest_state()
+    ro, rdo = st.r.copy(), st.rdot.copy()
     worst = 0.0
     for _ in range(10):
         st = rdsim.step(P.rm, P.model, st, P.f_ext, cfg)
         ro, rdo, _, _ = ors.step(S, ro, rdo, P.f_ext, ocfg(cfg))
-        worst = max(worst, rel(st.r, ro), rel(st.rdot, rdo) * 1e-2)
+        worst = max(worst, rel(st.r, ro), rel(st.rdot, rdo))
     assert worst <= 1e-10, worst
 
 
