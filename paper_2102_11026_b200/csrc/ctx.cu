@@ -22,6 +22,7 @@
 #include "mlp_chain.cuh"
 #include "coupled_kernels.cuh"
 #include "gemm_ws.cuh"
+#include "ozaki_tc.cuh"
 
 namespace nlrom {
 void fc_forward(int order, int act, const GemmArgs& g, double* Y, int ldy, const double* bias, double* cache,
@@ -68,9 +69,11 @@ int gemm_launch_count = 0;
 //   no_shared_real  2 n_q dual columns per sim in the batched vhp backward
 //   cpc=K, cpm=K    element / mass row chunks walked per CTA (many sims)
 //   tangents=K      jet tangents per column group (1, 3, 5, 7 or 15)
+//   dmma_hidden     batched hidden jet layers on the fp64 DMMA kernels instead of the tcgen05
+//                   Ozaki-int8 GEMM (ozaki_tc.cuh)
 struct PathOpts {
   bool batched = false, unfused = false, hid_cp = false, bwd_cp = false, shared_real = false,
-       no_shared_real = false;
+       no_shared_real = false, dmma_hidden = false;
   int cpc = 0, cpm = 0, tangents = 0;
   static PathOpts from_env() {
     PathOpts o;
@@ -91,6 +94,7 @@ struct PathOpts {
       else if (key == "bwd_cp") o.bwd_cp = true;
       else if (key == "shared_real") o.shared_real = true;
       else if (key == "no_shared_real") o.no_shared_real = true;
+      else if (key == "dmma_hidden") o.dmma_hidden = true;
       else if (key == "cpc") o.cpc = val;
       else if (key == "cpm") o.cpm = val;
       else if (key == "tangents") o.tangents = val;
@@ -121,6 +125,7 @@ struct nlrom_ctx {
   std::vector<DBuf> W, WT, b;
   std::vector<int> ldW, ldWT;
   std::vector<DBuf> Wp, WTp;  // fused chains: padded copies (one TMA bulk copy per CTA slice)
+  std::vector<OzakiWeights> ozW;  // batched hidden layers on tcgen05: int8 digit tiles of W_l (ozaki_tc.cuh)
   int ldpf = 0, ldpb = 0;
   DBuf Alast, AT, Pb, U, mass;
   int ldlast = 0, wL1 = 0, next = 0;
@@ -203,7 +208,16 @@ int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL
 
 // ---------------------------------------------------------------- GEMM dispatch
 template <class Epi>
-void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st, bool big = false, bool cp_async = false) {
+void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st, bool big = false, bool cp_async = false,
+              const OzakiWeights* oz = nullptr) {
+  // big-tile hidden layers on the 5th-gen tensor cores: Ozaki-scheme fp64 on tcgen05.mma kind::i8
+  // (ozaki_tc.cuh; 1.75x the DMMA kernel at the cfg5 shape, ~1e-16 of sum |w||x|)
+  if (big && oz && oz->ready && 64 % G == 0 && g.M % oz::BM == 0 && g.K % oz::BK == 0 && g.ldb % 2 == 0 &&
+      !g.cstep) {
+    launch_ozaki<64>(oz->view(), OzakiBExp{nullptr, 0}, g, e, st);
+    ++gemm_launch_count;
+    return;
+  }
   // big-tile hidden layers on the warp-specialised TMA pipeline (16 consumer warps, 4 stages):
   // cfg5 hidden layers 14.76 -> 14.51 ms vs the cp.async CfgBig kernel (NLROM_PATH=hid_cp)
   if (big && 128 % G == 0 && !cp_async && g.K % 16 == 0 && g.lda % 2 == 0 && g.ldb % 2 == 0) {
@@ -437,7 +451,7 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
     const int compact = (l == c->L - 2) ? 1 : 0;
     GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
     EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, compact};
-    hid_gemm(c->G, g, e, c->st, c->batched, c->opt.hid_cp);
+    hid_gemm(c->G, g, e, c->st, c->batched, c->opt.hid_cp, l < (int)c->ozW.size() ? &c->ozW[l] : nullptr);
     in = c->H[l].p;
     ldin = c->ldH[l];
   }
@@ -1183,6 +1197,14 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->Cc = 2 + 2 * n_q;  // output-layer columns per sim: [D_1, 2 D_ss | (D_t, 2 D_tss + D_tr) x n_q]
     c->batched = c->n_sims * (4 + 4 * n_q) >= 2048 || c->opt.batched;
     choose_groups(n_q, w, c->batched, c->opt.tangents, c->G, c->gps);
+    if (c->batched && !c->opt.dmma_hidden) {
+      // hidden layers 1 .. L-2 (K = w) as int8 digit tiles for the tcgen05 Ozaki GEMM
+      c->ozW.resize(L - 1);
+      for (int l = 1; l < L - 1; ++l) {
+        const int in = c->widths[l], o = c->widths[l + 1];
+        if (o % oz::BM == 0 && in % oz::BK == 0) ozaki_upload(c->ozW[l], d->W[l], in, o, in);
+      }
+    }
     c->Cb = c->G * c->gps;
     c->ldq = round_up(n_q, 2);
     const int ncols = c->n_sims * c->Cb;

@@ -149,6 +149,26 @@ struct OzakiBExp {
   int nparts;   // <= 4
 };
 
+// Device copy of one layer's prepared A operand (digit tiles + row exponents).
+struct OzakiWeights {
+  unsigned char* tiles = nullptr;
+  int* exps = nullptr;
+  bool ready = false;
+  OzakiWeights() = default;
+  OzakiWeights(const OzakiWeights&) = delete;
+  OzakiWeights& operator=(const OzakiWeights&) = delete;
+  OzakiWeights(OzakiWeights&& o) noexcept : tiles(o.tiles), exps(o.exps), ready(o.ready) {
+    o.tiles = nullptr;
+    o.exps = nullptr;
+    o.ready = false;
+  }
+  ~OzakiWeights() {
+    if (tiles) cudaFree(tiles);
+    if (exps) cudaFree(exps);
+  }
+  OzakiA view() const { return OzakiA{tiles, exps}; }
+};
+
 inline void ozaki_prepare_a(const double* A, int lda, int M, int K, std::vector<unsigned char>& tiles,
                             std::vector<int>& exps) {
   using namespace oz;
@@ -528,6 +548,17 @@ void launch_ozaki(const OzakiA& a, const OzakiBExp& be, const GemmArgs& g, const
   cfg.attrs = at;
   cfg.numAttrs = 1;
   NL_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki_gemm<BN, Epi>, a, be, g, tiles_m, tiles_c, epi));
+}
+
+inline void ozaki_upload(OzakiWeights& w, const double* A, int lda, int M, int K) {
+  std::vector<unsigned char> tiles;
+  std::vector<int> exps;
+  ozaki_prepare_a(A, lda, M, K, tiles, exps);
+  NL_CUDA(cudaMalloc(&w.tiles, tiles.size()));
+  NL_CUDA(cudaMalloc(&w.exps, exps.size() * sizeof(int)));
+  NL_CUDA(cudaMemcpy(w.tiles, tiles.data(), tiles.size(), cudaMemcpyHostToDevice));
+  NL_CUDA(cudaMemcpy(w.exps, exps.data(), exps.size() * sizeof(int), cudaMemcpyHostToDevice));
+  w.ready = true;
 }
 
 }  // namespace nlrom
