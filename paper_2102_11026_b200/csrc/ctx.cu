@@ -126,6 +126,7 @@ struct nlrom_ctx {
   std::vector<int> ldW, ldWT;
   std::vector<DBuf> Wp, WTp;  // fused chains: padded copies (one TMA bulk copy per CTA slice)
   std::vector<OzakiWeights> ozW;  // batched hidden layers on tcgen05: int8 digit tiles of W_l (ozaki_tc.cuh)
+  unsigned* ozHW[2] = {nullptr, nullptr};  // ping-pong column-scale partials between hidden layers
   int ldpf = 0, ldpb = 0;
   DBuf Alast, AT, Pb, U, mass;
   int ldlast = 0, wL1 = 0, next = 0;
@@ -209,12 +210,12 @@ int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL
 // ---------------------------------------------------------------- GEMM dispatch
 template <class Epi>
 void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st, bool big = false, bool cp_async = false,
-              const OzakiWeights* oz = nullptr) {
+              const OzakiWeights* oz = nullptr, OzakiBExp be = OzakiBExp{nullptr, 0}) {
   // big-tile hidden layers on the 5th-gen tensor cores: Ozaki-scheme fp64 on tcgen05.mma kind::i8
   // (ozaki_tc.cuh; 1.75x the DMMA kernel at the cfg5 shape, ~1e-16 of sum |w||x|)
   if (big && oz && oz->ready && 64 % G == 0 && g.M % oz::BM == 0 && g.K % oz::BK == 0 && g.ldb % 2 == 0 &&
       !g.cstep) {
-    launch_ozaki<64>(oz->view(), OzakiBExp{nullptr, 0}, g, e, st);
+    launch_ozaki<64>(oz->view(), be, g, e, st);
     ++gemm_launch_count;
     return;
   }
@@ -451,7 +452,14 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
     const int compact = (l == c->L - 2) ? 1 : 0;
     GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
     EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, compact};
-    hid_gemm(c->G, g, e, c->st, c->batched, c->opt.hid_cp, l < (int)c->ozW.size() ? &c->ozW[l] : nullptr);
+    // tcgen05 Ozaki layers read their input's column scales from the previous layer's epilogue
+    const bool oz_here = c->batched && l < (int)c->ozW.size() && c->ozW[l].ready;
+    const bool oz_next = c->batched && l + 1 < (int)c->ozW.size() && c->ozW[l + 1].ready && !compact &&
+                         c->widths[l + 1] % 32 == 0 && c->ozHW[0];
+    if (oz_next) e.colhw = c->ozHW[l & 1];
+    const OzakiBExp be = (oz_here && l >= 1 && c->ozHW[0]) ? OzakiBExp{c->ozHW[(l - 1) & 1], c->widths[l] / 32}
+                                                          : OzakiBExp{nullptr, 0};
+    hid_gemm(c->G, g, e, c->st, c->batched, c->opt.hid_cp, oz_here ? &c->ozW[l] : nullptr, be);
     in = c->H[l].p;
     ldin = c->ldH[l];
   }
@@ -1197,15 +1205,19 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     c->Cc = 2 + 2 * n_q;  // output-layer columns per sim: [D_1, 2 D_ss | (D_t, 2 D_tss + D_tr) x n_q]
     c->batched = c->n_sims * (4 + 4 * n_q) >= 2048 || c->opt.batched;
     choose_groups(n_q, w, c->batched, c->opt.tangents, c->G, c->gps);
+    c->Cb = c->G * c->gps;
     if (c->batched && !c->opt.dmma_hidden) {
       // hidden layers 1 .. L-2 (K = w) as int8 digit tiles for the tcgen05 Ozaki GEMM
       c->ozW.resize(L - 1);
+      int maxw = 0;
       for (int l = 1; l < L - 1; ++l) {
         const int in = c->widths[l], o = c->widths[l + 1];
-        if (o % oz::BM == 0 && in % oz::BK == 0) ozaki_upload(c->ozW[l], d->W[l], in, o, in);
+        if (o % oz::BM == 0 && in % oz::BK == 0 && in <= 256) ozaki_upload(c->ozW[l], d->W[l], in, o, in);
+        maxw = std::max(maxw, in);
       }
+      const size_t hwn = (size_t)c->n_sims * c->Cb * (size_t)ceil_div(maxw, 32);
+      for (auto& p : c->ozHW) NL_CUDA(cudaMalloc(&p, std::max<size_t>(hwn, 1) * sizeof(unsigned)));
     }
-    c->Cb = c->G * c->gps;
     c->ldq = round_up(n_q, 2);
     const int ncols = c->n_sims * c->Cb;
     c->X0.alloc((size_t)ncols * c->ldq);
@@ -1324,6 +1336,8 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->evK) cudaEventDestroy(c->evK);
   if (c->evM) cudaEventDestroy(c->evM);
   if (c->evP) cudaEventDestroy(c->evP);
+  for (auto p : c->ozHW)
+    if (p) cudaFree(p);
   delete c;
 }
 

@@ -170,9 +170,23 @@ struct EpiJet {
   int gps;            // groups per simulation
   int n_q;            // tangent directions per simulation
   int compact;        // 1: write the output layout per sim (next layer is linear): [h_1, 2 h_ss | (h_t, 2 h_tss + h_tr) x n_q]
+  // Column-scale partials for a tcgen05 Ozaki consumer (ozaki_tc.cuh), non-compact layout only:
+  // colhw[c * (M / 32) + m / 32] = max over the 32 rows m of the high word of |Y[c][m]| (needs
+  // M % 32 == 0 and 32-row-aligned warps: tile rows and thread counts multiples of 32).
+  unsigned* colhw = nullptr;
   __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
     double* Yz = Y + (size_t)t.z * strideY;
     const int nk = (group - 4) / 4;           // tangents per group
+    const bool hw = colhw != nullptr && !compact;
+    const int lane = tid & 31;
+    unsigned hw0 = 0u, hw1 = 0u;              // this lane's columns: lane and 32 + lane of the group
+    auto note = [&](int j, double v) {        // warp max over the 32 rows of column j's |v| high word
+      const unsigned r = __reduce_max_sync(0xffffffffu, (unsigned)__double2hiint(fabs(v)));
+      if ((j & 31) == lane) {
+        if (j < 32) hw0 = r;
+        else hw1 = r;
+      }
+    };
     const int cs = 2 + 2 * n_q;               // output-layout columns per sim
     const int ngt = t.bn / group;             // groups in this tile
     for (int i = tid; i < t.bm * ngt; i += nt) {
@@ -193,6 +207,9 @@ struct EpiJet {
       if (!compact) {
 #pragma unroll
         for (int s = 0; s < 4; ++s) Yz[(size_t)(cg + s) * ldy + m] = o[s];
+        if (hw)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) note(s, o[s]);
       } else if (gl == 0) {
         Yz[(size_t)(sim * cs) * ldy + m] = o[0];
         Yz[(size_t)(sim * cs + 1) * ldy + m] = 2.0 * o[2];
@@ -212,11 +229,19 @@ struct EpiJet {
           const size_t col = (size_t)(cg + 4 + 4 * k);
 #pragma unroll
           for (int s = 0; s < 4; ++s) Yz[(col + s) * ldy + m] = yo[s];
+          if (hw)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) note(4 + 4 * k + s, yo[s]);
         }
         if (Cz && kg < n_q) {  // sin'(z0 + y0 e) = cos z0 - sin z0 y0 e (dual), for the vhp backward
           Cz[(size_t)(2 * kg) * ldcache + m] = jc.c1;
           Cz[(size_t)(2 * kg + 1) * ldcache + m] = jc.ns * y[0];
         }
+      }
+      if (hw) {
+        const int parts = g.M >> 5, rg = m >> 5;
+        if (lane < group) colhw[(size_t)(cg + lane) * parts + rg] = hw0;
+        if (lane + 32 < group) colhw[(size_t)(cg + 32 + lane) * parts + rg] = hw1;
       }
     }
   }

@@ -20,10 +20,10 @@
 //              operand layout, so one cp.async.bulk per K chunk (28 KB) lands a stage
 //   warp 1     TMEM owner + MMA issuer (one thread): 28 tcgen05.mma (M = 128, N = 64, K = 32) per
 //              K chunk, tcgen05.commit frees the stage; a final commit hands the tile to the epilogue
-//   warps 2-5  epilogue (TMEM lane quarters 2, 3, 0, 1): tcgen05.ld the 7 accumulators, exact
+//   warps 2-9  epilogue (two warps per TMEM lane quarter, each half of the columns): tcgen05.ld the 7 accumulators, exact
 //              int64 recombination, fp64 tile in shared memory, then the same Epi functor as the
 //              DMMA kernels (bias + jet sin, vhp epilogues, ...)
-//   warps 6-13 B converters: per tile the column exponents (max over K), per K chunk the 7 int8
+//   warps 10-13 B converters: per tile the column exponents (max over K), per K chunk the 7 int8
 //              slice planes of the fp64 activations written straight into the UMMA core-matrix
 //              layout (no swizzle, K-major: 8 rows x 16 B cores, LBO = 128 B, SBO = 256 B)
 #pragma once
@@ -43,8 +43,10 @@ constexpr int BM = 128, BK = 32;
 constexpr int A_SLICE = BM * BK;             // bytes per slice plane of a stage
 constexpr int A_STAGE = S * A_SLICE;         // 28 KB
 constexpr int LDC = BM + 2;
-constexpr int NCONV = 256;      // B converter threads (warps 6 .. 13)
-constexpr int NT = 192 + NCONV;
+constexpr int NEPI = 256;       // epilogue threads (warps 2 .. 9: two warps per TMEM lane quarter)
+constexpr int NCONV = 128;      // B converter threads (warps 10 .. 13)
+constexpr int EPI_W0 = 2, CONV_W0 = 2 + NEPI / 32;
+constexpr int NT = 64 + NEPI + NCONV;
 constexpr uint32_t TMEM_COLS = 512;
 
 // Tile configuration per column-tile width BN (32 or 64 columns).
@@ -58,7 +60,7 @@ struct Cfg {
   static constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + CS_BYTES + 512;
   // two accumulator sets (the next tile's MMAs overlap this tile's drain) when they fit in TMEM
   static constexpr int NBUF = 2 * NACC * BN <= (int)TMEM_COLS ? 2 : 1;
-  static constexpr int KPT = BN * BK / NCONV;   // K elements per converter thread per chunk (4 or 8)
+  static constexpr int KPT = BN * BK / NCONV;   // K elements per converter thread per chunk (8 or 16)
   static_assert(BN == 32 || BN == 64, "column tile");
 };
 
@@ -129,7 +131,11 @@ __host__ __device__ __forceinline__ uint32_t digit(long long qb, int t) {   // t
 }
 __device__ __forceinline__ long long fixed55(double x, double scale55) { return balanced(__double2ll_rz(x * scale55)); }
 // exponent E of a row / column with max|x| < (127/128) 2^E (0 for an all-zero one)
-__host__ __device__ __forceinline__ int exp_of(double amax) { return scale_exp(amax * (128.0 / 127.0)); }
+// (clamped at -900 so that the 2^(55 - E) scale and the 2^(E - 62) recombination stay normal)
+__host__ __device__ __forceinline__ int exp_of(double amax) {
+  const int e = scale_exp(amax * (128.0 / 127.0));
+  return e < -900 ? -900 : e;
+}
 
 }  // namespace oz
 
@@ -141,12 +147,13 @@ struct OzakiA {
   const int* row_exp;           // [M]
 };
 
-// Column exponents of the B operand: max over `nparts` per-column partials written by the
-// producing layer's epilogue (int, exponent E with max|x| < 2^E, column-major [C][nparts]); with
-// parts == nullptr the kernel computes them itself (a pre-pass over each column tile).
+// Column scales of the B operand from partials written by the producing layer's epilogue
+// (EpiJet::colhw): parts[c * nparts + p] = max over a row group of the high word of |x|, so
+// exp_of(hiword:0xFFFFFFFF) bounds the column maximum; with parts == nullptr the kernel computes
+// the column maxima itself (a pre-pass over each column tile).
 struct OzakiBExp {
-  const int* parts;
-  int nparts;   // <= 4
+  const unsigned* parts;
+  int nparts;   // <= 8
 };
 
 // Device copy of one layer's prepared A operand (digit tiles + row exponents).
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
   uint64_t* tfull = bar + 3 * STAGES;    // [NBUF] accumulators complete (commit)
   uint64_t* tempty = tfull + 2;          // [NBUF] accumulators drained (one arrival per epilogue warp)
   uint64_t* eready = tfull + 4;          // [2] column exponents of a tile written (NCONV converters)
-  uint64_t* efree = tfull + 6;           // [2] column exponents of a tile consumed (128 epilogue)
+  uint64_t* efree = tfull + 6;           // [2] column exponents of a tile consumed (NEPI epilogue threads)
   uint64_t* tdone = tfull + 8;           // every MMA of this CTA complete (before TMEM dealloc)
   int* colE = reinterpret_cast<int*>(tfull + 10);  // [2][BN]
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(colE + 2 * BN);
@@ -232,9 +239,9 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
-      mbar_init(tempty + i, 4);
+      mbar_init(tempty + i, NEPI / 32);
       mbar_init(eready + i, NCONV);
-      mbar_init(efree + i, 128);
+      mbar_init(efree + i, NEPI);
     }
     mbar_init(tdone, 1);
     fence_mbar_init();
@@ -324,12 +331,12 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       tc_commit(tdone);
       mbar_wait_cta(tdone, 0);
     }
-  } else if (warp >= 6) {
-    // --------------------------------------------------------------- B converters (warps 6 .. 13)
+  } else if (warp >= CONV_W0) {
+    // --------------------------------------------------------------- B converters (warps 10 .. 13)
     pdl_wait();
-    const int ct = tid - 6 * 32;     // 0 .. NCONV-1
-    constexpr int TPC = NCONV / BN;  // threads per column (4 or 8), each KPT consecutive K per chunk
-    constexpr int PF = KPT == 4 ? 4 : 2;   // chunks in flight per thread (register ring)
+    const int ct = tid - CONV_W0 * 32;   // 0 .. NCONV-1
+    constexpr int TPC = NCONV / BN;  // threads per column (2 or 4), each KPT consecutive K per chunk
+    constexpr int PF = KPT == 8 ? 4 : 2;   // chunks in flight per thread (register ring)
     const int cl = ct / TPC, kq = ct % TPC;
     const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const long long total = (long long)my_tiles * nk;
@@ -358,12 +365,11 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
     // column exponent of tile j for this thread's column: max over the producer's partials (up to
     // MAXP, loaded one tile ahead and reduced when the tile starts), or (no partials) a pre-pass
     // over the column by the TPC threads that share it
-    constexpr int MAXP = 4;
-    auto load_parts = [&](int j, int (&pp)[MAXP]) {
+    constexpr int MAXP = 8;
+    auto load_parts = [&](int j, unsigned (&pp)[MAXP]) {
       const int c = j < my_tiles ? col_of(j) : g.C;
 #pragma unroll
-      for (int p = 0; p < MAXP; ++p)
-        pp[p] = (c < g.C && p < bexp.nparts) ? bexp.parts[(size_t)c * bexp.nparts + p] : (p == 0 ? 0 : -2000);
+      for (int p = 0; p < MAXP; ++p) pp[p] = (c < g.C && p < bexp.nparts) ? bexp.parts[(size_t)c * bexp.nparts + p] : 0u;
     };
     auto prepass_exp = [&](int j) -> int {
       const int c = j < my_tiles ? col_of(j) : g.C;
@@ -374,7 +380,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       for (int o = 1; o < TPC; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
       return exp_of(m);
     };
-    int pp_next[MAXP];
+    unsigned pp_next[MAXP];
     if (bexp.parts) load_parts(0, pp_next);
     double xr[PF][KPT];
 #pragma unroll
@@ -393,9 +399,10 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
           // tile j starts: publish its column exponents (epilogue scale), fetch tile j + 1's
           int e;
           if (bexp.parts) {
-            e = pp_next[0];
+            unsigned hw = pp_next[0];
 #pragma unroll
-            for (int p = 1; p < MAXP; ++p) e = max(e, pp_next[p]);
+            for (int p = 1; p < MAXP; ++p) hw = max(hw, pp_next[p]);
+            e = hw ? exp_of(__hiloint2double((int)hw, (int)0xFFFFFFFFu)) : 0;   // bounds the column max
             load_parts(j + 1, pp_next);
           } else {
             e = prepass_exp(j);
@@ -429,10 +436,10 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
         unsigned char* dst = sB + st * C::B_STAGE + oz::core_off(cl, kq * KPT);
 #pragma unroll
         for (int t2 = 0; t2 < S; ++t2) {
-          if constexpr (KPT == 8)
-            *reinterpret_cast<uint2*>(dst + t2 * C::B_SLICE) = make_uint2(w[t2][0], w[t2][1]);
+          if constexpr (KPT == 16)
+            *reinterpret_cast<uint4*>(dst + t2 * C::B_SLICE) = make_uint4(w[t2][0], w[t2][1], w[t2][2], w[t2][3]);
           else
-            *reinterpret_cast<uint32_t*>(dst + t2 * C::B_SLICE) = w[t2][0];
+            *reinterpret_cast<uint2*>(dst + t2 * C::B_SLICE) = make_uint2(w[t2][0], w[t2][1]);
         }
         fence_proxy_async();     // generic-proxy stores -> visible to the tensor core (async proxy)
         __syncwarp();
@@ -449,10 +456,11 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       }
     }
   } else {
-    // --------------------------------------------------------------- epilogue (warps 2-5)
+    // --------------------------------------------------------------- epilogue (warps 2 .. 9)
     pdl_wait();
     const int q = warp & 3;              // TMEM lane quarter of this warp
-    const int et = tid - 2 * 32;          // 0..127
+    const int et = tid - EPI_W0 * 32;     // 0 .. NEPI-1
+    const int chalf = (warp - EPI_W0) >> 2;   // which half of the tile's columns this warp drains
     const int row_l = q * 32 + lane;      // tile row = TMEM lane
     int j = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
@@ -473,9 +481,9 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       const int m = m0 + row_l;
       const int em = (m < g.M) ? a.row_exp[m] : 0;
       const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * NACC * BN);
-      named_bar_sync(1, 128);  // the previous tile's epilogue is done with Cs
+      named_bar_sync(1, NEPI);  // the previous tile's epilogue is done with Cs
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 16; ++ch) {
+      for (int ch = chalf * (BN / 32); ch < (chalf + 1) * (BN / 32); ++ch) {
         int acc[NACC][16];
 #pragma unroll
         for (int d = 0; d < NACC; ++d) oz::tmem_ld16(tacc + (uint32_t)(d * BN + ch * 16), acc[d]);
@@ -488,7 +496,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
                                ((long long)acc[5][i] << 8) + (long long)acc[6][i];
           const int E = em + colE[(j & 1) * BN + cl];
           // x_a x_b = q_a q_b 2^{E-110} = 2^{E+2} sum_d acc_d 2^{-8d} = hi 2^{E-30} + lo 2^{E-62}
-          Cs[cl * LDC + row_l] = fma((double)hi, oz::pow2(E - 30), (double)lo * oz::pow2(E - 62));
+          Cs[cl * LDC + row_l] = E < -960 ? 0.0 : fma((double)hi, oz::pow2(E - 30), (double)lo * oz::pow2(E - 62));
         }
       }
       tc_fence_before();
@@ -498,10 +506,10 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + buf);   // TMEM may take the next tiles' accumulators
       mbar_arrive(efree + (j & 1));
-      named_bar_sync(1, 128);
+      named_bar_sync(1, NEPI);
       Tile tile{Cs, LDC, m0, c0, BM, BN, 0};
 #ifndef OZ_PROBE_NO_EPI
-      epi(tile, g, et, 128);
+      epi(tile, g, et, NEPI);
 #endif
     }
   }
