@@ -80,10 +80,10 @@ int main(int argc, char** argv) {
     NL_CUDA(cudaMemcpy(bigB.p, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice));
   }
   GemmArgs gb{dA.p, bigB.p, K, K, M, CT, K, 0, 0};
-  int* dEx;  // precomputed column exponents (1 part per column): all columns in (-1, 1)
+  unsigned* dEx;  // precomputed column scales (1 part per column): high word of 1.0 (|x| < 1)
   NL_CUDA(cudaMalloc(&dEx, CT * 4));
   {
-    std::vector<int> ex(CT, 1);  // max|x| < 1 < (127/128) 2^1
+    std::vector<unsigned> ex(CT, 0x3FF00000u);
     NL_CUDA(cudaMemcpy(dEx, ex.data(), CT * 4, cudaMemcpyHostToDevice));
   }
   const OzakiBExp pre{dEx, 1}, self{nullptr, 0};
