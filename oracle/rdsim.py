@@ -150,8 +150,9 @@ class NewtonDivergence(RuntimeError):
         self.last_norm = last_norm
 
 
-def step(sim, r_bar, rdot_bar, f_ext, cfg):
-    """One implicit timestep. Returns (r, rdot, iters, ||phi||)."""
+def step(sim, r_bar, rdot_bar, f_ext, cfg, trace=None):
+    """One implicit timestep. Returns (r, rdot, iters, ||phi||); ``trace``
+    (a list) receives the line-search halvings of every Newton iteration."""
     r_bar = np.asarray(r_bar, dtype=float)
     rdot_bar = np.asarray(rdot_bar, dtype=float)
     state = (r_bar, rdot_bar)
@@ -173,13 +174,15 @@ def step(sim, r_bar, rdot_bar, f_ext, cfg):
         S = system_jacobian(sim, r, state, f_ext, cfg)
         dr = scipy.linalg.lu_solve(scipy.linalg.lu_factor(S), -phi)
         t = 1.0
-        for _ in range(11):
+        for k in range(11):
             r_try = r + t * dr
             phi_try = residual(sim, r_try, state, f_ext, cfg)
             n_try = float(np.linalg.norm(phi_try))
             if not cfg.line_search or n_try < nrm:
                 break
             t *= 0.5
+        if trace is not None:
+            trace.append(k)
         r, phi, nrm = r_try, phi_try, n_try
         it += 1
     return r, (r - r_bar) / cfg.dt, it, nrm

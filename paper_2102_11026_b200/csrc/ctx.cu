@@ -23,6 +23,7 @@
 #include "coupled_kernels.cuh"
 #include "gemm_ws.cuh"
 #include "ozaki_tc.cuh"
+#include "newton_kernels.cuh"
 
 namespace nlrom {
 void fc_forward(int order, int act, const GemmArgs& g, double* Y, int ldy, const double* bias, double* cache,
@@ -165,6 +166,9 @@ struct nlrom_ctx {
   // graphs
   cudaGraphExec_t gE = nullptr, gJ = nullptr, gIter = nullptr;
   cudaGraphExec_t gStep = nullptr;  // whole fixed-iteration step incl. pinned H2D / D2H (nlrom_step)
+  cudaGraphExec_t gAdapt = nullptr; // whole adaptive step: conditional while nodes (newton_kernels.cuh)
+  std::string adapt_key;
+  DBuf ad;                          // adaptive Newton state (NT_SIZE doubles)
   std::string step_key;
   std::string graph_key;
   int launches_E = 0, launches_J = 0;
@@ -1320,6 +1324,7 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->gJ) cudaGraphExecDestroy(c->gJ);
   if (c->gIter) cudaGraphExecDestroy(c->gIter);
   if (c->gStep) cudaGraphExecDestroy(c->gStep);
+  if (c->gAdapt) cudaGraphExecDestroy(c->gAdapt);
   for (auto g : c->gC)
     if (g) cudaGraphExecDestroy(g);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1544,54 +1549,104 @@ extern "C" int nlrom_cubature_integrate(nlrom_ctx* c, const double* r, int integ
   CTX_END(c)
 }
 
-// ---------------------------------------------------------------- step
-static void run_step(nlrom_ctx* c, const nlrom_simcfg& cfg, nlrom_step_info* info) {
-  const int nn = c->n_sims * c->n;
-  ensure_graphs(c, cfg);
-  launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg.dt, nn);
-  if (cfg.fixed_iters > 0) {
-    for (int it = 0; it < cfg.fixed_iters; ++it) NL_CUDA(cudaGraphLaunch(c->gIter, c->st));
-    NL_CUDA(cudaGraphLaunch(c->gE, c->st));
-    check_status(c);
-    double nrm = 0;
-    NL_CUDA(cudaMemcpyAsync(&nrm, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
-    NL_CUDA(cudaStreamSynchronize(c->st));
-    if (info) { info->iters = cfg.fixed_iters; info->res_norm = nrm; info->status = 0; }
-    return;
-  }
-  if (c->n_sims != 1) throw Error(NLROM_ERR_ARG, "adaptive Newton requires a single-sim context");
-  NL_CUDA(cudaGraphLaunch(c->gE, c->st));
-  double nrm = 0;
-  NL_CUDA(cudaMemcpyAsync(&nrm, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
-  NL_CUDA(cudaStreamSynchronize(c->st));
-  int it = 0;
-  while (nrm > cfg.newton_tol) {
-    if (it >= cfg.max_iters) {
-      c->last_norm = nrm;
-      char buf[160];
-      snprintf(buf, sizeof buf, "Newton did not converge in %d iterations; last residual norm %.3e", cfg.max_iters, nrm);
-      throw Error(NLROM_ERR_NEWTON, buf);
-    }
-    NL_CUDA(cudaGraphLaunch(c->gJ, c->st));
-    check_status(c);
-    NL_CUDA(cudaMemcpyAsync(c->rsave.p, c->r.p, nn * 8, cudaMemcpyDeviceToDevice, c->st));
-    double t = 1.0, ntry = 0;
-    for (int k = 0; k < 11; ++k) {
-      launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rsave.p, (const double*)c->dr.p, t, nn);
-      NL_CUDA(cudaGraphLaunch(c->gE, c->st));
-      NL_CUDA(cudaMemcpyAsync(&ntry, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
-      NL_CUDA(cudaStreamSynchronize(c->st));
-      if (!std::isfinite(ntry)) throw Error(NLROM_ERR_NONFINITE, "non-finite residual");
-      if (!cfg.line_search || ntry < nrm) break;
-      t *= 0.5;
-    }
-    nrm = ntry;
-    ++it;
-  }
-  c->last_norm = nrm;
-  if (info) { info->iters = it; info->res_norm = nrm; info->status = 0; }
+// ---------------------------------------------------------------- adaptive step graph
+// Adds a conditional while node after the current capture dependencies of c->st and returns its
+// body graph (to be captured after the enclosing capture ends).
+static cudaGraph_t add_while_node(nlrom_ctx* c, cudaGraphConditionalHandle h) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t graph;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  NL_CUDA(cudaStreamGetCaptureInfo(c->st, &cs, nullptr, &graph, &deps, &nd));
+  if (cs != cudaStreamCaptureStatusActive) throw Error(NLROM_ERR_CUDA, "adaptive graph: stream not capturing");
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  NL_CUDA(cudaGraphAddNode(&node, graph, deps, nd, &p));
+  NL_CUDA(cudaStreamUpdateCaptureDependencies(c->st, &node, 1, cudaStreamSetCaptureDependencies));
+  return p.conditional.phGraph_out[0];
 }
 
+static cudaGraph_t capture_graph_of(nlrom_ctx* c) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t graph;
+  NL_CUDA(cudaStreamGetCaptureInfo(c->st, &cs, nullptr, &graph, nullptr, nullptr));
+  return graph;
+}
+
+// The whole adaptive timestep as ONE graph (single sim): pinned H2D of r_bar, rdot_bar, f_ext,
+// predictor, E, then the Newton / line-search loops as nested conditional while nodes, rdot and
+// the pinned D2H of r, rdot and the Newton state -- one launch and one host sync per step.
+static void ensure_adaptive_graph(nlrom_ctx* c, const nlrom_simcfg& cfg, double* hi, double* ho) {
+  ensure_graphs(c, cfg);
+  char kb[256];
+  snprintf(kb, sizeof kb, "%s|%.17g|%d|%d|%p|%p", c->graph_key.c_str(), cfg.newton_tol, cfg.max_iters,
+           cfg.line_search, (void*)hi, (void*)ho);
+  if (c->gAdapt && c->adapt_key == kb) return;
+  if (c->gAdapt) cudaGraphExecDestroy(c->gAdapt);
+  c->gAdapt = nullptr;
+  if (!c->ad.p) c->ad.alloc(NT_SIZE);
+  const int n = c->n;
+  const size_t N = (size_t)c->N;
+  const int nb = std::min(256, round_up(n, 32));
+  cudaGraph_t G = nullptr, bodyO = nullptr, bodyI = nullptr;
+  cudaGraphConditionalHandle hO, hI;
+  gemm_launch_count = 0;
+  // prologue + outer while node + epilogue
+  NL_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  try {
+    NL_CUDA(cudaGraphConditionalHandleCreate(&hO, capture_graph_of(c), 0, 0));
+    NL_CUDA(cudaMemcpyAsync(c->rbar.p, hi, (size_t)n * 8, cudaMemcpyHostToDevice, c->st));
+    NL_CUDA(cudaMemcpyAsync(c->rdbar.p, hi + n, (size_t)n * 8, cudaMemcpyHostToDevice, c->st));
+    NL_CUDA(cudaMemcpyAsync(c->fext.p, hi + 2 * n, N * 8, cudaMemcpyHostToDevice, c->st));
+    launch(c, k_axpy, grid1(n), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg.dt, n);
+    phase_E(c, cfg);
+    launch(c, k_nt_init, 1, 1, 0, hO, (const double*)c->norm.p, c->ad.p, cfg.newton_tol, cfg.max_iters);
+    bodyO = add_while_node(c, hO);
+    launch(c, k_rdot, grid1(n), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg.dt, n);
+    NL_CUDA(cudaMemcpyAsync(ho, c->r.p, (size_t)n * 8, cudaMemcpyDeviceToHost, c->st));
+    NL_CUDA(cudaMemcpyAsync(ho + n, c->rdot.p, (size_t)n * 8, cudaMemcpyDeviceToHost, c->st));
+    NL_CUDA(cudaMemcpyAsync(ho + 2 * n, c->ad.p, NT_SIZE * 8, cudaMemcpyDeviceToHost, c->st));
+  } catch (...) {
+    cudaStreamEndCapture(c->st, &G);
+    if (G) cudaGraphDestroy(G);
+    throw;
+  }
+  NL_CUDA(cudaStreamEndCapture(c->st, &G));
+  try {
+    // Newton iteration: J -> dr, then the line search while node, then the convergence test
+    NL_CUDA(cudaStreamBeginCaptureToGraph(c->st, bodyO, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    NL_CUDA(cudaGraphConditionalHandleCreate(&hI, bodyO, 0, 0));
+    phase_J(c, cfg, false);
+    launch(c, k_nt_ls_begin, 1, nb, 0, hI, (const int*)c->status.p, (const double*)c->r.p, c->rsave.p, c->ad.p, n);
+    bodyI = add_while_node(c, hI);
+    launch(c, k_nt_check, 1, 1, 0, hO, c->ad.p, cfg.newton_tol, cfg.max_iters);
+    NL_CUDA(cudaStreamEndCapture(c->st, &bodyO));
+    // one line-search trial: r = rsave + t dr, E(r)
+    NL_CUDA(cudaStreamBeginCaptureToGraph(c->st, bodyI, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    launch(c, k_nt_axpy, 1, nb, 0, c->r.p, (const double*)c->rsave.p, (const double*)c->dr.p,
+           (const double*)c->ad.p, n);
+    phase_E(c, cfg);
+    launch(c, k_nt_ls_check, 1, 1, 0, hI, (const double*)c->norm.p, c->ad.p, cfg.line_search);
+    NL_CUDA(cudaStreamEndCapture(c->st, &bodyI));
+    NL_CUDA(cudaGraphInstantiate(&c->gAdapt, G, 0));
+  } catch (...) {
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(c->st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      cudaGraph_t tmp;
+      cudaStreamEndCapture(c->st, &tmp);
+    }
+    cudaGraphDestroy(G);
+    throw;
+  }
+  cudaGraphDestroy(G);
+  c->adapt_key = kb;
+}
+
+// ---------------------------------------------------------------- step
 extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar, const double* fext,
                           const nlrom_simcfg* cfg, double* r_out, double* rdot_out, nlrom_step_info* info) {
   CTX_TRY(c)
@@ -1645,13 +1700,32 @@ extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar,
     c->last_norm = ho[2 * nn];
     if (info) { info->iters = cfg->fixed_iters; info->res_norm = ho[2 * nn]; info->status = 0; }
   } else {
-    set_state(c, nullptr, rbar, rdbar, fext);
-    run_step(c, *cfg, info);
-    launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg->dt,
-           nn);
-    d2h(c, r_out, c->r, nn);
-    d2h(c, rdot_out, c->rdot, nn);
+    if (c->n_sims != 1) throw Error(NLROM_ERR_ARG, "adaptive Newton requires a single-sim context");
+    const int n = c->n;
+    c->hin.alloc(2 * (size_t)n + c->N);
+    c->hout.alloc(2 * (size_t)n + NT_SIZE);
+    double* hi = c->hin.p;
+    double* ho = c->hout.p;
+    memcpy(hi, rbar, (size_t)n * 8);
+    memcpy(hi + n, rdbar, (size_t)n * 8);
+    memcpy(hi + 2 * n, fext, (size_t)c->N * 8);
+    ensure_adaptive_graph(c, *cfg, hi, ho);
+    NL_CUDA(cudaGraphLaunch(c->gAdapt, c->st));
     NL_CUDA(cudaStreamSynchronize(c->st));
+    const double* st = ho + 2 * n;
+    const int status = (int)st[NT_STATUS], it = (int)st[NT_IT];
+    const double nrm = st[NT_NORM];
+    c->last_norm = nrm;
+    if (status == NT_SINGULAR) throw Error(NLROM_ERR_NONFINITE, "singular system Jacobian (zero pivot in LU)");
+    if (status == NT_NONFINITE) throw Error(NLROM_ERR_NONFINITE, "non-finite residual");
+    if (status == NT_MAXITER) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "Newton did not converge in %d iterations; last residual norm %.17g", cfg->max_iters, nrm);
+      throw Error(NLROM_ERR_NEWTON, buf);
+    }
+    memcpy(r_out, ho, (size_t)n * 8);
+    memcpy(rdot_out, ho + n, (size_t)n * 8);
+    if (info) { info->iters = it; info->res_norm = nrm; info->status = 0; }
   }
   CTX_END(c)
 }

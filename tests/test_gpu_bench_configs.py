@@ -84,3 +84,51 @@ def test_cfg5_full_scale_sampled_sims(cuda_ok):
         ro, rdo, _, _ = ors.step(S, rb[i].copy(), rdb[i].copy(), fe[i], ocfg(cfg))
         assert rel(r[i], ro) <= 1e-10, i
         assert rel(rd[i], rdo) <= 1e-8, i
+
+
+# ------------------------------------------------------------------ adaptive Newton on the device
+def test_cfg2_adaptive_steps_device_loop(cfg2):
+    """rdsim.step in adaptive mode runs the Newton / line-search loops as conditional graph nodes
+    (newton_kernels.cuh): iteration counts and states equal the oracle's host loop at cfg2."""
+    from paper_2102_11026_b200 import rdsim
+    P, S = cfg2
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, newton_tol=1e-9)
+    st = P.rest_state()
+    ro, rdo = st.r.copy(), st.rdot.copy()
+    for _ in range(6):
+        st, (it, nrm) = rdsim.step(P.rm, P.model, st, P.f_ext, cfg, return_info=True)
+        ro, rdo, ito, nro = ors.step(S, ro, rdo, P.f_ext, ocfg(cfg))
+        assert it == ito and nrm <= cfg.newton_tol
+        assert rel(st.r, ro) <= 1e-10
+
+
+def test_adaptive_line_search_and_limits(cuda_ok):
+    """Hard states (scaled random r_bar, rdot_bar): at 0.45 Newton converges in 6 iterations, at
+    0.5 the backtracking line search engages every iteration (oracle halvings 4, 2, 5 after a full
+    first step) and 4 iterations do not converge -- the device loop raises NewtonDivergence with
+    the oracle's last norm. max_iters = 2 at a 1e-300 tolerance raises after 2 iterations."""
+    from paper_2102_11026_b200.problem import build_problem
+    from paper_2102_11026_b200 import rdsim
+    from paper_2102_11026_b200.daereduce import ReducedState
+    from paper_2102_11026_b200._lib import NewtonDivergence
+    from oracle.rdsim import NewtonDivergence as ONewtonDivergence
+    P = build_problem("cfg2", n_fc=4)
+    S = oracle_sim(P)
+    _, rb, rdb = P.random_state()
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, newton_tol=1e-8, max_iters=30, line_search=True)
+    ro, rdo, ito, nro = ors.step(S, 0.45 * rb, 0.45 * rdb, P.f_ext, ocfg(cfg))
+    st, (it, nrm) = rdsim.step(P.rm, P.model, ReducedState(0.45 * rb, 0.45 * rdb, cfg.dt), P.f_ext, cfg,
+                               return_info=True)
+    assert it == ito and rel(st.r, ro) <= 1e-9
+    cfg4 = rdsim.SimConfig(dt=P.cfg.dt, newton_tol=1e-8, max_iters=4, line_search=True)
+    halvings = []
+    with pytest.raises(ONewtonDivergence) as eo:
+        ors.step(S, 0.5 * rb, 0.5 * rdb, P.f_ext, ocfg(cfg4), trace=halvings)
+    assert sum(halvings) > 0, halvings
+    with pytest.raises(NewtonDivergence) as eg:
+        rdsim.step(P.rm, P.model, ReducedState(0.5 * rb, 0.5 * rdb, cfg.dt), P.f_ext, cfg4)
+    assert abs(eg.value.last_norm - eo.value.last_norm) <= 1e-8 * eo.value.last_norm
+    tight = rdsim.SimConfig(dt=P.cfg.dt, newton_tol=1e-300, max_iters=2)
+    with pytest.raises(NewtonDivergence) as ei:
+        rdsim.step(P.rm, P.model, ReducedState(rb, rdb, cfg.dt), P.f_ext, tight)
+    assert "2 iterations" in str(ei.value)
