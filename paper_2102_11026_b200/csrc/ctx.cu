@@ -915,17 +915,19 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
   const int n = c->n;
   const double* Gt = add_vhp ? (const double*)c->Gt.p : nullptr;
   auto go = [&](auto kern) {
-    launch(c, kern, c->n_sims, 256, lu_blocked_smem_bytes(n + nx, c->n_q), (const double*)c->S.p,
+    launch(c, kern, c->n_sims, 256, lu_lookahead_smem_bytes(n + nx, c->n_q), (const double*)c->S.p,
            (const double*)c->phi.p, c->dr.p, c->r.p, n, apply ? 1 : 0, c->status.p, xrhs, nx, xout, Gt, c->ldGt,
            c->n_p);
   };
-  // 8-column panels factored by one warp in registers (bitwise equal to the one-barrier-per-pivot
-  // k_lu_solve; tools/probes/lu_blocked_probe.cu). Retired variants (warp-register,
-  // column-cyclic, rank-2, look-ahead, split front/back): DESIGN.md §8b, tools/probes/retired/
+  // One warp owns the pivot chain (4-column panels in registers, the next panel brought up to date
+  // by the same warp), 7 warps apply the trailing updates: bitwise equal to the one-barrier-per-pivot
+  // k_lu_solve; as fast at n = 60, 10-35% faster at n = 70..124 (tools/probes/lu_blocked_probe.cu,
+  // profiles/r02_lu_probe.txt). Retired variants (warp-register, column-cyclic, rank-2, look-ahead
+  // pivot, split front/back, k_lu_blocked): DESIGN.md §8b, tools/probes/retired/
   switch (lu_nb(n + nx)) {
-    case 4: go(k_lu_blocked<4>); break;
-    case 6: go(k_lu_blocked<6>); break;
-    default: go(k_lu_blocked<8>); break;
+    case 4: go(k_lu_lookahead<4>); break;
+    case 6: go(k_lu_lookahead<6>); break;
+    default: go(k_lu_lookahead<8>); break;
   }
 }
 
@@ -1298,9 +1300,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_blocked<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_blocked<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_lu_blocked<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_lookahead<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_lookahead<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_lu_lookahead<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

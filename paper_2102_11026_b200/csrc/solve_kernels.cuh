@@ -546,43 +546,48 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
   if (tid == 0) status[sim] = 0;
 }
 
-// Blocked form of k_lu_solve (same pivots, same multipliers, same fma sequence per element:
-// bitwise-equal results, tools/probes/lu_blocked_probe.cu). The per-pivot-step work that must be
-// serial runs in ONE warp on 8-column panels held in registers (lane owns rows lane + 32u):
-// exact argmax by integer REDUX, the pivot row's panel entries by shuffles, multipliers and the
-// rank-1 update of the remaining panel columns -- no CTA barrier inside a panel. Per panel the
-// CTA then (1) forms the pivot rows' trailing entries u_kj = A[p_k][j] after the panel's earlier
-// steps (a thread per column), (2) applies the panel's 8 rank-1 updates to its register block
-// in step order and writes it back to the shared mirror: 3 barriers per 8 pivots instead of one
-// per pivot with a full matrix write-back each. Gauss-Jordan (every non-pivot row eliminated)
-// and implicit pivoting as k_lu_solve.
 #ifdef LU_TRACE
-__device__ long long g_lu_trace[4 * 16 + 2];
+__device__ long long g_lu_trace[4 * 16 + 2];   // tools/probes/lu_blocked_probe.cu -DLU_TRACE
+__device__ long long g_lu_trace_u[4 * 16];
 #endif
-template <int NB>
-__global__ void __launch_bounds__(256) k_lu_blocked(const double* __restrict__ S, const double* __restrict__ phi,
-                                                     double* __restrict__ dr, double* __restrict__ r, int n, int apply,
-                                                     int* __restrict__ status, const double* __restrict__ xrhs, int nx,
-                                                     double* __restrict__ xout, const double* __restrict__ Gt, int ldg,
-                                                     int n_p) {
+// Look-ahead panel LU (same pivots, same multipliers, same fma sequence per element as
+// k_lu_solve: bitwise-equal results, tools/probes/lu_blocked_probe.cu). One warp owns the pivot
+// chain: it factors an 8-column panel in registers (exact REDUX argmax, reciprocal of |p| from the
+// reduced key while the row index reduction and the pivot-row shuffles run, multipliers, rank-1
+// updates of the remaining panel columns), publishes the panel's multipliers, and then brings the
+// NEXT panel's 8 columns up to date itself (pivot-row entries from its own registers, the
+// u-chain of the panel's pivot rows, 8 fmas per element) -- so it never waits for the trailing
+// update. Warps 1-7 apply each published panel to the columns beyond the next panel; a column is
+// owned by one warp for the whole factorisation (column j -> warp 1 + j mod 7), so updates of one
+// column need no cross-warp ordering. Hand-offs are counters in shared memory (the panel warp
+// waits for the trailing update of panel P-1 before reading panel P+1's columns), no CTA barrier
+// inside the factorisation. Gauss-Jordan form and implicit pivoting as k_lu_solve.
+template <int NB, int PW = 4>
+__global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__ S, const double* __restrict__ phi,
+                                                       double* __restrict__ dr, double* __restrict__ r, int n, int apply,
+                                                       int* __restrict__ status, const double* __restrict__ xrhs, int nx,
+                                                       double* __restrict__ xout, const double* __restrict__ Gt, int ldg,
+                                                       int n_p) {
   pdl_wait();
   pdl_launch();
   constexpr int D = 16 * NB;
   constexpr int LDF = D + 1;
-  constexpr int PW = 8;                // panel width
-  constexpr int R = D / 32;            // panel rows per lane
-  extern __shared__ double M[];        // [D][LDF] | vhp block [n_q][n_q] | Mul [D][PW] | U [PW][LDF]
+  constexpr int R = D / 32;            // rows per lane (PW: panel width)
+  constexpr int NU = 7;                // trailing-update warps
+  extern __shared__ double M[];        // [D][LDF] | vhp block [n_q][n_q] | Mul [2][D][PW]
   __shared__ int pivrow[D];
   __shared__ double rdiag[D];
-  __shared__ int bad_s;
+  __shared__ volatile int fact_cnt;    // panels factored (multipliers published)
+  __shared__ volatile int upd_cnt[NU]; // panels applied by each update warp
+  __shared__ volatile int bad_s;
   const int sim = blockIdx.x;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31, warp = tid >> 5;
   const double* Ss = S + (size_t)sim * n * n;
   const int nq = n - n_p;
   double* Vs = M + D * LDF;
   double* Mul = Vs + nq * nq;
-  double* Ub = Mul + D * PW;
-  const int ncol = n + 1 + nx;         // live columns (matrix, -phi, extra right-hand sides)
+  const int ncol = n + 1 + nx;
+  const int npan = (n + PW - 1) / PW;
   for (int idx = tid; idx < D * D; idx += 256) {
     const int i = idx / D, j = idx % D;
     double* dst = M + i * LDF + j;
@@ -596,41 +601,41 @@ __global__ void __launch_bounds__(256) k_lu_blocked(const double* __restrict__ S
       const int k = idx / nq, i = idx % nq;
       cp_async8(Vs + idx, Gt + ((size_t)sim * 2 * nq + 2 * k + 1) * ldg + i);
     }
-  if (tid == 0) bad_s = 0;
+  if (tid == 0) {
+    fact_cnt = 0;
+    bad_s = 0;
+  }
+  if (tid < NU) upd_cnt[tid] = 0;
   cp_async_all_wait();
   __syncthreads();
-  // rhs = -phi, S_base + diag(0, vhp); every element is read and rewritten by its own thread
 #pragma unroll
   for (int a = 0; a < NB; ++a)
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int i = ty + 16 * a, j = tx + 16 * b;
       double v = M[i * LDF + j];
-      if (j == n) v = -v;
+      if (j == n) v = -v;  // rhs = -phi
       if (Gt && i >= n_p && j >= n_p && i < n && j < n) v += Vs[(j - n_p) * nq + (i - n_p)];
       M[i * LDF + j] = v;
     }
-  // the panel warp's rows lane + 32 u: pivot already (rows >= n never are)
-  bool used[R];
-#pragma unroll
-  for (int u = 0; u < R; ++u) used[u] = lane + 32 * u >= n;
   __syncthreads();
-#ifdef LU_TRACE
-  if (tid == 0) g_lu_trace[0] = clock64();
-#endif
-  for (int c0 = 0; c0 < n; c0 += PW) {
-    const int kw = min(PW, n - c0);
-#ifdef LU_TRACE
-    if (tid == 0) g_lu_trace[1 + 4 * (c0 / PW)] = clock64();
-#endif
-    if (warp == 0) {
-      // ---- panel: pivots c0 .. c0 + kw - 1 in registers, no CTA barrier
-      double pv[R][PW];
+  if (warp == 0) {
+    // ------------------------------------------------------------------ pivot-chain warp
+    bool used[R];
 #pragma unroll
-      for (int u = 0; u < R; ++u)
+    for (int u = 0; u < R; ++u) used[u] = lane + 32 * u >= n;
+    double pv[R][PW];
 #pragma unroll
-        for (int c = 0; c < PW; ++c) pv[u][c] = M[(lane + 32 * u) * LDF + c0 + c];
+    for (int u = 0; u < R; ++u)
+#pragma unroll
+      for (int c = 0; c < PW; ++c) pv[u][c] = c < n ? M[(lane + 32 * u) * LDF + c] : 0.0;
+    for (int P = 0; P < npan; ++P) {
+      const int c0 = P * PW, kw = min(PW, n - c0);
+      double* MulP = Mul + (P & 1) * D * PW;
       bool bad = false;
+#ifdef LU_TRACE
+      if (lane == 0 && P < 16) g_lu_trace[4 * P] = clock64();
+#endif
 #pragma unroll
       for (int kk = 0; kk < PW; ++kk) {
         if (kk >= kw || bad) break;
@@ -641,19 +646,16 @@ __global__ void __launch_bounds__(256) k_lu_blocked(const double* __restrict__ S
           const double v = fabs(pv[u][kk]);
           if (!used[u] && v > best) { best = v; bi = lane + 32 * u; }
         }
-        // exact argmax of |a_ik| over unused rows, lowest row on ties (LAPACK idamax order)
         const unsigned long long key = (best >= 0.0) ? (unsigned long long)__double_as_longlong(best) : 0ull;
         const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
         const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
         const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-        // 1 / |p| from the reduced key, overlapping the row-index reduction and the shuffles
         const double rabs = recip_fast(__hiloint2double((int)mhi, (int)mlo));
         const int piv = (int)__reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? (unsigned)bi : 0x7fffffffu);
         if (!(mhi | mlo) || piv >= n) { bad = true; break; }
         const int up = piv >> 5, lp = piv & 31;
 #pragma unroll
         for (int u = 0; u < R; ++u) used[u] = used[u] || (u == up && lane == lp);
-        // the pivot row's panel entries kk .. kw-1 from their owner lane
         double prow[PW];
 #pragma unroll
         for (int c = kk; c < PW; ++c) {
@@ -671,92 +673,177 @@ __global__ void __launch_bounds__(256) k_lu_blocked(const double* __restrict__ S
         for (int u = 0; u < R; ++u) {
           const int i = lane + 32 * u;
           const double m = (i < n && i != piv) ? pv[u][kk] * rp : 0.0;
-          Mul[i * PW + kk] = m;
+          MulP[i * PW + kk] = m;
 #pragma unroll
           for (int c = kk + 1; c < PW; ++c) pv[u][c] = fma(-m, prow[c], pv[u][c]);
         }
       }
-      if (bad && lane == 0) bad_s = 1;
-    }
-    __syncthreads();
+      __syncwarp();
+      if (bad) {
+        if (lane == 0) {
+          bad_s = 1;
+          __threadfence_block();
+          fact_cnt = 1 << 30;
+        }
+        break;
+      }
+      if (lane == 0) {
+        __threadfence_block();
+        fact_cnt = P + 1;   // the update warps may apply panel P
+      }
 #ifdef LU_TRACE
-    if (tid == 0) g_lu_trace[2 + 4 * (c0 / PW)] = clock64();
+      if (lane == 0 && P < 16) g_lu_trace[4 * P + 1] = clock64();
 #endif
-    if (bad_s) break;
-    // ---- pivot rows' trailing entries: u_kj = A[p_k][j] after the panel's steps < k
-    // (all loads issued before the chain and the stores)
-    const int jlo = c0 + kw;
-    if (jlo + tid < ncol) {
-      const int j = jlo + tid;
-      int pk[PW];
-      double raw[PW], mk[PW][PW];
-#pragma unroll
-      for (int kk = 0; kk < PW; ++kk) pk[kk] = kk < kw ? pivrow[c0 + kk] : 0;
-#pragma unroll
-      for (int kk = 0; kk < PW; ++kk) {
-        raw[kk] = M[pk[kk] * LDF + j];
-#pragma unroll
-        for (int k2 = 0; k2 < kk; ++k2) mk[kk][k2] = Mul[pk[kk] * PW + k2];
-      }
-      double u[PW];
-#pragma unroll
-      for (int kk = 0; kk < PW; ++kk) {
-        double v = raw[kk];
-#pragma unroll
-        for (int k2 = 0; k2 < kk; ++k2) v = fma(-mk[kk][k2], u[k2], v);
-        u[kk] = v;
-      }
-#pragma unroll
-      for (int kk = 0; kk < PW; ++kk)
-        if (kk < kw) Ub[kk * LDF + j] = u[kk];
-    }
-    __syncthreads();
+      if (P + 1 < npan) {
+        // next panel's columns: up to date through panel P - 1 once the update warps are done with it
+        if (P >= 1) {
+          if (lane == 0)
+            while (upd_cnt[0] < P) {}
+          __syncwarp();
+        }
 #ifdef LU_TRACE
-    if (tid == 0) g_lu_trace[3 + 4 * (c0 / PW)] = clock64();
+        if (lane == 0 && P < 16) g_lu_trace[4 * P + 2] = clock64();
 #endif
-    // ---- the panel's rank-1 updates on every row's trailing block (shared matrix), in step order;
-    // the thread's u values and multipliers are loaded once, before any store
-    {
-      // NB <= 4: every operand of the thread's 4 x 4 block in registers; wider blocks (n > 63)
-      // row by row to stay within the register file
-      constexpr int AR = NB <= 4 ? NB : 1;
-      double ub[NB][PW];
+        const int c1 = c0 + PW, kw1 = min(PW, n - c1);
+        int pk[PW];
+        double mrow[R][PW], mk[PW][PW];
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int j = tx + 16 * b;
+        for (int kk = 0; kk < PW; ++kk) {
+          pk[kk] = kk < kw ? pivrow[c0 + kk] : 0;  // pivrow / MulP of this panel: this warp's own stores
 #pragma unroll
-        for (int kk = 0; kk < PW; ++kk) ub[b][kk] = (kk < kw && 16 * b + 15 >= jlo) ? Ub[kk * LDF + j] : 0.0;
-      }
-#pragma unroll
-      for (int a0 = 0; a0 < NB; a0 += AR) {
-        double m[AR][PW], v[AR][NB];
-#pragma unroll
-        for (int a = 0; a < AR; ++a) {
-          const int i = ty + 16 * (a0 + a);
-#pragma unroll
-          for (int kk = 0; kk < PW; ++kk) m[a][kk] = kk < kw ? Mul[i * PW + kk] : 0.0;
-#pragma unroll
-          for (int b = 0; b < NB; ++b) v[a][b] = (16 * b + 15 >= jlo) ? M[i * LDF + tx + 16 * b] : 0.0;
+          for (int k2 = 0; k2 < PW; ++k2) mk[kk][k2] = (kk < kw && k2 < kk) ? MulP[pk[kk] * PW + k2] : 0.0;
         }
 #pragma unroll
-        for (int a = 0; a < AR; ++a)
+        for (int u = 0; u < R; ++u)
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            if (16 * b + 15 < jlo) continue;  // column block eliminated (uniform)
+          for (int kk = 0; kk < PW; ++kk) mrow[u][kk] = kk < kw ? MulP[(lane + 32 * u) * PW + kk] : 0.0;
+        // 4 columns at a time: the panel's pivot rows at these columns straight from the shared
+        // matrix (up to date through panel P - 1, broadcast loads), their u-chains (independent
+        // across the 4 columns), then every lane's rows
+        static_assert(PW % 4 == 0, "panel width");
 #pragma unroll
-            for (int kk = 0; kk < PW; ++kk) v[a][b] = fma(-m[a][kk], ub[b][kk], v[a][b]);
+        for (int c4 = 0; c4 < PW; c4 += 4) {
+          double raw[4][PW], x[4][R];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const bool live = c4 + c < kw1;
+#pragma unroll
+            for (int kk = 0; kk < PW; ++kk) raw[c][kk] = (live && kk < kw) ? M[pk[kk] * LDF + c1 + c4 + c] : 0.0;
+#pragma unroll
+            for (int u = 0; u < R; ++u) x[c][u] = live ? M[(lane + 32 * u) * LDF + c1 + c4 + c] : 0.0;
           }
+          double uk[4][PW];
 #pragma unroll
-        for (int a = 0; a < AR; ++a)
+          for (int kk = 0; kk < PW; ++kk)
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            const int j = tx + 16 * b;
-            if (j >= jlo && j < ncol) M[(ty + 16 * (a0 + a)) * LDF + j] = v[a][b];
-          }
+            for (int c = 0; c < 4; ++c) {
+              double v = raw[c][kk];
+#pragma unroll
+              for (int k2 = 0; k2 < kk; ++k2) v = fma(-mk[kk][k2], uk[c][k2], v);
+              uk[c][kk] = v;
+            }
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+              double v = x[c][u];
+#pragma unroll
+              for (int kk = 0; kk < PW; ++kk) v = fma(-mrow[u][kk], uk[c][kk], v);
+              pv[u][c4 + c] = v;
+            }
+        }
       }
     }
-    __syncthreads();
+  } else {
+    // ------------------------------------------------------------------ trailing-update warps
+    // work unit = (32-column group, 16-row block), lanes = columns; unit u belongs to warp 1 + u % 7
+    // for the whole factorisation. Per panel: every unit's u-chain from the pivot rows (read by all
+    // units before any unit writes: named barrier), then its rows.
+    constexpr int RB = 16, NRB = D / RB;
+    const int uw = warp - 1, ut = tid - 32;
+    const int ngrp = (ncol + 31) / 32;
+    for (int P = 0; P < npan; ++P) {
+#ifdef LU_TRACE
+      if (ut == 0 && P < 16) g_lu_trace_u[4 * P] = clock64();
+#endif
+      if (lane == 0)
+        while (fact_cnt < P + 1) {}
+      __syncwarp();   // the publisher fenced before its flag store; our loads follow the flag read
+      if (bad_s) break;
+#ifdef LU_TRACE
+      if (ut == 0 && P < 16) g_lu_trace_u[4 * P + 1] = clock64();
+#endif
+      const int c0 = P * PW, kw = min(PW, n - c0);
+      const double* MulP = Mul + (P & 1) * D * PW;
+      const int c1 = c0 + PW;
+      const int jlo = (P + 1 < npan) ? c1 + min(PW, n - c1) : c0 + kw;   // beyond the next panel
+      int pk[PW];
+      double mk[PW][PW];
+#pragma unroll
+      for (int kk = 0; kk < PW; ++kk) {
+        pk[kk] = kk < kw ? pivrow[c0 + kk] : 0;
+#pragma unroll
+        for (int k2 = 0; k2 < PW; ++k2) mk[kk][k2] = (kk < kw && k2 < kk) ? MulP[pk[kk] * PW + k2] : 0.0;
+      }
+      // u-chains of this warp's units (one per column group it owns: the same for all its row blocks)
+      constexpr int MAXU = (4 * NRB + NU - 1) / NU;   // units per warp (<= 4 column groups)
+      double uk[MAXU][PW];
+      int nu = 0;
+#pragma unroll
+      for (int q = 0; q < MAXU; ++q) {
+        const int unit = uw + q * NU, g = unit / NRB;
+        const int j = g * 32 + lane;
+        const bool live = g < ngrp && j >= jlo && j < ncol;
+#pragma unroll
+        for (int kk = 0; kk < PW; ++kk) {
+          double v = (live && kk < kw) ? M[pk[kk] * LDF + j] : 0.0;
+#pragma unroll
+          for (int k2 = 0; k2 < kk; ++k2) v = fma(-mk[kk][k2], uk[q][k2], v);
+          uk[q][kk] = v;
+        }
+        nu += g < ngrp;
+      }
+      named_bar_sync(1, 32 * NU);   // all pivot-row entries read before any unit writes
+#ifdef LU_TRACE
+      if (ut == 0 && P < 16) g_lu_trace_u[4 * P + 2] = clock64();
+#endif
+#pragma unroll
+      for (int q = 0; q < MAXU; ++q) {
+        const int unit = uw + q * NU, g = unit / NRB, blk = unit % NRB;
+        const int j = g * 32 + lane;
+        if (g >= ngrp || g * 32 + 31 < jlo) continue;   // warp-uniform
+        const bool live = j >= jlo && j < ncol;
+        // all loads of the block before its stores (the compiler cannot tell rows apart)
+        double v[RB];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+          const int i = blk * RB + rr;
+          v[rr] = (live && i < n) ? M[i * LDF + j] : 0.0;
+        }
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+          const double* mi = MulP + (blk * RB + rr) * PW;
+#pragma unroll
+          for (int kk = 0; kk < PW; ++kk) v[rr] = fma(-mi[kk], uk[q][kk], v[rr]);
+        }
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+          const int i = blk * RB + rr;
+          if (live && i < n) M[i * LDF + j] = v[rr];
+        }
+      }
+#ifdef LU_TRACE
+      if (ut == 0 && P < 16) g_lu_trace_u[4 * P + 3] = clock64();
+#endif
+      named_bar_sync(1, 32 * NU);   // this panel's writes done before the next panel's reads
+      if (ut == 0) {
+        __threadfence_block();
+        upd_cnt[0] = P + 1;
+      }
+      (void)nu;
+    }
   }
+  __syncthreads();
   if (bad_s) {
     if (tid == 0) status[sim] = 1;
     return;
@@ -781,11 +868,12 @@ inline size_t lu_smem_bytes(int n, int nq = 0) {
   const int D = 16 * lu_nb(n);
   return (size_t)D * (D + 1) * 8 + (size_t)nq * nq * 8;
 }
-// k_lu_blocked: + panel multipliers [D][8] and the pivot rows' trailing entries [8][D + 1]
-inline size_t lu_blocked_smem_bytes(int n, int nq = 0) {
+// k_lu_lookahead: + double-buffered panel multipliers [2][D][PW <= 8]
+inline size_t lu_lookahead_smem_bytes(int n, int nq = 0) {
   const int D = 16 * lu_nb(n);
-  return lu_smem_bytes(n, nq) + (size_t)D * 8 * 8 + (size_t)8 * (D + 1) * 8;
+  return lu_smem_bytes(n, nq) + (size_t)2 * D * 8 * 8;
 }
+
 
 // r = base + t * dr ; rdot = (r - r_bar)/dt ; elementwise product
 __global__ void k_axpy(double* __restrict__ out, const double* __restrict__ base, const double* __restrict__ d,

@@ -9,6 +9,9 @@
 #include <vector>
 #include <random>
 #include "../../paper_2102_11026_b200/csrc/solve_kernels.cuh"
+#ifndef LU_PW
+#define LU_PW 4
+#endif
 using namespace nlrom;
 
 template <int NB>
@@ -37,10 +40,11 @@ int run(int n, int n_p, int nx, bool vhp) {
   cudaMemcpy(dG, Gt.data(), 2 * nq * nq * 8, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(k_lu_solve<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   cudaFuncSetAttribute(k_lu_blocked<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(k_lu_lookahead<NB, LU_PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   const double* G = vhp ? dG : nullptr;
-  const size_t s1 = lu_smem_bytes(n + nx, nq), s2 = lu_blocked_smem_bytes(n + nx, nq);
+  const size_t s1 = lu_smem_bytes(n + nx, nq), s2 = lu_lookahead_smem_bytes(n + nx, nq);
   auto one = [&](bool blocked, double* ddr, double* dxo) {
-    if (blocked) k_lu_blocked<NB><<<1, 256, s2>>>(dS, dphi, ddr, dr, n, 0, st, nx ? dX : nullptr, nx, dxo, G, nq, n_p);
+    if (blocked) k_lu_lookahead<NB, LU_PW><<<1, 256, s2>>>(dS, dphi, ddr, dr, n, 0, st, nx ? dX : nullptr, nx, dxo, G, nq, n_p);
     else k_lu_solve<NB><<<1, 256, s1>>>(dS, dphi, ddr, dr, n, 0, st, nx ? dX : nullptr, nx, dxo, G, nq, n_p);
   };
   one(false, ddr1, dxo1);
@@ -68,18 +72,21 @@ int run(int n, int n_p, int nx, bool vhp) {
     cudaEventElapsedTime(&t[v], e0, e1);
   }
 #ifdef LU_TRACE
-  {
+  if (n == 60) {
     one(true, ddr2, dxo2);
     cudaDeviceSynchronize();
     long long tr[66];
     cudaMemcpyFromSymbol(tr, g_lu_trace, sizeof tr);
-    printf("  trace (cycles): start->first panel %lld\n", tr[1] - tr[0]);
-    for (int p = 0; p * 8 < n; ++p)
-      printf("  panel %d: factor %lld  u-chain %lld  update %lld\n", p, tr[2 + 4 * p] - tr[1 + 4 * p],
-             tr[3 + 4 * p] - tr[2 + 4 * p], (p + 1) * 8 < n ? tr[1 + 4 * (p + 1)] - tr[3 + 4 * p] : -1LL);
+    long long tu[64];
+    cudaMemcpyFromSymbol(tu, g_lu_trace_u, sizeof tu);
+    for (int p = 0; p < 15; ++p)
+      printf("  panel %d: factor %lld  wait %lld  lookahead %lld | upd: spin %lld chains %lld rows %lld (fact pub at +%lld)\n", p,
+             tr[4 * p + 1] - tr[4 * p], tr[4 * p + 2] - tr[4 * p + 1], p < 14 ? tr[4 * (p + 1)] - tr[4 * p + 2] : -1LL,
+             tu[4 * p + 1] - tu[4 * p], tu[4 * p + 2] - tu[4 * p + 1], tu[4 * p + 3] - tu[4 * p + 2],
+             tu[4 * p + 1] - tr[4 * p + 1]);
   }
 #endif
-  printf("n=%3d n_p=%2d nx=%d vhp=%d NB=%d  k_lu_solve %6.2f us  k_lu_blocked %6.2f us  %s (max |d| %.1e)  %s\n", n,
+  printf("n=%3d n_p=%2d nx=%d vhp=%d NB=%d  k_lu_solve %6.2f us  k_lu_lookahead %6.2f us  %s (max |d| %.1e)  %s\n", n,
          n_p, nx, (int)vhp, NB, t[0] * 5, t[1] * 5, same ? "BITWISE" : "DIFFER", md,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(dS); cudaFree(dphi); cudaFree(ddr1); cudaFree(ddr2); cudaFree(dr); cudaFree(dX); cudaFree(dxo1);
