@@ -824,7 +824,8 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
         for (int rr = 0; rr < RB; ++rr) {
           const double* mi = MulP + (blk * RB + rr) * PW;
 #pragma unroll
-          for (int kk = 0; kk < PW; ++kk) v[rr] = fma(-mi[kk], uk[q][kk], v[rr]);
+          for (int kk = 0; kk < PW; ++kk)   // (entries kk >= kw of a short last panel are never written)
+            if (kk < kw) v[rr] = fma(-mi[kk], uk[q][kk], v[rr]);
         }
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr) {

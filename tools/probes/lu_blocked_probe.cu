@@ -39,7 +39,7 @@ int run(int n, int n_p, int nx, bool vhp) {
   if (nx) cudaMemcpy(dX, X.data(), nx * n * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dG, Gt.data(), 2 * nq * nq * 8, cudaMemcpyHostToDevice);
   cudaFuncSetAttribute(k_lu_solve<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  cudaFuncSetAttribute(k_lu_blocked<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  
   cudaFuncSetAttribute(k_lu_lookahead<NB, LU_PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   const double* G = vhp ? dG : nullptr;
   const size_t s1 = lu_smem_bytes(n + nx, nq), s2 = lu_lookahead_smem_bytes(n + nx, nq);
