@@ -6,7 +6,7 @@ import sys
 
 _impl = importlib.import_module("paper_2102_11026_b200")
 _MODULES = ("mcx", "densenet", "diffops", "elastic", "daereduce", "neucubature", "rdsim", "artifacts",
-            "substructure", "posegen", "fullspace", "shard")
+            "substructure", "posegen", "fullspace", "shard", "cli")
 
 
 def __getattr__(name):

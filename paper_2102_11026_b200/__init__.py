@@ -13,6 +13,6 @@ from . import mcx  # noqa: F401  (pure value type, no device needed)
 def __getattr__(name):
     import importlib
     if name in ("densenet", "diffops", "elastic", "daereduce", "neucubature", "rdsim", "session", "synth",
-                "problem", "_lib", "posegen", "fullspace", "artifacts", "substructure", "shard"):
+                "problem", "_lib", "posegen", "fullspace", "artifacts", "substructure", "shard", "cli"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -236,10 +236,89 @@ def backward(net: DenseNet, x, upstream, want_params: bool = False):
     return res, grads
 
 
-def adam_train(net, dataset, loss, cfg: TrainConfig):
-    """Offline DAE / cubature training is out of scope for the
-    B200 hot path ("OUT OF SCOPE — offline training")."""
-    raise NotImplementedError("adam_train is offline training, out of scope (SURVEY.md §2, §8f rank 4)")
+def lr_at(cfg: TrainConfig, epoch: int) -> float:
+    """Learning rate in effect during ``epoch`` (0-based): the base rate times every schedule
+    factor whose epoch has been completed ({300: 0.8, 3000: 0.8} from 1e-3 gives
+    6.4e-4 after epoch 3000)."""
+    lr = float(cfg.learning_rate)
+    for e, f in sorted((cfg.schedule or {}).items()):
+        if epoch >= int(e):
+            lr *= float(f)
+    return lr
+
+
+def _torch_forward(net: DenseNet, params, x):
+    """Differentiable forward of a real DenseNet on a (batch, in_dim) tensor (layers as in
+    ``forward``; params: {layer index: (W, b)} tensors; filter bases from the net)."""
+    import torch
+    h = x
+    for i, s in enumerate(net.layers):
+        if s.kind == "fully_connected":
+            W, b = params[i]
+            h = h @ W.T + b
+        elif s.kind == "filter":
+            U = torch.as_tensor(net.bases[i], dtype=h.dtype, device=h.device)
+            h = h - (h @ U) @ U.T
+        elif s.kind == "activation_sin":
+            h = torch.sin(h)
+        elif s.kind == "activation_square":
+            h = h * h
+        elif s.kind == "activation_softmax":
+            h = torch.softmax(h, dim=-1)
+    return h
+
+
+def adam_train(net: DenseNet, dataset, loss="mse", cfg: TrainConfig | None = None, device=None, seed=None):
+    """Adam training of a DenseNet (§5.2 "use PyTorch and Adam").
+
+    dataset: (X, Y) with X (S, in_dim) and Y (S, out_dim). loss: "mse" -- per-sample mean squared
+    error over the output components -- or a callable (pred, target) -> per-sample losses. The
+    per-sample losses are multiplied by ``cfg.sample_weights`` (default 1) and averaged; the
+    learning rate follows ``cfg.schedule`` (``lr_at``); minibatches are shuffled by ``seed``
+    (default net.seed or 0). fp64 torch on CUDA when available. Returns (trained copy of net,
+    epoch-loss curve); a NaN loss raises FloatingPointError with the epoch and batch."""
+    import torch
+    cfg = cfg or TrainConfig()
+    X, Y = (np.asarray(a, dtype=float) for a in dataset)
+    if X.ndim != 2 or Y.ndim != 2 or X.shape[0] != Y.shape[0] or X.shape[0] == 0:
+        raise ValueError("dataset must be (X (S, in), Y (S, out)) with S >= 1")
+    if X.shape[1] != net.in_dim or Y.shape[1] != net.out_dim:
+        raise ValueError("dimension mismatch (SPEC.md:143)")
+    S = X.shape[0]
+    w = np.ones(S) if cfg.sample_weights is None else np.asarray(cfg.sample_weights, dtype=float)
+    if w.shape != (S,):
+        raise ValueError("sample_weights must have one entry per sample")
+    dev = torch.device(device) if device is not None else (
+        torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu"))
+    dt = torch.float64
+    fcs = [i for i, s in enumerate(net.layers) if s.kind == "fully_connected"]
+    params = {i: (torch.tensor(net.weights[i], dtype=dt, device=dev, requires_grad=True),
+                  torch.tensor(net.biases[i], dtype=dt, device=dev, requires_grad=True)) for i in fcs}
+    opt = torch.optim.Adam([p for i in fcs for p in params[i]], lr=lr_at(cfg, 0))
+    Xt, Yt, wt = (torch.as_tensor(a, dtype=dt, device=dev) for a in (X, Y, w))
+    per_sample = (lambda p, t: ((p - t) ** 2).mean(dim=1)) if loss == "mse" else loss
+    gen = torch.Generator(device="cpu")
+    gen.manual_seed(int(seed if seed is not None else (net.seed or 0)))
+    bs = max(1, min(int(cfg.batch_size), S))
+    curve = []
+    for epoch in range(int(cfg.epochs)):
+        for g in opt.param_groups:
+            g["lr"] = lr_at(cfg, epoch)
+        perm = torch.randperm(S, generator=gen).to(dev)
+        tot = 0.0
+        for b0 in range(0, S, bs):
+            idx = perm[b0:b0 + bs]
+            l = (per_sample(_torch_forward(net, params, Xt[idx]), Yt[idx]) * wt[idx]).sum() / S
+            if not torch.isfinite(l):
+                raise FloatingPointError(f"adam_train: non-finite loss at epoch {epoch}, batch {b0 // bs}")
+            opt.zero_grad(set_to_none=True)
+            l.backward()
+            opt.step()
+            tot += float(l.detach())
+        curve.append(tot)
+    out = DenseNet(net.layers, {i: params[i][0].detach().cpu().numpy().copy() for i in fcs},
+                   {i: params[i][1].detach().cpu().numpy().copy() for i in fcs}, dict(net.bases), net.seed)
+    return out, curve
 
 
 def make_decoder(Ws, bs, U):
