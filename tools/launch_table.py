@@ -1,5 +1,5 @@
 """Summarise an ncu --metrics gpu__time_duration.sum launch list: one Newton iteration
-(from k_seed_jet to k_lu_solve) of the captured graph, per-kernel device time."""
+(from k_seed_jet to the LU kernel) of the captured graph, per-kernel device time."""
 import csv
 import io
 import sys
@@ -25,7 +25,7 @@ def iteration(seq):
     starts = [i for i, s in enumerate(seq) if s[0].endswith("k_seed_jet") or "k_mlp_jet_fwd" in s[0]]
     best = None
     for i0 in starts:
-        ends = [i for i in range(i0, len(seq)) if "k_lu_solve" in seq[i][0]]
+        ends = [i for i in range(i0, len(seq)) if ("k_lu_solve" in seq[i][0] or "k_lu_lookahead" in seq[i][0])]
         # a graph replay is a few dozen launches; the per-stage timing loops after it are not
         if ends and ends[0] - i0 < 48 and any("k_cubature" in s[0] for s in seq[i0:ends[0]]):
             best = (i0, ends[0])
