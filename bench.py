@@ -52,17 +52,27 @@ def config_dict(world):
 
 
 def peaks():
+    """(MEASURED_PEAKS.json, tensor peaks). The tensor peaks come from profiles/r02_tc_peaks.json
+    (tools/tc_peaks.py: fp64 DMMA and tcgen05 kind::i8, clocks sampled) or, without it, the
+    round-1 fp64 probe (profiles/fp64_peak.json)."""
     p = {}
     try:
         p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    fp64 = None
+    tc = {"fp64": None, "i8": None, "source": "absent"}
     try:
-        fp64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["dmma_tflops"]
+        t = json.load(open(os.path.join(ROOT, "profiles", "r02_tc_peaks.json")))
+        tc = {"fp64": t["dmma_tflops"], "i8": t["i8_n64_tops"],
+              "source": "profiles/r02_tc_peaks.json (tools/probes/tc_peak.cu, clocks sampled): fp64 DMMA, "
+                        "tcgen05 kind::i8 M=128 N=64 (MEASURED_PEAKS.json has neither)"}
     except Exception:
-        pass
-    return p, fp64
+        try:
+            tc["fp64"] = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["dmma_tflops"]
+            tc["source"] = "profiles/fp64_peak.json: measured DMMA.8x8x4 fp64 (MEASURED_PEAKS.json has no fp64 entry)"
+        except Exception:
+            pass
+    return p, tc
 
 
 class ClockSampler:
@@ -193,25 +203,55 @@ def decoder_flops(P, n_sims=1):
     return F, executed
 
 
-def decoder_roofline(P, stage_ms, n_sims, fp64):
+def decoder_roofline(P, stage_ms, n_sims, tc, tc_layers=0, cols=None):
     """Roofline of the decoder bundle (hidden jet chain + output layer + vhp backward chain).
-    `achieved` counts the flops the kernels EXECUTE (the fp64 tensor pipe's real work);
-    the §8d algorithmic figure of the reference pass structure is reported separately as the
-    work the collapsed bundle replaces (it is not a pipe fraction)."""
+
+    `achieved` counts the work the kernels EXECUTE on their pipe; the §8d algorithmic figure of
+    the reference pass structure is reported separately as the work the collapsed bundle
+    replaces (it is not a pipe fraction). When `tc_layers` hidden layers run on the tcgen05
+    Ozaki GEMM (batched contexts), the hidden stage is measured in executed kind::i8 ops (28
+    digit-pair MMAs per K block over the 64-padded columns) against the kind::i8 peak, the other
+    stages in fp64 flops against the DMMA peak, and `frac` is the time-weighted mean of the two
+    pipe fractions (the share of the bundle's time its pipes would be busy at peak)."""
+    fp64 = tc["fp64"]
     F, ex = decoder_flops(P, n_sims)
     dec_ms = stage_ms[0] + stage_ms[1] + stage_ms[2]
     executed = ex * n_sims / (dec_ms * 1e-3) / 1e12
     algorithmic = F * n_sims / (dec_ms * 1e-3) / 1e12
-    return {"bound": "tensor",
-            "kernel": "decoder bundle: hidden jet layers + output GEMM (EpiJetOutC) + vhp backprop layers, fp64 DMMA",
-            "achieved": executed, "peak": fp64, "unit": "TFLOP/s",
-            "frac": (executed / fp64) if fp64 else None, "traffic": None,
-            "peak_source": "profiles/fp64_peak.json: measured DMMA.8x8x4 fp64 (MEASURED_PEAKS.json has no fp64 entry)",
-            "kernel_ms": dec_ms, "executed_flops_per_launch": ex * n_sims,
-            "algorithmic": {"flops_per_launch": F * n_sims, "tflops_equivalent": algorithmic,
-                            "def": "SURVEY.md §8d F_dec = (18 n_q+6)(2 sum in*out + 4 N n_p) per sim: the "
-                                   "reference's 4 n_q + 2 passes; the jet bundle executes fewer columns"},
-            "stages_ms": {"hidden_jet": stage_ms[0], "output_gemm": stage_ms[1], "vhp_bwd": stage_ms[2]}}
+    out = {"bound": "tensor",
+           "kernel": "decoder bundle: hidden jet layers + output GEMM (EpiJetOutC) + vhp backprop layers, fp64 DMMA",
+           "achieved": executed, "peak": fp64, "unit": "TFLOP/s",
+           "frac": (executed / fp64) if fp64 else None, "traffic": None, "peak_source": tc["source"],
+           "kernel_ms": dec_ms, "executed_flops_per_launch": ex * n_sims,
+           "algorithmic": {"flops_per_launch": F * n_sims, "tflops_equivalent": algorithmic,
+                           "def": "SURVEY.md §8d F_dec = (18 n_q+6)(2 sum in*out + 4 N n_p) per sim: the "
+                                  "reference's 4 n_q + 2 passes; the jet bundle executes fewer columns"},
+           "stages_ms": {"hidden_jet": stage_ms[0], "output_gemm": stage_ms[1], "vhp_bwd": stage_ms[2]}}
+    if tc_layers and cols:
+        c = P.cfg
+        w = c.width
+        cpad = -(-cols // 64) * 64
+        i8_ops = tc_layers * 28 * 2.0 * w * w * cpad
+        i8_tops = i8_ops / (stage_ms[0] * 1e-3) / 1e12
+        G, gps = jet_groups(c.n_q, True)
+        dmma_fl = ex * n_sims - 2.0 * G * gps * n_sims * w * w * tc_layers   # seed layer stays on DMMA
+        dmma_ms = stage_ms[1] + stage_ms[2]
+        dmma_tf = dmma_fl / (dmma_ms * 1e-3) / 1e12
+        f_i8 = (i8_tops / tc["i8"]) if tc["i8"] else None
+        f_dm = (dmma_tf / fp64) if fp64 else None
+        out["kernel"] = ("decoder bundle: %d hidden jet layers on tcgen05 kind::i8 (Ozaki, 7 digits) + seed layer, "
+                         "output GEMM and vhp backprop on fp64 DMMA" % tc_layers)
+        out["unit"] = "pipe fraction (time-weighted)"
+        out["achieved"] = (f_i8 * stage_ms[0] + f_dm * dmma_ms) / dec_ms if f_i8 is not None and f_dm is not None else None
+        out["peak"] = 1.0
+        out["frac"] = out["achieved"]
+        out["pipes"] = {
+            "tcgen05_i8": {"stage": "hidden_jet", "achieved": i8_tops, "peak": tc["i8"], "unit": "TOP/s",
+                           "frac": f_i8, "executed_ops_per_launch": i8_ops,
+                           "fp64_equivalent_tflops": (ex * n_sims - dmma_fl) / (stage_ms[0] * 1e-3) / 1e12},
+            "fp64_dmma": {"stage": "output_gemm + vhp_bwd", "achieved": dmma_tf, "peak": fp64, "unit": "TFLOP/s",
+                          "frac": f_dm, "executed_flops_per_launch": dmma_fl}}
+    return out
 
 
 # --------------------------------------------------------------------------- extra legs
@@ -289,11 +329,12 @@ def batched_leg(args, rank, world):
     torch.cuda.synchronize()
     barrier(world)
     ms = barrier_max(world, float(each.mean()))
-    _, fp64 = peaks()
+    pk, tc = peaks()
+    fp64 = tc["fp64"]
     stage_ms = s.bench_kernels(3, flush_l2=True)
-    roof = decoder_roofline(P, stage_ms, ns, fp64)
+    G, gps = jet_groups(P.cfg.n_q, True)
+    roof = decoder_roofline(P, stage_ms, ns, tc, s.tc_layers(), ns * G * gps)
     cub_ms, cub_bytes = s.bench_cubature(5, flush_l2=True)
-    pk, _ = peaks()
     hbm = pk.get("hbm_gbs")
     cub_gbs = cub_bytes / (cub_ms * 1e-3) / 1e9
     traffic = None
@@ -593,9 +634,10 @@ def run_ours(args):
 
     # roofline: stages timed live with CUDA events on the context stream (L2 flushed before each
     # launch); in-graph share of the decoder bundle from the prefix-graph profile
-    pk, fp64 = peaks()
+    pk, tc = peaks()
+    fp64 = tc["fp64"]
     stage_ms = s.bench_kernels(max(20, args.steps // 4), flush_l2=True)
-    roof = decoder_roofline(P, stage_ms, 1, fp64)
+    roof = decoder_roofline(P, stage_ms, 1, tc)
     roof["share_of_step_isolated"] = roof["kernel_ms"] / ms_iter
     roof["lu_ms_isolated"] = stage_ms[3]
     try:

@@ -239,6 +239,10 @@ NLROM_API int nlrom_train_forces(nlrom_ctx* ctx, const double* rs, int n_poses, 
 /* Number of kernel launches of one Newton iteration (for bench "gpu_launches"). */
 NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
 
+/* Number of decoder hidden layers that run on the tcgen05 kind::i8 Ozaki GEMM (batched
+ * contexts; 0 = every layer on fp64 DMMA). bench.py uses it to pick the roofline peak. */
+NLROM_API int nlrom_tc_layers(nlrom_ctx* ctx);
+
 /* Profiling: prefix-graph timing of one Newton iteration. For k = 1..min(cap, launches) the
  * first k launches are captured as a graph and timed over n_iters replays (L2 flushed before
  * each): ms[k-1] - ms[k-2] is launch k's marginal in-graph cost. names receives the kernel

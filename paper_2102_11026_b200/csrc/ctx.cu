@@ -1957,6 +1957,12 @@ extern "C" int nlrom_bench_cubature(nlrom_ctx* c, int n_iters, int flush_l2, flo
 }
 
 extern "C" int nlrom_launches_per_iteration(nlrom_ctx* c) { return c ? c->launches_E + c->launches_J : 0; }
+extern "C" int nlrom_tc_layers(nlrom_ctx* c) {
+  int k = 0;
+  if (c)
+    for (auto& w : c->ozW) k += w.ready ? 1 : 0;
+  return k;
+}
 
 // Prefix-graph timing: for k = 1 .. n, capture the first k launches of one Newton iteration
 // (E + J + update) as a graph and time n_iters replays (L2 flushed before each); ms[k-1] is the

@@ -260,6 +260,10 @@ class Session:
     def launches_per_iteration(self):
         return int(self._L.nlrom_launches_per_iteration(self._h))
 
+    def tc_layers(self):
+        """Decoder hidden layers on the tcgen05 Ozaki GEMM (0: all on fp64 DMMA)."""
+        return int(self._L.nlrom_tc_layers(self._h))
+
 
 def _uploaded_arrays(rm, model, cm):
     """Every host array a Session copies to the device (decoder, basis, mesh, set, weight net)."""

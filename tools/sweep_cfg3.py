@@ -24,7 +24,7 @@ def main():
     from paper_2102_11026_b200.problem import build_problem
     from paper_2102_11026_b200 import rdsim
     from paper_2102_11026_b200.session import Session
-    _, fp64 = bench.peaks()
+    _, tc = bench.peaks()
     for L in args.depth:
         for nq in args.nq:
             P = build_problem("cfg2", n_q=nq, n_fc=L)
@@ -38,14 +38,15 @@ def main():
             s.bench_iterations(5)
             tot, _ = s.bench_iterations(args.iters)
             st = s.bench_kernels(max(10, args.iters // 4))
-            roof = bench.decoder_roofline(P, st, ns, fp64)
+            G, gps = bench.jet_groups(nq, s.tc_layers() > 0)
+            roof = bench.decoder_roofline(P, st, ns, tc, s.tc_layers(), ns * G * gps)
             print(json.dumps({"n_q": nq, "depth": L, "n_sims": ns, "ms_per_iteration": tot / args.iters,
                               "sim_iterations_per_s": ns * 1e3 / (tot / args.iters),
                               "hz_3_iters": 1000.0 / (3 * tot / args.iters),
                               "decoder_ms": roof["kernel_ms"], "lu_ms": st[3],
-                              "F_dec_gflop": roof["algorithmic_flops_per_launch"] / 1e9,
-                              "decoder_tflops_alg": roof["achieved"], "frac_alg": roof["frac"],
-                              "executed_frac": roof["executed_frac"], "executed_tflops": roof["executed_tflops"],
+                              "F_dec_gflop": roof["algorithmic"]["flops_per_launch"] / 1e9,
+                              "decoder_tflops_alg": roof["algorithmic"]["tflops_equivalent"],
+                              "executed_frac": roof["frac"], "pipes": roof.get("pipes"),
                               "stages_ms": roof["stages_ms"], "launches": s.launches_per_iteration()}),
                   flush=True)
             del s
