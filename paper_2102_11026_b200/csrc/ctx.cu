@@ -55,6 +55,11 @@ struct CubSet {
   int epc = 1, nchunk = 0;  // elements per chunk; partials per sim (CTAs along x)
   int nech = 0, cpc = 1;     // element chunks; element chunks per CTA (nchunk = ceil(nech / cpc))
   DBuf fe_w, part_f, part_K, f;
+  // many sims: k_cub_sims (one CTA per sim, B-projected 9-row Gram) with the B columns of the
+  // constant U block precomputed per set element (n, 9, n_p); ti = Gram row tiles (n < 8 ti)
+  bool sims = false;
+  int ti = 0;
+  DBuf BU;
 };
 
 int gemm_launch_count = 0;
@@ -72,9 +77,12 @@ int gemm_launch_count = 0;
 //   tangents=K      jet tangents per column group (1, 3, 5, 7 or 15)
 //   dmma_hidden     batched hidden jet layers on the fp64 DMMA kernels instead of the tcgen05
 //                   Ozaki-int8 GEMM (ozaki_tc.cuh)
+//   cub_chunked     many sims: the element-chunk cubature kernel (k_cubature, 12-row Gram) instead
+//                   of the per-sim B-projected kernel (k_cub_sims)
 struct PathOpts {
   bool batched = false, unfused = false, hid_cp = false, bwd_cp = false, shared_real = false,
-       no_shared_real = false, dmma_hidden = false;
+       no_shared_real = false, dmma_hidden = false, cub_chunked = false;
+  int cub_minb = 0;
   int cpc = 0, cpm = 0, tangents = 0;
   static PathOpts from_env() {
     PathOpts o;
@@ -96,6 +104,8 @@ struct PathOpts {
       else if (key == "shared_real") o.shared_real = true;
       else if (key == "no_shared_real") o.no_shared_real = true;
       else if (key == "dmma_hidden") o.dmma_hidden = true;
+      else if (key == "cub_chunked") o.cub_chunked = true;
+      else if (key == "cub_minb") o.cub_minb = val;
       else if (key == "cpc") o.cpc = val;
       else if (key == "cpm") o.cpm = val;
       else if (key == "tangents") o.tangents = val;
@@ -288,7 +298,7 @@ void choose_groups(int n_q, int width, bool batched, int forced, int& G, int& gp
 void upload(DBuf& d, const double* h, size_t n);
 
 void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std::vector<int>& rows_host,
-               int epc, const double* Dm_host, const double* vol_host) {
+               int epc, const double* Dm_host, const double* vol_host, const double* U_host = nullptr) {
   s.n = (int)elems.size();
   s.elems.upload(elems.data(), elems.size());
   {
@@ -341,6 +351,32 @@ void build_set(nlrom_ctx* c, CubSet& s, const std::vector<int>& elems, const std
     if (c->opt.cpc > 0) s.cpc = std::max(1, std::min(s.nech, c->opt.cpc));
   }
   s.nchunk = ceil_div(s.nech, s.cpc);
+  // many sims with a small reduced space: one CTA per sim (k_cub_sims), one partial per sim
+  const int np = c->n_p;
+  s.ti = std::max(1, ceil_div(n + 1, 8));
+  s.sims = U_host && c->n_sims > 1 && s.ti <= 4 && s.n > 0 && !c->opt.cub_chunked &&
+           cub_sims_smem(n, np, s.ti) <= 110 * 1024;
+  if (s.sims) {
+    s.nchunk = 1;
+    // BU[(i, a * 3 + y), j] = sum_v G[v][y] U[row(v, a)][j],  G[v] = row v - 1 of Dm^-1, G[0] = -sum
+    std::vector<double> bu((size_t)s.n * 9 * std::max(np, 1), 0.0);
+    for (int i = 0; i < s.n; ++i) {
+      const double* Di = Dm_host + (size_t)elems[i] * 9;
+      for (int aa = 0; aa < 3; ++aa)
+        for (int y = 0; y < 3; ++y)
+          for (int j = 0; j < np; ++j) {
+            double acc = 0.0;
+            for (int v = 0; v < 4; ++v) {
+              const int row = rows_host[(size_t)elems[i] * 12 + 3 * v + aa];
+              if (row < 0) continue;
+              const double g = v == 0 ? -(Di[y] + Di[3 + y] + Di[6 + y]) : Di[(v - 1) * 3 + y];
+              acc += g * U_host[(size_t)row * np + j];
+            }
+            bu[((size_t)i * 9 + aa * 3 + y) * np + j] = acc;
+          }
+    }
+    upload(s.BU, bu.data(), bu.size());
+  }
   s.fe_w.alloc((size_t)c->n_sims * std::max(s.n, 1) * 12);
   s.part_f.alloc((size_t)c->n_sims * s.nchunk * n);
   s.part_K.alloc((size_t)c->n_sims * s.nchunk * n * n);
@@ -509,6 +545,26 @@ void wnet_phase(nlrom_ctx* c) {
 
 // part: 0 forces + stiffness, 1 weighted element forces only (fe_w), 2 stiffness / Gram only
 void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true, bool early = true, int part = 0) {
+  if (s.sims && part == 0) {
+    CubSimsArgs a{s.rows_g.p, s.Dm_g.p, s.vol_g.p, s.BU.p, s.n, weighted ? c->wC.p : nullptr, c->u.p, c->Jt.p,
+                  c->N, c->n, c->n_p, c->ldjt, c->mu, c->lam, s.fe_w.p, s.part_f.p, s.part_K.p, 0};
+    const size_t smem = cub_sims_smem(c->n, c->n_p, s.ti);
+    const bool three = c->opt.cub_minb == 3;
+    switch (s.ti) {
+      case 1: launch(c, k_cub_sims<1, 2>, dim3(c->n_sims), 256, smem, a); break;
+      case 2: launch(c, k_cub_sims<2, 2>, dim3(c->n_sims), 256, smem, a); break;
+      case 3: launch(c, k_cub_sims<3, 2>, dim3(c->n_sims), 256, smem, a); break;
+      default:
+        if (three) launch(c, k_cub_sims<4, 3>, dim3(c->n_sims), 256, smem, a);
+        else launch(c, k_cub_sims<4, 2>, dim3(c->n_sims), 256, smem, a);
+        break;
+    }
+    if (scatter)
+      launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
+             (const int*)s.row_ptr.p, (const int*)s.entries.p, s.n_rows, (const double*)s.fe_w.p, s.n, s.f.p, c->N,
+             c->n_sims);
+    return;
+  }
   CubArgs a{s.elems.p, s.n, c->elem_rows.p, c->Dm_inv.p, c->vol.p, weighted ? c->wC.p : nullptr, c->u.p,
             part == 1 ? nullptr : c->Jt.p, c->N, c->n, c->ldjt, c->mu, c->lam, s.epc, s.fe_w.p, s.part_f.p,
             s.part_K.p, s.nchunk, nullptr, nullptr};
@@ -1157,10 +1213,10 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       // on the critical path keeps 2 per CTA (setCF)
       const bool split = !many;
       build_set(c, c->setC, cub, rows, many ? 8 : 12,
-                d->Dm_inv, d->vol);
+                d->Dm_inv, d->vol, many ? d->U : nullptr);
       if (split)
         build_set(c, c->setCF, cub, rows, 6, d->Dm_inv, d->vol);
-      build_set(c, c->setAll, all, rows, 8, d->Dm_inv, d->vol);
+      build_set(c, c->setAll, all, rows, 8, d->Dm_inv, d->vol, many ? d->U : nullptr);
     }
     // weight net (rows of the last layer restricted to C)
     {
@@ -1296,6 +1352,11 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     // kernel attributes for large dynamic shared memory
     NL_CUDA(cudaFuncSetAttribute(k_cubature<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_cubature<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_cub_sims<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_cub_sims<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_cub_sims<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_cub_sims<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_cub_sims<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

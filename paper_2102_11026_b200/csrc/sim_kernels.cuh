@@ -695,6 +695,299 @@ __global__ void __launch_bounds__(256, MINB) k_cubature(CubArgs a) {
   }
 }
 
+// -------------------------------------------------------------------- cubature, many sims
+// One CTA per sim (cfg5: 4096 sims x |C| = 100, n = 30). The reduced stiffness is projected
+// through the deformation-gradient map instead of the 12 DOF rows of J~:
+//   B_e = dF/dr (9 x n):  B[(a,y)] = sum_v G[v][y] J~[row(v,a)]    (G: rows of Dm^-1, g_0 = -sum)
+//   K~ += w_e V_e B_e^T dP(B_e),  f~ += w_e V_e B_e^T vec(P_e)      (dP = dF S + F dS: dP/dF of StVK)
+// which is J~_e^T (w K_e J~_e) and J~_e^T (w f_e) exactly (K_e = V G^T (dP/dF) G), with a 9-row
+// Gram per element instead of 12 and no 12 x 12 K_e. The constant U columns of J~ give constant
+// B columns, precomputed per set element at upload (BU, L2-resident); only the n_q J columns of
+// the element rows are gathered per sim. dP/dF is symmetric (a Hessian of the StVK energy), so
+// only the Gram's upper 8 x 8 tiles are computed (10 of 16 at n = 30) and mirrored on store.
+// Per CTA: physics of up to CS_SUPER elements (thread per element: F, S, w V, Dm^-1 to shared
+// memory, weighted element forces to fe_w), then chunks of CS_EPC elements: the chunk's J rows
+// land by cp.async (prefetched during the previous chunk's Gram), thread per (element, column)
+// builds the B and w V dP(B) panels, and the warps run the DMMA Gram over the panels, k-steps
+// dealt round-robin over the sim so every warp carries every tile: accumulators stay in
+// registers for the whole sim and are summed over warps once, in a fixed order (deterministic).
+struct CubSimsArgs {
+  const int* rows_g;    // (n_elems, 12) free-DOF rows (-1 fixed)
+  const double* Dm_g;   // (n_elems, 9)
+  const double* vol_g;  // (n_elems)
+  const double* BU;     // (n_elems, 9, n_p): B columns of the constant U block
+  int n_elems;
+  const double* w;      // (n_sims, n_elems) weights (nullptr: 1)
+  const double* u;      // (n_sims, N)
+  const double* Jt;     // (n_sims, N, ldjt): [U | J]
+  int N, n, n_p, ldjt;
+  double mu, lam;
+  double* fe_w;         // (n_sims, n_elems, 12) weighted element forces
+  double* part_f;       // (n_sims, n)   one partial per sim
+  double* part_K;       // (n_sims, n*n)
+  int skip_fe;
+};
+constexpr int CS_EPC = 8, CS_SUPER = 128, CS_FS = 25;  // FS: F 9 | S 6 | w V | Dm^-1 9
+__host__ __device__ inline int cub_sims_ldq(int n_q) { return (n_q + 1) & ~1; }
+inline size_t cub_sims_smem(int n, int n_p, int ti) {
+  const int ldp = gram_ld(n), nt = ti * (ti + 1) / 2;
+  const size_t panels = (size_t)2 * CS_EPC * 9 * ldp;
+  return ((size_t)CS_SUPER * CS_FS + (size_t)CS_EPC * 12 * cub_sims_ldq(n - n_p) +
+          std::max(panels, (size_t)8 * nt * 64)) * 8;
+}
+
+__device__ __forceinline__ void stvk_dP(const double* F, const double* S6, double lam2, double mu, const double* dF,
+                                        double* dP) {
+  // X = F^T dF, dS = mu (X + X^T) + lam tr(X) I, dP = dF S + F dS   (S6: S00 S11 S22 S01 S02 S12)
+  double X[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) X[i * 3 + j] = F[i] * dF[j] + F[3 + i] * dF[3 + j] + F[6 + i] * dF[6 + j];
+  const double tr = lam2 * (X[0] + X[4] + X[8]);
+  const double dS00 = 2.0 * mu * X[0] + tr, dS11 = 2.0 * mu * X[4] + tr, dS22 = 2.0 * mu * X[8] + tr;
+  const double dS01 = mu * (X[1] + X[3]), dS02 = mu * (X[2] + X[6]), dS12 = mu * (X[5] + X[7]);
+  const double dS[9] = {dS00, dS01, dS02, dS01, dS11, dS12, dS02, dS12, dS22};
+  const double S[9] = {S6[0], S6[3], S6[4], S6[3], S6[1], S6[5], S6[4], S6[5], S6[2]};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      dP[a * 3 + j] = dF[a * 3] * S[j] + dF[a * 3 + 1] * S[3 + j] + dF[a * 3 + 2] * S[6 + j] + F[a * 3] * dS[j] +
+                      F[a * 3 + 1] * dS[3 + j] + F[a * 3 + 2] * dS[6 + j];
+}
+
+template <int TI, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_cub_sims(CubSimsArgs a) {
+  constexpr int NT = TI * (TI + 1) / 2;  // upper 8 x 8 tiles of the (n x n+1) Gram
+  extern __shared__ __align__(16) double sh[];
+  const int n = a.n, n_p = a.n_p, nq = n - n_p, ldq = cub_sims_ldq(nq), ldp = gram_ld(n);
+  double* FS = sh;                               // [CS_SUPER][CS_FS]
+  double* Jg = FS + CS_SUPER * CS_FS;            // [CS_EPC * 12][ldq]  J columns of the chunk's rows
+  double* Bp = Jg + CS_EPC * 12 * ldq;           // [CS_EPC * 9][ldp]   B rows (+ reduction space)
+  double* Wp = Bp + CS_EPC * 9 * ldp;            // [CS_EPC * 9][ldp]   w V dP(B) rows | w V vec(P)
+  const int sim = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* u = a.u + (size_t)sim * a.N;
+  const double* Jq = a.Jt + (size_t)sim * a.N * a.ldjt + n_p;
+  const bool v16 = ((n_p | a.ldjt) & 1) == 0;    // 16-byte aligned J columns
+  pdl_wait();
+  pdl_launch();
+  // J rows of elements c0 .. c0 + CS_EPC - 1 into Jg by cp.async, two threads per row (measured
+  // faster than one TMA bulk copy per 160-byte row: 0.70 vs 0.98 ms at cfg5), fixed rows zeroed
+  auto gather = [&](int c0) {
+    constexpr int TPR = 2;
+    if (tid < CS_EPC * 12 * TPR) {
+      const int rr = tid / TPR, h = tid % TPR;
+      const int ei = c0 + rr / 12;
+      const int row = ei < a.n_elems ? a.rows_g[(size_t)c0 * 12 + rr] : -1;
+      double* dst = Jg + rr * ldq;
+      const double* src = Jq + (size_t)max(row, 0) * a.ldjt;
+      if (v16) {
+        for (int k = 2 * h; k < nq; k += 2 * TPR) {
+          if (row >= 0) cp_async16(dst + k, src + k, true);
+          else dst[k] = dst[k + 1] = 0.0;
+        }
+      } else {
+        for (int k = h; k < nq; k += TPR) {
+          if (row >= 0) cp_async8(dst + k, src + k);
+          else dst[k] = 0.0;
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  double acc[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  int ks_glob = 0;
+  const double lam = a.lam, mu = a.mu;
+  // this thread's panel tasks (chunk-invariant): (element, column) over the n columns, then the
+  // CS_EPC force columns (j = n; they fall in one warp); <= 2 per thread since n < 32
+  int tk_el[2], tk_j[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int t = tid + q * 256;
+    const bool fcol = t >= CS_EPC * n;
+    tk_el[q] = t < CS_EPC * (n + 1) ? (fcol ? t - CS_EPC * n : t / n) : -1;
+    tk_j[q] = fcol ? n : t - (t / n) * n;
+  }
+  gather(0);
+  for (int s0 = 0; s0 < a.n_elems; s0 += CS_SUPER) {
+    const int ns = min(CS_SUPER, a.n_elems - s0);
+    if (tid < ns) {
+      // ------------------------------------------------ element physics (thread per element)
+      const int ei = s0 + tid;
+      double uv[12], Di[9];
+#pragma unroll
+      for (int l = 0; l < 12; ++l) {
+        const int row = a.rows_g[(size_t)ei * 12 + l];
+        uv[l] = row >= 0 ? u[row] : 0.0;
+      }
+#pragma unroll
+      for (int l = 0; l < 9; ++l) Di[l] = a.Dm_g[(size_t)ei * 9 + l];
+      const double V = a.vol_g[ei];
+      const double we = a.w ? a.w[(size_t)sim * a.n_elems + ei] : 1.0;
+      double F[9];
+#pragma unroll
+      for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+        for (int y = 0; y < 3; ++y) {
+          double f = 0.0;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) f = fma(uv[(i + 1) * 3 + aa] - uv[aa], Di[i * 3 + y], f);
+          F[aa * 3 + y] = f + (aa == y ? 1.0 : 0.0);
+        }
+      double C[6];  // F^T F: 00 11 22 01 02 12
+      C[0] = F[0] * F[0] + F[3] * F[3] + F[6] * F[6];
+      C[1] = F[1] * F[1] + F[4] * F[4] + F[7] * F[7];
+      C[2] = F[2] * F[2] + F[5] * F[5] + F[8] * F[8];
+      C[3] = F[0] * F[1] + F[3] * F[4] + F[6] * F[7];
+      C[4] = F[0] * F[2] + F[3] * F[5] + F[6] * F[8];
+      C[5] = F[1] * F[2] + F[4] * F[5] + F[7] * F[8];
+      const double trE = 0.5 * (C[0] + C[1] + C[2] - 3.0);
+      double S6[6];
+#pragma unroll
+      for (int l = 0; l < 3; ++l) S6[l] = mu * (C[l] - 1.0) + lam * trE;
+#pragma unroll
+      for (int l = 3; l < 6; ++l) S6[l] = mu * C[l];
+      double* fs = FS + tid * CS_FS;
+#pragma unroll
+      for (int l = 0; l < 9; ++l) fs[l] = F[l];
+#pragma unroll
+      for (int l = 0; l < 6; ++l) fs[9 + l] = S6[l];
+      fs[15] = we * V;
+#pragma unroll
+      for (int l = 0; l < 9; ++l) fs[16 + l] = Di[l];
+      if (!a.skip_fe) {
+        // f_e[(v, aa)] = V sum_y P[aa][y] G[v][y],  P = F S
+        const double S[9] = {S6[0], S6[3], S6[4], S6[3], S6[1], S6[5], S6[4], S6[5], S6[2]};
+        double P[9];
+        mat3_mul(F, S, P);
+        double* fo = a.fe_w + ((size_t)sim * a.n_elems + ei) * 12;
+#pragma unroll
+        for (int aa = 0; aa < 3; ++aa) {
+          double pg[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            pg[i] = P[aa * 3] * Di[i * 3] + P[aa * 3 + 1] * Di[i * 3 + 1] + P[aa * 3 + 2] * Di[i * 3 + 2];
+          fo[aa] = -we * V * (pg[0] + pg[1] + pg[2]);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) fo[(i + 1) * 3 + aa] = we * V * pg[i];
+        }
+      }
+    }
+    for (int c0 = s0; c0 < s0 + ns; c0 += CS_EPC) {
+      cp_async_all_wait();
+      __syncthreads();  // the chunk's J rows landed, FS written, the previous Gram done with B / W
+      // ---------------------------------------------------- B and w V dP(B) panels
+      const int ne = min(CS_EPC, a.n_elems - c0);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int el = tk_el[q], j = tk_j[q];
+        if (el < 0) continue;
+        double* bcol = Bp + el * 9 * ldp + j;
+        double* wcol = Wp + el * 9 * ldp + j;
+        if (el >= ne) {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) bcol[k * ldp] = wcol[k * ldp] = 0.0;
+          continue;
+        }
+        const double* fs = FS + (c0 - s0 + el) * CS_FS;
+        double F[9], S6[6];
+#pragma unroll
+        for (int l = 0; l < 9; ++l) F[l] = fs[l];
+#pragma unroll
+        for (int l = 0; l < 6; ++l) S6[l] = fs[9 + l];
+        const double wv = fs[15];
+        if (j == n) {  // force column: w V vec(P)
+          const double S[9] = {S6[0], S6[3], S6[4], S6[3], S6[1], S6[5], S6[4], S6[5], S6[2]};
+          double P[9];
+          mat3_mul(F, S, P);
+#pragma unroll
+          for (int k = 0; k < 9; ++k) wcol[k * ldp] = wv * P[k];  // (B column n only reaches unstored outputs)
+          continue;
+        }
+        double dF[9];
+        if (j < n_p) {
+          const double* bu = a.BU + (size_t)(c0 + el) * 9 * n_p + j;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) dF[k] = bu[k * n_p];
+        } else {
+          const double* jr = Jg + el * 12 * ldq + (j - n_p);
+          double x[12];
+#pragma unroll
+          for (int l = 0; l < 12; ++l) x[l] = jr[l * ldq];
+#pragma unroll
+          for (int aa = 0; aa < 3; ++aa)
+#pragma unroll
+            for (int y = 0; y < 3; ++y) {
+              double f = 0.0;
+#pragma unroll
+              for (int i = 0; i < 3; ++i) f = fma(x[(i + 1) * 3 + aa] - x[aa], fs[16 + i * 3 + y], f);
+              dF[aa * 3 + y] = f;
+            }
+        }
+        double dP[9];
+        stvk_dP(F, S6, lam, mu, dF, dP);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          bcol[k * ldp] = dF[k];
+          wcol[k * ldp] = wv * dP[k];
+        }
+      }
+      __syncthreads();  // panels complete; Jg free
+      if (c0 + CS_EPC < a.n_elems) gather(c0 + CS_EPC);  // lands during the Gram
+      // ---------------------------------------------------- Gram: upper tiles of B^T W
+      constexpr int KS = CS_EPC * 9 / 4;
+      const int kq = lane & 3, r8 = lane >> 2;
+      for (int ks = (warp - ks_glob) & 7; ks < KS; ks += 8) {
+        const double* bx = Bp + (4 * ks + kq) * ldp + r8;
+        const double* wy = Wp + (4 * ks + kq) * ldp + r8;
+        double av[TI], bv[TI];
+#pragma unroll
+        for (int t = 0; t < TI; ++t) {
+          av[t] = bx[8 * t];
+          bv[t] = wy[8 * t];
+        }
+        int t = 0;
+#pragma unroll
+        for (int bi = 0; bi < TI; ++bi)
+#pragma unroll
+          for (int bj = bi; bj < TI; ++bj, ++t) dmma(acc[t][0], acc[t][1], av[bi], bv[bj]);
+      }
+      ks_glob = (ks_glob + KS) & 7;
+    }
+  }
+  // ------------------------------------------------------------ fixed-order sum over warps
+  __syncthreads();
+  double* red = Bp;  // [8][NT][64]
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    red[(warp * NT + t) * 64 + 2 * lane] = acc[t][0];
+    red[(warp * NT + t) * 64 + 2 * lane + 1] = acc[t][1];
+  }
+  __syncthreads();
+  double* K = a.part_K + (size_t)sim * n * n;
+  double* f = a.part_f + (size_t)sim * n;
+  for (int idx = tid; idx < NT * 64; idx += blockDim.x) {
+    const int t = idx >> 6, q = idx & 63, ln = q >> 1, e = q & 1;
+    double v = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) v += red[(w8 * NT + t) * 64 + q];
+    int bi = 0, rem = t;
+    while (rem >= TI - bi) { rem -= TI - bi; ++bi; }
+    const int bj = bi + rem;
+    const int i = bi * 8 + (ln >> 2), j = bj * 8 + 2 * (ln & 3) + e;
+    if (i >= n) continue;
+    if (j < n) {
+      K[(size_t)i * n + j] = v;
+      if (bi != bj) K[(size_t)j * n + i] = v;
+    } else if (j == n) {
+      f[i] = v;
+    }
+  }
+}
+
 // Deterministic scatter of weighted element forces into the free-DOF vector (CSR over rows).
 __global__ void k_scatter_rows(const int* __restrict__ row_ids, const int* __restrict__ row_ptr,
                                const int* __restrict__ entries, int n_rows, const double* __restrict__ fe_w,

@@ -223,15 +223,16 @@ def test_trajectory_100_steps(cfg1, integ):
 def test_multi_sim(cfg1, batched, monkeypatch):
     """n_sims independent simulations through one context == the single-sim oracle per sim.
     batched=True forces the big-tile per-layer GEMM path used for thousands of sims (cfg5);
-    "cpc" additionally makes each cubature CTA walk 4 element chunks of its sim (shared-memory
-    Gram accumulation, prefetched rows, the 3-CTA/SM kernel) as at cfg5 scale."""
+    "cpc" runs the element-chunk cubature kernel (cub_chunked) with each CTA walking 4 element
+    chunks of its sim (shared-memory Gram accumulation, prefetched rows, the 3-CTA/SM kernel);
+    the other batched variants use the per-sim B-projected kernel (k_cub_sims) of cfg5."""
     from paper_2102_11026_b200 import rdsim
     from paper_2102_11026_b200.session import Session
     P, S = cfg1
     path = {False: None, True: "batched",
             # + the shared-real vhp backward (default only at >= 4 waves of CTAs), 4 element /
             # mass row chunks per cubature / mass CTA
-            "cpc": "batched,cpc=4,shared_real,cpm=4",
+            "cpc": "batched,cpc=4,shared_real,cpm=4,cub_chunked",
             "sharedcp": "batched,shared_real,bwd_cp",        # shared-real vhp on the cp.async GEMM
             "noshare": "batched,no_shared_real,hid_cp",      # 2 n_q dual columns; cp.async hidden layers
             }[batched]
