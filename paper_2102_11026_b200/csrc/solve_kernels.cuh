@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
 }
 
 #ifdef LU_TRACE
-__device__ long long g_lu_trace[4 * 16 + 2];   // tools/probes/lu_blocked_probe.cu -DLU_TRACE
+__device__ long long g_lu_trace[4 * 16 + 6];   // tools/probes/lu_blocked_probe.cu -DLU_TRACE: panels | start, staged, factored, end
 __device__ long long g_lu_trace_u[4 * 16];
 #endif
 // Look-ahead panel LU (same pivots, same multipliers, same fma sequence per element as
@@ -570,6 +570,9 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
                                                        int n_p) {
   pdl_wait();
   pdl_launch();
+#ifdef LU_TRACE
+  if (threadIdx.x == 0) g_lu_trace[64] = clock64();
+#endif
   constexpr int D = 16 * NB;
   constexpr int LDF = D + 1;
   constexpr int R = D / 32;            // rows per lane (PW: panel width)
@@ -588,37 +591,84 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
   double* Mul = Vs + nq * nq;
   const int ncol = n + 1 + nx;
   const int npan = (n + PW - 1) / PW;
-  for (int idx = tid; idx < D * D; idx += 256) {
-    const int i = idx / D, j = idx % D;
-    double* dst = M + i * LDF + j;
-    if (i < n && j < n) cp_async8(dst, Ss + (size_t)i * n + j);
-    else if (i < n && j == n) cp_async8(dst, phi + (size_t)sim * n + i);
-    else if (i < n && j > n && j <= n + nx) cp_async8(dst, xrhs + ((size_t)sim * nx + (j - n - 1)) * n + i);
-    else *dst = 0.0;
-  }
-  if (Gt)
-    for (int idx = tid; idx < nq * nq; idx += 256) {
-      const int k = idx / nq, i = idx % nq;
-      cp_async8(Vs + idx, Gt + ((size_t)sim * 2 * nq + 2 * k + 1) * ldg + i);
+  if constexpr (NB > 6) {
+    // wide matrices: asynchronous copies, then one pass (negate phi, add the vhp block); the
+    // one-pass register staging below measured slower here (n = 100, 124)
+    for (int idx = tid; idx < D * D; idx += 256) {
+      const int i = idx / D, j = idx % D;
+      double* dst = M + i * LDF + j;
+      if (i < n && j < n) cp_async8(dst, Ss + (size_t)i * n + j);
+      else if (i < n && j == n) cp_async8(dst, phi + (size_t)sim * n + i);
+      else if (i < n && j > n && j <= n + nx) cp_async8(dst, xrhs + ((size_t)sim * nx + (j - n - 1)) * n + i);
+      else *dst = 0.0;
     }
+    if (Gt)
+      for (int idx = tid; idx < nq * nq; idx += 256) {
+        const int k = idx / nq, i = idx % nq;
+        cp_async8(Vs + idx, Gt + ((size_t)sim * 2 * nq + 2 * k + 1) * ldg + i);
+      }
+    cp_async_all_wait();
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < NB; ++a)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int i = ty + 16 * a, j = tx + 16 * b;
+        double v = M[i * LDF + j];
+        if (j == n) v = -v;  // rhs = -phi
+        if (Gt && i >= n_p && j >= n_p && i < n && j < n) v += Vs[(j - n_p) * nq + (i - n_p)];
+        M[i * LDF + j] = v;
+      }
+  } else {
+    // staging in one pass: every thread loads its (row, column) entries of [S + diag(0, V) | -phi |
+    // extra rhs] straight from global memory (all loads in flight at once; the vhp block V[i][j] =
+    // Gt[2 j + 1][i] of the sim) and stores them once. Thread (ty, tx) owns rows ty + 16 a, columns
+    // tx + 16 b.
+    double stg[NB][NB];
+#pragma unroll
+    for (int a = 0; a < NB; ++a)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int i = ty + 16 * a, j = tx + 16 * b;
+        double v = 0.0;
+        if (i < n) {
+          if (j < n) v = Ss[(size_t)i * n + j];
+          else if (j == n) v = -phi[(size_t)sim * n + i];
+          else if (j <= n + nx) v = xrhs[((size_t)sim * nx + (j - n - 1)) * n + i];
+        }
+        stg[a][b] = v;
+      }
+    if (Gt) {
+#pragma unroll
+      for (int a = 0; a < NB; ++a)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int i = ty + 16 * a, j = tx + 16 * b;
+          if (i >= n_p && j >= n_p && i < n && j < n)
+            stg[a][b] += Gt[((size_t)sim * 2 * nq + 2 * (j - n_p) + 1) * ldg + (i - n_p)];
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NB; ++a)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) M[(ty + 16 * a) * LDF + tx + 16 * b] = stg[a][b];
+  }
+  // the iterate's entries this thread will update at the end (apply), fetched while the LU runs
+  double r_old[(D + 255) / 256];
+#pragma unroll
+  for (int q = 0; q < (D + 255) / 256; ++q) {
+    const int t = tid + 256 * q;
+    r_old[q] = (NB <= 6 && apply && t < n) ? r[(size_t)sim * n + t] : 0.0;
+  }
   if (tid == 0) {
     fact_cnt = 0;
     bad_s = 0;
   }
   if (tid < NU) upd_cnt[tid] = 0;
-  cp_async_all_wait();
   __syncthreads();
-#pragma unroll
-  for (int a = 0; a < NB; ++a)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int i = ty + 16 * a, j = tx + 16 * b;
-      double v = M[i * LDF + j];
-      if (j == n) v = -v;  // rhs = -phi
-      if (Gt && i >= n_p && j >= n_p && i < n && j < n) v += Vs[(j - n_p) * nq + (i - n_p)];
-      M[i * LDF + j] = v;
-    }
-  __syncthreads();
+#ifdef LU_TRACE
+  if (threadIdx.x == 0) g_lu_trace[65] = clock64();
+#endif
   if (warp == 0) {
     // ------------------------------------------------------------------ pivot-chain warp
     bool used[R];
@@ -845,6 +895,9 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
     }
   }
   __syncthreads();
+#ifdef LU_TRACE
+  if (threadIdx.x == 0) g_lu_trace[66] = clock64();
+#endif
   if (bad_s) {
     if (tid == 0) status[sim] = 1;
     return;
@@ -854,12 +907,19 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
     const double x = M[pivrow[kk] * LDF + n + col] * rdiag[kk];
     if (col == 0) {
       dr[(size_t)sim * n + kk] = x;
-      if (apply) r[(size_t)sim * n + kk] += x;
+      if (apply) {
+        if constexpr (NB <= 6) r[(size_t)sim * n + kk] = r_old[t / 256] + x;   // t < n <= D: this thread's prefetch
+        else r[(size_t)sim * n + kk] += x;
+      }
     } else {
       xout[((size_t)sim * nx + col - 1) * n + kk] = x;
     }
   }
   if (tid == 0) status[sim] = 0;
+#ifdef LU_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) g_lu_trace[67] = clock64();
+#endif
 }
 
 // n: unknowns + extra right-hand sides (D >= n + 1 columns incl. -phi)

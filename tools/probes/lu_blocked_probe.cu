@@ -75,10 +75,12 @@ int run(int n, int n_p, int nx, bool vhp) {
   if (n == 60) {
     one(true, ddr2, dxo2);
     cudaDeviceSynchronize();
-    long long tr[66];
+    long long tr[70];
     cudaMemcpyFromSymbol(tr, g_lu_trace, sizeof tr);
     long long tu[64];
     cudaMemcpyFromSymbol(tu, g_lu_trace_u, sizeof tu);
+    printf("  phases (cycles): staging %lld  factor %lld  solve+store %lld  | total %lld\n", tr[65] - tr[64],
+           tr[66] - tr[65], tr[67] - tr[66], tr[67] - tr[64]);
     for (int p = 0; p < 15; ++p)
       printf("  panel %d: factor %lld  wait %lld  lookahead %lld | upd: spin %lld chains %lld rows %lld (fact pub at +%lld)\n", p,
              tr[4 * p + 1] - tr[4 * p], tr[4 * p + 2] - tr[4 * p + 1], p < 14 ? tr[4 * (p + 1)] - tr[4 * p + 2] : -1LL,
