@@ -546,6 +546,9 @@ __global__ void __launch_bounds__(256) k_lu_solve(const double* __restrict__ S, 
   if (tid == 0) status[sim] = 0;
 }
 
+#ifndef LU_RB
+#define LU_RB 16   // trailing-update row block (tools/probes/lu_blocked_probe.cu -DLU_RB=8)
+#endif
 #ifdef LU_TRACE
 __device__ long long g_lu_trace[4 * 16 + 6];   // tools/probes/lu_blocked_probe.cu -DLU_TRACE: panels | start, staged, factored, end
 __device__ long long g_lu_trace_u[4 * 16];
@@ -588,7 +591,7 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
   const double* Ss = S + (size_t)sim * n * n;
   const int nq = n - n_p;
   double* Vs = M + D * LDF;
-  double* Mul = Vs + nq * nq;
+  double* Mul = Vs + ((nq * nq + 1) & ~1);   // 16-byte aligned multiplier panels
   const int ncol = n + 1 + nx;
   const int npan = (n + PW - 1) / PW;
   if constexpr (NB > 6) {
@@ -809,7 +812,7 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
     // work unit = (32-column group, 16-row block), lanes = columns; unit u belongs to warp 1 + u % 7
     // for the whole factorisation. Per panel: every unit's u-chain from the pivot rows (read by all
     // units before any unit writes: named barrier), then its rows.
-    constexpr int RB = 16, NRB = D / RB;
+    constexpr int RB = LU_RB, NRB = D / RB;
     const int uw = warp - 1, ut = tid - 32;
     const int ngrp = (ncol + 31) / 32;
     for (int P = 0; P < npan; ++P) {
@@ -872,10 +875,14 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
         }
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr) {
-          const double* mi = MulP + (blk * RB + rr) * PW;
+          // the row's PW multipliers as 16-byte broadcast loads (half the shared-memory wavefronts)
+          const double2* mi = reinterpret_cast<const double2*>(MulP + (blk * RB + rr) * PW);
 #pragma unroll
-          for (int kk = 0; kk < PW; ++kk)   // (entries kk >= kw of a short last panel are never written)
-            if (kk < kw) v[rr] = fma(-mi[kk], uk[q][kk], v[rr]);
+          for (int k2 = 0; k2 < PW / 2; ++k2) {
+            const double2 m2 = mi[k2];   // (entries kk >= kw of a short last panel are never written)
+            if (2 * k2 < kw) v[rr] = fma(-m2.x, uk[q][2 * k2], v[rr]);
+            if (2 * k2 + 1 < kw) v[rr] = fma(-m2.y, uk[q][2 * k2 + 1], v[rr]);
+          }
         }
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr) {
@@ -932,7 +939,7 @@ inline size_t lu_smem_bytes(int n, int nq = 0) {
 // k_lu_lookahead: + double-buffered panel multipliers [2][D][PW <= 8]
 inline size_t lu_lookahead_smem_bytes(int n, int nq = 0) {
   const int D = 16 * lu_nb(n);
-  return lu_smem_bytes(n, nq) + (size_t)2 * D * 8 * 8;
+  return lu_smem_bytes(n, nq) + (size_t)2 * D * 8 * 8 + 16;
 }
 
 
