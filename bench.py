@@ -63,9 +63,10 @@ def peaks():
     tc = {"fp64": None, "i8": None, "source": "absent"}
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "r02_tc_peaks.json")))
-        tc = {"fp64": t["dmma_tflops"], "i8": t["i8_n64_tops"],
+        tc = {"fp64": t["dmma_tflops"], "i8": t["i8_best_tops"],
               "source": "profiles/r02_tc_peaks.json (tools/probes/tc_peak.cu, clocks sampled): fp64 DMMA, "
-                        "tcgen05 kind::i8 M=128 N=64 (MEASURED_PEAKS.json has neither)"}
+                        "tcgen05 kind::i8 M=128 N>=128 (the Ozaki MMAs are mostly N=128..256 runs of digit "
+                        "planes); MEASURED_PEAKS.json has neither"}
     except Exception:
         try:
             tc["fp64"] = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["dmma_tflops"]
@@ -203,16 +204,17 @@ def decoder_flops(P, n_sims=1):
     return F, executed
 
 
-def decoder_roofline(P, stage_ms, n_sims, tc, tc_layers=0, cols=None):
+def decoder_roofline(P, stage_ms, n_sims, tc, tc_info=(0, 0, 0)):
     """Roofline of the decoder bundle (hidden jet chain + output layer + vhp backward chain).
 
     `achieved` counts the work the kernels EXECUTE on their pipe; the §8d algorithmic figure of
     the reference pass structure is reported separately as the work the collapsed bundle
-    replaces (it is not a pipe fraction). When `tc_layers` hidden layers run on the tcgen05
-    Ozaki GEMM (batched contexts), the hidden stage is measured in executed kind::i8 ops (28
-    digit-pair MMAs per K block over the 64-padded columns) against the kind::i8 peak, the other
-    stages in fp64 flops against the DMMA peak, and `frac` is the time-weighted mean of the two
-    pipe fractions (the share of the bundle's time its pipes would be busy at peak)."""
+    replaces (it is not a pipe fraction). Batched contexts run most of the bundle's GEMMs on the
+    tcgen05 Ozaki GEMM (tc_info = hidden layers, output layer, vhp backward layers on it): those
+    are counted in executed kind::i8 ops (28 digit-pair MMAs per 32-deep K chunk over the
+    128-row / 64-column padded tiles) against the measured kind::i8 peak, the remaining DMMA
+    GEMMs in fp64 flops against the DMMA peak, and `frac` is the time-weighted mean of the
+    stages' pipe fractions (the share of the bundle's time its pipes would be busy at peak)."""
     fp64 = tc["fp64"]
     F, ex = decoder_flops(P, n_sims)
     dec_ms = stage_ms[0] + stage_ms[1] + stage_ms[2]
@@ -227,30 +229,41 @@ def decoder_roofline(P, stage_ms, n_sims, tc, tc_layers=0, cols=None):
                            "def": "SURVEY.md §8d F_dec = (18 n_q+6)(2 sum in*out + 4 N n_p) per sim: the "
                                   "reference's 4 n_q + 2 passes; the jet bundle executes fewer columns"},
            "stages_ms": {"hidden_jet": stage_ms[0], "output_gemm": stage_ms[1], "vhp_bwd": stage_ms[2]}}
-    if tc_layers and cols:
+    n_hid, n_out, n_bwd = tc_info
+    if n_hid or n_out or n_bwd:
         c = P.cfg
-        w = c.width
-        cpad = -(-cols // 64) * 64
-        i8_ops = tc_layers * 28 * 2.0 * w * w * cpad
-        i8_tops = i8_ops / (stage_ms[0] * 1e-3) / 1e12
-        G, gps = jet_groups(c.n_q, True)
-        dmma_fl = ex * n_sims - 2.0 * G * gps * n_sims * w * w * tc_layers   # seed layer stays on DMMA
-        dmma_ms = stage_ms[1] + stage_ms[2]
-        dmma_tf = dmma_fl / (dmma_ms * 1e-3) / 1e12
-        f_i8 = (i8_tops / tc["i8"]) if tc["i8"] else None
-        f_dm = (dmma_tf / fp64) if fp64 else None
-        out["kernel"] = ("decoder bundle: %d hidden jet layers on tcgen05 kind::i8 (Ozaki, 7 digits) + seed layer, "
-                         "output GEMM and vhp backprop on fp64 DMMA" % tc_layers)
+        w, n_q, N = c.width, c.n_q, P.model.N
+        G, gps = jet_groups(n_q, True)
+        up = lambda x, m: -(-x // m) * m
+        P1 = 1 + n_q
+        ocs = (64 // P1) * P1
+        i8 = [n_hid * 28 * 2.0 * w * w * up(n_sims * G * gps, 64),
+              n_out * 28 * 2.0 * up(N, 128) * w * up(n_sims * (2 + 2 * n_q), 64),
+              n_bwd * 28 * 2.0 * w * w * (-(-(n_sims * P1) // ocs) * 64)]
+        # fp64 flops of the stages' remaining DMMA GEMMs: the seed layer (K = n_q), the vhp seed
+        # (P W_L)^T a and the last backward layer (M = n_q)
+        dm = [2.0 * G * gps * n_sims * w * n_q,
+              0.0 if n_out else 2.0 * (2 + 2 * n_q) * n_sims * N * w,
+              2.0 * n_sims * N * w + 2.0 * n_sims * P1 * w * n_q]
+        stages = []
+        for k, name in enumerate(("hidden_jet", "output_gemm", "vhp_bwd")):
+            t = stage_ms[k] * 1e-3
+            f_i8 = i8[k] / t / 1e12 / tc["i8"] if tc["i8"] else None
+            f_dm = dm[k] / t / 1e12 / fp64 if fp64 else None
+            stages.append({"stage": name, "ms": stage_ms[k], "i8_ops": i8[k], "i8_tops": i8[k] / t / 1e12,
+                           "fp64_flops": dm[k], "fp64_tflops": dm[k] / t / 1e12,
+                           "pipe_frac": (f_i8 or 0.0) + (f_dm or 0.0)})
+        frac = sum(st["pipe_frac"] * st["ms"] for st in stages) / dec_ms
+        out["kernel"] = ("decoder bundle on tcgen05 kind::i8 (Ozaki fp64, 7 digits): %d hidden jet layers, "
+                         "%s, %d vhp backward layers; seed / vhp-seed / last backward GEMMs on fp64 DMMA"
+                         % (n_hid, "output layer" if n_out else "output layer on DMMA", n_bwd))
         out["unit"] = "pipe fraction (time-weighted)"
-        out["achieved"] = (f_i8 * stage_ms[0] + f_dm * dmma_ms) / dec_ms if f_i8 is not None and f_dm is not None else None
+        out["achieved"] = frac
         out["peak"] = 1.0
-        out["frac"] = out["achieved"]
-        out["pipes"] = {
-            "tcgen05_i8": {"stage": "hidden_jet", "achieved": i8_tops, "peak": tc["i8"], "unit": "TOP/s",
-                           "frac": f_i8, "executed_ops_per_launch": i8_ops,
-                           "fp64_equivalent_tflops": (ex * n_sims - dmma_fl) / (stage_ms[0] * 1e-3) / 1e12},
-            "fp64_dmma": {"stage": "output_gemm + vhp_bwd", "achieved": dmma_tf, "peak": fp64, "unit": "TFLOP/s",
-                          "frac": f_dm, "executed_flops_per_launch": dmma_fl}}
+        out["frac"] = frac
+        out["pipes"] = {"i8_peak_tops": tc["i8"], "fp64_peak_tflops": fp64, "stages": stages,
+                        "i8_ops_per_launch": sum(i8), "i8_tops": sum(i8) / (dec_ms * 1e-3) / 1e12,
+                        "fp64_equivalent_tflops": executed}
     return out
 
 
@@ -332,8 +345,7 @@ def batched_leg(args, rank, world):
     pk, tc = peaks()
     fp64 = tc["fp64"]
     stage_ms = s.bench_kernels(3, flush_l2=True)
-    G, gps = jet_groups(P.cfg.n_q, True)
-    roof = decoder_roofline(P, stage_ms, ns, tc, s.tc_layers(), ns * G * gps)
+    roof = decoder_roofline(P, stage_ms, ns, tc, s.tc_info())
     cub_ms, cub_bytes = s.bench_cubature(5, flush_l2=True)
     hbm = pk.get("hbm_gbs")
     cub_gbs = cub_bytes / (cub_ms * 1e-3) / 1e9

@@ -243,6 +243,10 @@ NLROM_API int nlrom_launches_per_iteration(nlrom_ctx* ctx);
  * contexts; 0 = every layer on fp64 DMMA). bench.py uses it to pick the roofline peak. */
 NLROM_API int nlrom_tc_layers(nlrom_ctx* ctx);
 
+/* Which decoder GEMMs of a batched context run on the tcgen05 Ozaki GEMM: out[0] = hidden jet
+ * layers, out[1] = output layer (0 / 1), out[2] = shared-real vhp backward layers. */
+NLROM_API int nlrom_tc_info(nlrom_ctx* ctx, int* out);
+
 /* Profiling: prefix-graph timing of one Newton iteration. For k = 1..min(cap, launches) the
  * first k launches are captured as a graph and timed over n_iters replays (L2 flushed before
  * each): ms[k-1] - ms[k-2] is launch k's marginal in-graph cost. names receives the kernel

@@ -25,7 +25,7 @@ EXPORTED = [
     "nlrom_system_jacobian", "nlrom_delta_j", "nlrom_fictitious_force", "nlrom_wnet_forward",
     "nlrom_cubature_integrate", "nlrom_full_displacement", "nlrom_jtilde", "nlrom_step", "nlrom_step_device",
     "nlrom_bench_iterations", "nlrom_bench_replays", "nlrom_iterate", "nlrom_get_iterate", "nlrom_set_iterate",
-    "nlrom_launches_per_iteration", "nlrom_tc_layers", "nlrom_element_forces",
+    "nlrom_launches_per_iteration", "nlrom_tc_layers", "nlrom_tc_info", "nlrom_element_forces",
     "nlrom_element_reduced_forces", "nlrom_bench_kernels", "nlrom_bench_cubature", "nlrom_train_forces", "nlrom_stream", "nlrom_coupled_setup",
     "nlrom_coupled_begin", "nlrom_coupled_eval", "nlrom_coupled_update", "nlrom_coupled_read",
     "nlrom_coupled_launches", "nlrom_bench_prefix", "nlrom_debug_poison_shared_memory",
@@ -116,6 +116,7 @@ def lib():
             "nlrom_bench_iterations": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
             "nlrom_launches_per_iteration": (C.c_int, [vp]),
             "nlrom_tc_layers": (C.c_int, [vp]),
+            "nlrom_tc_info": (C.c_int, [vp, ip]),
             "nlrom_bench_replays": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float)]),
             "nlrom_iterate": (C.c_int, [vp, C.c_int]),
             "nlrom_get_iterate": (C.c_int, [vp, dp, dp, dp]),

@@ -79,10 +79,12 @@ int gemm_launch_count = 0;
 //                   Ozaki-int8 GEMM (ozaki_tc.cuh)
 //   cub_chunked     many sims: the element-chunk cubature kernel (k_cubature, 12-row Gram) instead
 //                   of the per-sim B-projected kernel (k_cub_sims)
+//   dmma_bwd        batched shared-real vhp backward layers on the fp64 DMMA kernel instead of the
+//                   tcgen05 Ozaki GEMM
+//   dmma_out        batched output layer on the fp64 DMMA kernel instead of the tcgen05 Ozaki GEMM
 struct PathOpts {
   bool batched = false, unfused = false, hid_cp = false, bwd_cp = false, shared_real = false,
-       no_shared_real = false, dmma_hidden = false, cub_chunked = false;
-  int cub_minb = 0;
+       no_shared_real = false, dmma_hidden = false, cub_chunked = false, dmma_bwd = false, dmma_out = false;
   int cpc = 0, cpm = 0, tangents = 0;
   static PathOpts from_env() {
     PathOpts o;
@@ -105,7 +107,8 @@ struct PathOpts {
       else if (key == "no_shared_real") o.no_shared_real = true;
       else if (key == "dmma_hidden") o.dmma_hidden = true;
       else if (key == "cub_chunked") o.cub_chunked = true;
-      else if (key == "cub_minb") o.cub_minb = val;
+      else if (key == "dmma_bwd") o.dmma_bwd = true;
+      else if (key == "dmma_out") o.dmma_out = true;
       else if (key == "cpc") o.cpc = val;
       else if (key == "cpm") o.cpm = val;
       else if (key == "tangents") o.tangents = val;
@@ -137,6 +140,9 @@ struct nlrom_ctx {
   std::vector<int> ldW, ldWT;
   std::vector<DBuf> Wp, WTp;  // fused chains: padded copies (one TMA bulk copy per CTA slice)
   std::vector<OzakiWeights> ozW;  // batched hidden layers on tcgen05: int8 digit tiles of W_l (ozaki_tc.cuh)
+  std::vector<OzakiWeights> ozWT;  // batched shared-real vhp backward layers: digit tiles of W_l^T
+  OzakiWeights ozWL;               // batched output layer: digit tiles of P W_L (N rows, zero-padded to 128)
+  unsigned* ozBHW[2] = {nullptr, nullptr};  // ping-pong column-scale partials between backward layers
   unsigned* ozHW[2] = {nullptr, nullptr};  // ping-pong column-scale partials between hidden layers
   int ldpf = 0, ldpb = 0;
   DBuf Alast, AT, Pb, U, mass;
@@ -395,13 +401,22 @@ using CfgOutWs = WsCfg<48, 128, 3, 4, 6>;  // 12 consumer warps (16 x 32 warp ti
 // (16 x 64 tiles, 420 CTAs: fastest of 48x128 / 48x64 / 24x64 / 16x64 / 8x64 in the cfg2 graph)
 using CfgOutWs64c = WsCfg<16, 64, 2, 2, 6>;
 
+// the output layer on tcgen05: the compact last hidden layer writes its column scales for it
+bool out_on_tc(nlrom_ctx* c) {
+  return c->batched && c->ozWL.ready && c->ozHW[0] && c->wL1 % 32 == 0 && c->ldlast % 2 == 0 && !c->next &&
+         c->Cc % 2 == 0;
+}
+
 void output_layer(nlrom_ctx* c) {
   GemmArgs g{c->Alast.p, c->H[c->L - 2].p, c->ldlast, c->ldlast, c->N, c->n_sims * c->Cc, c->wL1 + c->next, 0, 0};
   EpiJetOutC e{c->Pb.p, c->U.p, c->r.p, c->u.p, c->value.p, c->hvv.p, c->Jt.p, c->dJ.p, c->ldjt, c->lddj,
                c->n_p, c->n_q};
-  // batched: the cp.async big-tile kernel (the warp-specialised pipeline measured slower here:
-  // 3.38 vs 3.06 ms at cfg5, the EpiJetOutC scatter dominates the tile)
-  if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
+  // batched: tcgen05 Ozaki GEMM over the compact columns (their column scales from the last hidden
+  // layer's epilogue), else the cp.async big-tile kernel (the warp-specialised pipeline measured
+  // slower here: 3.38 vs 3.06 ms at cfg5, the EpiJetOutC scatter dominates the tile)
+  if (c->batched && out_on_tc(c)) {
+    launch_ozaki<64>(c->ozWL.view(), OzakiBExp{c->ozHW[(c->L - 2) & 1], c->wL1 / 32}, g, e, c->st);
+  } else if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
   else if (c->ldlast % 2 == 0 && g.C <= 64) launch_gemm_ws<CfgOutWs64c>(g, e, c->st);
   else if (c->ldlast % 2 == 0) launch_gemm_ws<CfgOutWs>(g, e, c->st);
   else launch_gemm<CfgOutC>(g, e, c->st);
@@ -494,8 +509,9 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
     EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, compact};
     // tcgen05 Ozaki layers read their input's column scales from the previous layer's epilogue
     const bool oz_here = c->batched && l < (int)c->ozW.size() && c->ozW[l].ready;
-    const bool oz_next = c->batched && l + 1 < (int)c->ozW.size() && c->ozW[l + 1].ready && !compact &&
-                         c->widths[l + 1] % 32 == 0 && c->ozHW[0];
+    const bool oz_next = (c->batched && l + 1 < (int)c->ozW.size() && c->ozW[l + 1].ready && !compact &&
+                          c->widths[l + 1] % 32 == 0 && c->ozHW[0]) ||
+                         (compact && out_on_tc(c));
     if (oz_next) e.colhw = c->ozHW[l & 1];
     const OzakiBExp be = (oz_here && l >= 1 && c->ozHW[0]) ? OzakiBExp{c->ozHW[(l - 1) & 1], c->widths[l] / 32}
                                                           : OzakiBExp{nullptr, 0};
@@ -549,15 +565,12 @@ void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true,
     CubSimsArgs a{s.rows_g.p, s.Dm_g.p, s.vol_g.p, s.BU.p, s.n, weighted ? c->wC.p : nullptr, c->u.p, c->Jt.p,
                   c->N, c->n, c->n_p, c->ldjt, c->mu, c->lam, s.fe_w.p, s.part_f.p, s.part_K.p, 0};
     const size_t smem = cub_sims_smem(c->n, c->n_p, s.ti);
-    const bool three = c->opt.cub_minb == 3;
+    // two CTAs per SM (128 registers): the 3-CTA / 80-register build spills and measured 2x slower
     switch (s.ti) {
       case 1: launch(c, k_cub_sims<1, 2>, dim3(c->n_sims), 256, smem, a); break;
       case 2: launch(c, k_cub_sims<2, 2>, dim3(c->n_sims), 256, smem, a); break;
       case 3: launch(c, k_cub_sims<3, 2>, dim3(c->n_sims), 256, smem, a); break;
-      default:
-        if (three) launch(c, k_cub_sims<4, 3>, dim3(c->n_sims), 256, smem, a);
-        else launch(c, k_cub_sims<4, 2>, dim3(c->n_sims), 256, smem, a);
-        break;
+      default: launch(c, k_cub_sims<4, 2>, dim3(c->n_sims), 256, smem, a); break;
     }
     if (scatter)
       launch(c, k_scatter_rows, grid1((long long)s.n_rows * c->n_sims), 256, 0, (const int*)s.row_ids.p,
@@ -824,7 +837,25 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
            (const double*)caches[l_top].p, ldcs[l_top], npass_per_sim, D0.p);
     DBuf* cur = &D0;
     DBuf* nxt = &D1;
+    // tcgen05 Ozaki layers (ozaki_tc.cuh): 64-column tiles of whole sims; each layer's epilogue
+    // writes the next Ozaki layer's column-scale partials (the first one scans its input)
+    const int ocs = (64 / P1) * P1;
+    auto oz_bwd = [&](int l) {
+      return l >= 1 && l < (int)c->ozWT.size() && c->ozWT[l].ready && ocs >= P1 && ldcs[l] % 2 == 0 &&
+             c->ozBHW[0] != nullptr;
+    };
     for (int l = c->L - 2; l >= 1; --l) {
+      if (oz_bwd(l)) {
+        GemmArgs g{c->WT[l].p, cur->p, c->ldWT[l], ldcs[l], c->widths[l], ncs, c->widths[l + 1], 0, 0, ocs};
+        const bool from_oz = oz_bwd(l + 1) && l + 1 <= c->L - 2;
+        const OzakiBExp be = from_oz ? OzakiBExp{c->ozBHW[(l + 1) & 1], c->widths[l + 1] / 32} : OzakiBExp{nullptr, 0};
+        EpiBwdShared e{nxt->p, ldcs[l - 1], caches[l - 1].p, npass_per_sim};
+        if (oz_bwd(l - 1) && c->widths[l] % 32 == 0) e.colhw = c->ozBHW[l & 1];
+        launch_ozaki<64>(c->ozWT[l].view(), be, g, e, c->st);
+        ++gemm_launch_count;
+        std::swap(cur, nxt);
+        continue;
+      }
       GemmArgs g{c->WT[l].p, cur->p, c->ldWT[l], ldcs[l], c->widths[l], ncs, c->widths[l + 1], 0, 0, cstep};
       // warp-specialised TMA pipeline with sim-aligned column tiles: cfg5 vhp 5.14 -> 4.77 ms
       if (!c->opt.bwd_cp && c->widths[l + 1] % 16 == 0 && c->ldWT[l] % 2 == 0 && ldcs[l] % 2 == 0)
@@ -1179,6 +1210,9 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         }
       }
       upload_matrix(c->Alast, A.data(), N, w, c->ldlast);
+      if ((c->n_sims * (4 + 4 * n_q) >= 2048 || c->opt.batched) && !c->opt.dmma_hidden && !c->opt.dmma_out &&
+          w % oz::BK == 0 && w <= 256)
+        ozaki_upload(c->ozWL, A.data(), w, N, w);
       if (c->n_sims > 1) {
         std::vector<double> At((size_t)w * N);
         for (int r = 0; r < N; ++r)
@@ -1277,8 +1311,23 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         if (o % oz::BM == 0 && in % oz::BK == 0 && in <= 256) ozaki_upload(c->ozW[l], d->W[l], in, o, in);
         maxw = std::max(maxw, in);
       }
-      const size_t hwn = (size_t)c->n_sims * c->Cb * (size_t)ceil_div(maxw, 32);
+      const size_t hwn = (size_t)c->n_sims * c->Cb * (size_t)ceil_div(std::max(maxw, c->wL1), 32);
       for (auto& p : c->ozHW) NL_CUDA(cudaMalloc(&p, std::max<size_t>(hwn, 1) * sizeof(unsigned)));
+      if (!c->opt.dmma_bwd) {
+        // shared-real vhp backward layers 1 .. L-2: W_l^T (widths[l] x widths[l+1]) as digit tiles
+        c->ozWT.resize(L - 1);
+        for (int l = 1; l < L - 1; ++l) {
+          const int in = c->widths[l], o = c->widths[l + 1];   // W_l^T: M = in, K = o
+          if (in % oz::BM == 0 && o % oz::BK == 0 && o <= 256) {
+            std::vector<double> wt((size_t)in * o);
+            for (int r = 0; r < o; ++r)
+              for (int k = 0; k < in; ++k) wt[(size_t)k * o + r] = d->W[l][(size_t)r * in + k];
+            ozaki_upload(c->ozWT[l], wt.data(), o, in, o);
+          }
+        }
+        const size_t bhw = (size_t)c->n_sims * (1 + n_q) * (size_t)ceil_div(maxw, 32);
+        for (auto& p : c->ozBHW) NL_CUDA(cudaMalloc(&p, std::max<size_t>(bhw, 1) * sizeof(unsigned)));
+      }
     }
     c->ldq = round_up(n_q, 2);
     const int ncols = c->n_sims * c->Cb;
@@ -1356,7 +1405,6 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     NL_CUDA(cudaFuncSetAttribute(k_cub_sims<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_cub_sims<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_cub_sims<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    NL_CUDA(cudaFuncSetAttribute(k_cub_sims<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_wnet_tail2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1404,6 +1452,8 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   if (c->evK) cudaEventDestroy(c->evK);
   if (c->evM) cudaEventDestroy(c->evM);
   if (c->evP) cudaEventDestroy(c->evP);
+  for (auto p : c->ozBHW)
+    if (p) cudaFree(p);
   for (auto p : c->ozHW)
     if (p) cudaFree(p);
   delete c;
@@ -2018,6 +2068,14 @@ extern "C" int nlrom_bench_cubature(nlrom_ctx* c, int n_iters, int flush_l2, flo
 }
 
 extern "C" int nlrom_launches_per_iteration(nlrom_ctx* c) { return c ? c->launches_E + c->launches_J : 0; }
+extern "C" int nlrom_tc_info(nlrom_ctx* c, int* out) {
+  if (!c || !out) return NLROM_ERR_ARG;
+  out[0] = out[1] = out[2] = 0;
+  for (auto& w : c->ozW) out[0] += w.ready ? 1 : 0;
+  out[1] = out_on_tc(c) ? 1 : 0;
+  for (auto& w : c->ozWT) out[2] += w.ready ? 1 : 0;
+  return NLROM_OK;
+}
 extern "C" int nlrom_tc_layers(nlrom_ctx* c) {
   int k = 0;
   if (c)

@@ -111,21 +111,46 @@ struct EpiBwdShared {
   int ldy;
   const double* fcache;
   int npass;
+  // column-scale partials for a tcgen05 Ozaki consumer (as EpiJet::colhw): colhw[c * (M / 32) +
+  // m / 32] = max over 32 rows of the high word of |Y[c][m]| (tile rows, thread counts multiples of 32)
+  unsigned* colhw = nullptr;
   __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
     const int P1 = 1 + npass;
-    for (int i = tid; i < t.bm * t.bn; i += nt) {
-      const int cl = i / t.bm, ml = i % t.bm;
-      const int c = t.c0 + cl, m = t.m0 + ml;
-      if (m >= g.M || c >= g.C) continue;
-      const int sim = c / P1, s = c % P1;
-      const double d0 = t.Cs[(cl - s) * t.ldc + ml];
-      const double* F = fcache + (size_t)sim * 2 * npass * ldy;
-      const double f0 = F[m];
-      if (s == 0) {
-        Y[(size_t)c * ldy + m] = d0 * f0;
-      } else {
-        const double f1 = F[(size_t)(2 * (s - 1) + 1) * ldy + m];
-        Y[(size_t)c * ldy + m] = fma(t.Cs[cl * t.ldc + ml], f0, d0 * f1);
+    const double* __restrict__ fc = fcache;
+    double* __restrict__ y = Y;
+    // four elements per thread per round: every cache load of the round is issued before any store
+    // (the compiler cannot reorder the loads past stores to Y on its own)
+    constexpr int U = 4;
+    const int total = t.bm * t.bn;
+    for (int i0 = tid; i0 < total; i0 += U * nt) {
+      double f0[U], f1[U], cv[U], dv[U];
+      int cc[U], mm[U], ss[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nt;
+        const int cl = i / t.bm, ml = i % t.bm;
+        const int c = t.c0 + cl, m = t.m0 + ml;
+        ok[u] = i < total && m < g.M && c < g.C;   // warp-uniform when bm % 32 == 0 and M % 32 == 0
+        const int sim = ok[u] ? c / P1 : 0, sv = ok[u] ? c % P1 : 0;
+        cc[u] = c;
+        mm[u] = m;
+        ss[u] = sv;
+        const double* F = fc + (size_t)sim * 2 * npass * ldy;
+        f0[u] = ok[u] ? F[m] : 0.0;
+        f1[u] = (ok[u] && sv > 0) ? F[(size_t)(2 * (sv - 1) + 1) * ldy + m] : 0.0;
+        dv[u] = ok[u] ? t.Cs[(cl - sv) * t.ldc + ml] : 0.0;
+        cv[u] = ok[u] ? t.Cs[cl * t.ldc + ml] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
+        const double v = ss[u] == 0 ? dv[u] * f0[u] : fma(cv[u], f0[u], dv[u] * f1[u]);
+        y[(size_t)cc[u] * ldy + mm[u]] = v;
+        if (colhw) {
+          const unsigned r = __reduce_max_sync(0xffffffffu, (unsigned)__double2hiint(fabs(v)));
+          if ((tid & 31) == 0) colhw[(size_t)cc[u] * (g.M >> 5) + (mm[u] >> 5)] = r;
+        }
       }
     }
   }
@@ -170,7 +195,7 @@ struct EpiJet {
   int gps;            // groups per simulation
   int n_q;            // tangent directions per simulation
   int compact;        // 1: write the output layout per sim (next layer is linear): [h_1, 2 h_ss | (h_t, 2 h_tss + h_tr) x n_q]
-  // Column-scale partials for a tcgen05 Ozaki consumer (ozaki_tc.cuh), non-compact layout only:
+  // Column-scale partials for a tcgen05 Ozaki consumer (ozaki_tc.cuh), either layout:
   // colhw[c * (M / 32) + m / 32] = max over the 32 rows m of the high word of |Y[c][m]| (needs
   // M % 32 == 0 and 32-row-aligned warps: tile rows and thread counts multiples of 32).
   unsigned* colhw = nullptr;
@@ -178,7 +203,12 @@ struct EpiJet {
     double* Yz = Y + (size_t)t.z * strideY;
     const int nk = (group - 4) / 4;           // tangents per group
     const bool hw = colhw != nullptr && !compact;
+    const bool hwc = colhw != nullptr && compact;   // compact layout: one partial per written column
     const int lane = tid & 31;
+    auto note_c = [&](size_t col, int m, double v) {
+      const unsigned r = __reduce_max_sync(0xffffffffu, (unsigned)__double2hiint(fabs(v)));
+      if (lane == 0) colhw[col * (size_t)(g.M >> 5) + (m >> 5)] = r;
+    };
     unsigned hw0 = 0u, hw1 = 0u;              // this lane's columns: lane and 32 + lane of the group
     auto note = [&](int j, double v) {        // warp max over the 32 rows of column j's |v| high word
       const unsigned r = __reduce_max_sync(0xffffffffu, (unsigned)__double2hiint(fabs(v)));
@@ -213,6 +243,10 @@ struct EpiJet {
       } else if (gl == 0) {
         Yz[(size_t)(sim * cs) * ldy + m] = o[0];
         Yz[(size_t)(sim * cs + 1) * ldy + m] = 2.0 * o[2];
+        if (hwc) {
+          note_c((size_t)(sim * cs), m, o[0]);
+          note_c((size_t)(sim * cs + 1), m, 2.0 * o[2]);
+        }
       }
       for (int k = 0; k < nk; ++k) {
         const int kg = gl * nk + k;           // tangent index within the simulation
@@ -223,8 +257,13 @@ struct EpiJet {
         jet_tangent(jc, y, yo);
         if (compact) {
           const size_t col = (size_t)(sim * cs + 2 + 2 * kg);
+          const double v1 = fma(2.0, yo[2], yo[3]);
           Yz[col * ldy + m] = yo[0];
-          Yz[(col + 1) * ldy + m] = fma(2.0, yo[2], yo[3]);
+          Yz[(col + 1) * ldy + m] = v1;
+          if (hwc) {
+            note_c(col, m, yo[0]);
+            note_c(col + 1, m, v1);
+          }
         } else {
           const size_t col = (size_t)(cg + 4 + 4 * k);
 #pragma unroll

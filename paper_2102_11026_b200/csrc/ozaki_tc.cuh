@@ -179,9 +179,10 @@ struct OzakiWeights {
 inline void ozaki_prepare_a(const double* A, int lda, int M, int K, std::vector<unsigned char>& tiles,
                             std::vector<int>& exps) {
   using namespace oz;
-  const int nk = K / BK, tm_n = M / BM;
+  // rows past M (the last 128-row tile of a ragged M) are zero digits with exponent 0
+  const int nk = K / BK, tm_n = (M + BM - 1) / BM;
   tiles.assign((size_t)tm_n * nk * A_STAGE, 0);
-  exps.assign(M, 0);
+  exps.assign((size_t)tm_n * BM, 0);
   for (int m = 0; m < M; ++m) {
     double amax = 0.0;
     for (int k = 0; k < K; ++k) amax = std::max(amax, std::fabs(A[(size_t)m * lda + k]));
@@ -340,7 +341,10 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
     const int cl = ct / TPC, kq = ct % TPC;
     const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const long long total = (long long)my_tiles * nk;
-    auto col_of = [&](int j) { return ((blockIdx.x + j * gridDim.x) / tiles_m) * BN + cl; };
+    // column of this thread in its j-th tile; tiles start every cs columns (GemmArgs.cstep: tiles of
+    // whole column groups) and columns cl >= cs of a tile are padding (zeros, never stored)
+    const int cs = g.cstep ? g.cstep : BN;
+    auto col_of = [&](int j) { return cl < cs ? ((blockIdx.x + j * gridDim.x) / tiles_m) * cs + cl : g.C; };
     // load pointer (tile jl, chunk kl) runs PF chunks ahead of the slicing position
     int jl = 0, kl = 0;
     auto load_chunk = [&](double (&x)[KPT]) {
@@ -465,7 +469,8 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
     int j = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
       const int tm = t % tiles_m, tc = t / tiles_m;
-      const int m0 = tm * BM, c0 = tc * BN;
+      const int cs = g.cstep ? g.cstep : BN;
+      const int m0 = tm * BM, c0 = tc * cs;
       const int buf = NBUF == 2 ? (j & 1) : 0;
       const int use = NBUF == 2 ? (j >> 1) : j;
       {
@@ -507,7 +512,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       if (lane == 0) mbar_arrive(tempty + buf);   // TMEM may take the next tiles' accumulators
       mbar_arrive(efree + (j & 1));
       named_bar_sync(1, NEPI);
-      Tile tile{Cs, LDC, m0, c0, BM, BN, 0};
+      Tile tile{Cs, LDC, m0, c0, BM, cs, 0};
 #ifndef OZ_PROBE_NO_EPI
       epi(tile, g, et, NEPI);
 #endif
@@ -532,8 +537,9 @@ inline int sm_count_oz() {
   return n;
 }
 
-// Launch over all column tiles (persistent grid of one CTA per SM). Requirements: M % 128 == 0,
-// K % 32 == 0, ldb even and g.B 16-byte aligned, the Epi column groups divide BN; g.cstep = 0.
+// Launch over all column tiles (persistent grid of one CTA per SM). Requirements: K % 32 == 0
+// (M ragged: the prepared A operand is zero-padded to 128-row tiles, the epilogue skips m >= M), ldb even and g.B 16-byte aligned, the Epi column groups divide BN (or g.cstep <= BN
+// columns per tile, then the epilogue sees t.bn = cstep).
 template <int BN, class Epi>
 void launch_ozaki(const OzakiA& a, const OzakiBExp& be, const GemmArgs& g, const Epi& epi, cudaStream_t st) {
   using C = oz::Cfg<BN>;
@@ -543,7 +549,7 @@ void launch_ozaki(const OzakiA& a, const OzakiBExp& be, const GemmArgs& g, const
     NL_CUDA(cudaFuncSetAttribute(k_ozaki_gemm<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     configured = true;
   }
-  const int tiles_m = g.M / oz::BM, tiles_c = ceil_div(g.C, BN);
+  const int tiles_m = ceil_div(g.M, oz::BM), tiles_c = ceil_div(g.C, g.cstep ? g.cstep : BN);
   const int ntiles = tiles_m * tiles_c;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(std::max(1, std::min(ntiles, sm_count_oz())));

@@ -264,6 +264,12 @@ class Session:
         """Decoder hidden layers on the tcgen05 Ozaki GEMM (0: all on fp64 DMMA)."""
         return int(self._L.nlrom_tc_layers(self._h))
 
+    def tc_info(self):
+        """(hidden layers, output layer 0/1, vhp backward layers) on the tcgen05 Ozaki GEMM."""
+        out = np.zeros(3, dtype=np.int32)
+        self._chk(self._L.nlrom_tc_info(self._h, out.ctypes.data_as(C.POINTER(C.c_int))))
+        return tuple(int(x) for x in out)
+
 
 def _uploaded_arrays(rm, model, cm):
     """Every host array a Session copies to the device (decoder, basis, mesh, set, weight net)."""

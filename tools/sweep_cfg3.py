@@ -38,8 +38,7 @@ def main():
             s.bench_iterations(5)
             tot, _ = s.bench_iterations(args.iters)
             st = s.bench_kernels(max(10, args.iters // 4))
-            G, gps = bench.jet_groups(nq, s.tc_layers() > 0)
-            roof = bench.decoder_roofline(P, st, ns, tc, s.tc_layers(), ns * G * gps)
+            roof = bench.decoder_roofline(P, st, ns, tc, s.tc_info())
             print(json.dumps({"n_q": nq, "depth": L, "n_sims": ns, "ms_per_iteration": tot / args.iters,
                               "sim_iterations_per_s": ns * 1e3 / (tot / args.iters),
                               "hz_3_iters": 1000.0 / (3 * tot / args.iters),
