@@ -111,7 +111,7 @@ def lib():
             "nlrom_cubature_integrate": (C.c_int, [vp, dp, C.c_int, dp, dp]),
             "nlrom_full_displacement": (C.c_int, [vp, dp, dp]),
             "nlrom_jtilde": (C.c_int, [vp, dp, dp]),
-            "nlrom_step": (C.c_int, [vp, dp, dp, dp, C.POINTER(SimCfg), dp, dp, C.POINTER(StepInfo)]),
+            "nlrom_step": (C.c_int, [vp, vp, vp, vp, C.POINTER(SimCfg), vp, vp, C.POINTER(StepInfo)]),
             "nlrom_step_device": (C.c_int, [vp, vp, vp, vp, C.POINTER(SimCfg), vp, vp, vp]),
             "nlrom_bench_iterations": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
             "nlrom_launches_per_iteration": (C.c_int, [vp]),

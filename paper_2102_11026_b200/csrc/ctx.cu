@@ -685,7 +685,9 @@ bool early_wnet_ok(nlrom_ctx* c) {
 //   st2: wnet head -> tail (W) -> [wait K] k_cubature(stiffness) -> [wait M] k_reduce_S
 //   st3: [after the output layer] k_assemble_mass (M) -> [wait A] k_reduce_phi (P)
 //   (st2 and st3 joined before the LU)
-void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s) {
+// resid_only: the residual and ||phi|| alone (the step's final convergence evaluation): no mass
+// block, no stiffness / Gram launch, no S_base reduction, no vhp seed partials
+void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s, bool resid_only = false) {
   auto on = [&](cudaStream_t& other, auto fn) {
     std::swap(c->st, other);
     fn();
@@ -705,19 +707,23 @@ void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s) {
   });
   NL_CUDA(cudaEventRecord(c->evW, c->st2));
   output_layer(c);
-  NL_CUDA(cudaEventRecord(c->evFork, c->st));
-  NL_CUDA(cudaStreamWaitEvent(c->st3, c->evFork, 0));
-  on(c->st3, [&] { mass_block_launch(c, s, cfg.dt, cfg.drop_fict); });
-  NL_CUDA(cudaEventRecord(c->evM, c->st3));
+  if (!resid_only) {
+    NL_CUDA(cudaEventRecord(c->evFork, c->st));
+    NL_CUDA(cudaStreamWaitEvent(c->st3, c->evFork, 0));
+    on(c->st3, [&] { mass_block_launch(c, s, cfg.dt, cfg.drop_fict); });
+    NL_CUDA(cudaEventRecord(c->evM, c->st3));
+  }
   NL_CUDA(cudaStreamWaitEvent(c->st, c->evW, 0));
-  NL_CUDA(cudaEventRecord(c->evK, c->st));
-  NL_CUDA(cudaStreamWaitEvent(c->st2, c->evK, 0));
-  on(c->st2, [&] { cubature_phase(c, s, true, false, false, 2); });
+  if (!resid_only) {
+    NL_CUDA(cudaEventRecord(c->evK, c->st));
+    NL_CUDA(cudaStreamWaitEvent(c->st2, c->evK, 0));
+    on(c->st2, [&] { cubature_phase(c, s, true, false, false, 2); });
+  }
   CubSet& sf = c->setCF.n ? c->setCF : s;
   cubature_phase(c, sf, true, false, false, 1);
   // a (+ the vhp seed partials) on the critical path; phi and S_base on st2
   c->agemv = false;
-  const bool g = fused_vhp_backward(c, true) && c->wL1 <= 256 && c->ldlast % 2 == 0;
+  const bool g = !resid_only && fused_vhp_backward(c, true) && c->wL1 <= 256 && c->ldlast % 2 == 0;
   const int rc = g ? ASMA_GROWS : c->rpc, nch = g ? c->nchAa : c->nchA;
   AsmAArgs A{c->Jt.p, c->ldjt, c->mass.p, c->hvv.p, c->fext.p, c->r.p, c->rbar.p, c->rdbar.p,
              sf.rowptr_full.p, sf.entries.p, sf.fe_w.p, std::max(sf.n, 1), c->a.p, c->partPhi.p,
@@ -735,13 +741,15 @@ void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s) {
            c->phi.p, c->norm.p);
   });
   NL_CUDA(cudaEventRecord(c->evP, c->st3));
-  NL_CUDA(cudaStreamWaitEvent(c->st2, c->evM, 0));  // the mass block partials
-  on(c->st2, [&] {
-    const int n = c->n;
-    const int sblocks = ceil_div(n * n, 32);
-    launch(c, k_reduce_S, dim3(sblocks, c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
-           (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
-  });
+  if (!resid_only) {
+    NL_CUDA(cudaStreamWaitEvent(c->st2, c->evM, 0));  // the mass block partials
+    on(c->st2, [&] {
+      const int n = c->n;
+      const int sblocks = ceil_div(n * n, 32);
+      launch(c, k_reduce_S, dim3(sblocks, c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
+             (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
+    });
+  }
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evP, 0));
   NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));
 }
@@ -750,11 +758,11 @@ bool split_phase_ok(nlrom_ctx* c) {
   return c->rpc <= 128 && c->n <= 128;
 }
 
-void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true) {
+void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true, bool resid_only = false) {
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
   bool early_w = cfg.integration == 0 && early_wnet_ok(c) && fused_hidden_forward(c, cfg.dt, cfg.drop_fict);
   if (early_w && split_phase_ok(c)) {
-    phase_E_split(c, cfg, s);
+    phase_E_split(c, cfg, s, resid_only);
     if (join_side) NL_CUDA(cudaStreamWaitEvent(c->st, c->evJoin2, 0));
     return;
   }
@@ -1794,7 +1802,7 @@ extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar,
           phase_E(c, *cfg, false);
           phase_J(c, *cfg, true, nullptr, 0, nullptr, true);
         }
-        phase_E(c, *cfg);
+        phase_E(c, *cfg, true, /*resid_only=*/true);   // ||phi|| of the final iterate
         launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p,
                1.0 / cfg->dt, nn);
         NL_CUDA(cudaMemcpyAsync(ho, c->r.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));

@@ -199,8 +199,10 @@ class Session:
         rdot = np.empty(self.n_sims * self.n)
         info = _lib.StepInfo()
         c = _simcfg(cfg)
-        self._chk(self._L.nlrom_step(self._h, _lib.dptr(rb), _lib.dptr(rd), _lib.dptr(fe), C.byref(c),
-                                     _lib.dptr(r), _lib.dptr(rdot), C.byref(info)))
+        # raw addresses (c_void_p arguments): the per-call ctypes pointer objects are the largest
+        # host cost of a step call after the device work
+        self._chk(self._L.nlrom_step(self._h, rb.ctypes.data, rd.ctypes.data, fe.ctypes.data, C.byref(c),
+                                     r.ctypes.data, rdot.ctypes.data, C.byref(info)))
         return r, rdot, info.iters, info.res_norm
 
     def step_device(self, r_bar, rdot_bar, f_ext, cfg, r_out, rdot_out, stream_ptr):
@@ -284,7 +286,10 @@ def _uploaded_arrays(rm, model, cm):
 
 
 def _fingerprint(arrs):
-    return tuple((id(a), a.__array_interface__["data"][0], a.shape) for a in arrs)
+    # identity and size: an array object keeps its buffer unless resized in place (which changes
+    # its size), and the uploaded arrays are frozen read-only, so (id, size) identifies the data
+    # (reading the data pointer per array costs ~1 us each on every step call)
+    return tuple(map(id, arrs)), tuple(a.size for a in arrs)
 
 
 _MAX_SESSIONS_PER_MODEL = 4
