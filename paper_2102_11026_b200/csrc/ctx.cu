@@ -1218,8 +1218,10 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
         }
       }
       upload_matrix(c->Alast, A.data(), N, w, c->ldlast);
+      // (K = w >= 128: at cfg4's w = 64 the two-chunk K loop leaves the Ozaki tile overhead-bound,
+      // 0.94 vs 0.82 ms per coupled iteration with the DMMA output layer)
       if ((c->n_sims * (4 + 4 * n_q) >= 2048 || c->opt.batched) && !c->opt.dmma_hidden && !c->opt.dmma_out &&
-          w % oz::BK == 0 && w <= 256)
+          w % oz::BK == 0 && w >= 128 && w <= 256)
         ozaki_upload(c->ozWL, A.data(), w, N, w);
       if (c->n_sims > 1) {
         std::vector<double> At((size_t)w * N);
