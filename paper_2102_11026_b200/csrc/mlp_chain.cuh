@@ -166,9 +166,29 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
       double c[4][2] = {};
       const double* wrow = Ws + (tm * 8 + (lane >> 2)) * LDWS + (lane & 3);
       const double* xcol = Xc + (lane & 3) * LDX + tn * 8 + (lane >> 2);
-      for (int k0 = 0; k0 < Kp; k0 += 16) {
+      // operands one 16-deep step ahead of the DMMAs (the shared-memory loads were the chain's
+      // dominant stall: short scoreboard on every DMMA)
+      double wa[4], xb[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], wrow[k0 + 4 * u], xcol[(k0 + 4 * u) * LDX]);
+      for (int u = 0; u < 4; ++u) {
+        wa[u] = wrow[4 * u];
+        xb[u] = xcol[(4 * u) * LDX];
+      }
+      for (int k0 = 0; k0 < Kp; k0 += 16) {
+        const int k1 = k0 + 16 < Kp ? k0 + 16 : k0;   // last step: a harmless reload
+        double wn[4], xn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          wn[u] = wrow[k1 + 4 * u];
+          xn[u] = xcol[(k1 + 4 * u) * LDX];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], wa[u], xb[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          wa[u] = wn[u];
+          xb[u] = xn[u];
+        }
       }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -223,7 +243,9 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
     }
     if (!last) {
       // broadcast the R x G slice to every CTA of the cluster: warp -> destination CTA,
-      // 16-byte distributed-shared-memory stores of whole rows
+      // 16-byte distributed-shared-memory stores of whole rows (stores straight from the epilogue,
+      // 2 x 16 B per task and destination, measured slower: the cluster barrier then waits on
+      // many more outstanding remote stores, 6.9k vs 6.0k cycles per layer)
       __syncthreads();
       CHAIN_MARK(l, 3);
       constexpr int C2 = G / 2;  // 16-byte chunks per row
@@ -234,8 +256,7 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
           *reinterpret_cast<double2*>(Xr + (r0 + rr) * LDX + c2) = *reinterpret_cast<const double2*>(Os + rr * LDX + c2);
         }
       }
-    }
-    CHAIN_MARK(l, 4);
+    }    CHAIN_MARK(l, 4);
     cluster.sync();  // next activation complete in every CTA; Xc, Ys and Os free for reuse
     CHAIN_MARK(l, 5);
   }
@@ -377,9 +398,30 @@ __global__ void __launch_bounds__(256) k_mlp_dual_bwd(MlpBwdArgs a) {
         double c[4][2] = {};
         const double* wrow = Ws + (tm * 8 + (lane >> 2)) * LDWS + (lane & 3);
         const double* xcol = Xc + (lane & 3) * LDX + tn * 8 + (lane >> 2);
-        for (int k0 = 16 * (ks * n16 / KSPL); k0 < 16 * ((ks + 1) * n16 / KSPL); k0 += 16) {
+        const int kb = 16 * (ks * n16 / KSPL), ke = 16 * ((ks + 1) * n16 / KSPL);
+        if (kb < ke) {   // operands one step ahead of the DMMAs (as in the forward chain)
+          double wa[4], xb[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], wrow[k0 + 4 * u], xcol[(k0 + 4 * u) * LDX]);
+          for (int u = 0; u < 4; ++u) {
+            wa[u] = wrow[kb + 4 * u];
+            xb[u] = xcol[(kb + 4 * u) * LDX];
+          }
+          for (int k0 = kb; k0 < ke; k0 += 16) {
+            const int k1 = k0 + 16 < ke ? k0 + 16 : k0;
+            double wn[4], xn[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              wn[u] = wrow[k1 + 4 * u];
+              xn[u] = xcol[(k1 + 4 * u) * LDX];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dmma(c[u][0], c[u][1], wa[u], xb[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              wa[u] = wn[u];
+              xb[u] = xn[u];
+            }
+          }
         }
         double* Yp = Ys + ks * G * (R + 1);
 #pragma unroll
