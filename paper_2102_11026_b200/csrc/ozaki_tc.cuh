@@ -15,7 +15,7 @@
 // rounds once:   y = 2^{e_m + f_c + 2} (hi 2^-32 + lo 2^-64)      (one fma)
 // The result agrees with an fp64 GEMM to ~1e-15 of sum_k |a_k||b_k| (tests/test_gpu_ozaki.py).
 //
-// Kernel (persistent, 1 CTA / SM, 14 warps):
+// Kernel (persistent, 1 CTA / SM, 18 warps):
 //   warp 0     A producer: the weight slices are pre-tiled at upload in exactly the shared-memory
 //              operand layout, so one cp.async.bulk per K chunk (28 KB) lands a stage
 //   warp 1     TMEM owner + MMA issuer (one thread): 28 tcgen05.mma (M = 128, N = 64, K = 32) per
@@ -23,7 +23,7 @@
 //   warps 2-9  epilogue (two warps per TMEM lane quarter, each half of the columns): tcgen05.ld the 7 accumulators, exact
 //              int64 recombination, fp64 tile in shared memory, then the same Epi functor as the
 //              DMMA kernels (bias + jet sin, vhp epilogues, ...)
-//   warps 10-13 B converters: per tile the column exponents (max over K), per K chunk the 7 int8
+//   warps 10-17 B converters: per tile the column exponents (max over K), per K chunk the 7 int8
 //              slice planes of the fp64 activations written straight into the UMMA core-matrix
 //              layout (no swizzle, K-major: 8 rows x 16 B cores, LBO = 128 B, SBO = 256 B)
 #pragma once
@@ -44,7 +44,10 @@ constexpr int A_SLICE = BM * BK;             // bytes per slice plane of a stage
 constexpr int A_STAGE = S * A_SLICE;         // 28 KB
 constexpr int LDC = BM + 2;
 constexpr int NEPI = 256;       // epilogue threads (warps 2 .. 9: two warps per TMEM lane quarter)
-constexpr int NCONV = 128;      // B converter threads (warps 10 .. 13)
+#ifndef OZ_NCONV
+#define OZ_NCONV 256
+#endif
+constexpr int NCONV = OZ_NCONV; // B converter threads (warps 10 ..): 256 measured 0.85 vs 0.95-1.0 ms with 128 (probe)
 constexpr int EPI_W0 = 2, CONV_W0 = 2 + NEPI / 32;
 constexpr int NT = 64 + NEPI + NCONV;
 constexpr uint32_t TMEM_COLS = 512;
@@ -62,6 +65,7 @@ struct Cfg {
   static constexpr int NBUF = 2 * NACC * BN <= (int)TMEM_COLS ? 2 : 1;
   static constexpr int KPT = BN * BK / NCONV;   // K elements per converter thread per chunk (8 or 16)
   static_assert(BN == 32 || BN == 64, "column tile");
+  static_assert(KPT >= 8, "converter granularity");
 };
 
 // byte offset of element (row, k) inside one K-major no-swizzle slice plane (rows x 32 B)
@@ -103,6 +107,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&r)[16]) {
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, int (&r)[16]) { tmem_ld16(taddr, r); }
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, int (&r)[8]) { tmem_ld8(taddr, r); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ double pow2(int k) {  // 2^k for k in [-1022, 1023]
@@ -333,11 +344,11 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       mbar_wait_cta(tdone, 0);
     }
   } else if (warp >= CONV_W0) {
-    // --------------------------------------------------------------- B converters (warps 10 .. 13)
+    // --------------------------------------------------------------- B converters (warps 10 .. 17)
     pdl_wait();
     const int ct = tid - CONV_W0 * 32;   // 0 .. NCONV-1
     constexpr int TPC = NCONV / BN;  // threads per column (2 or 4), each KPT consecutive K per chunk
-    constexpr int PF = KPT == 8 ? 4 : 2;   // chunks in flight per thread (register ring)
+    constexpr int PF = (KPT == 8 && NCONV <= 128) ? 4 : 2;   // chunks in flight per thread (register ring)
     const int cl = ct / TPC, kq = ct % TPC;
     const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const long long total = (long long)my_tiles * nk;
@@ -487,15 +498,20 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       const int em = (m < g.M) ? a.row_exp[m] : 0;
       const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * NACC * BN);
       named_bar_sync(1, NEPI);  // the previous tile's epilogue is done with Cs
+      // CW columns per TMEM load (x16 with 128 converter threads; x8 keeps the epilogue within the
+      // register budget of the 576-thread build with 256 converter threads)
+      constexpr int CW = NCONV > 128 ? 8 : 16;
 #pragma unroll 1
-      for (int ch = chalf * (BN / 32); ch < (chalf + 1) * (BN / 32); ++ch) {
-        int acc[NACC][16];
+      for (int ch = chalf * (BN / 2 / CW); ch < (chalf + 1) * (BN / 2 / CW); ++ch) {
+        int acc[NACC][CW];
 #pragma unroll
-        for (int d = 0; d < NACC; ++d) oz::tmem_ld16(tacc + (uint32_t)(d * BN + ch * 16), acc[d]);
+        for (int d = 0; d < NACC; ++d) {
+          oz::tmem_ld_n(tacc + (uint32_t)(d * BN + ch * CW), acc[d]);
+        }
         oz::tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int cl = ch * 16 + i;
+        for (int i = 0; i < CW; ++i) {
+          const int cl = ch * CW + i;
           const long long hi = ((long long)acc[0][i] << 16) + ((long long)acc[1][i] << 8) + (long long)acc[2][i];
           const long long lo = ((long long)acc[3][i] << 24) + ((long long)acc[4][i] << 16) +
                                ((long long)acc[5][i] << 8) + (long long)acc[6][i];
