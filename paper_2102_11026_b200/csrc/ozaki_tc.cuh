@@ -65,7 +65,7 @@ struct Cfg {
   static constexpr int NBUF = 2 * NACC * BN <= (int)TMEM_COLS ? 2 : 1;
   static constexpr int KPT = BN * BK / NCONV;   // K elements per converter thread per chunk (8 or 16)
   static_assert(BN == 32 || BN == 64, "column tile");
-  static_assert(KPT >= 8, "converter granularity");
+  static_assert(KPT >= 4, "converter granularity");
 };
 
 // byte offset of element (row, k) inside one K-major no-swizzle slice plane (rows x 32 B)
@@ -114,6 +114,11 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&r)[8]) {
 }
 __device__ __forceinline__ void tmem_ld_n(uint32_t taddr, int (&r)[16]) { tmem_ld16(taddr, r); }
 __device__ __forceinline__ void tmem_ld_n(uint32_t taddr, int (&r)[8]) { tmem_ld8(taddr, r); }
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, int (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ double pow2(int k) {  // 2^k for k in [-1022, 1023]
@@ -453,8 +458,10 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
         for (int t2 = 0; t2 < S; ++t2) {
           if constexpr (KPT == 16)
             *reinterpret_cast<uint4*>(dst + t2 * C::B_SLICE) = make_uint4(w[t2][0], w[t2][1], w[t2][2], w[t2][3]);
-          else
+          else if constexpr (KPT == 8)
             *reinterpret_cast<uint2*>(dst + t2 * C::B_SLICE) = make_uint2(w[t2][0], w[t2][1]);
+          else
+            *reinterpret_cast<uint32_t*>(dst + t2 * C::B_SLICE) = w[t2][0];
         }
         fence_proxy_async();     // generic-proxy stores -> visible to the tensor core (async proxy)
         __syncwarp();
@@ -500,7 +507,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       named_bar_sync(1, NEPI);  // the previous tile's epilogue is done with Cs
       // CW columns per TMEM load (x16 with 128 converter threads; x8 keeps the epilogue within the
       // register budget of the 576-thread build with 256 converter threads)
-      constexpr int CW = NCONV > 128 ? 8 : 16;
+      constexpr int CW = NCONV > 256 ? 4 : NCONV > 128 ? 8 : 16;
 #pragma unroll 1
       for (int ch = chalf * (BN / 2 / CW); ch < (chalf + 1) * (BN / 2 / CW); ++ch) {
         int acc[NACC][CW];
