@@ -118,38 +118,37 @@ struct EpiBwdShared {
     const int P1 = 1 + npass;
     const double* __restrict__ fc = fcache;
     double* __restrict__ y = Y;
-    // four elements per thread per round: every cache load of the round is issued before any store
-    // (the compiler cannot reorder the loads past stores to Y on its own)
-    constexpr int U = 4;
+    // U elements per thread per round: every cache load of the round is issued before any store
+    // (the compiler cannot reorder the loads past stores to Y on its own); only the two global
+    // loads per element are held across the round, the tile values are read from Cs afterwards
+    constexpr int U = 8;
     const int total = t.bm * t.bn;
     for (int i0 = tid; i0 < total; i0 += U * nt) {
-      double f0[U], f1[U], cv[U], dv[U];
-      int cc[U], mm[U], ss[U];
-      bool ok[U];
+      double f0[U], f1[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i = i0 + u * nt;
         const int cl = i / t.bm, ml = i % t.bm;
         const int c = t.c0 + cl, m = t.m0 + ml;
-        ok[u] = i < total && m < g.M && c < g.C;   // warp-uniform when bm % 32 == 0 and M % 32 == 0
-        const int sim = ok[u] ? c / P1 : 0, sv = ok[u] ? c % P1 : 0;
-        cc[u] = c;
-        mm[u] = m;
-        ss[u] = sv;
+        const bool ok = i < total && m < g.M && c < g.C;
+        const int sim = ok ? c / P1 : 0, sv = ok ? c % P1 : 0;
         const double* F = fc + (size_t)sim * 2 * npass * ldy;
-        f0[u] = ok[u] ? F[m] : 0.0;
-        f1[u] = (ok[u] && sv > 0) ? F[(size_t)(2 * (sv - 1) + 1) * ldy + m] : 0.0;
-        dv[u] = ok[u] ? t.Cs[(cl - sv) * t.ldc + ml] : 0.0;
-        cv[u] = ok[u] ? t.Cs[cl * t.ldc + ml] : 0.0;
+        f0[u] = ok ? F[m] : 0.0;
+        f1[u] = (ok && sv > 0) ? F[(size_t)(2 * (sv - 1) + 1) * ldy + m] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (!ok[u]) continue;
-        const double v = ss[u] == 0 ? dv[u] * f0[u] : fma(cv[u], f0[u], dv[u] * f1[u]);
-        y[(size_t)cc[u] * ldy + mm[u]] = v;
+        const int i = i0 + u * nt;
+        const int cl = i / t.bm, ml = i % t.bm;
+        const int c = t.c0 + cl, m = t.m0 + ml;
+        if (!(i < total && m < g.M && c < g.C)) continue;   // warp-uniform (bm, M multiples of 32)
+        const int sv = c % P1;
+        const double dv = t.Cs[(cl - sv) * t.ldc + ml];
+        const double v = sv == 0 ? dv * f0[u] : fma(t.Cs[cl * t.ldc + ml], f0[u], dv * f1[u]);
+        y[(size_t)c * ldy + m] = v;
         if (colhw) {
           const unsigned r = __reduce_max_sync(0xffffffffu, (unsigned)__double2hiint(fabs(v)));
-          if ((tid & 31) == 0) colhw[(size_t)cc[u] * (g.M >> 5) + (mm[u] >> 5)] = r;
+          if ((tid & 31) == 0) colhw[(size_t)c * (g.M >> 5) + (m >> 5)] = r;
         }
       }
     }
