@@ -43,7 +43,10 @@ constexpr int BM = 128, BK = 32;
 constexpr int A_SLICE = BM * BK;             // bytes per slice plane of a stage
 constexpr int A_STAGE = S * A_SLICE;         // 28 KB
 constexpr int LDC = BM + 2;
-constexpr int NEPI = 256;       // epilogue threads (warps 2 .. 9: two warps per TMEM lane quarter)
+#ifndef OZ_NEPI
+#define OZ_NEPI 256
+#endif
+constexpr int NEPI = OZ_NEPI;   // epilogue threads (warps 2 ..: NEPI / 128 warps per TMEM lane quarter)
 #ifndef OZ_NCONV
 #define OZ_NCONV 256
 #endif
@@ -482,7 +485,9 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
     pdl_wait();
     const int q = warp & 3;              // TMEM lane quarter of this warp
     const int et = tid - EPI_W0 * 32;     // 0 .. NEPI-1
-    const int chalf = (warp - EPI_W0) >> 2;   // which half of the tile's columns this warp drains
+    // which slice of the tile's columns this warp drains (NEPI / 128 slices; lane quarter = warp % 4)
+    constexpr int NSL = NEPI / 128;
+    const int chalf = (warp - EPI_W0) >> 2;
     const int row_l = q * 32 + lane;      // tile row = TMEM lane
     int j = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
@@ -507,9 +512,9 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       named_bar_sync(1, NEPI);  // the previous tile's epilogue is done with Cs
       // CW columns per TMEM load (x16 with 128 converter threads; x8 keeps the epilogue within the
       // register budget of the 576-thread build with 256 converter threads)
-      constexpr int CW = NCONV > 256 ? 4 : NCONV > 128 ? 8 : 16;
+      constexpr int CW = (NCONV > 256 || NEPI > 256) ? 4 : NCONV > 128 ? 8 : 16;
 #pragma unroll 1
-      for (int ch = chalf * (BN / 2 / CW); ch < (chalf + 1) * (BN / 2 / CW); ++ch) {
+      for (int ch = chalf * (BN / NSL / CW); ch < (chalf + 1) * (BN / NSL / CW); ++ch) {
         int acc[NACC][CW];
 #pragma unroll
         for (int d = 0; d < NACC; ++d) {
