@@ -239,12 +239,24 @@ def decoder_roofline(P, stage_ms, n_sims, tc, tc_info=(0, 0, 0)):
         ocs = (64 // P1) * P1
         i8 = [n_hid * 28 * 2.0 * w * w * up(n_sims * G * gps, 64),
               n_out * 28 * 2.0 * up(N, 128) * w * up(n_sims * (2 + 2 * n_q), 64),
-              n_bwd * 28 * 2.0 * w * w * (-(-(n_sims * P1) // ocs) * 64)]
-        # fp64 flops of the stages' remaining DMMA GEMMs: the seed layer (K = n_q), the vhp seed
-        # (P W_L)^T a and the last backward layer (M = n_q)
-        dm = [2.0 * G * gps * n_sims * w * n_q,
-              0.0 if n_out else 2.0 * (2 + 2 * n_q) * n_sims * N * w,
-              2.0 * n_sims * N * w + 2.0 * n_sims * P1 * w * n_q]
+              n_bwd * 28 * 2.0 * w * w * (-(-(n_sims * P1) // ocs) * 64) if ocs else 0.0]
+        # fp64 flops of the stages' remaining DMMA GEMMs: each stage's executed flops minus the
+        # GEMMs on tcgen05 (the seed layer K = n_q, the vhp seed (P W_L)^T a and the last backward
+        # layer M = n_q always stay on DMMA)
+        L = c.n_fc
+        hidden_mac = n_q * w + (L - 2) * w * w
+        batched = n_sims * (4 + 4 * n_q) >= 2048
+        bwd_cols = (1 + n_q) if n_bwd else None
+        if bwd_cols is None:
+            ctas2 = -(-(n_sims * 2 * n_q) // 128) * -(-w // 64)
+            bwd_cols = (1 + n_q) if (batched and ctas2 >= 4 * 148) else 2 * n_q
+        ex_stage = [2.0 * G * gps * n_sims * hidden_mac,
+                    2.0 * (2 + 2 * n_q) * n_sims * N * w,
+                    2.0 * n_sims * N * w + 2.0 * bwd_cols * n_sims * hidden_mac]
+        tc_f64 = [2.0 * G * gps * n_sims * w * w * n_hid,
+                  ex_stage[1] if n_out else 0.0,
+                  2.0 * (1 + n_q) * n_sims * w * w * n_bwd]
+        dm = [max(0.0, e - t) for e, t in zip(ex_stage, tc_f64)]
         stages = []
         for k, name in enumerate(("hidden_jet", "output_gemm", "vhp_bwd")):
             t = stage_ms[k] * 1e-3

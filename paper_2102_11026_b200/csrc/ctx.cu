@@ -228,13 +228,19 @@ size_t lu_smem(int n);
 int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL, (n + bs - 1) / bs)); }
 
 // ---------------------------------------------------------------- GEMM dispatch
+// tcgen05 Ozaki GEMMs only with >= 3 waves of 128 x 64 tiles over the SMs: the persistent kernel
+// balances poorly on fewer (cfg3 at 256 sims, n_q = 5: 192 tiles, 71.5k vs 77.5k sim-iterations/s
+// on the DMMA kernels)
+inline bool oz_enough_tiles(int M, int C, int cstep = 64) {
+  return (long long)ceil_div(M, 128) * ceil_div(C, cstep) >= 3LL * 148;
+}
 template <class Epi>
 void hid_gemm(int G, const GemmArgs& g, const Epi& e, cudaStream_t st, bool big = false, bool cp_async = false,
               const OzakiWeights* oz = nullptr, OzakiBExp be = OzakiBExp{nullptr, 0}) {
   // big-tile hidden layers on the 5th-gen tensor cores: Ozaki-scheme fp64 on tcgen05.mma kind::i8
   // (ozaki_tc.cuh; 1.75x the DMMA kernel at the cfg5 shape, ~1e-16 of sum |w||x|)
   if (big && oz && oz->ready && 64 % G == 0 && g.M % oz::BM == 0 && g.K % oz::BK == 0 && g.ldb % 2 == 0 &&
-      !g.cstep) {
+      !g.cstep && oz_enough_tiles(g.M, g.C)) {
     launch_ozaki<64>(oz->view(), be, g, e, st);
     ++gemm_launch_count;
     return;
@@ -403,8 +409,11 @@ using CfgOutWs64c = WsCfg<16, 64, 2, 2, 6>;
 
 // the output layer on tcgen05: the compact last hidden layer writes its column scales for it
 bool out_on_tc(nlrom_ctx* c) {
+  // (>= 8192 columns: below that the persistent 1-CTA/SM kernel costs the step more than it saves
+  // in the GEMM -- it cannot share SMs with the side-branch kernels: cfg3 at 256 sims, n_q = 5,
+  // 3072 columns, 71k vs 78k sim-iterations/s; n_q = 30, 15872 columns, 46k vs 43k)
   return c->batched && c->ozWL.ready && c->ozHW[0] && c->wL1 % 32 == 0 && c->ldlast % 2 == 0 && !c->next &&
-         c->Cc % 2 == 0;
+         c->Cc % 2 == 0 && oz_enough_tiles(c->N, c->n_sims * c->Cc) && c->n_sims * c->Cc >= 8192;
 }
 
 void output_layer(nlrom_ctx* c) {
@@ -510,7 +519,7 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
     // tcgen05 Ozaki layers read their input's column scales from the previous layer's epilogue
     const bool oz_here = c->batched && l < (int)c->ozW.size() && c->ozW[l].ready;
     const bool oz_next = (c->batched && l + 1 < (int)c->ozW.size() && c->ozW[l + 1].ready && !compact &&
-                          c->widths[l + 1] % 32 == 0 && c->ozHW[0]) ||
+                          c->widths[l + 1] % 32 == 0 && c->ozHW[0] && oz_enough_tiles(c->widths[l + 2], ncols)) ||
                          (compact && out_on_tc(c));
     if (oz_next) e.colhw = c->ozHW[l & 1];
     const OzakiBExp be = (oz_here && l >= 1 && c->ozHW[0]) ? OzakiBExp{c->ozHW[(l - 1) & 1], c->widths[l] / 32}
@@ -797,6 +806,15 @@ void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true, bool 
 
 // vhp backward: dual (NS = 2) passes, cache written by the bundle forward.
 // dcache: the caches hold sin'(z) as duals (the fused bundle's forward), not z.
+// the batched vhp backward with the real part shared across a sim's passes (EpiBwdShared): only
+// when the GEMMs are throughput-bound (>= 4 waves of CTAs in the 2 npass layout): with few CTAs
+// (cfg4: 25 per layer) fewer, longer tiles are slower (0.92 vs 0.85 ms)
+bool shared_real_bwd(nlrom_ctx* c, int npass_per_sim) {
+  const long long ctas2 = (long long)ceil_div(c->n_sims * 2 * npass_per_sim, CfgBig::BN) * ceil_div(c->wL1, CfgBig::BM);
+  return c->batched && 1 + npass_per_sim <= CfgBig::BN && (ctas2 >= 4 * 148 || c->opt.shared_real) &&
+         !c->opt.no_shared_real;
+}
+
 void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int npass_per_sim, std::vector<DBuf>& caches,
                       std::vector<int>& ldcs, DBuf& D0, DBuf& D1, DBuf& Gout, int ldG, bool dcache = false) {
   const int ncols = c->n_sims * npass_per_sim * NS;
@@ -833,11 +851,7 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
   const int l_top = c->L - 2;
   dim3 gd(ceil_div(c->wL1, 32), c->n_sims);
   const int P1 = 1 + npass_per_sim;
-  // shared real part only when the GEMMs are throughput-bound (>= 4 waves of CTAs in the 2 npass
-  // layout): with few CTAs (cfg4: 25 per layer) fewer, longer tiles are slower (0.92 vs 0.85 ms)
-  const long long ctas2 = (long long)ceil_div(c->n_sims * 2 * npass_per_sim, CfgBig::BN) * ceil_div(c->wL1, CfgBig::BM);
-  if (NS == 2 && !mc && dcache && c->batched && P1 <= CfgBig::BN &&
-      (ctas2 >= 4 * 148 || c->opt.shared_real) && !c->opt.no_shared_real) {
+  if (NS == 2 && !mc && dcache && shared_real_bwd(c, npass_per_sim)) {
     // shared real part (EpiBwdShared): 1 + npass columns per sim instead of 2 npass, tiles of
     // whole sims
     const int cstep = (CfgBig::BN / P1) * P1, ncs = c->n_sims * P1;
@@ -850,7 +864,7 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
     const int ocs = (64 / P1) * P1;
     auto oz_bwd = [&](int l) {
       return l >= 1 && l < (int)c->ozWT.size() && c->ozWT[l].ready && ocs >= P1 && ldcs[l] % 2 == 0 &&
-             c->ozBHW[0] != nullptr;
+             c->ozBHW[0] != nullptr && oz_enough_tiles(c->widths[l], ncs, ocs);
     };
     for (int l = c->L - 2; l >= 1; --l) {
       if (oz_bwd(l)) {
@@ -2081,9 +2095,14 @@ extern "C" int nlrom_launches_per_iteration(nlrom_ctx* c) { return c ? c->launch
 extern "C" int nlrom_tc_info(nlrom_ctx* c, int* out) {
   if (!c || !out) return NLROM_ERR_ARG;
   out[0] = out[1] = out[2] = 0;
-  for (auto& w : c->ozW) out[0] += w.ready ? 1 : 0;
+  for (int l = 0; l < (int)c->ozW.size(); ++l)
+    out[0] += (c->ozW[l].ready && oz_enough_tiles(c->widths[l + 1], c->n_sims * c->Cb)) ? 1 : 0;
   out[1] = out_on_tc(c) ? 1 : 0;
-  for (auto& w : c->ozWT) out[2] += w.ready ? 1 : 0;
+  // backward layers on tcgen05: the shared-real path with whole sims in a 64-column tile
+  const int P1 = 1 + c->n_q, ocs = (64 / P1) * P1;
+  if (shared_real_bwd(c, c->n_q) && ocs >= P1)
+    for (int l = 0; l < (int)c->ozWT.size(); ++l)
+      out[2] += (c->ozWT[l].ready && oz_enough_tiles(c->widths[l], c->n_sims * P1, ocs)) ? 1 : 0;
   return NLROM_OK;
 }
 extern "C" int nlrom_tc_layers(nlrom_ctx* c) {
