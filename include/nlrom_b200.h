@@ -185,7 +185,9 @@ NLROM_API int nlrom_element_reduced_forces(nlrom_ctx* ctx, const double* r, cons
 NLROM_API int nlrom_full_displacement(nlrom_ctx* ctx, const double* r, double* u);
 NLROM_API int nlrom_jtilde(nlrom_ctx* ctx, const double* q, double* Jt);
 
-/* rdsim.step: host state in / out */
+/* rdsim.step: host state in / out. In fixed-iteration mode (cfg->fixed_iters
+ * > 0) info may be NULL: the final residual of the last iterate (info->res_norm) is then not
+ * evaluated (one residual evaluation less per call); the pivot status is always checked. */
 NLROM_API int nlrom_step(nlrom_ctx* ctx, const double* r_bar, const double* rdot_bar, const double* f_ext,
                const nlrom_simcfg* cfg, double* r_out, double* rdot_out, nlrom_step_info* info);
 

@@ -1802,7 +1802,8 @@ extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar,
     int* hs = reinterpret_cast<int*>(ho + 2 * nn + 2);
     ensure_graphs(c, *cfg);
     char kb[96];
-    snprintf(kb, sizeof kb, "|%d|%p|%p", cfg->fixed_iters, (void*)hi, (void*)ho);
+    const bool want_norm = info != nullptr;   // the final residual only when the caller reads it
+    snprintf(kb, sizeof kb, "|%d|%p|%p|%d", cfg->fixed_iters, (void*)hi, (void*)ho, (int)want_norm);
     const std::string key = c->graph_key + kb;
     if (!c->gStep || c->step_key != key) {
       // the whole step as ONE graph: pinned H2D, predictor, the Newton iterations, the final
@@ -1818,12 +1819,12 @@ extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar,
           phase_E(c, *cfg, false);
           phase_J(c, *cfg, true, nullptr, 0, nullptr, true);
         }
-        phase_E(c, *cfg, true, /*resid_only=*/true);   // ||phi|| of the final iterate
+        if (want_norm) phase_E(c, *cfg, true, /*resid_only=*/true);   // ||phi|| of the final iterate
         launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p,
                1.0 / cfg->dt, nn);
         NL_CUDA(cudaMemcpyAsync(ho, c->r.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
         NL_CUDA(cudaMemcpyAsync(ho + nn, c->rdot.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
-        NL_CUDA(cudaMemcpyAsync(ho + 2 * nn, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
+        if (want_norm) NL_CUDA(cudaMemcpyAsync(ho + 2 * nn, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
         NL_CUDA(cudaMemcpyAsync(hs, c->status.p, c->n_sims * sizeof(int), cudaMemcpyDeviceToHost, c->st));
       }, nullptr);
       c->step_key = key;

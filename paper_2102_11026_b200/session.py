@@ -193,16 +193,21 @@ class Session:
                                                 _lib.dptr(rd), _lib.dptr(fe), C.byref(c), _lib.dptr(out)))
         return out[0] if self.n_sims == 1 else out
 
-    def step(self, r_bar, rdot_bar, f_ext, cfg):
+    def step(self, r_bar, rdot_bar, f_ext, cfg, want_norm=True):
+        """One timestep of every sim: (r, rdot, iterations, ||phi||). With fixed iterations and
+        want_norm=False the final residual is not evaluated and ||phi|| is returned as None."""
         rb, rd, fe = self._state(r_bar, rdot_bar, f_ext)
         r = np.empty(self.n_sims * self.n)
         rdot = np.empty(self.n_sims * self.n)
         info = _lib.StepInfo()
         c = _simcfg(cfg)
+        skip = (not want_norm) and c.fixed_iters > 0
         # raw addresses (c_void_p arguments): the per-call ctypes pointer objects are the largest
         # host cost of a step call after the device work
         self._chk(self._L.nlrom_step(self._h, rb.ctypes.data, rd.ctypes.data, fe.ctypes.data, C.byref(c),
-                                     r.ctypes.data, rdot.ctypes.data, C.byref(info)))
+                                     r.ctypes.data, rdot.ctypes.data, None if skip else C.byref(info)))
+        if skip:
+            return r, rdot, c.fixed_iters, None
         return r, rdot, info.iters, info.res_norm
 
     def step_device(self, r_bar, rdot_bar, f_ext, cfg, r_out, rdot_out, stream_ptr):

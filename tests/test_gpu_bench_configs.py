@@ -43,6 +43,23 @@ def test_cfg2_ten_steps_three_iterations(cfg2):
     assert worst <= 1e-10, worst
 
 
+def test_cfg2_step_norm_optional(cfg2):
+    """rdsim.step evaluates the final residual of a fixed-iteration step only when it returns it
+    (return_info): the state is bitwise the same either way, and the returned norm is the
+    oracle's ||phi|| at the final iterate."""
+    from paper_2102_11026_b200 import rdsim
+    P, S = cfg2
+    cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=3)
+    st = P.rest_state()
+    a = rdsim.step(P.rm, P.model, st, P.f_ext, cfg)
+    b, (iters, nrm) = rdsim.step(P.rm, P.model, st, P.f_ext, cfg, return_info=True)
+    assert iters == 3
+    assert np.array_equal(a.r, b.r) and np.array_equal(a.rdot, b.rdot)
+    ro, _, _, nrm_o = ors.step(S, st.r.copy(), st.rdot.copy(), P.f_ext, ocfg(cfg))
+    assert rel(b.r, ro) <= 1e-10
+    assert abs(nrm - nrm_o) <= 1e-8 * max(nrm_o, 1e-300) + 1e-12
+
+
 def test_cfg2_timed_graph(cfg2):
     from paper_2102_11026_b200 import rdsim
     from paper_2102_11026_b200.session import session_for
