@@ -14,16 +14,25 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(io.StringIO(out)))
 i = [k for k, r in enumerate(rows) if r and r[0] == "Address"][0]
 hdr = rows[i]
-data = [r for r in rows[i + 1:] if len(r) == len(hdr)]
+data = [r for r in rows[i + 1:] if len(r) == len(hdr) and r[0].startswith("0x")]
+
+
+def num(x):
+    try:
+        return int(float(x or 0))
+    except ValueError:
+        return 0
+
+
 sc = [k for k, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 tot = collections.Counter()
 for r in data:
     for k in sc:
-        tot[hdr[k]] += int(r[k] or 0)
+        tot[hdr[k]] += num(r[k])
 allc = sum(tot.values()) or 1
 print("stall totals:", ", ".join(f"{k[6:]} {100 * v / allc:.1f}%" for k, v in tot.most_common(8)))
 si = hdr.index("Warp Stall Sampling (All Samples)")
-data.sort(key=lambda r: -int(r[si] or 0))
+data.sort(key=lambda r: -num(r[si]))
 for r in data[:top]:
-    reasons = sorted(((int(r[k] or 0), hdr[k][6:]) for k in sc), reverse=True)[:3]
-    print(f"{int(r[si]):6d} {r[1][:60]:60s} " + " ".join(f"{n}:{v}" for v, n in reasons if v))
+    reasons = sorted(((num(r[k]), hdr[k][6:]) for k in sc), reverse=True)[:3]
+    print(f"{num(r[si]):6d} {r[1][:60]:60s} " + " ".join(f"{n}:{v}" for v, n in reasons if v))
