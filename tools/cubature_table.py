@@ -67,6 +67,10 @@ def main():
             row[f"neural_K{K}_test_error"] = ct.cubature_error(te, cm.C, W)
             row[f"neural_K{K}_train_error"] = ct.cubature_error(ts, cm.C, Wtr)
             row[f"neural_K{K}_s"] = tn
+            # diagnostic: the neural set with fixed NNLS weights (set quality vs weight-net quality)
+            A, b = ct._stacked(ts)
+            wn, _ = ct.nnls(A[np.asarray(cm.C)].T, b)
+            row[f"neural_K{K}_set_nnls_test_error"] = ct.cubature_error(te, cm.C, wn)
         rows.append(row)
         print(json.dumps(row), flush=True)
     print(json.dumps({"cfg": args.cfg, "train_poses": args.train, "test_poses": args.test,
