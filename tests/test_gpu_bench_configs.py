@@ -81,12 +81,14 @@ def test_cfg2_timed_graph(cfg2):
         assert abs(nrm[0] - np.linalg.norm(phio)) <= 1e-10 * np.linalg.norm(phio)
 
 
-def test_cfg5_full_scale_sampled_sims(cuda_ok):
+@pytest.mark.parametrize("total", [4096, 1000])
+def test_cfg5_full_scale_sampled_sims(cuda_ok, total):
+    """4096 sims: the benchmarked configuration; 1000 sims: ragged tcgen05 column tiles (the output
+    layer's 42000 and the backward's 21000 columns are not multiples of their 64 / 63-column tiles)."""
     from paper_2102_11026_b200.problem import build_problem
     from paper_2102_11026_b200 import rdsim
     from paper_2102_11026_b200.shard import SimShard
     P = build_problem("cfg5")
-    total = 4096
     n = P.cfg.n_p + P.cfg.n_q
     rng = np.random.default_rng(4)
     rb = rng.uniform(-0.05, 0.05, (total, n))
@@ -94,6 +96,7 @@ def test_cfg5_full_scale_sampled_sims(cuda_ok):
     scale = rng.uniform(0.5, 1.5, total)
     fe = scale[:, None] * P.f_ext[None, :]
     sh = SimShard(P.rm, P.model, P.cm, total, rank=0, world=1)
+    assert sh.session.tc_info() == (8, 1, 8)   # hidden, output and backward GEMMs on tcgen05
     cfg = rdsim.SimConfig(dt=P.cfg.dt, fixed_iters=2)
     r, rd, _ = sh.step(rb, rdb, fe, cfg)
     S = oracle_sim(P)
