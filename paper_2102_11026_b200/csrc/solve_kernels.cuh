@@ -579,7 +579,10 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
   constexpr int D = 16 * NB;
   constexpr int LDF = D + 1;
   constexpr int R = D / 32;            // rows per lane (PW: panel width)
-  constexpr int NU = 7;                // trailing-update warps
+#ifndef LU_SOLO
+#define LU_SOLO 0   // 1: warp 4 idles so the pivot-chain warp has its scheduler (SMSP 0) to itself
+#endif
+  constexpr int NU = LU_SOLO ? 6 : 7;  // trailing-update warps
   extern __shared__ double M[];        // [D][LDF] | vhp block [n_q][n_q] | Mul [2][D][PW]
   __shared__ int pivrow[D];
   __shared__ double rdiag[D];
@@ -807,13 +810,13 @@ __global__ void __launch_bounds__(256) k_lu_lookahead(const double* __restrict__
         }
       }
     }
-  } else {
+  } else if (!(LU_SOLO && warp == 4)) {
     // ------------------------------------------------------------------ trailing-update warps
     // work unit = (32-column group, 16-row block), lanes = columns; unit u belongs to warp 1 + u % 7
     // for the whole factorisation. Per panel: every unit's u-chain from the pivot rows (read by all
     // units before any unit writes: named barrier), then its rows.
     constexpr int RB = LU_RB, NRB = D / RB;
-    const int uw = warp - 1, ut = tid - 32;
+    const int uw = (LU_SOLO && warp > 4) ? warp - 2 : warp - 1, ut = tid - 32;
     const int ngrp = (ncol + 31) / 32;
     for (int P = 0; P < npan; ++P) {
 #ifdef LU_TRACE
