@@ -683,6 +683,9 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
 // join_side = false leaves the phi / S_base branch open for phase_J (one-graph Newton iteration)
 // Early weight net: the net's layer 1 is folded onto the hidden chain's output (k_wnet_head), so
 // head + tail run on a side branch concurrently with the output layer instead of after it.
+// CTAs per sim of k_wnet_head: 8 output rows each (32 threads per row)
+int wnet_head_split(nlrom_ctx* c) { return c->wn % 8 == 0 && c->wn >= 8 ? c->wn / 8 : 1; }
+
 bool early_wnet_ok(nlrom_ctx* c) {
   return c->wA1.p && !c->batched && c->wn >= 16 && c->wn % 2 == 0 && 256 % c->wn == 0 &&
          c->wL1 + c->n_p + 1 <= 1024 && c->n_cub > 0 && wnet_head_smem(c->wn, c->wA1ld) <= 220 * 1024;
@@ -705,7 +708,8 @@ void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s, bool resid_
   NL_CUDA(cudaEventRecord(c->evWf, c->st));
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evWf, 0));
   on(c->st2, [&] {
-    launch(c, k_wnet_head, c->n_sims, 256, wnet_head_smem(c->wn, c->wA1ld), (const double*)c->H[c->L - 2].p,
+    launch(c, k_wnet_head, dim3(wnet_head_split(c), c->n_sims), 256,
+           wnet_head_smem(c->wn / wnet_head_split(c), c->wA1ld), (const double*)c->H[c->L - 2].p,
            c->ldH[c->L - 2], c->Cc, (const double*)c->r.p, c->n, c->n_p, c->wL1, (const double*)c->wA1.p, c->wA1ld,
            c->wn, c->wpart.p);
     const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + c->wn) * 8;
@@ -779,7 +783,8 @@ void phase_E(nlrom_ctx* c, const nlrom_simcfg& cfg, bool join_side = true, bool 
     NL_CUDA(cudaEventRecord(c->evWf, c->st));
     NL_CUDA(cudaStreamWaitEvent(c->st2, c->evWf, 0));
     std::swap(c->st, c->st2);
-    launch(c, k_wnet_head, c->n_sims, 256, wnet_head_smem(c->wn, c->wA1ld), (const double*)c->H[c->L - 2].p, c->ldH[c->L - 2], c->Cc,
+    launch(c, k_wnet_head, dim3(wnet_head_split(c), c->n_sims), 256, wnet_head_smem(c->wn / wnet_head_split(c), c->wA1ld),
+           (const double*)c->H[c->L - 2].p, c->ldH[c->L - 2], c->Cc,
            (const double*)c->r.p, c->n, c->n_p, c->wL1, (const double*)c->wA1.p, c->wA1ld, c->wn, c->wpart.p);
     const size_t wsm = (size_t)(5 * c->wn + 64 + 2 * c->wn * c->wn + 64 * c->wn + c->wn) * 8;
     launch(c, k_wnet_tail2, dim3(std::max(1, ceil_div(c->n_cub, 64)), c->n_sims), 256, wsm + 16,

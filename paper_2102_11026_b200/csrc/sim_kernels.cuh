@@ -278,24 +278,28 @@ __device__ __forceinline__ double wnet_row_tpr(const double* __restrict__ W, int
 // output layer executes; k_wnet_tail2 (n_split = 1) adds b1 and finishes the net. The folded
 // matrix (wn x ldF, constant) lands in shared memory by one TMA bulk copy issued BEFORE the
 // dependency wait, i.e. while the hidden chain still runs.
-inline size_t wnet_head_smem(int wn, int ldF) { return (size_t)wn * ldF * 8 + 1024 * 8 + 16; }
+inline size_t wnet_head_smem(int rows, int ldF) { return (size_t)rows * ldF * 8 + 1024 * 8 + 16; }
 
+// grid (wn / rows per CTA, n_sims): each CTA lands only its rows of F by TMA (8 rows = 18 KB at
+// cfg2 instead of all 64 = 147 KB in one CTA: the single bulk copy was the kernel's latency)
 __global__ void __launch_bounds__(256) k_wnet_head(const double* __restrict__ H, int ldH, int cs,
                                                    const double* __restrict__ r, int n, int n_p, int w,
                                                    const double* __restrict__ F, int ldF, int wn,
                                                    double* __restrict__ part) {
   extern __shared__ __align__(16) double hs[];
-  double* Fs = hs;                   // [wn][ldF]
-  double* x = Fs + (size_t)wn * ldF;  // [<= 1024]
+  const int rpc = wn / gridDim.x;     // rows of this CTA (divides wn; 256 / rpc a power of two <= 32)
+  const int r0 = blockIdx.x * rpc;
+  double* Fs = hs;                    // [rpc][ldF]
+  double* x = Fs + (size_t)rpc * ldF;  // [<= 1024]
   uint64_t* bar = reinterpret_cast<uint64_t*>(x + 1024);
-  const int sim = blockIdx.x, tid = threadIdx.x;
+  const int sim = blockIdx.y, tid = threadIdx.x;
   const int K = w + n_p + 1;
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    const uint32_t bytes = (uint32_t)(wn * ldF * 8);
+    const uint32_t bytes = (uint32_t)(rpc * ldF * 8);
     mbar_expect_tx(bar, bytes);
-    tma_g2s(Fs, F, bytes, bar);
+    tma_g2s(Fs, F + (size_t)r0 * ldF, bytes, bar);
   }
   pdl_wait();
   pdl_launch();
@@ -303,10 +307,10 @@ __global__ void __launch_bounds__(256) k_wnet_head(const double* __restrict__ H,
     x[k] = k < w ? H[(size_t)sim * cs * ldH + k] : (k < w + n_p ? r[(size_t)sim * n + (k - w)] : 1.0);
   __syncthreads();
   mbar_wait(bar, 0);
-  const int tpr = blockDim.x / wn;  // threads per output row (wn divides 256)
+  const int tpr = blockDim.x / rpc;  // threads per output row
   const int m = tid / tpr, q = tid % tpr;
   double a0 = 0.0, a1 = 0.0;
-  if (m < wn) {
+  if (m < rpc) {
     const double* Fm = Fs + (size_t)m * ldF;
     int k = q;
     for (; k + tpr < K; k += 2 * tpr) {
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(256) k_wnet_head(const double* __restrict__ H,
   }
   double acc = a0 + a1;
   for (int o = tpr >> 1; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (m < wn && q == 0) part[(size_t)sim * wn + m] = acc;
+  if (m < rpc && q == 0) part[(size_t)sim * wn + r0 + m] = acc;
 }
 
 __global__ void __launch_bounds__(256) k_wnet_tail2(const double* __restrict__ part, int n_split, int wn,
