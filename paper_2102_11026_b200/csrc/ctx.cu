@@ -224,7 +224,6 @@ void launch(nlrom_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_
   ++gemm_launch_count;
 }
 
-size_t lu_smem(int n);
 int grid1(long long n, int bs = 256) { return (int)std::max(1LL, std::min(2048LL, (n + bs - 1) / bs)); }
 
 // ---------------------------------------------------------------- GEMM dispatch
@@ -1060,11 +1059,6 @@ void full_S(nlrom_ctx* c, const nlrom_simcfg& cfg) {
   const int n = c->n;
   launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
          (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
-}
-
-size_t lu_smem(int n) {
-  const int ld = ((n + 1) & 1) ? (n + 1) : (n + 2);
-  return (size_t)n * ld * 8 + (size_t)n * 4 + 16;
 }
 
 std::string cfg_key(const nlrom_simcfg& cfg) {

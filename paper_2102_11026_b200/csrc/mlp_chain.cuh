@@ -228,11 +228,9 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
       if (last) {
         // compact layout for the linear output layer: base once per sim, tangents by index
         if (unit == 0 && gl == 0) {
-#pragma unroll
           a.Hout[(size_t)(sim * cs) * a.ldH + m] = o[0];            // value slot
           a.Hout[(size_t)(sim * cs + 1) * a.ldH + m] = 2.0 * o[2];  // 2 h_ss -> hvv
         } else if (unit > 0 && kg < a.n_q) {
-#pragma unroll
           a.Hout[(size_t)(sim * cs + 2 + 2 * kg) * a.ldH + m] = o[0];                     // h_t -> J
           a.Hout[(size_t)(sim * cs + 3 + 2 * kg) * a.ldH + m] = fma(2.0, o[2], o[3]);  // 2 h_tss + h_tr -> dJ
         }
