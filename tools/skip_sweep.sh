@@ -1,8 +1,13 @@
 #!/bin/bash
-# Critical-path experiment: bench value with groups of kernels dropped from the graph
-# (NLROM_DEBUG_SKIP; needs a library built with -DNLROM_TIMING_EXPERIMENTS, results are wrong,
-# timing shows what the iteration waits on; bench.py refuses to run with it set).
-for s in "" "k_assemble_mass,k_reduce_phi,k_reduce_S" "k_wnet" "k_cubature" "k_lu_solve" "k_mlp_dual_bwd" "gemm_ws" "k_mlp_jet_fwd" "k_assemble_a,k_gemv_t2"; do
-  v=$(NLROM_DEBUG_SKIP="$s" timeout 300 python bench.py --steps 200 --no-batched --no-coupled --no-fullspace --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; print('%.4f' % json.loads(sys.stdin.read())['value'])" 2>/dev/null)
-  echo "skip=[$s] ms=$v"
+# Critical-path experiment: cfg2 ms per Newton iteration with kernels dropped from the graph
+# (NLROM_DEBUG_SKIP; results are wrong, the timing shows what the iteration waits on).
+# Needs a library built with -DNLROM_TIMING_EXPERIMENTS (never the release build):
+#   cd paper_2102_11026_b200/csrc && for f in net ctx fullspace; do nvcc -O3 -std=c++17 \
+#     --expt-relaxed-constexpr -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+#     -gencode arch=compute_100a,code=sm_100a -DNLROM_TIMING_EXPERIMENTS -c $f.cu -o /tmp/x/$f.o; done
+#   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static /tmp/x/*.o -o <lib>
+# then (on the GPU box): cp <lib> paper_2102_11026_b200/libnlrom_b200.so; bash tools/skip_sweep.sh
+for s in "" "gemm_ws" "k_wnet" "k_cubature" "k_assemble_a" "k_assemble_mass" "k_reduce_phi" "k_reduce_S" \
+         "k_mlp_dual_bwd" "k_lu_lookahead"; do
+  NLROM_DEBUG_SKIP="$s" timeout -s KILL 120 python tools/skip_sweep.py 2>&1 | tail -1
 done
