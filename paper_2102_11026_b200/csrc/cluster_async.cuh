@@ -94,6 +94,17 @@ __device__ __forceinline__ void named_bar_sync(int id, int cnt) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
 }
 
+// bulk copy from this CTA's shared memory into (possibly another) CTA of the cluster; completes
+// `bytes` transaction bytes on the destination's mbarrier (both shared::cluster addresses)
+__device__ __forceinline__ void bulk_s2s(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "r"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// every committed bulk copy of this thread has finished READING its source
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

@@ -23,6 +23,9 @@ namespace nlrom {
 constexpr int MLP_MAXL = 16;
 
 // Optional phase timestamps (tools/probes/chain_probe.cu): CTA (0,0) thread 0, per layer.
+#ifndef MLP_BULK
+#define MLP_BULK 1   // bulk shared-memory copies + per-buffer mbarriers instead of DSMEM stores + cluster.sync
+#endif
 #ifdef NLROM_CHAIN_TRACE
 __device__ long long g_chain_trace[MLP_MAXL][6];
 __device__ long long g_bwd_trace[MLP_MAXL + 1][6];
@@ -67,7 +70,7 @@ struct MlpPlan {
   static __host__ __device__ int kp(int kmax) { return (kmax + 15) & ~15; }
   static __host__ __device__ int ldws(int kmax) { return kp(kmax) + 4; }
   static __host__ __device__ size_t bytes(int kmax) {
-    return (size_t)(2 * kp(kmax) * LDX + 2 * R * ldws(kmax) + 2 * R + G * (R + 1) + R * LDX) * 8 + 16;
+    return (size_t)(2 * kp(kmax) * LDX + 2 * R * ldws(kmax) + 2 * R + G * (R + 1) + R * LDX) * 8 + 32;
   }
 };
 
@@ -118,12 +121,27 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
     tma_g2s(Wbuf(l & 1), a.Wp[l] + (size_t)r0 * LDWS, (uint32_t)(R * LDWS * 8), bar);
     tma_g2s(Bbuf(l & 1), a.b[l] + r0, (uint32_t)(R * 8), bar);
   };
+  // activation hand-off (MLP_BULK): each CTA sends its R x LDX slice of layer l's output to every
+  // CTA of the cluster with ONE bulk shared-memory copy per destination, completing transaction
+  // bytes on the destination's per-buffer mbarrier xbar[(l + 1) & 1]; the next layer waits on its
+  // own barrier instead of a cluster-wide barrier. A buffer's next phase is armed (expect_tx) before
+  // this CTA sends the slice every peer needs to produce that phase's data, so no copy can complete
+  // on an unarmed phase; a peer writes buffer b only after it consumed our slice of the input held
+  // there two layers ago, i.e. after we finished reading b (no write-after-read race).
+  uint64_t* xbar = wbar + 2;
+  constexpr uint32_t SLICE = (uint32_t)(R * P::LDX * 8);
   if (tid == 0) {
     mbar_init(wbar, 1);
     mbar_init(wbar + 1, 1);
+    if (MLP_BULK) {
+      mbar_init(xbar, 1);
+      mbar_init(xbar + 1, 1);
+    }
     fence_mbar_init();
+    if (MLP_BULK && a.L1 >= 2) mbar_expect_tx(xbar + 1, CS * SLICE);   // input of layer 1
     issue_w(0);  // layer-0 weights do not depend on the producer: before the dependency wait
   }
+  if (MLP_BULK) cluster_sync_all();   // every CTA's barriers exist (and are armed) before anyone sends
   pdl_wait();
   pdl_launch();
   // seed of this group: X[0][i][c], i < n_q; rows n_q .. kmax of X[0] and rows w .. kmax of X[1]
@@ -155,6 +173,7 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
     if (l + 1 < a.L1 && tid == 0) issue_w(l + 1);  // buffer (l+1)&1 was last read by layer l-1
     CHAIN_MARK(l, 0);
     if (l == 0) __syncthreads();  // seed (barrier init) visible
+    if (MLP_BULK && l >= 1) mbar_wait(xbar + (l & 1), (uint32_t)(((l - 1) >> 1) & 1));   // input l complete
     mbar_wait(wbar + (l & 1), (l >> 1) & 1);  // this layer's weights have landed
     CHAIN_MARK(l, 1);
     // DMMA: warp -> 8x8 tiles of the R x G slice, 4 interleaved K chains; K padded to 16 with zeros
@@ -196,6 +215,7 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
         Ys[col * (R + 1) + row] = (c[0][e] + c[1][e]) + (c[2][e] + c[3][e]);
       }
     }
+    if (MLP_BULK && tid == 0) bulk_wait_read0();   // the previous layer's copies have read Os
     __syncthreads();
     CHAIN_MARK(l, 2);
     // jet-sin epilogue on the R rows; broadcast the activated slice to every CTA of the cluster
@@ -239,24 +259,43 @@ __global__ void __launch_bounds__(256) k_mlp_jet_fwd(MlpFwdArgs a) {
         for (int s = 0; s < 4; ++s) Os[rr * LDX + col + s] = o[s];
       }
     }
-    if (!last) {
-      // broadcast the R x G slice to every CTA of the cluster: warp -> destination CTA,
-      // 16-byte distributed-shared-memory stores of whole rows (stores straight from the epilogue,
-      // 2 x 16 B per task and destination, measured slower: the cluster barrier then waits on
-      // many more outstanding remote stores, 6.9k vs 6.0k cycles per layer)
-      __syncthreads();
+    if (!last && MLP_BULK) {
+      __syncthreads();   // Os complete
       CHAIN_MARK(l, 3);
-      constexpr int C2 = G / 2;  // 16-byte chunks per row
-      for (int dst = warp; dst < CS; dst += NTH / 32) {
-        double* Xr = cluster.map_shared_rank(Xn, dst);
-        for (int t = lane; t < R * C2; t += 32) {
-          const int rr = t / C2, c2 = (t % C2) * 2;
-          *reinterpret_cast<double2*>(Xr + (r0 + rr) * LDX + c2) = *reinterpret_cast<const double2*>(Os + rr * LDX + c2);
+      if (tid == 0) {
+        // arm the phase of buffer l & 1 that holds input l + 2 (input l's phase completed above)
+        if (l + 2 < a.L1) mbar_expect_tx(xbar + (l & 1), CS * SLICE);
+        fence_proxy_async();   // Os (generic stores) visible to the bulk copies
+        const uint32_t src = smem_u32(Os), dst0 = smem_u32(Xn + r0 * LDX), bar0 = smem_u32(xbar + ((l + 1) & 1));
+        for (int d = 0; d < CS; ++d) {
+          const int dst = (rank + d) % CS;   // staggered destinations
+          bulk_s2s(mapa(dst0, dst), src, SLICE, mapa(bar0, dst));
+        }
+        bulk_commit();
+      }
+      CHAIN_MARK(l, 4);
+      CHAIN_MARK(l, 5);
+    } else {
+      if (!last) {
+        // broadcast the R x G slice to every CTA of the cluster: warp -> destination CTA,
+        // 16-byte distributed-shared-memory stores of whole rows (stores straight from the
+        // epilogue, 2 x 16 B per task and destination, measured slower: the cluster barrier then
+        // waits on many more outstanding remote stores, 6.9k vs 6.0k cycles per layer)
+        __syncthreads();
+        CHAIN_MARK(l, 3);
+        constexpr int C2 = G / 2;  // 16-byte chunks per row
+        for (int dst = warp; dst < CS; dst += NTH / 32) {
+          double* Xr = cluster.map_shared_rank(Xn, dst);
+          for (int t = lane; t < R * C2; t += 32) {
+            const int rr = t / C2, c2 = (t % C2) * 2;
+            *reinterpret_cast<double2*>(Xr + (r0 + rr) * LDX + c2) = *reinterpret_cast<const double2*>(Os + rr * LDX + c2);
+          }
         }
       }
-    }    CHAIN_MARK(l, 4);
-    cluster.sync();  // next activation complete in every CTA; Xc, Ys and Os free for reuse
-    CHAIN_MARK(l, 5);
+      CHAIN_MARK(l, 4);
+      cluster.sync();  // next activation complete in every CTA; Xc, Ys and Os free for reuse
+      CHAIN_MARK(l, 5);
+    }
   }
 }
 
