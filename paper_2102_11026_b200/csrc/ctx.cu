@@ -23,6 +23,7 @@
 #include "coupled_kernels.cuh"
 #include "gemm_ws.cuh"
 #include "ozaki_tc.cuh"
+#include "ozaki_chain.cuh"
 #include "newton_kernels.cuh"
 
 namespace nlrom {
@@ -82,9 +83,12 @@ int gemm_launch_count = 0;
 //   dmma_bwd        batched shared-real vhp backward layers on the fp64 DMMA kernel instead of the
 //                   tcgen05 Ozaki GEMM
 //   dmma_out        batched output layer on the fp64 DMMA kernel instead of the tcgen05 Ozaki GEMM
+//   oz_fp64_chain   tcgen05 hidden layers hand their activations to the next one in fp64 (the
+//                   consumer converts) instead of as digit tiles (ozaki_chain.cuh)
 struct PathOpts {
   bool batched = false, unfused = false, hid_cp = false, bwd_cp = false, shared_real = false,
-       no_shared_real = false, dmma_hidden = false, cub_chunked = false, dmma_bwd = false, dmma_out = false;
+       no_shared_real = false, dmma_hidden = false, cub_chunked = false, dmma_bwd = false, dmma_out = false,
+       oz_fp64_chain = false;
   int cpc = 0, cpm = 0, tangents = 0;
   static PathOpts from_env() {
     PathOpts o;
@@ -109,6 +113,7 @@ struct PathOpts {
       else if (key == "cub_chunked") o.cub_chunked = true;
       else if (key == "dmma_bwd") o.dmma_bwd = true;
       else if (key == "dmma_out") o.dmma_out = true;
+      else if (key == "oz_fp64_chain") o.oz_fp64_chain = true;
       else if (key == "cpc") o.cpc = val;
       else if (key == "cpm") o.cpm = val;
       else if (key == "tangents") o.tangents = val;
@@ -144,6 +149,7 @@ struct nlrom_ctx {
   OzakiWeights ozWL;               // batched output layer: digit tiles of P W_L (N rows, zero-padded to 128)
   unsigned* ozBHW[2] = {nullptr, nullptr};  // ping-pong column-scale partials between backward layers
   unsigned* ozHW[2] = {nullptr, nullptr};  // ping-pong column-scale partials between hidden layers
+  int* ozDE[2] = {nullptr, nullptr};        // ping-pong column exponents of the digit chain (ozaki_chain.cuh)
   int ldpf = 0, ldpb = 0;
   DBuf Alast, AT, Pb, U, mass;
   int ldlast = 0, wL1 = 0, next = 0;
@@ -510,6 +516,19 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
          drop_fict);
   const double* in = c->X0.p;
   int ldin = c->ldq;
+  // hidden layer l runs on the tcgen05 Ozaki GEMM (the dispatch rule of hid_gemm)
+  auto oz_runs = [&](int l) {
+    if (!c->batched || l < 0 || l >= (int)c->ozW.size() || !c->ozW[l].ready) return false;
+    const int ldb = l == 0 ? c->ldq : c->ldH[l - 1];
+    return 64 % c->G == 0 && c->widths[l + 1] % oz::BM == 0 && c->widths[l] % oz::BK == 0 && ldb % 2 == 0 &&
+           oz_enough_tiles(c->widths[l + 1], ncols);
+  };
+  // digit chain: a tcgen05 layer of width 256 whose consumer is a tcgen05 hidden layer hands over
+  // digit tiles (ozaki_chain.cuh); its buffer H[l] holds them (7 of the 8 bytes per element)
+  auto dig_out = [&](int l) {
+    return !c->opt.oz_fp64_chain && c->ozDE[0] && 32 % c->G == 0 && l + 1 <= c->L - 2 && oz_runs(l) && oz_runs(l + 1) &&
+           c->widths[l + 1] == 256 && (size_t)round_up(ncols, 64) * 7 <= (size_t)ncols * c->ldH[l] * 8;
+  };
   for (int l = 0; l + 1 < c->L; ++l) {
     // the last hidden layer writes the de-replicated layout (its consumer is linear)
     const int compact = (l == c->L - 2) ? 1 : 0;
@@ -521,9 +540,29 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
                           c->widths[l + 1] % 32 == 0 && c->ozHW[0] && oz_enough_tiles(c->widths[l + 2], ncols)) ||
                          (compact && out_on_tc(c));
     if (oz_next) e.colhw = c->ozHW[l & 1];
-    const OzakiBExp be = (oz_here && l >= 1 && c->ozHW[0]) ? OzakiBExp{c->ozHW[(l - 1) & 1], c->widths[l] / 32}
-                                                          : OzakiBExp{nullptr, 0};
-    hid_gemm(c->G, g, e, c->st, c->batched, c->opt.hid_cp, oz_here ? &c->ozW[l] : nullptr, be);
+    const bool din = dig_out(l - 1), dout = dig_out(l);
+    if (din || dout) {
+      OzakiBExp be = OzakiBExp{nullptr, 0};
+      if (din) {
+        be.dig = reinterpret_cast<const unsigned char*>(c->H[l - 1].p);
+        be.dexp = c->ozDE[(l - 1) & 1];
+      } else if (l >= 1 && c->ozHW[0]) {
+        be = OzakiBExp{c->ozHW[(l - 1) & 1], c->widths[l] / 32};
+      }
+      if (dout) {
+        EpiJetDig ed{c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, reinterpret_cast<unsigned char*>(c->H[l].p),
+                     c->ozDE[l & 1]};
+        if (din) launch_ozaki<64, EpiJetDig, true>(c->ozW[l].view(), be, g, ed, c->st);
+        else launch_ozaki<64, EpiJetDig, false>(c->ozW[l].view(), be, g, ed, c->st);
+      } else {
+        launch_ozaki<64, EpiJet, true>(c->ozW[l].view(), be, g, e, c->st);
+      }
+      ++gemm_launch_count;
+    } else {
+      const OzakiBExp be = (oz_here && l >= 1 && c->ozHW[0]) ? OzakiBExp{c->ozHW[(l - 1) & 1], c->widths[l] / 32}
+                                                            : OzakiBExp{nullptr, 0};
+      hid_gemm(c->G, g, e, c->st, c->batched, c->opt.hid_cp, oz_here ? &c->ozW[l] : nullptr, be);
+    }
     in = c->H[l].p;
     ldin = c->ldH[l];
   }
@@ -1336,6 +1375,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       }
       const size_t hwn = (size_t)c->n_sims * c->Cb * (size_t)ceil_div(std::max(maxw, c->wL1), 32);
       for (auto& p : c->ozHW) NL_CUDA(cudaMalloc(&p, std::max<size_t>(hwn, 1) * sizeof(unsigned)));
+      for (auto& p : c->ozDE) NL_CUDA(cudaMalloc(&p, (size_t)round_up(c->n_sims * c->Cb, 64) * sizeof(int)));
       if (!c->opt.dmma_bwd) {
         // shared-real vhp backward layers 1 .. L-2: W_l^T (widths[l] x widths[l+1]) as digit tiles
         c->ozWT.resize(L - 1);
@@ -1385,7 +1425,7 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       while (c->rpcM > 16 && mass_smem(c) > 200 * 1024) c->rpcM /= 2;
     }
     c->nchM = ceil_div(N, c->rpcM);
-    if (c->ldjt == gram_ld(c->n) && c->lddj % 2 == 0 && c->n_sims > 1) {
+    if (c->ldjt == gram_ld(c->n) && c->lddj % 2 == 0 && (c->n_sims > 1 || c->opt.cpm > 0)) {
       // many sims: a CTA walks several row chunks of its sim (>= ~2 waves of 2 CTAs per SM)
       const int rows_ch = c->nchM;
       c->cpmM = (int)std::max(1LL, std::min<long long>(rows_ch, (long long)c->n_sims * rows_ch / (148 * 2 * 2)));
@@ -1478,6 +1518,8 @@ extern "C" void nlrom_destroy(nlrom_ctx* c) {
   for (auto p : c->ozBHW)
     if (p) cudaFree(p);
   for (auto p : c->ozHW)
+    if (p) cudaFree(p);
+  for (auto p : c->ozDE)
     if (p) cudaFree(p);
   delete c;
 }

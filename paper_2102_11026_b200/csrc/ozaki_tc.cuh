@@ -26,7 +26,18 @@
 //   warps 10-17 B converters: per tile the column exponents (max over K), per K chunk the 7 int8
 //              slice planes of the fp64 activations written straight into the UMMA core-matrix
 //              layout (no swizzle, K-major: 8 rows x 16 B cores, LBO = 128 B, SBO = 256 B)
+//
+// Digit chain (hidden -> hidden layers, BDIG = true and / or a digit-producing Epi): a layer whose
+// consumer is another tcgen05 hidden layer writes its output directly as the consumer's B stage
+// tiles (7 digit planes per 64 columns x 32 K, the layout above) plus one exponent per column, so
+// the consumer lands B by TMA like A and needs no converter warps (warps 2-17 all drain / run the
+// epilogue). The producer's two m-tile CTAs of a column tile (M = 256) form a cluster pair and
+// exchange their column maxima (st.async into the peer's shared memory) so both convert against
+// the same column exponent; every element is converted once (the fp64 path converts each column
+// once per m tile) and the fp64 activations are never written or re-read. Same digits and
+// exponents as the converters: results are bitwise equal to the fp64 hand-off.
 #pragma once
+#include <type_traits>
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -50,7 +61,10 @@ constexpr int NEPI = OZ_NEPI;   // epilogue threads (warps 2 ..: NEPI / 128 warp
 #ifndef OZ_NCONV
 #define OZ_NCONV 256
 #endif
-constexpr int NCONV = OZ_NCONV; // B converter threads (warps 10 ..): 256 measured 0.85 vs 0.95-1.0 ms with 128 (probe)
+constexpr int NCONV = OZ_NCONV;
+#ifndef OZ_DIG_SPLIT
+#define OZ_DIG_SPLIT 1   // B from digits: drain warps / functor warps on two fp64 tiles (0.86 vs 0.94 ms, cfg5)
+#endif // B converter threads (warps 10 ..): 256 measured 0.85 vs 0.95-1.0 ms with 128 (probe)
 constexpr int EPI_W0 = 2, CONV_W0 = 2 + NEPI / 32;
 constexpr int NT = 64 + NEPI + NCONV;
 constexpr uint32_t TMEM_COLS = 512;
@@ -61,9 +75,17 @@ struct Cfg {
   static constexpr int BN = BN_;
   static constexpr int B_SLICE = BN * BK;
   static constexpr int B_STAGE = S * B_SLICE;
+#ifdef OZ_STAGES64
+  static constexpr int STAGES = BN == 32 ? 4 : OZ_STAGES64;   // probe override
+#else
   static constexpr int STAGES = BN == 32 ? 4 : 3;
+#endif
   static constexpr int CS_BYTES = BN * LDC * 8;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + CS_BYTES + 512;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + CS_BYTES + 2048;
+  // B from digit tiles: both operands by TMA; with OZ_DIG_SPLIT two fp64 tiles (8 warps drain TMEM
+  // into one while 8 run the epilogue functor on the other) and therefore 2 stages
+  static constexpr int STAGES_DIG = OZ_DIG_SPLIT ? 2 : STAGES;
+  static constexpr int SMEM_BYTES_DIG = 1024 + STAGES_DIG * (A_STAGE + B_STAGE) + (OZ_DIG_SPLIT ? 2 : 1) * CS_BYTES + 2048;
   // two accumulator sets (the next tile's MMAs overlap this tile's drain) when they fit in TMEM
   static constexpr int NBUF = 2 * NACC * BN <= (int)TMEM_COLS ? 2 : 1;
   static constexpr int KPT = BN * BK / NCONV;   // K elements per converter thread per chunk (8 or 16)
@@ -149,6 +171,19 @@ __host__ __device__ __forceinline__ uint32_t digit(long long qb, int t) {   // t
   return ((uint32_t)(qb >> (8 * (S - 1 - t))) & 0xFFu) ^ 0x80u;
 }
 __device__ __forceinline__ long long fixed55(double x, double scale55) { return balanced(__double2ll_rz(x * scale55)); }
+// digit plane t of four balanced values as one word (byte k = digit of value k): the same bytes as
+// digit(), gathered with byte permutes (byte 6 - t of each q', low digits with the 0x80 bias removed)
+__device__ __forceinline__ uint32_t pack_plane(long long q0, long long q1, long long q2, long long q3, int t) {
+  const int bi = S - 1 - t;
+  const bool h = bi >= 4;
+  const uint32_t w0 = h ? (uint32_t)((unsigned long long)q0 >> 32) : (uint32_t)q0;
+  const uint32_t w1 = h ? (uint32_t)((unsigned long long)q1 >> 32) : (uint32_t)q1;
+  const uint32_t w2 = h ? (uint32_t)((unsigned long long)q2 >> 32) : (uint32_t)q2;
+  const uint32_t w3 = h ? (uint32_t)((unsigned long long)q3 >> 32) : (uint32_t)q3;
+  const uint32_t sel = (uint32_t)((bi & 3) | (((bi & 3) + 4) << 4));
+  const uint32_t r = __byte_perm(__byte_perm(w0, w1, sel), __byte_perm(w2, w3, sel), 0x5410);
+  return t == 0 ? r : r ^ 0x80808080u;
+}
 // exponent E of a row / column with max|x| < (127/128) 2^E (0 for an all-zero one)
 // (clamped at -900 so that the 2^(55 - E) scale and the 2^(E - 62) recombination stay normal)
 __host__ __device__ __forceinline__ int exp_of(double amax) {
@@ -173,7 +208,25 @@ struct OzakiA {
 struct OzakiBExp {
   const unsigned* parts;
   int nparts;   // <= 8
+  // digit-chain input (k_ozaki_gemm<.., BDIG = true>): the B stage tiles [C/64][K/32][S][64 x 32 B]
+  // and the column exponents [C/64 * 64] written by the producing layer (EpiJetDig)
+  const unsigned char* dig = nullptr;
+  const int* dexp = nullptr;
 };
+
+// Digit-producing epilogues (EpiJetDig, ozaki_chain.cuh) get this context from the kernel.
+struct DigCtx {
+  double* Cs;          // the fp64 tile [BN][LDC]; reused as the 4 x B_STAGE staging of the digits
+  unsigned* colmax;    // [64] this CTA's column maxima (high words of |y|)
+  int* colEs;          // [64] the pair's column exponents
+  unsigned* xslot;     // [2][64] the peer's column maxima (written by the peer with st.async)
+  uint64_t* xbar;      // [2] tx barriers of xslot
+  int j;               // tile counter of this CTA
+};
+template <class E, class = void>
+struct digits_out : std::false_type {};
+template <class E>
+struct digits_out<E, std::void_t<decltype(E::kDigitsOut)>> : std::bool_constant<E::kDigitsOut> {};
 
 // Device copy of one layer's prepared A operand (digit tiles + row exponents).
 struct OzakiWeights {
@@ -217,7 +270,7 @@ inline void ozaki_prepare_a(const double* A, int lda, int M, int K, std::vector<
 }
 
 #ifdef OZ_TRACE
-__device__ unsigned long long g_oz_trace[8];  // MMA: wait tempty, wait A, wait B; epi: wait tfull, drain
+__device__ unsigned long long g_oz_trace[12];  // MMA: wait tempty, wait A, wait B; epi: wait tfull, drain
 #define OZ_T0() const long long _t0 = clock64()
 #define OZ_T1(i) atomicAdd(&g_oz_trace[i], (unsigned long long)(clock64() - _t0))
 #else
@@ -225,19 +278,29 @@ __device__ unsigned long long g_oz_trace[8];  // MMA: wait tempty, wait A, wait 
 #define OZ_T1(i)
 #endif
 
-template <int BN, class Epi>
+template <int BN, class Epi, bool BDIG = false>
 __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp bexp, GemmArgs g, int tiles_m, int tiles_c,
                                                          Epi epi) {
   using namespace oz;
   using C = Cfg<BN>;
-  constexpr int STAGES = C::STAGES, NBUF = C::NBUF, KPT = C::KPT;
+  constexpr int STAGES = BDIG ? C::STAGES_DIG : C::STAGES, NBUF = C::NBUF, KPT = C::KPT;
+  constexpr bool SPLIT = BDIG && OZ_DIG_SPLIT;
+  constexpr int CS_REGION = SPLIT ? 2 * C::CS_BYTES : C::CS_BYTES;
+  // B from digit tiles (TMA): no converter warps, their threads drain / run the epilogue
+  constexpr int NE = BDIG ? NEPI + NCONV : NEPI;
+  constexpr int NC = BDIG ? 0 : NCONV;
+  constexpr int CONV_W = 2 + NE / 32;
+  constexpr bool DOUT = digits_out<Epi>::value;
+  static_assert(!DOUT || BN == 64, "digit output tiles are 64 columns");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by pointer arithmetic on the __shared__ array (an integer round trip
+  // would hide the address space and turn every shared access into a generic LD.E / ST.E)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sA = base;                                   // STAGES x A_STAGE
   unsigned char* sB = base + STAGES * A_STAGE;                // STAGES x B_STAGE
   double* Cs = reinterpret_cast<double*>(sB + STAGES * C::B_STAGE);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(Cs) + C::CS_BYTES);
-  uint64_t* fullA = bar;                 // [STAGES]  tx bytes of the weight slices
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(Cs) + CS_REGION);
+  uint64_t* fullA = bar;                 // [STAGES]  tx bytes of the weight slices (+ B digit tiles)
   uint64_t* fullB = bar + STAGES;        // [STAGES]  one arrival per converter warp
   uint64_t* empty = bar + 2 * STAGES;    // [STAGES]  tcgen05.commit
   uint64_t* tfull = bar + 3 * STAGES;    // [NBUF] accumulators complete (commit)
@@ -245,8 +308,14 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
   uint64_t* eready = tfull + 4;          // [2] column exponents of a tile written (NCONV converters)
   uint64_t* efree = tfull + 6;           // [2] column exponents of a tile consumed (NEPI epilogue threads)
   uint64_t* tdone = tfull + 8;           // every MMA of this CTA complete (before TMEM dealloc)
-  int* colE = reinterpret_cast<int*>(tfull + 10);  // [2][BN]
-  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(colE + 2 * BN);
+  uint64_t* xbar = tfull + 9;            // [2] digit output: the peer's column maxima landed
+  uint64_t* csfull = tfull + 11;         // [2] SPLIT: fp64 tile drained (drain threads)
+  uint64_t* csfree = tfull + 13;         // [2] SPLIT: fp64 tile consumed (functor threads)
+  int* colE = reinterpret_cast<int*>(tfull + 15);  // [2][BN]
+  unsigned* xslot = reinterpret_cast<unsigned*>(colE + 2 * BN);  // [2][64]
+  unsigned* colmax = xslot + 128;                                // [64]
+  int* colEs = reinterpret_cast<int*>(colmax + 64);              // [64]
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(colEs + 64);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nk = g.K / BK;
   const int ntiles = tiles_m * tiles_c;
@@ -254,17 +323,24 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(fullA + s, 1);
-      mbar_init(fullB + s, NCONV / 32);
+      mbar_init(fullB + s, NC ? NC / 32 : 1);
       mbar_init(empty + s, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
-      mbar_init(tempty + i, NEPI / 32);
-      mbar_init(eready + i, NCONV);
-      mbar_init(efree + i, NEPI);
+      mbar_init(tempty + i, SPLIT ? NE / 64 : NE / 32);
+      mbar_init(eready + i, NC ? NC : 1);
+      mbar_init(efree + i, NE);
+      mbar_init(xbar + i, 1);
+      mbar_init(csfull + i, SPLIT ? NE / 2 : 1);
+      mbar_init(csfree + i, SPLIT ? NE / 2 : 1);
     }
     mbar_init(tdone, 1);
     fence_mbar_init();
+    if constexpr (DOUT) {   // the peer's column maxima of tiles 0 and 1 (64 x 4 bytes each)
+      mbar_expect_tx(xbar, 256);
+      mbar_expect_tx(xbar + 1, 256);
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_s)),
@@ -274,11 +350,14 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // digit output: the peer's barriers are initialised before any st.async reaches them
+  if constexpr (DOUT) cluster_sync_all();
   const uint32_t tmem = *tmem_base_s;
 
   if (warp == 0) {
-    // --------------------------------------------------------------- A producer (weights)
+    // --------------------------------------------------------------- A (+ B digit tiles) producer
     if (lane == 0) {
+      if constexpr (BDIG) pdl_wait();   // the B tiles are the previous layer's output
       int st = 0;
       uint32_t ph = 0;
       bool wrapped = false;   // the ring has been filled once: wait for the stage's previous use
@@ -286,8 +365,11 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
         const int tm = t % tiles_m;
         for (int kc = 0; kc < nk; ++kc) {
           if (wrapped) mbar_wait_cta(empty + st, ph ^ 1u);
-          mbar_expect_tx(fullA + st, A_STAGE);
+          mbar_expect_tx(fullA + st, BDIG ? A_STAGE + C::B_STAGE : A_STAGE);
           tma_g2s(sA + st * A_STAGE, a.tiles + ((size_t)tm * nk + kc) * A_STAGE, A_STAGE, fullA + st);
+          if constexpr (BDIG)
+            tma_g2s(sB + st * C::B_STAGE, bexp.dig + ((size_t)(t / tiles_m) * nk + kc) * C::B_STAGE, C::B_STAGE,
+                    fullA + st);
           if (++st == STAGES) {
             st = 0;
             ph ^= 1u;
@@ -324,7 +406,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
             mbar_wait_cta(fullA + st, ph);
             OZ_T1(1);
           }
-          {
+          if constexpr (!BDIG) {
             OZ_T0();
             mbar_wait_cta(fullB + st, ph);
             OZ_T1(2);
@@ -351,10 +433,11 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       tc_commit(tdone);
       mbar_wait_cta(tdone, 0);
     }
-  } else if (warp >= CONV_W0) {
+  } else if (warp >= CONV_W) {
+    if constexpr (!BDIG) {
     // --------------------------------------------------------------- B converters (warps 10 .. 17)
     pdl_wait();
-    const int ct = tid - CONV_W0 * 32;   // 0 .. NCONV-1
+    const int ct = tid - CONV_W * 32;   // 0 .. NCONV-1
     constexpr int TPC = NCONV / BN;  // threads per column (2 or 4), each KPT consecutive K per chunk
     constexpr int PF = (KPT == 8 && NCONV <= 128) ? 4 : 2;   // chunks in flight per thread (register ring)
     const int cl = ct / TPC, kq = ct % TPC;
@@ -480,13 +563,91 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
         }
       }
     }
+    }
+  } else if (SPLIT) {
+    if constexpr (SPLIT) {
+    // ------------------------------------------ epilogue, B from digits: warps 2-9 drain TMEM into one
+    // of two fp64 tiles while warps 10-17 run the Epi functor on the other
+    pdl_wait();
+    constexpr int NDR = NE / 2, NFN = NE / 2;
+    constexpr int CSD = BN * LDC;   // doubles per fp64 tile
+    if (warp < EPI_W0 + NDR / 32) {
+      const int q = warp & 3;
+      const int chalf = (warp - EPI_W0) >> 2;   // column half
+      const int row_l = q * 32 + lane;
+      int j = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+        const int tm = t % tiles_m, tc = t / tiles_m;
+        const int m0 = tm * BM, c0 = tc * BN;
+        const int buf = NBUF == 2 ? (j & 1) : 0;
+        const int use = NBUF == 2 ? (j >> 1) : j;
+        double* Csb = Cs + (j & 1) * CSD;
+        const int ecol = __ldg(bexp.dexp + c0 + chalf * 32 + lane);   // this half's column exponents
+        {
+          OZ_T0();
+          mbar_wait_cta(tfull + buf, (uint32_t)(use & 1));
+          if (tid == EPI_W0 * 32) OZ_T1(4);
+        }
+        tc_fence_after();
+        if (j >= 2) mbar_wait_cta(csfree + (j & 1), (uint32_t)(((j >> 1) - 1) & 1));
+        const int m = m0 + row_l;
+        const int em = (m < g.M) ? a.row_exp[m] : 0;
+        const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * NACC * BN + chalf * 32);
+        constexpr int CW = 8;
+#pragma unroll 1
+        for (int ch = 0; ch < 32 / CW; ++ch) {
+          int acc[NACC][CW];
+#pragma unroll
+          for (int d = 0; d < NACC; ++d) oz::tmem_ld_n(tacc + (uint32_t)(d * BN + ch * CW), acc[d]);
+          oz::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < CW; ++i) {
+            const int cl = ch * CW + i;
+            const long long hi = ((long long)acc[0][i] << 16) + ((long long)acc[1][i] << 8) + (long long)acc[2][i];
+            const long long lo = ((long long)acc[3][i] << 24) + ((long long)acc[4][i] << 16) +
+                                 ((long long)acc[5][i] << 8) + (long long)acc[6][i];
+            const int E = em + __shfl_sync(0xffffffffu, ecol, cl);
+            Csb[(chalf * 32 + cl) * LDC + row_l] =
+                E < -960 ? 0.0 : fma((double)hi, oz::pow2(E - 30), (double)lo * oz::pow2(E - 62));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + buf);   // TMEM may take the next tile's accumulators
+        mbar_arrive(csfull + (j & 1));
+      }
+    } else {
+      const int ft = tid - (EPI_W0 * 32 + NDR);   // 0 .. NFN-1
+      int j = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+        const int tm = t % tiles_m, tc = t / tiles_m;
+        double* Csb = Cs + (j & 1) * CSD;
+        mbar_wait_cta(csfull + (j & 1), (uint32_t)((j >> 1) & 1));
+        Tile tile{Csb, LDC, tm * BM, tc * BN, BM, BN, 0};
+        OZ_T0();
+#ifndef OZ_PROBE_NO_EPI
+        if constexpr (DOUT) {
+          epi.template dig_out<NFN, 64>(tile, g, ft, DigCtx{Csb, colmax, colEs, xslot, xbar, j});
+          if (ft == 0) bulk_wait_read0();   // the digit store has read the staging (this fp64 tile)
+        } else {
+          epi(tile, g, ft, NFN);
+        }
+#endif
+        if (ft == 0) OZ_T1(6);
+        mbar_arrive(csfree + (j & 1));
+      }
+      if constexpr (DOUT) {
+        if (ft == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // digit stores complete
+      }
+    }
+    }
   } else {
-    // --------------------------------------------------------------- epilogue (warps 2 .. 9)
+    // --------------------------------------------------------------- epilogue (warps 2 .. CONV_W - 1)
     pdl_wait();
     const int q = warp & 3;              // TMEM lane quarter of this warp
-    const int et = tid - EPI_W0 * 32;     // 0 .. NEPI-1
-    // which slice of the tile's columns this warp drains (NEPI / 128 slices; lane quarter = warp % 4)
-    constexpr int NSL = NEPI / 128;
+    const int et = tid - EPI_W0 * 32;     // 0 .. NE-1
+    // which slice of the tile's columns this warp drains (NE / 128 slices; lane quarter = warp % 4)
+    constexpr int NSL = NE / 128;
     const int chalf = (warp - EPI_W0) >> 2;
     const int row_l = q * 32 + lane;      // tile row = TMEM lane
     int j = 0;
@@ -502,17 +663,23 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
         if (et == 0) OZ_T1(4);
       }
       tc_fence_after();
-      mbar_wait_cta(eready + (j & 1), (uint32_t)((j >> 1) & 1));
+      if constexpr (!BDIG) mbar_wait_cta(eready + (j & 1), (uint32_t)((j >> 1) & 1));
 #ifdef OZ_TRACE
       const long long _td = clock64();
 #endif
       const int m = m0 + row_l;
       const int em = (m < g.M) ? a.row_exp[m] : 0;
       const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * NACC * BN);
-      named_bar_sync(1, NEPI);  // the previous tile's epilogue is done with Cs
+      if constexpr (DOUT) {
+        if (et == 0) bulk_wait_read0();   // the previous tile's digit store has read the staging (Cs)
+      }
+      named_bar_sync(1, NE);  // the previous tile's epilogue is done with Cs
       // CW columns per TMEM load (x16 with 128 converter threads; x8 keeps the epilogue within the
       // register budget of the 576-thread build with 256 converter threads)
-      constexpr int CW = (NCONV > 256 || NEPI > 256) ? 4 : NCONV > 128 ? 8 : 16;
+      constexpr int CW = BDIG ? 8 : (NCONV > 256 || NEPI > 256) ? 4 : NCONV > 128 ? 8 : 16;
+      constexpr int SLW = BN / NSL;   // columns drained by this warp
+      // BDIG: this warp's column exponents, one per lane (shuffled per column below)
+      const int ecol = BDIG ? __ldg(bexp.dexp + c0 + chalf * SLW + (lane % SLW)) : 0;
 #pragma unroll 1
       for (int ch = chalf * (BN / NSL / CW); ch < (chalf + 1) * (BN / NSL / CW); ++ch) {
         int acc[NACC][CW];
@@ -527,7 +694,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
           const long long hi = ((long long)acc[0][i] << 16) + ((long long)acc[1][i] << 8) + (long long)acc[2][i];
           const long long lo = ((long long)acc[3][i] << 24) + ((long long)acc[4][i] << 16) +
                                ((long long)acc[5][i] << 8) + (long long)acc[6][i];
-          const int E = em + colE[(j & 1) * BN + cl];
+          const int E = em + (BDIG ? __shfl_sync(0xffffffffu, ecol, cl - chalf * SLW) : colE[(j & 1) * BN + cl]);
           // x_a x_b = q_a q_b 2^{E-110} = 2^{E+2} sum_d acc_d 2^{-8d} = hi 2^{E-30} + lo 2^{E-62}
           Cs[cl * LDC + row_l] = E < -960 ? 0.0 : fma((double)hi, oz::pow2(E - 30), (double)lo * oz::pow2(E - 62));
         }
@@ -538,16 +705,26 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
 #endif
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + buf);   // TMEM may take the next tiles' accumulators
-      mbar_arrive(efree + (j & 1));
-      named_bar_sync(1, NEPI);
+      if constexpr (!BDIG) mbar_arrive(efree + (j & 1));
+      named_bar_sync(1, NE);
       Tile tile{Cs, LDC, m0, c0, BM, cs, 0};
 #ifndef OZ_PROBE_NO_EPI
-      epi(tile, g, et, NEPI);
+      OZ_T0();
+      if constexpr (DOUT)
+        epi.template dig_out<NE, 64>(tile, g, et, DigCtx{Cs, colmax, colEs, xslot, xbar, j});
+      else
+        epi(tile, g, et, NE);
+      if (et == 0) OZ_T1(6);
 #endif
+    }
+    if constexpr (DOUT) {
+      if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // digit stores complete
     }
   }
   tc_fence_before();
   __syncthreads();
+  // digit output: no CTA of the pair leaves while the other may still write into its shared memory
+  if constexpr (DOUT) cluster_sync_all();
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -566,30 +743,46 @@ inline int sm_count_oz() {
 }
 
 // Launch over all column tiles (persistent grid of one CTA per SM). Requirements: K % 32 == 0
-// (M ragged: the prepared A operand is zero-padded to 128-row tiles, the epilogue skips m >= M), ldb even and g.B 16-byte aligned, the Epi column groups divide BN (or g.cstep <= BN
-// columns per tile, then the epilogue sees t.bn = cstep).
-template <int BN, class Epi>
+// (M ragged: the prepared A operand is zero-padded to 128-row tiles, the epilogue skips m >= M), ldb
+// even and g.B 16-byte aligned, the Epi column groups divide BN (or g.cstep <= BN columns per tile,
+// then the epilogue sees t.bn = cstep). BDIG: B from digit tiles (be.dig / be.dexp, C padded to
+// whole 64-column tiles). A digit-producing Epi (EpiJetDig) runs as cluster pairs over the two
+// m tiles of M = 256 (tiles_m == 2, even grid).
+template <int BN, class Epi, bool BDIG = false>
 void launch_ozaki(const OzakiA& a, const OzakiBExp& be, const GemmArgs& g, const Epi& epi, cudaStream_t st) {
   using C = oz::Cfg<BN>;
-  if (!launch_gate((const void*)k_ozaki_gemm<BN, Epi>)) return;
+  constexpr bool DOUT = digits_out<Epi>::value;
+  auto kern = k_ozaki_gemm<BN, Epi, BDIG>;
+  if (!launch_gate((const void*)kern)) return;
   static bool configured = false;
   if (!configured) {
-    NL_CUDA(cudaFuncSetAttribute(k_ozaki_gemm<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+    NL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 BDIG ? C::SMEM_BYTES_DIG : C::SMEM_BYTES));
     configured = true;
   }
   const int tiles_m = ceil_div(g.M, oz::BM), tiles_c = ceil_div(g.C, g.cstep ? g.cstep : BN);
   const int ntiles = tiles_m * tiles_c;
+  if (DOUT && (tiles_m != 2 || g.cstep)) {
+    fprintf(stderr, "nlrom: digit-output Ozaki layer needs M = 256 (got %d)\n", g.M);
+    abort();
+  }
+  int grid = std::max(1, std::min(ntiles, sm_count_oz()));
+  if (DOUT) grid &= ~1;   // cluster pairs
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(std::max(1, std::min(ntiles, sm_count_oz())));
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(oz::NT);
-  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.dynamicSmemBytes = BDIG ? C::SMEM_BYTES_DIG : C::SMEM_BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = DOUT ? 2 : 1;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
-  NL_CUDA(cudaLaunchKernelEx(&cfg, k_ozaki_gemm<BN, Epi>, a, be, g, tiles_m, tiles_c, epi));
+  cfg.numAttrs = DOUT ? 2 : 1;
+  NL_CUDA(cudaLaunchKernelEx(&cfg, kern, a, be, g, tiles_m, tiles_c, epi));
 }
 
 inline void ozaki_upload(OzakiWeights& w, const double* A, int lda, int M, int K) {

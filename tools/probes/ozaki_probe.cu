@@ -10,7 +10,7 @@
 #endif
 #include <vector>
 #include <random>
-#include "../../paper_2102_11026_b200/csrc/ozaki_tc.cuh"
+#include "../../paper_2102_11026_b200/csrc/ozaki_chain.cuh"
 #include "../../paper_2102_11026_b200/csrc/gemm_ws.cuh"
 using namespace nlrom;
 
@@ -24,6 +24,29 @@ void upload_matrix(DBuf& dst, const double* h, int rows, int cols, int ld, int r
   NL_CUDA(cudaMemcpy(dst.p, tmp.data(), tmp.size() * 8, cudaMemcpyHostToDevice));
 }
 }  // namespace nlrom
+
+// B operand as digit tiles (the digit chain's layout, ozaki_chain.cuh): [C/64][K/32][S][64 x 32 B]
+static void prepare_b_digits(const std::vector<double>& B, int C, int K, std::vector<unsigned char>& tiles,
+                             std::vector<int>& exps) {
+  using namespace oz;
+  const int tc_n = (C + 63) / 64, nk = K / BK;
+  const int BST = Cfg<64>::B_STAGE, BSL = Cfg<64>::B_SLICE;
+  tiles.assign((size_t)tc_n * nk * BST, 0);
+  exps.assign((size_t)tc_n * 64, 0);
+  for (int c = 0; c < C; ++c) {
+    double amax = 0.0;
+    for (int k = 0; k < K; ++k) amax = std::max(amax, std::fabs(B[(size_t)c * K + k]));
+    // the producer's rule: exp_of of the high-word bound of the column maximum
+    const unsigned hw = (unsigned)(__builtin_bit_cast(unsigned long long, amax) >> 32);
+    const int E = hw ? exp_of(__builtin_bit_cast(double, ((unsigned long long)hw << 32) | 0xFFFFFFFFull)) : 0;
+    exps[c] = E;
+    for (int k = 0; k < K; ++k) {
+      const long long qb = balanced((long long)std::trunc(std::ldexp(B[(size_t)c * K + k], QBITS - E)));
+      unsigned char* st = tiles.data() + ((size_t)(c / 64) * nk + k / BK) * BST;
+      for (int t = 0; t < S; ++t) st[t * BSL + core_off(c % 64, k % BK)] = (unsigned char)digit(qb, t);
+    }
+  }
+}
 
 int main(int argc, char** argv) {
   const int M = 256, K = 256;
@@ -71,6 +94,30 @@ int main(int argc, char** argv) {
     }
   printf("C=%d  max |y - ref| / sum|a||b| = %.3e   max rel (well-conditioned) = %.3e  %s\n", C, worst, worst_rel,
          worst < 2e-15 ? "OZAKI_OK" : "OZAKI_BAD");
+#if OZ_BN == 64
+  {  // B from digit tiles: bitwise equal to the converter path when the column scales agree
+    std::vector<unsigned char> bt;
+    std::vector<int> be;
+    prepare_b_digits(B, C, K, bt, be);
+    unsigned char* dBt;
+    int* dBe;
+    NL_CUDA(cudaMalloc(&dBt, bt.size()));
+    NL_CUDA(cudaMalloc(&dBe, be.size() * 4));
+    NL_CUDA(cudaMemcpy(dBt, bt.data(), bt.size(), cudaMemcpyHostToDevice));
+    NL_CUDA(cudaMemcpy(dBe, be.data(), be.size() * 4, cudaMemcpyHostToDevice));
+    OzakiBExp bd{nullptr, 0};
+    bd.dig = dBt;
+    bd.dexp = dBe;
+    DBuf dY3((size_t)C * M);
+    launch_ozaki<64, EpiStore, true>(oa, bd, ga, EpiStore{dY3.p, M, 0, nullptr, 1, nullptr}, 0);
+    NL_CUDA(cudaDeviceSynchronize());
+    std::vector<double> Y3((size_t)C * M);
+    NL_CUDA(cudaMemcpy(Y3.data(), dY3.p, Y3.size() * 8, cudaMemcpyDeviceToHost));
+    double w3 = 0;
+    for (size_t i = 0; i < Y3.size(); ++i) w3 = std::max(w3, std::fabs(Y3[i] - Y[i]));
+    printf("BDIG vs converter: max |diff| = %.3e (%s)\n", w3, w3 == 0 ? "bitwise" : "DIFFERENT");
+  }
+#endif
   // timing at the cfg5 hidden-layer shape
   const int CT = 393216;
   DBuf bigB((size_t)CT * K), bigY((size_t)CT * M);
@@ -110,9 +157,74 @@ int main(int argc, char** argv) {
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(&t_ws, e0, e1);
   const double fl = 2.0 * M * K * (double)CT;
+  float t_dig = 0;
+#if OZ_BN == 64
+  {
+    std::vector<double> hb((size_t)CT * K);
+    NL_CUDA(cudaMemcpy(hb.data(), bigB.p, hb.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<unsigned char> bt;
+    std::vector<int> be;
+    prepare_b_digits(hb, CT, K, bt, be);
+    unsigned char* dBt;
+    int* dBe;
+    NL_CUDA(cudaMalloc(&dBt, bt.size()));
+    NL_CUDA(cudaMalloc(&dBe, be.size() * 4));
+    NL_CUDA(cudaMemcpy(dBt, bt.data(), bt.size(), cudaMemcpyHostToDevice));
+    NL_CUDA(cudaMemcpy(dBe, be.data(), be.size() * 4, cudaMemcpyHostToDevice));
+    OzakiBExp bd{nullptr, 0};
+    bd.dig = dBt;
+    bd.dexp = dBe;
+    launch_ozaki<64, EpiStore, true>(oa, bd, gb, EpiStore{bigY.p, M, 0, nullptr, 1, nullptr}, 0);
+    cudaEventRecord(e0);
+    for (int rep = 0; rep < 5; ++rep) launch_ozaki<64, EpiStore, true>(oa, bd, gb, EpiStore{bigY.p, M, 0, nullptr, 1, nullptr}, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&t_dig, e0, e1);
+#ifdef OZ_TRACE
+    unsigned long long z[12] = {};
+    cudaMemcpyToSymbol(g_oz_trace, z, sizeof z);
+    launch_ozaki<64, EpiStore, true>(oa, bd, gb, EpiStore{bigY.p, M, 0, nullptr, 1, nullptr}, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(z, g_oz_trace, sizeof z);
+    printf("BDIG per CTA (cycles): MMA wait tempty %.0f  wait A+B %.0f | drain wait tfull %.0f\n", z[0] / 148.0,
+           z[1] / 148.0, z[4] / 148.0);
+#endif
+    printf("BDIG (B digit tiles by TMA, EpiStore): %.3f ms (%.1f fp64-equiv TFLOP/s)\n", t_dig / 5,
+           fl / (t_dig / 5 * 1e-3) / 1e12);
+    // the digit chain's middle layer: B digits in, EpiJetDig (jet sin + digit tiles) out
+    {
+      unsigned char* dOut;
+      int* dOutE;
+      NL_CUDA(cudaMalloc(&dOut, bt.size()));
+      NL_CUDA(cudaMalloc(&dOutE, be.size() * 4));
+      DBuf bias(M);
+      NL_CUDA(cudaMemset(bias.p, 0, M * 8));
+      DBuf cache((size_t)(CT / 96) * 40 * M);
+      EpiJetDig ed{bias.p, getenv("OZ_NOCACHE") ? nullptr : cache.p, M, 32, 3, 20, dOut, dOutE};
+      float t_jd = 0;
+      launch_ozaki<64, EpiJetDig, true>(oa, bd, gb, ed, 0);
+      cudaEventRecord(e0);
+      for (int rep = 0; rep < 5; ++rep) launch_ozaki<64, EpiJetDig, true>(oa, bd, gb, ed, 0);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&t_jd, e0, e1);
+#ifdef OZ_TRACE
+      cudaMemcpyToSymbol(g_oz_trace, z, sizeof z);
+      launch_ozaki<64, EpiJetDig, true>(oa, bd, gb, ed, 0);
+      cudaDeviceSynchronize();
+      cudaMemcpyFromSymbol(z, g_oz_trace, sizeof z);
+      printf("BDIG+EpiJetDig per CTA (cycles): MMA wait tempty %.0f  wait A+B %.0f | epi wait tfull %.0f  drain %.0f  "
+             "functor %.0f (jet %.0f, colmax %.0f, exchange %.0f, convert %.0f, fence+bar %.0f, bulk read %.0f)\n",
+             z[0] / 148.0, z[1] / 148.0, z[4] / 148.0, z[5] / 148.0, z[6] / 148.0, z[2] / 148.0, z[3] / 148.0,
+             z[7] / 148.0, z[8] / 148.0, z[10] / 148.0, z[9] / 148.0);
+#endif
+      printf("BDIG + EpiJetDig: %.3f ms  (%s)\n", t_jd / 5, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+#endif
 #ifdef OZ_TRACE
   {
-    unsigned long long z[8] = {};
+    unsigned long long z[12] = {};
     cudaMemcpyToSymbol(g_oz_trace, z, sizeof z);
     launch_ozaki<OZ_BN>(oa, pre, gb, EpiStore{bigY.p, M, 0, nullptr, 1, nullptr}, 0);
     cudaDeviceSynchronize();
