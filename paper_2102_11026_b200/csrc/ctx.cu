@@ -511,9 +511,6 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
   }
   const int ncols = c->n_sims * c->Cb;
   const int nq = c->n_q;
-  launch(c, k_seed_jet, grid1((long long)ncols * nq), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p,
-         (const double*)c->rdbar.p, c->X0.p, c->ldq, c->n_p, nq, c->n, c->G, c->gps, c->n_sims, dt, c->alpha,
-         drop_fict);
   const double* in = c->X0.p;
   int ldin = c->ldq;
   // hidden layer l runs on the tcgen05 Ozaki GEMM (the dispatch rule of hid_gemm)
@@ -525,11 +522,31 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
   };
   // digit chain: a tcgen05 layer of width 256 whose consumer is a tcgen05 hidden layer hands over
   // digit tiles (ozaki_chain.cuh); its buffer H[l] holds them (7 of the 8 bytes per element)
+  // the seed layer fused with layer 1's B operand (k_seed_layer: layer 0 = three mat-vecs per group)
+  const bool seed_fused = c->L >= 3 && c->G >= 8 && 32 % c->G == 0 && c->widths[1] == 256 && c->ozDE[0] &&
+                          c->ldH[0] % 2 == 0 && c->ozHW[0] && oz_runs(1) &&
+                          (size_t)round_up(ncols, 64) * 7 <= (size_t)ncols * c->ldH[0] * 8;
   auto dig_out = [&](int l) {
+    if (l == 0) return seed_fused && !c->opt.oz_fp64_chain;
     return !c->opt.oz_fp64_chain && c->ozDE[0] && 32 % c->G == 0 && l + 1 <= c->L - 2 && oz_runs(l) && oz_runs(l + 1) &&
            c->widths[l + 1] == 256 && (size_t)round_up(ncols, 64) * 7 <= (size_t)ncols * c->ldH[l] * 8;
   };
-  for (int l = 0; l + 1 < c->L; ++l) {
+  if (seed_fused) {
+    SeedLayerArgs sa{(const double*)c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, c->n_p, nq, c->n,
+                     dt, c->alpha, drop_fict, (const double*)c->W[0].p, c->ldW[0], (const double*)c->b[0].p,
+                     c->cache[0].p, c->ldc[0], c->G, c->gps, ncols, reinterpret_cast<unsigned char*>(c->H[0].p),
+                     c->ozDE[0], c->H[0].p, c->ldH[0], c->ozHW[0]};
+    const bool dig = dig_out(0);
+    if (dig) launch(c, k_seed_layer<true>, ceil_div(ncols, 32), 256, seed_layer_smem(), sa);
+    else launch(c, k_seed_layer<false>, ceil_div(ncols, 32), 256, seed_layer_smem(), sa);
+    in = c->H[0].p;
+    ldin = c->ldH[0];
+  } else {
+    launch(c, k_seed_jet, grid1((long long)ncols * nq), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p,
+           (const double*)c->rdbar.p, c->X0.p, c->ldq, c->n_p, nq, c->n, c->G, c->gps, c->n_sims, dt, c->alpha,
+           drop_fict);
+  }
+  for (int l = seed_fused ? 1 : 0; l + 1 < c->L; ++l) {
     // the last hidden layer writes the de-replicated layout (its consumer is linear)
     const int compact = (l == c->L - 2) ? 1 : 0;
     GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
@@ -1464,6 +1481,8 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
     // kernel attributes for large dynamic shared memory
     NL_CUDA(cudaFuncSetAttribute(k_cubature<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_cubature<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_seed_layer<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NL_CUDA(cudaFuncSetAttribute(k_seed_layer<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_cub_sims<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_cub_sims<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     NL_CUDA(cudaFuncSetAttribute(k_cub_sims<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

@@ -162,4 +162,136 @@ struct EpiJetDig {
 
 };
 
+// Seed layer of the batched decoder fused with its consumer's B operand (hidden layer 1 on tcgen05).
+// The jet seed (k_seed_jet) is sparse -- per column group three base vectors (q, v, w) and unit
+// tangent vectors e_kg -- so layer 0 (w = 256 rows, K = n_q) is three mat-vecs per group and copies
+// of W_0's columns. One CTA per 32 columns (whole groups), one thread per row: z, the jet sin (bias,
+// vhp cache duals as EpiJet) into shared memory; then one thread per (column, 32-row K chunk) holds
+// its 32 values, and since the CTA has all 256 rows of its columns the column exponents need no
+// exchange. DIG: the digits go straight to the consumer's B tiles (the CTA's 1 KB half of each
+// (K chunk, plane) slice) plus the exponents; else the fp64 activations + EpiJet::colhw partials
+// (the fp64 hand-off of the same values, bitwise equal downstream).
+struct SeedLayerArgs {
+  const double* r;
+  const double* rbar;
+  const double* rdbar;
+  int n_p, n_q, n;
+  double dt, alpha;
+  int drop_fict;
+  const double* W0;   // (256 x n_q) row-major, ld ldW0
+  int ldW0;
+  const double* b0;
+  double* cache;      // layer-0 vhp cache, (n_sims * 2 n_q) x ldcache
+  int ldcache;
+  int G, gps, ncols;
+  unsigned char* dig; // DIG: [ceil(ncols / 64)][8][S][64 x 32 B]
+  int* dexp;          // DIG: [ceil(ncols / 64) * 64]
+  double* H;          // !DIG: (ncols x ldh)
+  int ldh;
+  unsigned* colhw;    // !DIG: [ncols][8]
+};
+constexpr int SEED_LDZ = 258;
+inline size_t seed_layer_smem() { return (size_t)32 * SEED_LDZ * 8 + 8 * 32 * 4 + 32 * 4; }
+
+template <bool DIG>
+__global__ void __launch_bounds__(256, 2) k_seed_layer(SeedLayerArgs a) {
+  using namespace oz;
+  extern __shared__ __align__(128) unsigned char sl_smem[];
+  double* Zs = reinterpret_cast<double*>(sl_smem);                       // [32][SEED_LDZ]
+  unsigned* part = reinterpret_cast<unsigned*>(Zs + 32 * SEED_LDZ);      // [8][32]
+  int* colEs = reinterpret_cast<int*>(part + 8 * 32);                    // [32]
+  pdl_wait();
+  pdl_launch();
+  const int m = threadIdx.x;
+  const int c0 = blockIdx.x * 32;
+  const int G = a.G, nk = (G - 4) / 4;
+  const double* Wr = a.W0 + (size_t)m * a.ldW0;
+  const double c3 = a.drop_fict ? (1.0 + a.alpha * a.dt) : (3.0 + a.alpha * a.dt);
+  for (int gt = 0; gt < 32 / G; ++gt) {
+    const int cg = c0 + gt * G;
+    double* zc = Zs + (gt * G) * SEED_LDZ + m;
+    if (cg >= a.ncols) {
+      for (int j = 0; j < G; ++j) zc[j * SEED_LDZ] = 0.0;
+      continue;
+    }
+    const int gg = cg / G, sim = gg / a.gps, gl = gg % a.gps;
+    const double* rs = a.r + (size_t)sim * a.n + a.n_p;
+    const double* rb = a.rbar + (size_t)sim * a.n + a.n_p;
+    const double* rdb = a.rdbar + (size_t)sim * a.n + a.n_p;
+    double zq = 0.0, zv = 0.0, zw = 0.0;
+    for (int i = 0; i < a.n_q; ++i) {
+      const double wi = Wr[i], q = rs[i], v = q - rb[i];
+      zq = fma(wi, q, zq);
+      zv = fma(wi, v, zv);
+      zw = fma(wi, c3 * v - a.dt * rdb[i], zw);
+    }
+    double z[4] = {zq + a.b0[m], a.drop_fict ? 0.0 : zv, 0.0, zw}, o[4];
+    JetCos jc;
+    jet_sin_base(z, o, jc);
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) zc[s2 * SEED_LDZ] = o[s2];
+    double* Cz = a.cache ? a.cache + (size_t)sim * 2 * a.n_q * a.ldcache : nullptr;
+    for (int k = 0; k < nk; ++k) {
+      const int kg = gl * nk + k;
+      const double y[4] = {kg < a.n_q ? Wr[kg] : 0.0, 0.0, 0.0, 0.0};
+      double yo[4];
+      jet_tangent(jc, y, yo);
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) zc[(4 + 4 * k + s2) * SEED_LDZ] = yo[s2];
+      if (Cz && kg < a.n_q) {
+        Cz[(size_t)(2 * kg) * a.ldcache + m] = jc.c1;
+        Cz[(size_t)(2 * kg + 1) * a.ldcache + m] = jc.ns * y[0];
+      }
+    }
+  }
+  __syncthreads();
+  const int c = m & 31, rg = m >> 5;   // column, 32-row group (= K chunk of the consumer)
+  const bool live = c0 + c < a.ncols;
+  double v[32];
+  {
+    const double2* src = reinterpret_cast<const double2*>(Zs + c * SEED_LDZ + rg * 32);
+#pragma unroll
+    for (int q2 = 0; q2 < 16; ++q2) {
+      const double2 w = src[q2];
+      v[2 * q2] = w.x;
+      v[2 * q2 + 1] = w.y;
+    }
+  }
+  unsigned hw = 0u;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) hw = max(hw, (unsigned)__double2hiint(fabs(v[q])));
+  if constexpr (!DIG) {
+    if (live) a.colhw[(size_t)(c0 + c) * 8 + rg] = hw;
+    for (int cc = 0; cc < 32 && c0 + cc < a.ncols; ++cc) a.H[(size_t)(c0 + cc) * a.ldh + m] = Zs[cc * SEED_LDZ + m];
+  } else {
+    part[rg * 32 + c] = hw;
+    __syncthreads();
+    if (m < 32) {
+      unsigned h = 0u;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) h = max(h, part[p * 32 + m]);
+      const int E = h ? exp_of(__hiloint2double((int)h, (int)0xFFFFFFFFu)) : 0;
+      colEs[m] = E;
+      a.dexp[c0 + m] = E;
+    }
+    __syncthreads();
+    const double sc = pow2(QBITS - colEs[c]);
+    long long qv[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) qv[q] = fixed55(v[q], sc);
+    // this CTA's 32 columns are rows (c0 % 64) .. + 31 of the 64-row plane slices (their 1 KB half)
+    unsigned char* dst = a.dig + ((size_t)(c0 / 64) * 8 + rg) * Cfg<64>::B_STAGE + (c0 % 64) * BK;
+#pragma unroll
+    for (int t2 = 0; t2 < S; ++t2) {
+#pragma unroll
+      for (int qb = 0; qb < 2; ++qb) {
+        const long long* q4 = qv + 16 * qb;
+        *reinterpret_cast<uint4*>(dst + t2 * Cfg<64>::B_SLICE + core_off(c, 16 * qb)) =
+            make_uint4(pack_plane(q4[0], q4[1], q4[2], q4[3], t2), pack_plane(q4[4], q4[5], q4[6], q4[7], t2),
+                       pack_plane(q4[8], q4[9], q4[10], q4[11], t2), pack_plane(q4[12], q4[13], q4[14], q4[15], t2));
+      }
+    }
+  }
+}
+
 }  // namespace nlrom
