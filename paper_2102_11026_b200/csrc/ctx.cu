@@ -663,6 +663,17 @@ void cubature_phase(nlrom_ctx* c, CubSet& s, bool weighted, bool scatter = true,
          c->n_sims);
 }
 
+// S = mass-block partials + dt^2 (cubature K~ partials) (+ the vhp block Gt)
+void reduce_S_launch(nlrom_ctx* c, CubSet& s, const double* Gt, double dt) {
+  const int n = c->n;
+  if (c->n_sims > 1)
+    launch(c, k_reduce_S_flat, grid1((long long)c->n_sims * n * n), 256, 0, (const double*)c->partA.p, c->nchM,
+           (const double*)s.part_K.p, s.nchunk, Gt, c->ldGt, n, c->n_p, c->n_q, dt, c->S.p, c->n_sims);
+  else
+    launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
+           (const double*)s.part_K.p, s.nchunk, Gt, c->ldGt, n, c->n_p, c->n_q, dt, c->S.p);
+}
+
 void assemble_launch(nlrom_ctx* c, CubSet& s, double dt, int drop_fict, int mode) {
   AsmArgs A{c->Jt.p, c->ldjt, c->dJ.p, c->lddj, c->mass.p, c->hvv.p, s.f.p, c->fext.p, c->r.p, c->rbar.p,
             c->rdbar.p, c->a.p, c->partA.p, c->partPhi.p, c->N, c->n, c->n_p, c->n_q, c->rpc, c->nchA, dt,
@@ -713,7 +724,8 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
                s.rowptr_full.p, s.entries.p, s.fe_w.p, std::max(s.n, 1), c->a.p, c->partPhi.p,
                c->N, c->n, rc, nch, dt, c->alpha, drop_fict,
                (const double*)c->Alast.p, c->ldlast, c->wL1, g ? c->bpart.p : nullptr};
-    launch(c, k_assemble_a, dim3(nch, c->n_sims), 256, 0, A);
+    if (g) launch(c, k_assemble_a<true>, dim3(nch, c->n_sims), 256, 0, A);
+    else launch(c, k_assemble_a<false>, dim3(nch, c->n_sims), 256, 0, A);
     c->agemv = g;
     c->nphi = nch;
   } else {
@@ -727,10 +739,7 @@ void assemble_phase(nlrom_ctx* c, CubSet& s, double dt, int drop_fict) {
   std::swap(c->st, c->st2);
   launch(c, k_reduce_phi, c->n_sims, 256, (size_t)8 * c->n * 8, (const double*)c->partPhi.p, c->nphi, c->n,
          c->phi.p, c->norm.p);
-  const int n = c->n;
-  const int sblocks = ceil_div(n * n, 32);
-  launch(c, k_reduce_S, dim3(sblocks, c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
-         (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, dt, c->S.p);
+  reduce_S_launch(c, s, nullptr, dt);
   std::swap(c->st, c->st2);
   NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));
 }
@@ -797,7 +806,8 @@ void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s, bool resid_
              sf.rowptr_full.p, sf.entries.p, sf.fe_w.p, std::max(sf.n, 1), c->a.p, c->partPhi.p,
              c->N, c->n, rc, nch, cfg.dt, c->alpha, cfg.drop_fict,
              (const double*)c->Alast.p, c->ldlast, c->wL1, g ? c->bpart.p : nullptr};
-  launch(c, k_assemble_a, dim3(nch, c->n_sims), 256, 0, A);
+  if (g) launch(c, k_assemble_a<true>, dim3(nch, c->n_sims), 256, 0, A);
+  else launch(c, k_assemble_a<false>, dim3(nch, c->n_sims), 256, 0, A);
   c->agemv = g;
   c->nphi = nch;
   // phi on st3 (after the mass block), S_base on st2 (after the stiffness launch and the mass
@@ -811,12 +821,7 @@ void phase_E_split(nlrom_ctx* c, const nlrom_simcfg& cfg, CubSet& s, bool resid_
   NL_CUDA(cudaEventRecord(c->evP, c->st3));
   if (!resid_only) {
     NL_CUDA(cudaStreamWaitEvent(c->st2, c->evM, 0));  // the mass block partials
-    on(c->st2, [&] {
-      const int n = c->n;
-      const int sblocks = ceil_div(n * n, 32);
-      launch(c, k_reduce_S, dim3(sblocks, c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
-             (const double*)s.part_K.p, s.nchunk, (const double*)nullptr, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
-    });
+    on(c->st2, [&] { reduce_S_launch(c, s, nullptr, cfg.dt); });
   }
   NL_CUDA(cudaStreamWaitEvent(c->st2, c->evP, 0));
   NL_CUDA(cudaEventRecord(c->evJoin2, c->st2));
@@ -1112,9 +1117,7 @@ void phase_J(nlrom_ctx* c, const nlrom_simcfg& cfg, bool apply, const double* xr
 // S with the vhp block (system_jacobian API; the Newton iteration adds it inside the LU)
 void full_S(nlrom_ctx* c, const nlrom_simcfg& cfg) {
   CubSet& s = cfg.integration == 1 ? c->setAll : c->setC;
-  const int n = c->n;
-  launch(c, k_reduce_S, dim3(ceil_div(n * n, 32), c->n_sims), 256, 0, (const double*)c->partA.p, c->nchM,
-         (const double*)s.part_K.p, s.nchunk, (const double*)c->Gt.p, c->ldGt, n, c->n_p, c->n_q, cfg.dt, c->S.p);
+  reduce_S_launch(c, s, c->Gt.p, cfg.dt);
 }
 
 std::string cfg_key(const nlrom_simcfg& cfg) {

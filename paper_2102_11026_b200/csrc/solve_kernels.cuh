@@ -208,6 +208,10 @@ struct AsmAArgs {
 // per chunk (the chain's prologue sums the chunk partials): each thread owns one column of P W_L
 // and loads its RC entries (constants) before the dependency wait.
 constexpr int ASMA_GROWS = 32;
+// GP = false (no vhp seed partials: the batched path): 8 threads per row for the dot products and
+// the gather (coalesced 64-byte row segments, 4 rows per warp) and no (P W_L) registers, so 4x the
+// resident warps (cfg5: 0.67 ms, 24% warps active with the 2-threads-per-row GP layout).
+template <bool GP>
 __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
   __shared__ double cs[128];
   __shared__ double as[128];
@@ -215,9 +219,9 @@ __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
   const int chunk = blockIdx.x, sim = blockIdx.y, tid = threadIdx.x;
   const int n = A.n;
   const double ah = A.alpha * A.dt;
-  double pw[ASMA_GROWS];
-  const bool gcol = A.gpart && tid < A.M;
-  if (A.gpart) {
+  double pw[GP ? ASMA_GROWS : 1];
+  const bool gcol = GP && A.gpart && tid < A.M;
+  if (GP && A.gpart) {
 #pragma unroll
     for (int rl = 0; rl < ASMA_GROWS; ++rl) {
       const int row = chunk * A.RC + rl;
@@ -231,7 +235,37 @@ __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
   __syncthreads();
   const int row0 = chunk * A.RC;
   const double* Jsim = A.Jt + (size_t)sim * A.N * A.ldjt;
-  {
+  if constexpr (!GP) {
+    pdl_wait();
+    pdl_launch();
+    for (int rl0 = 0; rl0 < A.RC; rl0 += 32) {
+      const int rl = rl0 + (tid >> 3), h = tid & 7;
+      const int row = row0 + rl;
+      double acc = 0.0, fs = 0.0;
+      if (rl < A.RC && row < A.N) {
+        const double* Jr = Jsim + (size_t)row * A.ldjt;
+        for (int j = h; j < n; j += 8) acc = fma(Jr[j], cs[j], acc);
+        const double* fw = A.fe_w + (size_t)sim * A.n_elems * 12;
+        for (int k = A.rowptr[row] + h; k < A.rowptr[row + 1]; k += 8) fs += fw[A.entries[k]];
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        fs += __shfl_xor_sync(0xffffffffu, fs, o);
+      }
+      if (h == 0 && rl < A.RC) {
+        double av = 0.0;
+        if (row < A.N) {
+          const size_t o = (size_t)sim * A.N + row;
+          const double m = A.mass[row];
+          av = m * acc + A.dt * A.dt * (fs - A.fext[o]);
+          if (!A.drop_fict) av += m * A.hvv[o];
+          A.a[o] = av;
+        }
+        as[rl] = av;
+      }
+    }
+  } else {
     const int rl = tid >> 1, h = tid & 1;
     const int row = row0 + rl;
     double acc = 0.0, fs = 0.0;
@@ -260,7 +294,7 @@ __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
     }
   }
   __syncthreads();
-  if (A.gpart) {
+  if (GP && A.gpart) {
     double g0 = 0.0, g1 = 0.0;
 #pragma unroll
     for (int rl = 0; rl < ASMA_GROWS; rl += 2) {
@@ -353,6 +387,27 @@ __global__ void k_reduce_S(const double* __restrict__ partA, int nchA, const dou
       S[(size_t)sim * nn + idx] = acc;
     }
     __syncthreads();
+  }
+}
+
+// k_reduce_S for many sims (each with few partials): one thread per output element (k_reduce_S's
+// 8-way CTA split left 7 of 8 threads idle and launched 29 x n_sims CTAs: cfg5 0.35 ms)
+__global__ void k_reduce_S_flat(const double* __restrict__ partA, int nchA, const double* __restrict__ partK,
+                                int nchK, const double* __restrict__ Gt, int ldg, int n, int n_p, int n_q, double dt,
+                                double* __restrict__ S, int n_sims) {
+  pdl_wait();
+  pdl_launch();
+  const int nn = n * n;
+  const long long total = (long long)n_sims * nn;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int sim = (int)(t / nn), idx = (int)(t % nn);
+    double a = 0.0, k = 0.0;
+    for (int c = 0; c < nchA; ++c) a += partA[((size_t)sim * nchA + c) * nn + idx];
+    for (int c = 0; c < nchK; ++c) k += partK[((size_t)sim * nchK + c) * nn + idx];
+    double acc = a + dt * dt * k;
+    const int i = idx / n, j = idx % n;
+    if (Gt && i >= n_p && j >= n_p) acc += Gt[((size_t)sim * 2 * n_q + 2 * (j - n_p) + 1) * ldg + (i - n_p)];
+    S[t] = acc;
   }
 }
 
