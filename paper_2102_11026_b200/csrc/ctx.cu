@@ -1098,6 +1098,11 @@ void launch_lu(nlrom_ctx* c, bool apply, const double* xrhs = nullptr, int nx = 
   // k_lu_solve; as fast at n = 60, 10-35% faster at n = 70..124 (tools/probes/lu_blocked_probe.cu,
   // profiles/r02_lu_probe.txt). Retired variants (warp-register, column-cyclic, rank-2, look-ahead
   // pivot, split front/back, k_lu_blocked): DESIGN.md §8b, tools/probes/retired/
+  if (c->n_sims > 1 && nx == 0 && n <= 32) {   // many small systems: a warp per system (k_lu_warp)
+    launch(c, k_lu_warp, ceil_div(c->n_sims, 8), 256, 0, (const double*)c->S.p, (const double*)c->phi.p, c->dr.p,
+           c->r.p, n, apply ? 1 : 0, c->status.p, Gt, c->ldGt, c->n_p, c->n_sims);
+    return;
+  }
   switch (lu_nb(n + nx)) {
     case 4: go(k_lu_lookahead<4>); break;
     case 6: go(k_lu_lookahead<6>); break;

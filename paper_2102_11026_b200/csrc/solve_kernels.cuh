@@ -320,6 +320,83 @@ __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
   }
 }
 
+// Many small systems (n <= 32: cfg5 solves 4096 of n = 30 per Newton iteration): one warp per
+// system instead of one CTA. Lane i owns row i of [S + diag(0, vhp) | -phi] in registers; partial
+// pivoting (max |a_ik| over rows i >= k, the lowest row on ties, as the CTA kernels) and Gauss-Jordan
+// elimination by shuffles -- no shared memory, no barriers; with k and j unrolled at compile time
+// only the live columns j >= k are exchanged. Same outputs as k_lu_lookahead (dr, r += dr when
+// apply, status 1 on a zero / non-finite pivot without writing dr).
+__global__ void __launch_bounds__(256) k_lu_warp(const double* __restrict__ S, const double* __restrict__ phi,
+                                                 double* __restrict__ dr, double* __restrict__ r, int n, int apply,
+                                                 int* __restrict__ status, const double* __restrict__ Gt, int ldg,
+                                                 int n_p, int n_sims) {
+  pdl_wait();
+  pdl_launch();
+  constexpr int NP = 33;   // n + 1 <= 33 columns [A | b]
+  const int lane = threadIdx.x & 31;
+  const int sim = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (sim >= n_sims) return;   // warp-uniform
+  const int nq = n - n_p;
+  double a[NP];
+  const double* Sr = S + (size_t)sim * n * n + (size_t)lane * n;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    double v = 0.0;
+    if (lane < n) {
+      if (j < n) v = Sr[j];
+      else if (j == n) v = -phi[(size_t)sim * n + lane];
+      if (Gt && lane >= n_p && j >= n_p && j < n) v += Gt[((size_t)sim * 2 * nq + 2 * (j - n_p) + 1) * ldg + (lane - n_p)];
+    }
+    a[j] = v;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < NP - 1; ++k) {
+    if (k >= n) break;   // uniform
+    // pivot row p: max |a_ik| over i >= k, the lowest i on ties
+    double v = (lane >= k && lane < n) ? fabs(a[k]) : -1.0;
+    int p = lane;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int op = __shfl_xor_sync(0xffffffffu, p, o);
+      if (ov > v || (ov == v && op < p)) {
+        v = ov;
+        p = op;
+      }
+    }
+    if (!(v > 0.0) || !isfinite(v)) bad = true;
+    // rows k and p exchange their live columns
+    const int src = lane == k ? p : (lane == p ? k : lane);
+#pragma unroll
+    for (int j = k; j < NP; ++j) a[j] = __shfl_sync(0xffffffffu, a[j], src);
+    const double rp = 1.0 / __shfl_sync(0xffffffffu, a[k], k);
+    const double l = a[k] * rp;
+#pragma unroll
+    for (int j = k + 1; j < NP; ++j) {
+      const double pkj = __shfl_sync(0xffffffffu, a[j], k);
+      if (lane != k) a[j] = fma(-l, pkj, a[j]);
+    }
+  }
+  if (bad) {
+    if (lane == 0) status[sim] = 1;
+    return;
+  }
+  // x_i = b_i / a_ii (row i is on lane i after the exchanges)
+  double d = 1.0, b = 0.0;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    if (j == lane) d = a[j];
+    if (j == n) b = a[j];
+  }
+  if (lane < n) {
+    const double x = b * (1.0 / d);
+    dr[(size_t)sim * n + lane] = x;
+    if (apply) r[(size_t)sim * n + lane] += x;
+  }
+  if (lane == 0) status[sim] = 0;
+}
+
 // phi = sum_chunks partphi (one CTA per sim; 8 chunk groups per output, smem combine), ||phi||_2
 __global__ void k_reduce_phi(const double* __restrict__ partphi, int nchunk, int n, double* __restrict__ phi,
                              double* __restrict__ norm) {
