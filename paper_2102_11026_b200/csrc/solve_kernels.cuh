@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(256) k_assemble_a(AsmAArgs A) {
 // elimination by shuffles -- no shared memory, no barriers; with k and j unrolled at compile time
 // only the live columns j >= k are exchanged. Same outputs as k_lu_lookahead (dr, r += dr when
 // apply, status 1 on a zero / non-finite pivot without writing dr).
-__global__ void __launch_bounds__(256) k_lu_warp(const double* __restrict__ S, const double* __restrict__ phi,
+__global__ void __launch_bounds__(256, 2) k_lu_warp(const double* __restrict__ S, const double* __restrict__ phi,
                                                  double* __restrict__ dr, double* __restrict__ r, int n, int apply,
                                                  int* __restrict__ status, const double* __restrict__ Gt, int ldg,
                                                  int n_p, int n_sims) {
