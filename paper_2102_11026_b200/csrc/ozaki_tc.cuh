@@ -82,10 +82,11 @@ struct Cfg {
 #endif
   static constexpr int CS_BYTES = BN * LDC * 8;
   static constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + CS_BYTES + 2048;
-  // B from digit tiles: both operands by TMA; with OZ_DIG_SPLIT two fp64 tiles (8 warps drain TMEM
-  // into one while 8 run the epilogue functor on the other) and therefore 2 stages
-  static constexpr int STAGES_DIG = OZ_DIG_SPLIT ? 2 : STAGES;
-  static constexpr int SMEM_BYTES_DIG = 1024 + STAGES_DIG * (A_STAGE + B_STAGE) + (OZ_DIG_SPLIT ? 2 : 1) * CS_BYTES + 2048;
+  // B from digit tiles: both operands by TMA. Split epilogue (digit-producing functors, OZ_DIG_SPLIT):
+  // two fp64 tiles (8 warps drain TMEM into one while 8 run the functor on the other) and therefore
+  // 2 stages; otherwise the sequential epilogue (16 warps) with the 3-stage ring.
+  static constexpr int STAGES_SPLIT = 2;
+  static constexpr int SMEM_BYTES_SPLIT = 1024 + STAGES_SPLIT * (A_STAGE + B_STAGE) + 2 * CS_BYTES + 2048;
   // two accumulator sets (the next tile's MMAs overlap this tile's drain) when they fit in TMEM
   static constexpr int NBUF = 2 * NACC * BN <= (int)TMEM_COLS ? 2 : 1;
   static constexpr int KPT = BN * BK / NCONV;   // K elements per converter thread per chunk (8 or 16)
@@ -283,8 +284,8 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
                                                          Epi epi) {
   using namespace oz;
   using C = Cfg<BN>;
-  constexpr int STAGES = BDIG ? C::STAGES_DIG : C::STAGES, NBUF = C::NBUF, KPT = C::KPT;
-  constexpr bool SPLIT = BDIG && OZ_DIG_SPLIT;
+  constexpr bool SPLIT = BDIG && digits_out<Epi>::value && OZ_DIG_SPLIT;
+  constexpr int STAGES = SPLIT ? C::STAGES_SPLIT : C::STAGES, NBUF = C::NBUF, KPT = C::KPT;
   constexpr int CS_REGION = SPLIT ? 2 * C::CS_BYTES : C::CS_BYTES;
   // B from digit tiles (TMA): no converter warps, their threads drain / run the epilogue
   constexpr int NE = BDIG ? NEPI + NCONV : NEPI;
@@ -752,12 +753,13 @@ template <int BN, class Epi, bool BDIG = false>
 void launch_ozaki(const OzakiA& a, const OzakiBExp& be, const GemmArgs& g, const Epi& epi, cudaStream_t st) {
   using C = oz::Cfg<BN>;
   constexpr bool DOUT = digits_out<Epi>::value;
+  constexpr bool SPLIT = BDIG && DOUT && OZ_DIG_SPLIT;
   auto kern = k_ozaki_gemm<BN, Epi, BDIG>;
   if (!launch_gate((const void*)kern)) return;
   static bool configured = false;
   if (!configured) {
     NL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 BDIG ? C::SMEM_BYTES_DIG : C::SMEM_BYTES));
+                                 SPLIT ? C::SMEM_BYTES_SPLIT : C::SMEM_BYTES));
     configured = true;
   }
   const int tiles_m = ceil_div(g.M, oz::BM), tiles_c = ceil_div(g.C, g.cstep ? g.cstep : BN);
@@ -771,7 +773,7 @@ void launch_ozaki(const OzakiA& a, const OzakiBExp& be, const GemmArgs& g, const
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(oz::NT);
-  cfg.dynamicSmemBytes = BDIG ? C::SMEM_BYTES_DIG : C::SMEM_BYTES;
+  cfg.dynamicSmemBytes = SPLIT ? C::SMEM_BYTES_SPLIT : C::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
