@@ -537,7 +537,8 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
                      c->cache[0].p, c->ldc[0], c->G, c->gps, ncols, reinterpret_cast<unsigned char*>(c->H[0].p),
                      c->ozDE[0], c->H[0].p, c->ldH[0], c->ozHW[0]};
     const bool dig = dig_out(0);
-    if (dig) launch(c, k_seed_layer<true>, ceil_div(ncols, 32), 256, seed_layer_smem(), sa);
+    // whole 64-column digit tiles: the CTAs past ncols write the padding half's zero digits
+    if (dig) launch(c, k_seed_layer<true>, round_up(ncols, 64) / 32, 256, seed_layer_smem(), sa);
     else launch(c, k_seed_layer<false>, ceil_div(ncols, 32), 256, seed_layer_smem(), sa);
     in = c->H[0].p;
     ldin = c->ldH[0];

@@ -77,12 +77,24 @@ def test_ozaki_hidden_layers_vs_oracle_and_dmma(cuda_ok, tmp_path):
     assert rel(oz["phi"], dm["phi"]) < 1e-11
 
 
-def test_digit_chain_bitwise(cuda_ok, tmp_path):
+@pytest.mark.parametrize("ns", [NS, 161])
+def test_digit_chain_bitwise(cuda_ok, tmp_path, ns):
     """Hidden layers handing digit tiles + exponents to each other (default) vs handing fp64
     activations that the consumer converts (NLROM_PATH=oz_fp64_chain): same digits, same
-    exponents, so every output is bitwise equal."""
-    dg = _run(tmp_path, "")
-    fp = _run(tmp_path, "oz_fp64_chain")
+    exponents, so every output is bitwise equal (161 sims: a half-empty last 64-column tile)."""
+    dg = _run(tmp_path, "", ns)
+    fp = _run(tmp_path, "oz_fp64_chain", ns)
     assert tuple(dg["tc"])[0] == 8
     for k in ("phi", "S", "r", "rd"):
         assert np.array_equal(dg[k], fp[k]), k
+    if ns % 2:   # the last sim's columns straddle the half-empty last tile: vs the oracle too
+        from paper_2102_11026_b200.problem import build_problem
+        from paper_2102_11026_b200 import rdsim
+        P = build_problem("cfg5")
+        S = oracle_sim(P)
+        n = P.cfg.n_p + P.cfg.n_q
+        i = ns - 1
+        r, rb, rdb = P.random_state(seed=70 + i)
+        oc = ocfg(rdsim.SimConfig(dt=P.cfg.dt))
+        assert rel(dg["phi"].reshape(ns, n)[i], ors.residual(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
+        assert rel(dg["S"][i], ors.system_jacobian(S, r, (rb, rdb), P.f_ext, oc)) < 1e-11
