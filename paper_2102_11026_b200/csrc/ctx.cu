@@ -1806,17 +1806,14 @@ static void ensure_adaptive_graph(nlrom_ctx* c, const nlrom_simcfg& cfg, double*
   NL_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
   try {
     NL_CUDA(cudaGraphConditionalHandleCreate(&hO, capture_graph_of(c), 0, 0));
-    NL_CUDA(cudaMemcpyAsync(c->rbar.p, hi, (size_t)n * 8, cudaMemcpyHostToDevice, c->st));
-    NL_CUDA(cudaMemcpyAsync(c->rdbar.p, hi + n, (size_t)n * 8, cudaMemcpyHostToDevice, c->st));
-    NL_CUDA(cudaMemcpyAsync(c->fext.p, hi + 2 * n, N * 8, cudaMemcpyHostToDevice, c->st));
-    launch(c, k_axpy, grid1(n), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg.dt, n);
+    // the host hand-off by kernels on the pinned staging (as nlrom_step's fixed-iteration graph)
+    launch(c, k_step_in, grid1((long long)std::max<size_t>(N, n)), 256, 0, (const double*)hi, c->rbar.p, c->rdbar.p,
+           c->fext.p, c->r.p, cfg.dt, n, (long long)N);
     phase_E(c, cfg);
     launch(c, k_nt_init, 1, 1, 0, hO, (const double*)c->norm.p, c->ad.p, cfg.newton_tol, cfg.max_iters);
     bodyO = add_while_node(c, hO);
-    launch(c, k_rdot, grid1(n), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p, 1.0 / cfg.dt, n);
-    NL_CUDA(cudaMemcpyAsync(ho, c->r.p, (size_t)n * 8, cudaMemcpyDeviceToHost, c->st));
-    NL_CUDA(cudaMemcpyAsync(ho + n, c->rdot.p, (size_t)n * 8, cudaMemcpyDeviceToHost, c->st));
-    NL_CUDA(cudaMemcpyAsync(ho + 2 * n, c->ad.p, NT_SIZE * 8, cudaMemcpyDeviceToHost, c->st));
+    launch(c, k_step_out, grid1(std::max(n, (int)NT_SIZE)), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p,
+           c->rdot.p, 1.0 / cfg.dt, n, (const double*)c->ad.p, (int)NT_SIZE, (const int*)nullptr, 1, ho, (int*)nullptr);
   } catch (...) {
     cudaStreamEndCapture(c->st, &G);
     if (G) cudaGraphDestroy(G);
@@ -1880,22 +1877,18 @@ extern "C" int nlrom_step(nlrom_ctx* c, const double* rbar, const double* rdbar,
       // residual, rdot and the pinned D2H of r, rdot, ||phi|| and the pivot status
       if (c->gStep) cudaGraphExecDestroy(c->gStep);
       c->gStep = capture(c, [&] {
-        NL_CUDA(cudaMemcpyAsync(c->rbar.p, hi, (size_t)nn * 8, cudaMemcpyHostToDevice, c->st));
-        NL_CUDA(cudaMemcpyAsync(c->rdbar.p, hi + nn, (size_t)nn * 8, cudaMemcpyHostToDevice, c->st));
-        NL_CUDA(cudaMemcpyAsync(c->fext.p, hi + 2 * nn, nf * 8, cudaMemcpyHostToDevice, c->st));
-        launch(c, k_axpy, grid1(nn), 256, 0, c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, cfg->dt,
-               nn);
+        // the host hand-off by two kernels on the pinned staging (k_step_in / k_step_out): the
+        // copy-engine nodes cost ~5 us each per step call at cfg2
+        launch(c, k_step_in, grid1((long long)std::max<size_t>(nf, nn)), 256, 0, (const double*)hi, c->rbar.p,
+               c->rdbar.p, c->fext.p, c->r.p, cfg->dt, nn, (long long)nf);
         for (int it = 0; it < cfg->fixed_iters; ++it) {
           phase_E(c, *cfg, false);
           phase_J(c, *cfg, true, nullptr, 0, nullptr, true);
         }
         if (want_norm) phase_E(c, *cfg, true, /*resid_only=*/true);   // ||phi|| of the final iterate
-        launch(c, k_rdot, grid1(nn), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p, c->rdot.p,
-               1.0 / cfg->dt, nn);
-        NL_CUDA(cudaMemcpyAsync(ho, c->r.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
-        NL_CUDA(cudaMemcpyAsync(ho + nn, c->rdot.p, (size_t)nn * 8, cudaMemcpyDeviceToHost, c->st));
-        if (want_norm) NL_CUDA(cudaMemcpyAsync(ho + 2 * nn, c->norm.p, 8, cudaMemcpyDeviceToHost, c->st));
-        NL_CUDA(cudaMemcpyAsync(hs, c->status.p, c->n_sims * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+        launch(c, k_step_out, grid1(std::max(nn, c->n_sims)), 256, 0, (const double*)c->r.p, (const double*)c->rbar.p,
+               c->rdot.p, 1.0 / cfg->dt, nn, (const double*)c->norm.p, want_norm ? 1 : 0, (const int*)c->status.p,
+               c->n_sims, ho, hs);
       }, nullptr);
       c->step_key = key;
     }

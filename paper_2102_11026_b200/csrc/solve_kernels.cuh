@@ -1091,6 +1091,43 @@ __global__ void k_rdot(const double* __restrict__ r, const double* __restrict__ 
   pdl_launch();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) rdot[i] = (r[i] - rbar[i]) * inv_dt;
 }
+// nlrom_step's host hand-off without copy-engine nodes: the step graph's first kernel reads the
+// pinned staging (r_bar | rdot_bar | f_ext) over the bus and forms the predictor (k_axpy), its last
+// writes r, rdot, ||phi|| and the pivot status into pinned memory (k_rdot) -- the same arithmetic
+// as k_axpy / k_rdot, two kernel nodes instead of seven memcpy nodes.
+__global__ void k_step_in(const double* __restrict__ hin, double* __restrict__ rbar, double* __restrict__ rdbar,
+                          double* __restrict__ fext, double* __restrict__ r, double t, int nn, long long nf) {
+  pdl_wait();
+  pdl_launch();
+  const long long tot = nf > nn ? nf : nn;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot; i += (long long)gridDim.x * blockDim.x) {
+    if (i < nn) {
+      const double base = hin[i], d = hin[nn + i];
+      rbar[i] = base;
+      rdbar[i] = d;
+      r[i] = base + t * d;
+    }
+    if (i < nf) fext[i] = hin[2 * (long long)nn + i];
+  }
+}
+__global__ void k_step_out(const double* __restrict__ r, const double* __restrict__ rbar, double* __restrict__ rdot,
+                           double inv_dt, int nn, const double* __restrict__ extra, int nextra,
+                           const int* __restrict__ status, int n_sims, double* __restrict__ ho, int* __restrict__ hs) {
+  pdl_wait();
+  pdl_launch();
+  const int tot = max(nn, max(nextra, status ? n_sims : 0));
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+    if (i < nn) {
+      const double ri = r[i];
+      const double rd = (ri - rbar[i]) * inv_dt;
+      rdot[i] = rd;
+      ho[i] = ri;
+      ho[nn + i] = rd;
+    }
+    if (i < nextra) ho[2 * nn + i] = extra[i];   // ||phi|| (fixed step) / the Newton state (adaptive)
+    if (status && i < n_sims) hs[i] = status[i];
+  }
+}
 __global__ void k_mul(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out, int n) {
   pdl_wait();
   pdl_launch();

@@ -50,8 +50,21 @@ class ReducedState:
     def __post_init__(self):
         self.r = np.asarray(self.r, dtype=float).copy()
         self.rdot = np.asarray(self.rdot, dtype=float).copy()
-        if self.r.shape != self.rdot.shape or not (np.all(np.isfinite(self.r)) and np.all(np.isfinite(self.rdot))):
-            raise ValueError("ReducedState must be finite with matching r / rdot (SPEC.md:452)")
+        _check_state(self.r, self.rdot)
+
+    @classmethod
+    def _owned(cls, r, rdot, dt):
+        """A state around fresh float64 arrays the caller gives up (no copies): rdsim.step's
+        device outputs. Same validation as the constructor."""
+        st = object.__new__(cls)
+        st.r, st.rdot, st.dt = r, rdot, dt
+        _check_state(r, rdot)
+        return st
+
+
+def _check_state(r, rdot):
+    if r.shape != rdot.shape or not (np.isfinite(r).all() and np.isfinite(rdot).all()):
+        raise ValueError("ReducedState must be finite with matching r / rdot (SPEC.md:452)")
 
 
 def _split(rm, r):

@@ -71,7 +71,7 @@ def step(rm: ReducedModel, model, state: ReducedState, f_ext, cfg: SimConfig, cm
     on the device; returns the new ReducedState (and (iters, ||phi||) if asked)."""
     # the final residual norm of a fixed-iteration step is evaluated only when it is returned
     r, rdot, iters, nrm = _sess(rm, model, cm).step(state.r, state.rdot, f_ext, cfg, want_norm=return_info)
-    new = ReducedState(r, rdot, cfg.dt)
+    new = ReducedState._owned(r, rdot, cfg.dt)
     return (new, (iters, nrm)) if return_info else new
 
 

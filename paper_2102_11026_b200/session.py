@@ -284,7 +284,8 @@ def _uploaded_arrays(rm, model, cm):
     nets = [rm.decoder] + ([cm.wnet] if cm is not None and cm.wnet is not None else [])
     for net in nets:
         for table in (net.weights, net.biases, net.bases):
-            arrs.extend(table[k] for k in sorted(table))
+            # insertion order: stable across calls (a key added / removed changes the fingerprint)
+            arrs.extend(table.values())
     if cm is not None:
         arrs.append(cm.C)
     return [a for a in arrs if isinstance(a, np.ndarray)]
