@@ -191,6 +191,7 @@ struct nlrom_ctx {
   cudaGraphExec_t gAdapt = nullptr; // whole adaptive step: conditional while nodes (newton_kernels.cuh)
   std::string adapt_key;
   DBuf ad;                          // adaptive Newton state (NT_SIZE doubles)
+  DBuf wsk;                         // batched weight-net layer 1: split-K partials [sim][split][wn]
   std::string step_key;
   std::string graph_key;
   int launches_E = 0, launches_J = 0;
@@ -595,9 +596,27 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
 void wnet_phase(nlrom_ctx* c) {
   int nsplit = c->wsplit;
   if (c->batched) {
-    // layer 1 for all sims as one GEMM: part (n_sims x wn) = u (n_sims x N) W1^T
-    GemmArgs g{c->W1.p, c->u.p, round_up(c->N, 2), c->N, c->wn, c->n_sims, c->N, 0, 0};
-    launch_gemm<CfgBig>(g, EpiStore{c->wpart.p, c->wn, 0, nullptr, 1, nullptr}, c->st);
+    // layer 1 for all sims as one GEMM: part (n_sims x wn) = u (n_sims x N) W1^T; few output tiles
+    // (M = wn) and K = N long: split K over blockIdx.z into [sim][split][wn] partials, then a
+    // fixed-order reduction (cfg5: 32 CTAs, 95 us unsplit)
+    const int M = c->wn, tiles = ceil_div(M, CfgBig::BM) * ceil_div(c->n_sims, CfgBig::BN);
+    int split = 1;
+    for (int sp : {16, 12, 10, 8, 6, 5, 4, 3, 2})
+      if (tiles * sp <= 2 * 148 * 2 && c->N % sp == 0 && (c->N / sp) % 2 == 0 && c->N / sp >= 64 &&
+          (size_t)c->n_sims * sp * M <= c->wsk.n) {
+        split = sp;
+        break;
+      }
+    if (split == 1) {
+      GemmArgs g{c->W1.p, c->u.p, round_up(c->N, 2), c->N, M, c->n_sims, c->N, 0, 0};
+      launch_gemm<CfgBig>(g, EpiStore{c->wpart.p, M, 0, nullptr, 1, nullptr}, c->st);
+    } else {
+      const int Kc = c->N / split;
+      GemmArgs g{c->W1.p, c->u.p, round_up(c->N, 2), c->N, M, c->n_sims, Kc, Kc, Kc};
+      launch_gemm<CfgBig>(g, EpiStore{c->wsk.p, split * M, M, nullptr, 1, nullptr}, c->st, split);
+      launch(c, k_reduce_cols, dim3(ceil_div(M, 32), c->n_sims), 256, 0, (const double*)c->wsk.p, split, M,
+             c->wpart.p);
+    }
     ++gemm_launch_count;
     nsplit = 1;
   } else {
@@ -1383,6 +1402,8 @@ extern "C" int nlrom_create(nlrom_ctx** out, int device, const nlrom_model_desc*
       c->wchunk = round_up(std::max(32, ceil_div(N, 148)), 32);
       c->wsplit = ceil_div(N, c->wchunk);
       c->wpart.alloc((size_t)c->wsplit * c->n_sims * wn);
+      if (c->n_sims * (4 + 4 * n_q) >= 2048 || c->opt.batched)   // the batched path (c->batched, below)
+        c->wsk.alloc((size_t)16 * c->n_sims * wn);
       c->wC.alloc((size_t)c->n_sims * std::max(1, c->n_cub));
     }
     // bundle buffers
