@@ -44,6 +44,9 @@ template <int G> using CfgOut = GemmCfg<64, G, 4, 1, 1, 32, 4>;
 // CTAs share an SM and one's epilogue overlaps the other's DMMA loop (tools/probes/gemm_probe.cu:
 // 26.7 TFLOP/s vs 22.1 for 32-wide K tiles at one CTA per SM, M = K = 256, 393k columns)
 using CfgBig = GemmCfg<64, 128, 2, 4, 1, 16, 3>;
+// the last shared-real vhp backward layer (M = n_q <= 24 output rows): 24-row tiles, K split over
+// two warps (CfgBig's 64-row tiles left 69% of the DMMA work on padding rows at n_q = 20)
+using CfgBwdLast = GemmCfg<24, 128, 1, 4, 2, 16, 3>;
 
 struct CubSet {
   IBuf elems;
@@ -974,7 +977,8 @@ void decoder_backward(nlrom_ctx* c, const double* a_vec, int NS, bool mc, int np
       std::swap(cur, nxt);
     }
     GemmArgs g{c->WT[0].p, cur->p, c->ldWT[0], ldcs[0], c->widths[0], ncs, c->widths[1], 0, 0, cstep};
-    launch_gemm<CfgBig>(g, EpiStoreShared{Gout.p, ldG, npass_per_sim}, c->st);
+    if (c->widths[0] <= 24 && c->widths[1] % 16 == 0) launch_gemm<CfgBwdLast>(g, EpiStoreShared{Gout.p, ldG, npass_per_sim}, c->st);
+    else launch_gemm<CfgBig>(g, EpiStoreShared{Gout.p, ldG, npass_per_sim}, c->st);
     ++gemm_launch_count;
     return;
   }
