@@ -433,7 +433,8 @@ void output_layer(nlrom_ctx* c) {
   // layer's epilogue), else the cp.async big-tile kernel (the warp-specialised pipeline measured
   // slower here: 3.38 vs 3.06 ms at cfg5, the EpiJetOutC scatter dominates the tile)
   if (c->batched && out_on_tc(c)) {
-    launch_ozaki<64>(c->ozWL.view(), OzakiBExp{c->ozHW[(c->L - 2) & 1], c->wL1 / 32}, g, e, c->st);
+    // row-major fp64 tile: coalesced J~ / dJ row stores (EpiJetOutCRow)
+    launch_ozaki<64>(c->ozWL.view(), OzakiBExp{c->ozHW[(c->L - 2) & 1], c->wL1 / 32}, g, EpiJetOutCRow{e}, c->st);
   } else if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
   else if (c->ldlast % 2 == 0 && g.C <= 64) launch_gemm_ws<CfgOutWs64c>(g, e, c->st);
   else if (c->ldlast % 2 == 0) launch_gemm_ws<CfgOutWs>(g, e, c->st);

@@ -327,6 +327,54 @@ struct EpiJetOutC {
   }
 };
 
+// EpiJetOutC for the tcgen05 output layer, which hands it the fp64 tile row-major (t.Cs[row * t.ldc
+// + col], ozaki_tc.cuh row_major_cs): the per-sim rows of J~ and dJ are contiguous in kg, so lanes
+// over the tile's column pairs store them coalesced (lanes over rows wrote 8 bytes per 256-byte J~
+// row); the base columns (u, D(q), hvv, with the U p dot product) keep lanes over rows.
+struct EpiJetOutCRow {
+  static constexpr bool kRowMajorCs = true;
+  EpiJetOutC o;
+  __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
+    const int N = g.M;
+    const int cs = 2 + 2 * o.n_q;
+    const int ngrp = t.bn / 2;
+    // base column pairs (rem == 0): at most ceil(t.bn / cs) + 1 per tile, lanes over rows
+    for (int p0 = (cs - t.c0 % cs) % cs; p0 < t.bn; p0 += cs) {
+      const int c = t.c0 + p0;
+      if (c >= g.C) break;
+      const int sim = c / cs;
+      for (int ml = tid; ml < t.bm; ml += nt) {
+        const int m = t.m0 + ml;
+        if (m >= N) continue;
+        const size_t sv = (size_t)sim * N + m;
+        const double* row = t.Cs + (size_t)ml * t.ldc + p0;
+        const double d1 = row[0] + o.bias[m];
+        double up = 0.0;
+        const double* Ur = o.U + (size_t)m * o.n_p;
+        const double* pz = o.r + (size_t)sim * (o.n_p + o.n_q);
+        for (int k = 0; k < o.n_p; ++k) up = fma(Ur[k], pz[k], up);
+        o.u[sv] = up + d1;
+        o.value[sv] = d1;
+        o.hvv[sv] = row[1];
+      }
+    }
+    // tangent column pairs: lanes over the pairs of a row
+    for (int i = tid; i < t.bm * ngrp; i += nt) {
+      const int q = i % ngrp, ml = i / ngrp;
+      const int m = t.m0 + ml;
+      const int c = t.c0 + 2 * q;
+      if (m >= N || c >= g.C) continue;
+      const int sim = c / cs, rem = c % cs;
+      if (rem == 0) continue;
+      const size_t sv = (size_t)sim * N + m;
+      const double* row = t.Cs + (size_t)ml * t.ldc + 2 * q;
+      const int kg = (rem - 2) >> 1;
+      o.Jt[sv * o.ldjt + o.n_p + kg] = row[0];
+      o.dJ[sv * o.lddj + kg] = row[1];
+    }
+  }
+};
+
 // Output layer of the fused bundle (linear + fused filter): from the jet columns
 //   value = D_1, J e_k = D_t, hvv = H(v,v) = 2 D_ss, dJ_k = S(e_k,v,v) + H(e_k,w) = 2 D_tss + D_tr
 // and u = U p + D(q). J is written into J~ = [U, J] (row-major, ldjt), dJ row-major (lddj).

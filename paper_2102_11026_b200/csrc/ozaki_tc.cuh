@@ -224,6 +224,12 @@ struct DigCtx {
   uint64_t* xbar;      // [2] tx barriers of xslot
   int j;               // tile counter of this CTA
 };
+// Epi functors that read the fp64 tile row-major (Cs[row * (BN + 1) + col]): lanes over columns
+// for coalesced row-major global stores (EpiJetOutCRow)
+template <class E, class = void>
+struct row_major_cs : std::false_type {};
+template <class E>
+struct row_major_cs<E, std::void_t<decltype(E::kRowMajorCs)>> : std::bool_constant<E::kRowMajorCs> {};
 template <class E, class = void>
 struct digits_out : std::false_type {};
 template <class E>
@@ -697,7 +703,9 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
                                ((long long)acc[5][i] << 8) + (long long)acc[6][i];
           const int E = em + (BDIG ? __shfl_sync(0xffffffffu, ecol, cl - chalf * SLW) : colE[(j & 1) * BN + cl]);
           // x_a x_b = q_a q_b 2^{E-110} = 2^{E+2} sum_d acc_d 2^{-8d} = hi 2^{E-30} + lo 2^{E-62}
-          Cs[cl * LDC + row_l] = E < -960 ? 0.0 : fma((double)hi, oz::pow2(E - 30), (double)lo * oz::pow2(E - 62));
+          const double yv = E < -960 ? 0.0 : fma((double)hi, oz::pow2(E - 30), (double)lo * oz::pow2(E - 62));
+          if constexpr (row_major_cs<Epi>::value) Cs[row_l * (BN + 1) + cl] = yv;
+          else Cs[cl * LDC + row_l] = yv;
         }
       }
       tc_fence_before();
@@ -708,7 +716,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
       if (lane == 0) mbar_arrive(tempty + buf);   // TMEM may take the next tiles' accumulators
       if constexpr (!BDIG) mbar_arrive(efree + (j & 1));
       named_bar_sync(1, NE);
-      Tile tile{Cs, LDC, m0, c0, BM, cs, 0};
+      Tile tile{Cs, row_major_cs<Epi>::value ? BN + 1 : LDC, m0, c0, BM, cs, 0};
 #ifndef OZ_PROBE_NO_EPI
       OZ_T0();
       if constexpr (DOUT)
