@@ -78,7 +78,11 @@ struct DBuf {
     n = count;
     if (count) {
       NL_CUDA(cudaMalloc(&p, count * sizeof(double)));
+      // the zero fill runs on the legacy stream, which does not order against the contexts'
+      // non-blocking streams: wait for it, or a kernel enqueued next on a context stream could
+      // write the buffer before the fill lands (a per-call diffop output read back as zeros)
       NL_CUDA(cudaMemset(p, 0, count * sizeof(double)));
+      NL_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
     }
   }
   void free() {
@@ -121,6 +125,7 @@ struct IBuf {
     if (count) {
       NL_CUDA(cudaMalloc(&p, count * sizeof(int)));
       NL_CUDA(cudaMemset(p, 0, count * sizeof(int)));
+      NL_CUDA(cudaStreamSynchronize(cudaStreamLegacy));   // (as DBuf::alloc)
     }
   }
   void upload(const int* h, size_t count) {
