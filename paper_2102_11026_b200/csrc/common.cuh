@@ -130,7 +130,10 @@ struct IBuf {
   }
   void upload(const int* h, size_t count) {
     alloc(count);
-    if (count) NL_CUDA(cudaMemcpy(p, h, count * sizeof(int), cudaMemcpyHostToDevice));
+    if (count) {
+      NL_CUDA(cudaMemcpy(p, h, count * sizeof(int), cudaMemcpyHostToDevice));
+      NL_CUDA(cudaStreamSynchronize(cudaStreamLegacy));   // pageable H2D: the DMA may still be in flight
+    }
   }
   void free() {
     if (p) cudaFree(p);

@@ -1195,7 +1195,12 @@ void ensure_graphs(nlrom_ctx* c, const nlrom_simcfg& cfg) {
 
 void upload(DBuf& d, const double* h, size_t n) {
   d.alloc(n);
-  if (n) NL_CUDA(cudaMemcpy(d.p, h, n * 8, cudaMemcpyHostToDevice));
+  if (n) {
+    NL_CUDA(cudaMemcpy(d.p, h, n * 8, cudaMemcpyHostToDevice));
+    // a pageable H2D returns once staged; the legacy stream does not order against the contexts'
+    // non-blocking streams, so wait for the DMA before kernels there may read the buffer
+    NL_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+  }
 }
 
 void h2d(nlrom_ctx* c, DBuf& d, const double* h, size_t n) {

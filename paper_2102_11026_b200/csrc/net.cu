@@ -15,8 +15,10 @@ namespace nlrom {
 void upload_matrix(DBuf& dst, const double* h, int rows, int cols, int ld, int rows_alloc) {
   if (rows_alloc < rows) rows_alloc = rows;
   dst.alloc((size_t)rows_alloc * ld);
-  if (rows && cols)
+  if (rows && cols) {
     NL_CUDA(cudaMemcpy2D(dst.p, (size_t)ld * 8, h, (size_t)cols * 8, (size_t)cols * 8, rows, cudaMemcpyHostToDevice));
+    NL_CUDA(cudaStreamSynchronize(cudaStreamLegacy));   // (as upload: pageable H2D vs non-blocking streams)
+  }
 }
 
 // (S, D, B) host-layout -> X_t[(b*S+s)][d] (ld)
@@ -169,6 +171,7 @@ extern "C" int nlrom_net_create(nlrom_net** out, int device, int n_layers, const
         upload_matrix(l.WT, wt.data(), l.in, l.out, l.ldwt);
         l.b.alloc(l.out);
         NL_CUDA(cudaMemcpy(l.b.p, d.b, l.out * 8, cudaMemcpyHostToDevice));
+        NL_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
       } else if (d.kind == NLROM_LAYER_FILTER) {
         if (l.in != l.out) throw Error(NLROM_ERR_DIM, "filter layers are square (SPEC.md:114)");
         l.nb = d.n_basis;
