@@ -292,10 +292,10 @@ def _uploaded_arrays(rm, model, cm):
 
 
 def _fingerprint(arrs):
-    # identity and size: an array object keeps its buffer unless resized in place (which changes
-    # its size), and the uploaded arrays are frozen read-only, so (id, size) identifies the data
+    # identity: the uploaded arrays are frozen read-only, so an array object keeps its buffer and
+    # contents (an in-place resize needs a writeable array) and its id identifies the data
     # (reading the data pointer per array costs ~1 us each on every step call)
-    return tuple(map(id, arrs)), tuple(a.size for a in arrs)
+    return tuple(map(id, arrs))
 
 
 _MAX_SESSIONS_PER_MODEL = 4
