@@ -508,6 +508,8 @@ bool fused_hidden_forward(nlrom_ctx* c, double dt, int drop_fict) {
   return false;
 }
 
+bool shared_real_bwd(nlrom_ctx* c, int npass_per_sim);
+
 // with_output = false: hidden layers only (stage timing of nlrom_bench_kernels).
 void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = true) {
   if (fused_hidden_forward(c, dt, drop_fict)) {
@@ -536,11 +538,13 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
     return !c->opt.oz_fp64_chain && c->ozDE[0] && 32 % c->G == 0 && l + 1 <= c->L - 2 && oz_runs(l) && oz_runs(l + 1) &&
            c->widths[l + 1] == 256 && (size_t)round_up(ncols, 64) * 7 <= (size_t)ncols * c->ldH[l] * 8;
   };
+  // the shared-real vhp backward reads one real part per sim and layer (EpiJet::real_once)
+  const bool real_once = shared_real_bwd(c, nq);
   if (seed_fused) {
     SeedLayerArgs sa{(const double*)c->r.p, (const double*)c->rbar.p, (const double*)c->rdbar.p, c->n_p, nq, c->n,
                      dt, c->alpha, drop_fict, (const double*)c->W[0].p, c->ldW[0], (const double*)c->b[0].p,
                      c->cache[0].p, c->ldc[0], c->G, c->gps, ncols, reinterpret_cast<unsigned char*>(c->H[0].p),
-                     c->ozDE[0], c->H[0].p, c->ldH[0], c->ozHW[0]};
+                     c->ozDE[0], c->H[0].p, c->ldH[0], c->ozHW[0], real_once ? 1 : 0};
     const bool dig = dig_out(0);
     // whole 64-column digit tiles: the CTAs past ncols write the padding half's zero digits
     if (dig) launch(c, k_seed_layer<true>, round_up(ncols, 64) / 32, 256, seed_layer_smem(), sa);
@@ -557,6 +561,7 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
     const int compact = (l == c->L - 2) ? 1 : 0;
     GemmArgs g{c->W[l].p, in, c->ldW[l], ldin, c->widths[l + 1], ncols, c->widths[l], 0, 0};
     EpiJet e{c->H[l].p, c->ldH[l], 0, c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, compact};
+    e.real_once = real_once ? 1 : 0;
     // tcgen05 Ozaki layers read their input's column scales from the previous layer's epilogue
     const bool oz_here = c->batched && l < (int)c->ozW.size() && c->ozW[l].ready;
     const bool oz_next = (c->batched && l + 1 < (int)c->ozW.size() && c->ozW[l + 1].ready && !compact &&
@@ -574,7 +579,7 @@ void bundle_forward(nlrom_ctx* c, double dt, int drop_fict, bool with_output = t
       }
       if (dout) {
         EpiJetDig ed{c->b[l].p, c->cache[l].p, c->ldc[l], c->G, c->gps, nq, reinterpret_cast<unsigned char*>(c->H[l].p),
-                     c->ozDE[l & 1]};
+                     c->ozDE[l & 1], real_once ? 1 : 0};
         if (din) launch_ozaki<64, EpiJetDig, true>(c->ozW[l].view(), be, g, ed, c->st);
         else launch_ozaki<64, EpiJetDig, false>(c->ozW[l].view(), be, g, ed, c->st);
       } else {

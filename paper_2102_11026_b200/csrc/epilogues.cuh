@@ -198,6 +198,9 @@ struct EpiJet {
   // colhw[c * (M / 32) + m / 32] = max over the 32 rows m of the high word of |Y[c][m]| (needs
   // M % 32 == 0 and 32-row-aligned warps: tile rows and thread counts multiples of 32).
   unsigned* colhw = nullptr;
+  // the vhp cache's real parts are the same for every tangent of a sim: with the shared-real
+  // backward (which reads only the first) write them once
+  int real_once = 0;
   __device__ void operator()(const Tile& t, const GemmArgs& g, int tid, int nt) const {
     double* Yz = Y + (size_t)t.z * strideY;
     const int nk = (group - 4) / 4;           // tangents per group
@@ -272,7 +275,7 @@ struct EpiJet {
             for (int s = 0; s < 4; ++s) note(4 + 4 * k + s, yo[s]);
         }
         if (Cz && kg < n_q) {  // sin'(z0 + y0 e) = cos z0 - sin z0 y0 e (dual), for the vhp backward
-          Cz[(size_t)(2 * kg) * ldcache + m] = jc.c1;
+          if (!real_once || kg == 0) Cz[(size_t)(2 * kg) * ldcache + m] = jc.c1;
           Cz[(size_t)(2 * kg + 1) * ldcache + m] = jc.ns * y[0];
         }
       }

@@ -23,6 +23,7 @@ struct EpiJetDig {
   int group, gps, n_q;
   unsigned char* dig;   // [ceil(C / 64)][M / 32][S][64 x 32 B]
   int* dexp;            // [ceil(C / 64) * 64]
+  int real_once = 0;    // vhp cache real parts once per sim (EpiJet::real_once)
 
   // BND = 64: a whole tile (one bulk store); BND = 32: one half tile of the consumer's 64-column B
   // tile (its 1 KB half of every (K chunk, plane) slice: 28 bulk stores).
@@ -66,7 +67,7 @@ struct EpiJetDig {
 #pragma unroll
         for (int s = 0; s < 4; ++s) cs0[(4 + 4 * k + s) * ldc] = yo[s];
         if (Cz && kg < n_q) {  // sin'(z0 + y0 e) = cos z0 - sin z0 y0 e (dual), for the vhp backward
-          Cz[(size_t)(2 * kg) * ldcache + m] = jc.c1;
+          if (!real_once || kg == 0) Cz[(size_t)(2 * kg) * ldcache + m] = jc.c1;
           Cz[(size_t)(2 * kg + 1) * ldcache + m] = jc.ns * y[0];
         }
       }
@@ -189,6 +190,7 @@ struct SeedLayerArgs {
   double* H;          // !DIG: (ncols x ldh)
   int ldh;
   unsigned* colhw;    // !DIG: [ncols][8]
+  int real_once;      // vhp cache real parts once per sim (EpiJet::real_once)
 };
 constexpr int SEED_LDZ = 258;
 inline size_t seed_layer_smem() { return (size_t)32 * SEED_LDZ * 8 + 8 * 32 * 4 + 32 * 4; }
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(256, 2) k_seed_layer(SeedLayerArgs a) {
 #pragma unroll
       for (int s2 = 0; s2 < 4; ++s2) zc[(4 + 4 * k + s2) * SEED_LDZ] = yo[s2];
       if (Cz && kg < a.n_q) {
-        Cz[(size_t)(2 * kg) * a.ldcache + m] = jc.c1;
+        if (!a.real_once || kg == 0) Cz[(size_t)(2 * kg) * a.ldcache + m] = jc.c1;
         Cz[(size_t)(2 * kg + 1) * a.ldcache + m] = jc.ns * y[0];
       }
     }
