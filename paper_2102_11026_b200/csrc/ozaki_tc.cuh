@@ -62,6 +62,9 @@ constexpr int NEPI = OZ_NEPI;   // epilogue threads (warps 2 ..: NEPI / 128 warp
 #define OZ_NCONV 256
 #endif
 constexpr int NCONV = OZ_NCONV;
+#ifndef OZ_B_PREFETCH
+#define OZ_B_PREFETCH 1
+#endif
 #ifndef OZ_DIG_SPLIT
 #define OZ_DIG_SPLIT 1   // B from digits: drain warps / functor warps on two fp64 tiles (0.86 vs 0.94 ms, cfg5)
 #endif // B converter threads (warps 10 ..): 256 measured 0.85 vs 0.95-1.0 ms with 128 (probe)
@@ -374,9 +377,19 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
           if (wrapped) mbar_wait_cta(empty + st, ph ^ 1u);
           mbar_expect_tx(fullA + st, BDIG ? A_STAGE + C::B_STAGE : A_STAGE);
           tma_g2s(sA + st * A_STAGE, a.tiles + ((size_t)tm * nk + kc) * A_STAGE, A_STAGE, fullA + st);
-          if constexpr (BDIG)
+          if constexpr (BDIG) {
             tma_g2s(sB + st * C::B_STAGE, bexp.dig + ((size_t)(t / tiles_m) * nk + kc) * C::B_STAGE, C::B_STAGE,
                     fullA + st);
+#if OZ_B_PREFETCH
+            // the next tile's digit chunk into L2 (the 2-stage ring of the split epilogue cannot hide
+            // a DRAM round trip per chunk)
+            const int tn = t + gridDim.x;
+            if (tn < ntiles) {
+              const unsigned char* pf = bexp.dig + ((size_t)(tn / tiles_m) * nk + kc) * C::B_STAGE;
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"((uint32_t)C::B_STAGE) : "memory");
+            }
+#endif
+          }
           if (++st == STAGES) {
             st = 0;
             ph ^= 1u;
