@@ -24,6 +24,9 @@
 #include "gemm_ws.cuh"
 #include "ozaki_tc.cuh"
 #include "ozaki_chain.cuh"
+#ifndef OZ_OUT_DIG
+#define OZ_OUT_DIG 1
+#endif
 #include "newton_kernels.cuh"
 
 namespace nlrom {
@@ -434,7 +437,24 @@ void output_layer(nlrom_ctx* c) {
   // slower here: 3.38 vs 3.06 ms at cfg5, the EpiJetOutC scatter dominates the tile)
   if (c->batched && out_on_tc(c)) {
     // row-major fp64 tile: coalesced J~ / dJ row stores (EpiJetOutCRow)
-    launch_ozaki<64>(c->ozWL.view(), OzakiBExp{c->ozHW[(c->L - 2) & 1], c->wL1 / 32}, g, EpiJetOutCRow{e}, c->st);
+    const OzakiBExp hw{c->ozHW[(c->L - 2) & 1], c->wL1 / 32};
+    const int C = g.C, Cpad = round_up(C, 64);
+    const bool dig = OZ_OUT_DIG && !c->opt.oz_fp64_chain && c->L >= 4 && c->ozDE[0] && g.K == 256 && c->wL1 == 256 &&
+                     (size_t)Cpad * 7 * 256 <= (size_t)c->n_sims * c->Cb * c->ldH[c->L - 3] * 8 &&
+                     Cpad <= round_up(c->n_sims * c->Cb, 64);
+    if (dig) {
+      // 8 m tiles per column: the input converted once (k_to_digits) into digit tiles landed by TMA
+      unsigned char* buf = reinterpret_cast<unsigned char*>(c->H[c->L - 3].p);   // consumed by the last hidden layer
+      int* dexp = c->ozDE[(c->L - 2) & 1];
+      launch(c, k_to_digits, ceil_div(Cpad * (g.K / 32), 256), 256, 0, (const double*)g.B, g.ldb, C, g.K, hw.parts,
+             hw.nparts, buf, dexp);
+      OzakiBExp be{nullptr, 0};
+      be.dig = buf;
+      be.dexp = dexp;
+      launch_ozaki<64, EpiJetOutCRow, true>(c->ozWL.view(), be, g, EpiJetOutCRow{e}, c->st);
+    } else {
+      launch_ozaki<64>(c->ozWL.view(), hw, g, EpiJetOutCRow{e}, c->st);
+    }
   } else if (c->batched) launch_gemm<CfgBig>(g, e, c->st);
   else if (c->ldlast % 2 == 0 && g.C <= 64) launch_gemm_ws<CfgOutWs64c>(g, e, c->st);
   else if (c->ldlast % 2 == 0) launch_gemm_ws<CfgOutWs>(g, e, c->st);

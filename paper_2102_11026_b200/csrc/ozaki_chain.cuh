@@ -296,4 +296,48 @@ __global__ void __launch_bounds__(256, 2) k_seed_layer(SeedLayerArgs a) {
   }
 }
 
+// fp64 activations -> the consumer's B digit tiles, for a consumer whose producer cannot write them
+// (the output layer: its input is the compact last hidden layer, and with 8 m tiles its converters
+// would convert every column 8 times). Column exponents from the producer's colhw partials by the
+// converters' rule, so the digits are exactly the converters'. One thread per (column, 32-row K
+// chunk); ceil(C / 64) * 64 columns (padding: zero digits, exponent 0).
+__global__ void __launch_bounds__(256) k_to_digits(const double* __restrict__ B, int ldb, int C, int K,
+                                                   const unsigned* __restrict__ parts, int nparts,
+                                                   unsigned char* __restrict__ dig, int* __restrict__ dexp) {
+  using namespace oz;
+  pdl_wait();
+  pdl_launch();
+  const int nk = K / BK;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(t % 32) + (int)(t / (32LL * nk)) * 32, kc = (int)((t / 32) % nk);
+  const int Cpad = (C + 63) / 64 * 64;
+  if (c >= Cpad) return;
+  const bool live = c < C;
+  unsigned hw = 0u;
+  if (live)
+    for (int p = 0; p < nparts; ++p) hw = max(hw, parts[(size_t)c * nparts + p]);
+  const int E = hw ? exp_of(__hiloint2double((int)hw, (int)0xFFFFFFFFu)) : 0;
+  if (kc == 0) dexp[c] = E;
+  const double sc = pow2(QBITS - E);
+  long long qv[32];
+  const double2* src = reinterpret_cast<const double2*>(B + (size_t)(live ? c : 0) * ldb + kc * BK);
+#pragma unroll
+  for (int q2 = 0; q2 < 16; ++q2) {
+    const double2 w = live ? src[q2] : make_double2(0.0, 0.0);
+    qv[2 * q2] = fixed55(w.x, sc);
+    qv[2 * q2 + 1] = fixed55(w.y, sc);
+  }
+  unsigned char* dst = dig + ((size_t)(c / 64) * nk + kc) * Cfg<64>::B_STAGE;
+#pragma unroll
+  for (int t2 = 0; t2 < S; ++t2) {
+#pragma unroll
+    for (int qb = 0; qb < 2; ++qb) {
+      const long long* q4 = qv + 16 * qb;
+      *reinterpret_cast<uint4*>(dst + t2 * Cfg<64>::B_SLICE + core_off(c % 64, 16 * qb)) =
+          make_uint4(pack_plane(q4[0], q4[1], q4[2], q4[3], t2), pack_plane(q4[4], q4[5], q4[6], q4[7], t2),
+                     pack_plane(q4[8], q4[9], q4[10], q4[11], t2), pack_plane(q4[12], q4[13], q4[14], q4[15], t2));
+    }
+  }
+}
+
 }  // namespace nlrom

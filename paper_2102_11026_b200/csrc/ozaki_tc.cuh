@@ -627,8 +627,9 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
             const long long lo = ((long long)acc[3][i] << 24) + ((long long)acc[4][i] << 16) +
                                  ((long long)acc[5][i] << 8) + (long long)acc[6][i];
             const int E = em + __shfl_sync(0xffffffffu, ecol, cl);
-            Csb[(chalf * 32 + cl) * LDC + row_l] =
-                E < -960 ? 0.0 : fma((double)hi, oz::pow2(E - 30), (double)lo * oz::pow2(E - 62));
+            const double yv = E < -960 ? 0.0 : fma((double)hi, oz::pow2(E - 30), (double)lo * oz::pow2(E - 62));
+            if constexpr (row_major_cs<Epi>::value) Csb[row_l * (BN + 1) + chalf * 32 + cl] = yv;
+            else Csb[(chalf * 32 + cl) * LDC + row_l] = yv;
           }
         }
         tc_fence_before();
@@ -643,7 +644,7 @@ __global__ void __launch_bounds__(oz::NT, 1) k_ozaki_gemm(OzakiA a, OzakiBExp be
         const int tm = t % tiles_m, tc = t / tiles_m;
         double* Csb = Cs + (j & 1) * CSD;
         mbar_wait_cta(csfull + (j & 1), (uint32_t)((j >> 1) & 1));
-        Tile tile{Csb, LDC, tm * BM, tc * BN, BM, BN, 0};
+        Tile tile{Csb, row_major_cs<Epi>::value ? BN + 1 : LDC, tm * BM, tc * BN, BM, BN, 0};
         OZ_T0();
 #ifndef OZ_PROBE_NO_EPI
         if constexpr (DOUT) {
